@@ -1,0 +1,245 @@
+/*
+ * hetsched_b200.h — C ABI of the B200-native graph-partition scheduler hot path.
+ *
+ * The reference (arXiv 1502.07451, package `hetsched`, /root/reference/pkg)
+ * has no FFI: its boundary is the Python API re-exported by
+ * pkg/src/hetsched/__init__.py:3-12. Every entry point below replaces the
+ * compute behind one of those Python functions; the Python package
+ * `paper_1502_07451_b200` keeps the reference names and signatures and calls
+ * these through ctypes (see INTEGRATION.md for the binding).
+ *
+ * Conventions
+ *  - All array arguments are DEVICE pointers (cudaMalloc / torch CUDA
+ *    tensors) unless the name ends in `_host`. The caller owns every buffer;
+ *    the library only allocates stream-ordered scratch (cudaMallocAsync).
+ *  - `stream` is a cudaStream_t passed as void*. Calls are asynchronous
+ *    unless documented otherwise; results are valid after the stream syncs.
+ *  - Return value: 0 (HS_OK) or a negative HS_E* status. The message of the
+ *    last failure on the calling thread is in hs_last_error().
+ *  - Node index space: a DAG's nodes are the reference's node ids sorted
+ *    ascending, numbered 0..n-1; `root` is the index of the SOURCE node.
+ *    "Kernel" index space: the n-1 non-root nodes in ascending id order
+ *    (the reference's graph.kernel_ids(), graph.py:92-94).
+ *  - Two-way part ids: 0 = CPU, 1 = GPU (METIS partition-file convention,
+ *    graphio.py:328). k-way part ids: 0..k-1.
+ *  - Floating point: fp64 everywhere; kernels on the bit-exact paths are
+ *    compiled without FMA contraction.
+ */
+#ifndef HETSCHED_B200_H
+#define HETSCHED_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HS_OK 0
+#define HS_EINVAL (-1)      /* bad argument (sizes, null pointers) */
+#define HS_ECUDA (-2)       /* CUDA runtime error */
+#define HS_ELIMIT (-3)      /* size beyond a documented limit */
+#define HS_EPOLICY (-4)     /* unknown policy id */
+#define HS_EDEADLOCK (-5)   /* simulation could not finish every node */
+#define HS_EPARTITION (-6)  /* partition precondition failed (zero weight, ...) */
+
+/* Directed task DAG, device CSR. Edges are stored once, sorted by
+ * (src, dst) — the reference's sorted(graph.edges) order (graph.py:114,
+ * partition.py:53). */
+typedef struct hs_dag {
+    int32_t n;               /* nodes, including the root */
+    int32_t root;            /* index of the SOURCE node */
+    int64_t m;               /* edges */
+    const int64_t *out_ptr;  /* [n+1] */
+    const int32_t *out_dst;  /* [m]   sorted by (src, dst) */
+    const int64_t *in_ptr;   /* [n+1] */
+    const int32_t *in_src;   /* [m]   per dst, ascending src (graph.py:89-90) */
+    const int32_t *in_eid;   /* [m]   edge index (out order) of each in-entry */
+    const double *w_cpu;     /* [n] */
+    const double *w_gpu;     /* [n] */
+    const double *w_xfer;    /* [m] out order */
+    const int64_t *bytes;    /* [m] out order */
+} hs_dag_t;
+
+/* A batch of independent DAGs packed back to back (config 5: one graph per
+ * simulation). Graph b owns nodes [node_off[b], node_off[b+1]) and edges
+ * [edge_off[b], edge_off[b+1]); indices inside the arrays are LOCAL to the
+ * graph (0..n_b-1 / 0..m_b-1); out_ptr/in_ptr are local too and have
+ * n_b+1 entries starting at node_off[b]+b. */
+typedef struct hs_dag_batch {
+    int32_t batch;
+    int64_t total_nodes;         /* node_off[batch] */
+    int64_t total_edges;         /* edge_off[batch] */
+    const int64_t *node_off;     /* [batch+1] */
+    const int64_t *edge_off;     /* [batch+1] */
+    const int32_t *root;         /* [batch] local root index */
+    const int64_t *out_ptr;      /* [node_off[batch] + batch] */
+    const int32_t *out_dst;
+    const int64_t *in_ptr;
+    const int32_t *in_src;
+    const int32_t *in_eid;
+    const double *w_cpu;
+    const double *w_gpu;
+    const double *w_xfer;
+    const int64_t *bytes;
+} hs_dag_batch_t;
+
+/* Undirected weighted graph over the kernels (root excluded), device CSR —
+ * the graph `fm_refine` builds (partition.py:153-158) and `emit_metis`
+ * exports (graphio.py:285-304). For the exact 2-way path the neighbour order
+ * of each vertex is the reference's (sorted-edge order); the k-way path is
+ * order-independent. */
+typedef struct hs_ugraph {
+    int32_t n;               /* vertices (kernels) */
+    int64_t nnz;             /* adjacency entries = 2 * undirected edges */
+    const int64_t *xadj;     /* [n+1] */
+    const int32_t *adjncy;   /* [nnz] */
+    const double *adjwgt;    /* [nnz] fp64 edge weights (exact 2-way path) */
+    const int64_t *adjwgt_i; /* [nnz] integer edge weights (k-way path) */
+    const double *vwgt;      /* [n]  fp64 vertex weights (exact 2-way path) */
+    const int64_t *vwgt_i;   /* [n]  integer vertex weights (k-way path) */
+} hs_ugraph_t;
+
+/* ---- status / library ------------------------------------------------ */
+const char *hs_last_error(void);
+const char *hs_version(void);
+/* Number of launches of this library's kernels since load (evidence for the
+ * bench's gpu_launches field). */
+int64_t hs_launch_count(void);
+
+/* ---- K0 exact sums (fsum) --------------------------------------------
+ * Replaces math.fsum in total_weights (graph.py:327-332) and
+ * workload_ratio (costs.py:239-253): out_host[0..2] = correctly rounded
+ * sums of w_cpu, w_gpu over nodes (root skipped unless include_root) and
+ * of w_xfer over all edges. Synchronous. */
+int hs_exact_totals(const hs_dag_t *g, int include_root, double *out_host, void *stream);
+
+/* ---- K2 evaluate -------------------------------------------------------
+ * Replaces partition.evaluate / _finish (partition.py:60-84) for `batch`
+ * two-way assignments of one DAG. part: [batch][n_kernels] int8 (0 CPU /
+ * 1 GPU). Per assignment: cut = Σ w_xfer over inter-kernel edges with
+ * different sides, cpu_w = Σ node weight on CPU, total = Σ node weight.
+ * mode 0: sums in the reference's sequential order (bit-exact with the
+ *         reference's builtin sum) — one thread per assignment;
+ * mode 1: correctly rounded sums (superaccumulator), fully parallel.
+ * weight_source: 0 = CPU weights, 1 = GPU weights (partition.py:48-49).
+ * out: cut[batch], cpu_w[batch], total[batch] (device). */
+int hs_evaluate2(const hs_dag_t *g, const int8_t *part, int32_t batch,
+                 int weight_source, int mode,
+                 double *cut, double *cpu_w, double *total, void *stream);
+
+/* k-way batched evaluation on the directed DAG (config 2): for each of
+ * `batch` assignments part[b][n] (int32, node index space, root's entry
+ * ignored) computes the integer edge cut over inter-kernel edges
+ * (cut_bytes: Σ bytes, cut_edges: count), per-part loads in int64 (from
+ * vwgt_i, [batch][k]) and the distinct-producer transfer count/bytes: one
+ * transfer per (producer u, consumer part p != part[u]) pair — the
+ * k-memory-node generalisation of the simulator's item dedup
+ * (sim.py:86-89,141-144); its bytes are those of u's first edge into p. */
+int hs_evaluate_kway(const hs_dag_t *g, const int32_t *part, int32_t batch, int32_t k,
+                     const int64_t *vwgt_i, int64_t *cut_bytes, int64_t *cut_edges,
+                     int64_t *loads, int64_t *xfer_count, int64_t *xfer_bytes,
+                     void *stream);
+
+/* ---- K7 levels / critical path ----------------------------------------
+ * level[n]: longest-path depth in edges from the root (root = 0).
+ * finish[n]: longest path with node duration min(w_cpu, w_gpu) and zero
+ * transfer cost — critical_path_lower_bound (sim.py:239-247); *cp_host =
+ * max(finish) (synchronous). mode 0 = min(cpu,gpu) durations; mode 1 =
+ * w_gpu only; mode 2 = w_cpu only. n_levels_host receives max level + 1. */
+int hs_levels(const hs_dag_t *g, int mode, int32_t *level, double *finish,
+              double *cp_host, int32_t *n_levels_host, void *stream);
+
+/* Level order: nodes sorted by (level, index) — order[n]. */
+int hs_level_order(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
+                   int32_t *order, void *stream);
+
+/* ---- K8 batched discrete-event simulation -----------------------------
+ * Replaces sim.simulate (sim.py:68-204) with EagerPolicy / DmdaPolicy /
+ * GraphPartitionPolicy (policies.py:19-99), one simulation per thread,
+ * bit-exact (fp64 add/max only, reference event order).
+ * policy: 0 eager, 1 dmda, 2 gp (pin[] required: node-index space,
+ * 0 CPU / 1 GPU, root entry ignored).
+ * Outputs per simulation: makespan, transfer_count, transfer_bytes,
+ * busy[2] (CPU, GPU ms), kpd[2] (kernels per device), status (0 ok,
+ * HS_EDEADLOCK). If ev != NULL, events are written to ev at offset
+ * ev_off[b] (capacity ev_off[b+1]-ev_off[b], >= 2*n_b + 2*m_b) and ev_count[b]
+ * receives the number written, in generation order (the caller sorts). */
+typedef struct hs_event {
+    double time;
+    int32_t kind;      /* 0 xfer_start, 1 xfer_end, 2 kernel_start, 3 kernel_end */
+    int32_t a;         /* kernel local index, or producer local index (item) */
+    int32_t b;         /* item consumer local index for root items, else -1 */
+    int32_t resource;  /* worker id, or -1 for the bus */
+} hs_event_t;
+
+int hs_simulate_batch(const hs_dag_batch_t *g, int policy, const int8_t *pin,
+                      int32_t cpu_workers, int32_t gpu_workers,
+                      double *makespan, int64_t *transfer_count, int64_t *transfer_bytes,
+                      double *busy, int64_t *kpd, int32_t *status,
+                      hs_event_t *ev, const int64_t *ev_off, int64_t *ev_count,
+                      void *stream);
+
+/* ---- K5/K6 exact two-way partitioner ----------------------------------
+ * Replaces partition_heuristic's restart loop + fm_refine
+ * (partition.py:137-295) with the reference's exact semantics: one CTA per
+ * start order runs _greedy_init -> _repair_balance -> fm_refine; moves,
+ * gains, prefix selection and fp64 rounding follow the reference exactly.
+ * orders: [n_orders][g->n] kernel positions. If start != NULL the greedy
+ * init and repair are skipped and every CTA refines start[n] (fm_refine).
+ * Outputs per order: assign[n_orders][n] (0 CPU/1 GPU), cut, err.
+ * weights: [n] node weights (the configured source), w_total = their
+ * builtin sum (host-computed in id order). */
+int hs_fm2(const hs_ugraph_t *g, const double *edge_w_sorted,
+           const int32_t *edge_u, const int32_t *edge_v, int64_t n_edges,
+           const double *weights, double r_cpu, double tol,
+           const int32_t *orders, int32_t n_orders, const int8_t *start,
+           int8_t *assign, double *cut, double *err, void *stream);
+
+/* Exhaustive 2-way oracle (brute_force_partition, partition.py:87-134) on
+ * the device for n <= 30 (the Python API keeps the reference's limit of 20).
+ * Writes the winning mask (bit n-1-k set = kernel k on GPU) to *mask_host
+ * and whether it is feasible. Synchronous. */
+int hs_brute2(int32_t n, const double *weights, double r_cpu, double tol,
+              const int32_t *edge_a, const int32_t *edge_b, const double *edge_w,
+              int64_t n_edges, int64_t *mask_host, int32_t *feasible_host, void *stream);
+
+/* ---- K1/K3/K4/K5/K6 multilevel k-way partitioner -----------------------
+ * Balanced min-cut k-way partition of the undirected integer-weighted
+ * graph (METIS_PartGraphKway's role): heavy-edge
+ * matching, contraction, parallel initial partitioning on the coarsest
+ * graph, projection and boundary refinement per level. Balance: for every
+ * part p, |w_p/total - tpwgts[p]| <= tol (SURVEY App. B k-way
+ * generalisation of partition.py:72). tpwgts_host: [k] host fractions.
+ * part: [n] int32 output. stats_host (optional, 8 entries): cut, levels,
+ * coarsest n, max |w_p/total - t_p| * 1e9, feasible, passes, -, -. */
+int hs_partition_kway(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host,
+                      double tol, uint64_t seed, int32_t *part, int64_t *stats_host,
+                      void *stream);
+
+/* Symmetrise a DAG into the kernel-space undirected graph used by
+ * hs_partition_kway (K1): root and root edges dropped, vertex v (kernel
+ * position) adjacent to every predecessor and successor, adjwgt_i from
+ * edge_w_i (out order), vwgt_i copied from node_w_i (node index space).
+ * xadj/adjncy/adjwgt_i/vwgt_i are caller buffers sized (n-1)+1 / 2m. */
+int hs_symmetrize(const hs_dag_t *g, const int64_t *edge_w_i, const int64_t *node_w_i,
+                  int64_t *xadj, int32_t *adjncy, int64_t *adjwgt_i, int64_t *vwgt_i,
+                  int64_t *nnz_host, void *stream);
+
+/* Device generator of the layered fan-in DAG family of configs 2 and 4:
+ * n kernels over ceil(sqrt(n)) layers, m inter-kernel edges spread as evenly
+ * as possible over the kernels past layer 0, predecessors drawn uniformly
+ * without replacement from all earlier layers by a counter-based RNG
+ * (splitmix64 of (seed, node, draw)), root edge to every layer-0 kernel.
+ * Writes the full DAG CSR (n+1 nodes incl. root at index 0) into caller
+ * buffers sized from hs_layered_sizes(). */
+int hs_layered_sizes(int64_t n_kernels, int64_t m_inter, int64_t *n_nodes_host,
+                     int64_t *n_edges_host);
+int hs_layered_generate(int64_t n_kernels, int64_t m_inter, uint64_t seed,
+                        int64_t *out_ptr, int32_t *out_dst, int64_t *in_ptr,
+                        int32_t *in_src, int32_t *in_eid, int32_t *layer_of,
+                        void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETSCHED_B200_H */

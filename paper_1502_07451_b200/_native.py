@@ -1,0 +1,275 @@
+"""ctypes binding of the C ABI in include/hetsched_b200.h (libhetsched_b200.so).
+
+This module is the only place the package touches the native library. There
+is no CPU fallback: importing it without the built library raises, and every
+call requires a CUDA device. Device buffers are torch CUDA tensors (torch is
+the allocator/stream plumbing only); calls run on torch's current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhetsched_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make` (or __graft_entry__.build()). "
+        "The hot path has no CPU fallback.")
+_lib = ctypes.CDLL(LIB_PATH)
+
+HS_EDEADLOCK = -5
+_c_void_p = ctypes.c_void_p
+_i32, _i64, _f64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"hetsched_b200 error {code}: {message}")
+        self.code = code
+        self.message = message
+
+
+class HsDag(ctypes.Structure):
+    _fields_ = [("n", _i32), ("root", _i32), ("m", _i64),
+                ("out_ptr", _c_void_p), ("out_dst", _c_void_p),
+                ("in_ptr", _c_void_p), ("in_src", _c_void_p), ("in_eid", _c_void_p),
+                ("w_cpu", _c_void_p), ("w_gpu", _c_void_p),
+                ("w_xfer", _c_void_p), ("bytes", _c_void_p)]
+
+
+class HsDagBatch(ctypes.Structure):
+    _fields_ = [("batch", _i32), ("total_nodes", _i64), ("total_edges", _i64),
+                ("node_off", _c_void_p), ("edge_off", _c_void_p), ("root", _c_void_p),
+                ("out_ptr", _c_void_p), ("out_dst", _c_void_p),
+                ("in_ptr", _c_void_p), ("in_src", _c_void_p), ("in_eid", _c_void_p),
+                ("w_cpu", _c_void_p), ("w_gpu", _c_void_p),
+                ("w_xfer", _c_void_p), ("bytes", _c_void_p)]
+
+
+class HsUGraph(ctypes.Structure):
+    _fields_ = [("n", _i32), ("nnz", _i64), ("xadj", _c_void_p), ("adjncy", _c_void_p),
+                ("adjwgt", _c_void_p), ("adjwgt_i", _c_void_p),
+                ("vwgt", _c_void_p), ("vwgt_i", _c_void_p)]
+
+
+class HsEvent(ctypes.Structure):
+    _fields_ = [("time", _f64), ("kind", _i32), ("a", _i32), ("b", _i32),
+                ("resource", _i32)]
+
+
+EVENT_DTYPE = np.dtype([("time", "<f8"), ("kind", "<i4"), ("a", "<i4"), ("b", "<i4"),
+                        ("resource", "<i4")])
+assert EVENT_DTYPE.itemsize == ctypes.sizeof(HsEvent)
+
+
+def _proto(name, *argtypes):
+    fn = getattr(_lib, name)
+    fn.restype = ctypes.c_int
+    fn.argtypes = list(argtypes)
+    return fn
+
+
+_P = _c_void_p
+_lib.hs_last_error.restype = ctypes.c_char_p
+_lib.hs_version.restype = ctypes.c_char_p
+_lib.hs_launch_count.restype = ctypes.c_int64
+_exact_totals = _proto("hs_exact_totals", _P, ctypes.c_int, _P, _P)
+_evaluate2 = _proto("hs_evaluate2", _P, _P, _i32, ctypes.c_int, ctypes.c_int, _P, _P, _P, _P)
+_evaluate_kway = _proto("hs_evaluate_kway", _P, _P, _i32, _i32, _P, _P, _P, _P, _P, _P, _P)
+_levels = _proto("hs_levels", _P, ctypes.c_int, _P, _P, _P, _P, _P)
+_level_order = _proto("hs_level_order", _P, _P, _i32, _P, _P)
+_simulate_batch = _proto("hs_simulate_batch", _P, ctypes.c_int, _P, _i32, _i32,
+                         _P, _P, _P, _P, _P, _P, _P, _P, _P, _P)
+
+
+def _opt(name, *argtypes):
+    return _proto(name, *argtypes) if hasattr(_lib, name) else None
+
+
+_fm2 = _opt("hs_fm2", _P, _P, _P, _P, _i64, _P, _f64, _f64, _P, _i32, _P, _P, _P, _P, _P)
+_brute2 = _opt("hs_brute2", _i32, _P, _f64, _f64, _P, _P, _P, _i64, _P, _P, _P)
+_partition_kway = _opt("hs_partition_kway", _P, _i32, _P, _f64, ctypes.c_uint64, _P, _P, _P)
+_symmetrize = _opt("hs_symmetrize", _P, _P, _P, _P, _P, _P, _P, _P, _P)
+_layered_sizes = _opt("hs_layered_sizes", _i64, _i64, _P, _P)
+_layered_generate = _opt("hs_layered_generate", _i64, _i64, ctypes.c_uint64,
+                         _P, _P, _P, _P, _P, _P, _P)
+
+
+def version() -> str:
+    return _lib.hs_version().decode()
+
+
+def launch_count() -> int:
+    return int(_lib.hs_launch_count())
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        raise NativeError(rc, _lib.hs_last_error().decode(errors="replace"))
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("hetsched_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback on the hot path")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    if t is None:
+        return None
+    assert t.is_cuda and t.is_contiguous(), "device tensors must be contiguous CUDA tensors"
+    return t.data_ptr()
+
+
+def _need(fn, name):
+    if fn is None:
+        raise NativeError(-1, f"{name} is not exported by {LIB_PATH}")
+    return fn
+
+
+# ---------------------------------------------------------------- wrappers --
+
+def exact_totals(csr, include_root: bool) -> Tuple[float, float, float]:
+    out = (ctypes.c_double * 3)()
+    check(_exact_totals(ctypes.byref(csr.struct()), int(include_root), out, stream_ptr()))
+    return out[0], out[1], out[2]
+
+
+def evaluate2(csr, parts: torch.Tensor, weight_source: int, mode: int):
+    """parts: int8 [B, n_kernels] device tensor. Returns (cut, cpu_w, total) f64 [B]."""
+    b = parts.shape[0]
+    dev = parts.device
+    cut = torch.empty(b, dtype=torch.float64, device=dev)
+    cpu_w = torch.empty_like(cut)
+    total = torch.empty_like(cut)
+    check(_evaluate2(ctypes.byref(csr.struct()), ptr(parts), b, weight_source, mode,
+                     ptr(cut), ptr(cpu_w), ptr(total), stream_ptr()))
+    return cut, cpu_w, total
+
+
+def evaluate_kway(csr, parts: torch.Tensor, k: int, vwgt_i: torch.Tensor):
+    """parts: int32 [B, n] (node index space). Returns dict of int64 tensors."""
+    b = parts.shape[0]
+    dev = parts.device
+    z = lambda *s: torch.empty(*s, dtype=torch.int64, device=dev)  # noqa: E731
+    out = dict(cut_bytes=z(b), cut_edges=z(b), loads=z(b, k), xfer_count=z(b),
+               xfer_bytes=z(b))
+    check(_evaluate_kway(ctypes.byref(csr.struct()), ptr(parts), b, k, ptr(vwgt_i),
+                         ptr(out["cut_bytes"]), ptr(out["cut_edges"]), ptr(out["loads"]),
+                         ptr(out["xfer_count"]), ptr(out["xfer_bytes"]), stream_ptr()))
+    return out
+
+
+def levels(csr, mode: int = 0, sync: bool = True):
+    dev = csr.device
+    level = torch.empty(csr.n, dtype=torch.int32, device=dev)
+    finish = torch.empty(csr.n, dtype=torch.float64, device=dev)
+    cp = ctypes.c_double(0.0)
+    nl = ctypes.c_int32(0)
+    check(_levels(ctypes.byref(csr.struct()), mode, ptr(level), ptr(finish),
+                  ctypes.byref(cp) if sync else None, ctypes.byref(nl) if sync else None,
+                  stream_ptr()))
+    return level, finish, cp.value, nl.value
+
+
+def level_order(csr, level: torch.Tensor, n_levels: int) -> torch.Tensor:
+    order = torch.empty(csr.n, dtype=torch.int32, device=csr.device)
+    check(_level_order(ctypes.byref(csr.struct()), ptr(level), n_levels, ptr(order),
+                       stream_ptr()))
+    return order
+
+
+def simulate_batch(batch, policy: int, pin: Optional[torch.Tensor], cpu_workers: int,
+                   gpu_workers: int, events: bool = False):
+    """Runs batch.batch simulations; returns a dict of device tensors."""
+    b = batch.batch
+    dev = batch.device
+    out = dict(
+        makespan=torch.empty(b, dtype=torch.float64, device=dev),
+        transfer_count=torch.empty(b, dtype=torch.int64, device=dev),
+        transfer_bytes=torch.empty(b, dtype=torch.int64, device=dev),
+        busy=torch.empty(b, 2, dtype=torch.float64, device=dev),
+        kpd=torch.empty(b, 2, dtype=torch.int64, device=dev),
+        status=torch.empty(b, dtype=torch.int32, device=dev),
+    )
+    ev = ev_off = ev_count = None
+    if events:
+        cap = 2 * (batch.node_counts + batch.edge_counts)
+        ev_off_h = np.zeros(b + 1, dtype=np.int64)
+        np.cumsum(cap, out=ev_off_h[1:])
+        ev_off = torch.from_numpy(ev_off_h).to(dev)
+        ev = torch.empty(int(ev_off_h[-1]) * EVENT_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        ev_count = torch.empty(b, dtype=torch.int64, device=dev)
+        out.update(events=ev, ev_off=ev_off, ev_count=ev_count)
+    check(_simulate_batch(ctypes.byref(batch.struct()), policy, ptr(pin), cpu_workers,
+                          gpu_workers, ptr(out["makespan"]), ptr(out["transfer_count"]),
+                          ptr(out["transfer_bytes"]), ptr(out["busy"]), ptr(out["kpd"]),
+                          ptr(out["status"]), ptr(ev), ptr(ev_off), ptr(ev_count),
+                          stream_ptr()))
+    return out
+
+
+def fm2(ug, edge_w, edge_u, edge_v, weights, r_cpu, tol, orders, start):
+    fn = _need(_fm2, "hs_fm2")
+    n_orders = orders.shape[0]
+    dev = weights.device
+    assign = torch.empty(n_orders, ug.n, dtype=torch.int8, device=dev)
+    cut = torch.empty(n_orders, dtype=torch.float64, device=dev)
+    err = torch.empty(n_orders, dtype=torch.float64, device=dev)
+    check(fn(ctypes.byref(ug.struct()), ptr(edge_w), ptr(edge_u), ptr(edge_v),
+             int(edge_w.numel()), ptr(weights), float(r_cpu), float(tol), ptr(orders),
+             n_orders, ptr(start), ptr(assign), ptr(cut), ptr(err), stream_ptr()))
+    return assign, cut, err
+
+
+def brute2(n, weights, r_cpu, tol, edge_a, edge_b, edge_w):
+    fn = _need(_brute2, "hs_brute2")
+    mask = ctypes.c_int64(0)
+    feas = ctypes.c_int32(0)
+    check(fn(n, ptr(weights), float(r_cpu), float(tol), ptr(edge_a), ptr(edge_b),
+             ptr(edge_w), int(edge_w.numel()), ctypes.byref(mask), ctypes.byref(feas),
+             stream_ptr()))
+    return mask.value, bool(feas.value)
+
+
+def partition_kway(ug, k: int, tpwgts, tol: float, seed: int, part: torch.Tensor):
+    fn = _need(_partition_kway, "hs_partition_kway")
+    tp = (ctypes.c_double * k)(*[float(x) for x in tpwgts])
+    stats = (ctypes.c_int64 * 8)()
+    check(fn(ctypes.byref(ug.struct()), k, tp, float(tol), ctypes.c_uint64(seed & (2**64 - 1)),
+             ptr(part), stats, stream_ptr()))
+    return list(stats)
+
+
+def symmetrize(csr, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i) -> int:
+    fn = _need(_symmetrize, "hs_symmetrize")
+    nnz = ctypes.c_int64(0)
+    check(fn(ctypes.byref(csr.struct()), ptr(edge_w_i), ptr(node_w_i), ptr(xadj),
+             ptr(adjncy), ptr(adjwgt_i), ptr(vwgt_i), ctypes.byref(nnz), stream_ptr()))
+    return nnz.value
+
+
+def layered_sizes(n_kernels: int, m_inter: int) -> Tuple[int, int]:
+    fn = _need(_layered_sizes, "hs_layered_sizes")
+    n, m = ctypes.c_int64(0), ctypes.c_int64(0)
+    check(fn(n_kernels, m_inter, ctypes.byref(n), ctypes.byref(m)))
+    return n.value, m.value
+
+
+def layered_generate(n_kernels, m_inter, seed, out_ptr, out_dst, in_ptr, in_src, in_eid,
+                     layer_of):
+    fn = _need(_layered_generate, "hs_layered_generate")
+    check(fn(n_kernels, m_inter, ctypes.c_uint64(seed & (2**64 - 1)), ptr(out_ptr),
+             ptr(out_dst), ptr(in_ptr), ptr(in_src), ptr(in_eid), ptr(layer_of),
+             stream_ptr()))

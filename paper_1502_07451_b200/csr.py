@@ -1,0 +1,220 @@
+"""Device-resident CSR layouts of task DAGs (the HBM data layout of the hot path).
+
+``DagCSR``  — one directed DAG: out-CSR sorted by (src, dst) (the reference's
+              ``sorted(graph.edges)`` order), in-CSR with ascending sources
+              (``graph.in_edges``, graph.py:89-90), fp64 node/edge weights,
+              int64 byte counts. int64 row pointers, int32 indices.
+``DagBatch`` — many small DAGs back to back (config 5's 4096 simulations).
+``TwoWayGraph`` — the undirected kernel graph ``fm_refine`` builds
+              (partition.py:153-158) with the reference's neighbour order, plus
+              the inter-kernel edge list in sorted order, for the exact 2-way
+              partitioner.
+
+Host-side construction from ``TaskGraph`` objects is numpy; graphs generated
+on the device (``layered``) never leave HBM.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+
+
+def _csr_ptr(keys: np.ndarray, n: int) -> np.ndarray:
+    ptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(keys, minlength=n), out=ptr[1:])
+    return ptr
+
+
+@dataclass
+class HostDag:
+    """numpy arrays of one DAG in node-index space (see include/hetsched_b200.h)."""
+    ids: np.ndarray        # int64 [n] original node ids, ascending
+    root: int              # index of the root, -1 if absent
+    src: np.ndarray        # int32 [m] sorted by (src, dst)
+    dst: np.ndarray        # int32 [m]
+    w_cpu: np.ndarray      # f64 [n]
+    w_gpu: np.ndarray      # f64 [n]
+    w_xfer: np.ndarray     # f64 [m]
+    bytes: np.ndarray      # int64 [m]
+
+    @property
+    def n(self) -> int:
+        return len(self.ids)
+
+    @property
+    def m(self) -> int:
+        return len(self.src)
+
+    def out_ptr(self) -> np.ndarray:
+        return _csr_ptr(self.src, self.n)
+
+    def in_order(self) -> np.ndarray:
+        return np.lexsort((self.src, self.dst)).astype(np.int32)
+
+    @classmethod
+    def from_taskgraph(cls, graph) -> "HostDag":
+        ids = np.array(sorted(graph.nodes), dtype=np.int64)
+        index = {int(i): k for k, i in enumerate(ids)}
+        items = sorted((index[u], index[v], e) for (u, v), e in graph.edges.items()
+                       if u in index and v in index)
+        m = len(items)
+        src = np.fromiter((t[0] for t in items), dtype=np.int32, count=m)
+        dst = np.fromiter((t[1] for t in items), dtype=np.int32, count=m)
+        w_xfer = np.fromiter((t[2].weight_xfer for t in items), dtype=np.float64, count=m)
+        nbytes = np.fromiter((t[2].bytes for t in items), dtype=np.int64, count=m)
+        nodes = [graph.nodes[int(i)] for i in ids]
+        w_cpu = np.fromiter((nd.weight_cpu for nd in nodes), dtype=np.float64, count=len(ids))
+        w_gpu = np.fromiter((nd.weight_gpu for nd in nodes), dtype=np.float64, count=len(ids))
+        root = index.get(graph.root, -1)
+        return cls(ids, root, src, dst, w_cpu, w_gpu, w_xfer, nbytes)
+
+
+class DagCSR:
+    """Device CSR of one DAG; see module docstring."""
+
+    def __init__(self, n: int, m: int, root: int, out_ptr, out_dst, in_ptr, in_src, in_eid,
+                 w_cpu, w_gpu, w_xfer, nbytes, ids: Optional[np.ndarray] = None,
+                 host: Optional[HostDag] = None):
+        self.n, self.m, self.root = int(n), int(m), int(root)
+        self.out_ptr, self.out_dst = out_ptr, out_dst
+        self.in_ptr, self.in_src, self.in_eid = in_ptr, in_src, in_eid
+        self.w_cpu, self.w_gpu, self.w_xfer, self.bytes = w_cpu, w_gpu, w_xfer, nbytes
+        self.ids = ids
+        self.host = host
+        self.device = out_ptr.device
+        self._struct = None
+        self._twoway = None
+
+    @classmethod
+    def from_host(cls, h: HostDag, device=None) -> "DagCSR":
+        dev = device or _native.device()
+        order = h.in_order()
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        return cls(h.n, h.m, h.root, t(h.out_ptr()), t(h.dst), t(_csr_ptr(h.dst, h.n)),
+                   t(h.src[order]), t(order), t(h.w_cpu), t(h.w_gpu), t(h.w_xfer),
+                   t(h.bytes), ids=h.ids, host=h)
+
+    @classmethod
+    def from_taskgraph(cls, graph) -> "DagCSR":
+        h = HostDag.from_taskgraph(graph)
+        if h.root < 0:
+            raise ValueError(f"root node {graph.root} missing")
+        return cls.from_host(h)
+
+    def struct(self) -> _native.HsDag:
+        if self._struct is None:
+            p = _native.ptr
+            self._struct = _native.HsDag(
+                self.n, self.root, self.m, p(self.out_ptr), p(self.out_dst), p(self.in_ptr),
+                p(self.in_src), p(self.in_eid), p(self.w_cpu), p(self.w_gpu), p(self.w_xfer),
+                p(self.bytes))
+        return self._struct
+
+    @property
+    def n_kernels(self) -> int:
+        return self.n - 1
+
+    def kernel_pos(self, idx: np.ndarray) -> np.ndarray:
+        return np.where(idx < self.root, idx, idx - 1)
+
+    def twoway(self) -> "TwoWayGraph":
+        if self._twoway is None:
+            self._twoway = TwoWayGraph.from_host(self.host, self.device)
+        return self._twoway
+
+
+class TwoWayGraph:
+    """Undirected kernel graph in the reference's adjacency order (partition.py:153-158).
+
+    Vertex k is the k-th non-root kernel in ascending id order. Neighbour
+    lists follow the sorted edge order, each inter-kernel edge (u, v)
+    contributing v to u's list and u to v's list. ``edge_*`` is the
+    inter-kernel edge list itself in sorted order (what ``_cut_edges`` walks).
+    """
+
+    def __init__(self, n, xadj, adjncy, adjwgt, edge_u, edge_v, edge_w):
+        self.n = n
+        self.xadj, self.adjncy, self.adjwgt = xadj, adjncy, adjwgt
+        self.edge_u, self.edge_v, self.edge_w = edge_u, edge_v, edge_w
+        self.vwgt = None
+        self._struct = None
+
+    @classmethod
+    def from_host(cls, h: HostDag, dev) -> "TwoWayGraph":
+        n = h.n - 1
+        keep = (h.src != h.root) & (h.dst != h.root)
+        kp = lambda a: np.where(a < h.root, a, a - 1).astype(np.int32)  # noqa: E731
+        eu, ev, ew = kp(h.src[keep]), kp(h.dst[keep]), h.w_xfer[keep]
+        ne = len(eu)
+        node = np.concatenate([eu, ev])
+        nbr = np.concatenate([ev, eu])
+        pos = np.concatenate([np.arange(ne), np.arange(ne)])
+        order = np.lexsort((pos, node))
+        t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+        return cls(n, t(_csr_ptr(node, n)), t(nbr[order].astype(np.int32)),
+                   t(np.concatenate([ew, ew])[order]), t(eu), t(ev), t(ew))
+
+    def struct(self) -> _native.HsUGraph:
+        if self._struct is None:
+            p = _native.ptr
+            self._struct = _native.HsUGraph(self.n, int(self.adjncy.numel()), p(self.xadj),
+                                            p(self.adjncy), p(self.adjwgt), None,
+                                            p(self.vwgt) if self.vwgt is not None else None,
+                                            None)
+        return self._struct
+
+
+class DagBatch:
+    """Many DAGs packed back to back (local indices per graph)."""
+
+    def __init__(self, hosts: Sequence[HostDag], device=None):
+        dev = device or _native.device()
+        self.device = dev
+        self.hosts = list(hosts)
+        b = len(hosts)
+        self.batch = b
+        self.node_counts = np.array([h.n for h in hosts], dtype=np.int64)
+        self.edge_counts = np.array([h.m for h in hosts], dtype=np.int64)
+        node_off = np.zeros(b + 1, dtype=np.int64)
+        edge_off = np.zeros(b + 1, dtype=np.int64)
+        np.cumsum(self.node_counts, out=node_off[1:])
+        np.cumsum(self.edge_counts, out=edge_off[1:])
+        self.node_off_h, self.edge_off_h = node_off, edge_off
+        out_ptr, in_ptr, in_src, in_eid = [], [], [], []
+        for h in hosts:
+            order = h.in_order()
+            out_ptr.append(h.out_ptr())
+            in_ptr.append(_csr_ptr(h.dst, h.n))
+            in_src.append(h.src[order])
+            in_eid.append(order)
+        cat = lambda xs, dt: torch.from_numpy(  # noqa: E731
+            np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros(0, dt), dtype=dt)).to(dev)
+        self.node_off = cat([node_off], np.int64)
+        self.edge_off = cat([edge_off], np.int64)
+        self.root = cat([np.array([h.root for h in hosts], dtype=np.int32)], np.int32)
+        self.out_ptr = cat(out_ptr, np.int64)
+        self.in_ptr = cat(in_ptr, np.int64)
+        self.out_dst = cat([h.dst for h in hosts], np.int32)
+        self.in_src = cat(in_src, np.int32)
+        self.in_eid = cat(in_eid, np.int32)
+        self.w_cpu = cat([h.w_cpu for h in hosts], np.float64)
+        self.w_gpu = cat([h.w_gpu for h in hosts], np.float64)
+        self.w_xfer = cat([h.w_xfer for h in hosts], np.float64)
+        self.bytes = cat([h.bytes for h in hosts], np.int64)
+        self._struct = None
+
+    def struct(self) -> _native.HsDagBatch:
+        if self._struct is None:
+            p = _native.ptr
+            self._struct = _native.HsDagBatch(
+                self.batch, int(self.node_off_h[-1]), int(self.edge_off_h[-1]),
+                p(self.node_off), p(self.edge_off), p(self.root), p(self.out_ptr),
+                p(self.out_dst), p(self.in_ptr), p(self.in_src), p(self.in_eid),
+                p(self.w_cpu), p(self.w_gpu), p(self.w_xfer), p(self.bytes))
+        return self._struct

@@ -1,0 +1,73 @@
+// Shared helpers for the hetsched_b200 C ABI: status plumbing, launch
+// accounting, stream-ordered scratch, small device utilities.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdarg.h>
+#include "../../include/hetsched_b200.h"
+
+namespace hs {
+
+void set_error(const char *fmt, ...);
+void count_launch(int64_t k = 1);
+
+#define HS_CHECK_CUDA(expr)                                                     \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::hs::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,                \
+                      cudaGetErrorString(_e));                                  \
+      return HS_ECUDA;                                                          \
+    }                                                                           \
+  } while (0)
+
+#define HS_CHECK_LAUNCH()                                                       \
+  do {                                                                          \
+    ::hs::count_launch();                                                       \
+    cudaError_t _e = cudaGetLastError();                                        \
+    if (_e != cudaSuccess) {                                                    \
+      ::hs::set_error("%s:%d launch: %s", __FILE__, __LINE__,                   \
+                      cudaGetErrorString(_e));                                  \
+      return HS_ECUDA;                                                          \
+    }                                                                           \
+  } while (0)
+
+#define HS_REQUIRE(cond, code, ...)                                             \
+  do {                                                                          \
+    if (!(cond)) {                                                              \
+      ::hs::set_error(__VA_ARGS__);                                             \
+      return (code);                                                            \
+    }                                                                           \
+  } while (0)
+
+// Stream-ordered scratch buffer that frees itself (cudaFreeAsync) on scope exit.
+template <typename T>
+struct Scratch {
+  T *p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t count, cudaStream_t stream) {
+    s = stream;
+    if (count == 0) count = 1;
+    return cudaMallocAsync((void **)&p, count * sizeof(T), stream);
+  }
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+  operator T *() const { return p; }
+};
+
+inline int grid_for(int64_t work, int block, int max_blocks = 148 * 32) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > max_blocks) g = max_blocks;
+  return (int)g;
+}
+
+// out[i] = i for i < n (stream-ordered).
+int iota32(int32_t *out, int64_t n, cudaStream_t s);
+
+// Number of SMs of the current device (cached).
+int sm_count();
+
+}  // namespace hs

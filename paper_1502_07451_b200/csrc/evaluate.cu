@@ -1,0 +1,261 @@
+// K0 exact totals and K2 evaluate (two-way and k-way) on the directed DAG CSR.
+//
+// Reference: partition.evaluate / _finish (pkg/src/hetsched/partition.py:60-84),
+// graph.total_weights (graph.py:327-332), costs.workload_ratio
+// (costs.py:239-253).
+#include "common.cuh"
+#include "numeric.cuh"
+
+namespace {
+
+using hs::kAccLimbs;
+
+__device__ __forceinline__ int kpos(int v, int root) { return v < root ? v : v - 1; }
+
+// ---------------------------------------------------------------- K0 -----
+// acc layout: [3][kAccLimbs] int64 (w_cpu, w_gpu, w_xfer).
+__global__ void totals_kernel(hs_dag_t g, int include_root, unsigned long long *acc) {
+  __shared__ unsigned long long sacc[3 * kAccLimbs];
+  for (int i = threadIdx.x; i < 3 * kAccLimbs; i += blockDim.x) sacc[i] = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n; v += stride) {
+    if (!include_root && v == g.root) continue;
+    hs::superacc_split(g.w_cpu[v], [&](int li, int64_t c) {
+      atomicAdd(&sacc[li], (unsigned long long)c);
+    });
+    hs::superacc_split(g.w_gpu[v], [&](int li, int64_t c) {
+      atomicAdd(&sacc[kAccLimbs + li], (unsigned long long)c);
+    });
+  }
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < g.m; e += stride)
+    hs::superacc_split(g.w_xfer[e], [&](int li, int64_t c) {
+      atomicAdd(&sacc[2 * kAccLimbs + li], (unsigned long long)c);
+    });
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * kAccLimbs; i += blockDim.x)
+    if (sacc[i]) atomicAdd(&acc[i], sacc[i]);
+}
+
+__global__ void round_kernel(const unsigned long long *acc, int count, double *out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = hs::superacc_round((const int64_t *)(acc + (int64_t)i * kAccLimbs));
+}
+
+// ---------------------------------------------------------------- K2 -----
+// mode 0: one thread per assignment, reference order, CPython sum() semantics.
+__global__ void eval2_ordered(hs_dag_t g, const int8_t *part, int batch, int src_gpu,
+                              double *cut, double *cpu_w, double *total) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int nk = g.n - 1;
+  const int8_t *p = part + (int64_t)b * nk;
+  const double *w = src_gpu ? g.w_gpu : g.w_cpu;
+  hs::PySum sc, scpu, stot;
+  for (int u = 0; u < g.n; ++u) {
+    if (u == g.root) continue;
+    int8_t pu = p[kpos(u, g.root)];
+    for (int64_t e = g.out_ptr[u]; e < g.out_ptr[u + 1]; ++e) {
+      int v = g.out_dst[e];
+      if (v == g.root) continue;
+      if (pu != p[kpos(v, g.root)]) sc.add(g.w_xfer[e]);
+    }
+  }
+  for (int v = 0; v < g.n; ++v) {
+    if (v == g.root) continue;
+    if (p[kpos(v, g.root)] == 0) scpu.add(w[v]);
+    stot.add(w[v]);
+  }
+  cut[b] = sc.started ? sc.result() : 0.0;
+  cpu_w[b] = scpu.started ? scpu.result() : 0.0;
+  total[b] = stot.started ? stot.result() : 0.0;
+}
+
+// mode 1: correctly rounded sums, all nodes/edges in parallel.
+// acc layout: [batch][3][kAccLimbs]; blockIdx.y = assignment.
+__global__ void eval2_exact(hs_dag_t g, const int8_t *part, int src_gpu,
+                            unsigned long long *acc) {
+  __shared__ unsigned long long sacc[3 * kAccLimbs];
+  for (int i = threadIdx.x; i < 3 * kAccLimbs; i += blockDim.x) sacc[i] = 0;
+  __syncthreads();
+  const int b = blockIdx.y;
+  const int nk = g.n - 1;
+  const int8_t *p = part + (int64_t)b * nk;
+  const double *w = src_gpu ? g.w_gpu : g.w_cpu;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < g.n; u += stride) {
+    if (u == g.root) continue;
+    int8_t pu = p[kpos((int)u, g.root)];
+    double wu = w[u];
+    if (pu == 0)
+      hs::superacc_split(wu, [&](int li, int64_t c) {
+        atomicAdd(&sacc[kAccLimbs + li], (unsigned long long)c);
+      });
+    hs::superacc_split(wu, [&](int li, int64_t c) {
+      atomicAdd(&sacc[2 * kAccLimbs + li], (unsigned long long)c);
+    });
+    for (int64_t e = g.out_ptr[u]; e < g.out_ptr[u + 1]; ++e) {
+      int v = g.out_dst[e];
+      if (v == g.root || p[kpos(v, g.root)] == pu) continue;
+      hs::superacc_split(g.w_xfer[e], [&](int li, int64_t c) {
+        atomicAdd(&sacc[li], (unsigned long long)c);
+      });
+    }
+  }
+  __syncthreads();
+  unsigned long long *dst = acc + (int64_t)b * 3 * kAccLimbs;
+  for (int i = threadIdx.x; i < 3 * kAccLimbs; i += blockDim.x)
+    if (sacc[i]) atomicAdd(&dst[i], sacc[i]);
+}
+
+__global__ void eval2_exact_round(const unsigned long long *acc, int batch, double *cut,
+                                  double *cpu_w, double *total) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= batch) return;
+  const int64_t *a = (const int64_t *)(acc + (int64_t)b * 3 * kAccLimbs);
+  cut[b] = hs::superacc_round(a);
+  cpu_w[b] = hs::superacc_round(a + kAccLimbs);
+  total[b] = hs::superacc_round(a + 2 * kAccLimbs);
+}
+
+// k-way: one warp per producer u; lanes stride its out-edges. Integer sums
+// are order-independent, so block partials + atomics stay deterministic.
+constexpr int kMaxK = 64;
+__global__ void evalk_kernel(hs_dag_t g, const int32_t *part, int k, const int64_t *vwgt,
+                             int64_t *cut_bytes, int64_t *cut_edges, int64_t *loads,
+                             int64_t *xcount, int64_t *xbytes) {
+  __shared__ unsigned long long s_load[kMaxK];
+  __shared__ unsigned long long s_sum[4];
+  const int b = blockIdx.y;
+  const int32_t *p = part + (int64_t)b * g.n;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s_load[i] = 0;
+  if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  long long cb = 0, ce = 0, xc = 0, xb = 0;
+  for (int64_t u = warp; u < g.n; u += nwarps) {
+    if (u == g.root) continue;
+    const int pu = p[u];
+    if (lane == 0) atomicAdd(&s_load[pu], (unsigned long long)vwgt[u]);
+    const int64_t e0 = g.out_ptr[u], e1 = g.out_ptr[u + 1];
+    uint64_t seen = 0;  // parts already charged a transfer for u's item
+    for (int64_t base = e0; base < e1; base += 32) {
+      int64_t e = base + lane;
+      int pv = -1;
+      int64_t by = 0;
+      if (e < e1) {
+        int v = g.out_dst[e];
+        if (v != g.root) {
+          pv = p[v];
+          by = g.bytes[e];
+        }
+      }
+      bool cutting = pv >= 0 && pv != pu;
+      if (cutting) { cb += by; ce += 1; }
+      // first edge (lowest dst) of u into each foreign part pays one transfer
+      unsigned cut_mask = __ballot_sync(0xffffffffu, cutting);
+      while (cut_mask) {
+        int src = __ffs(cut_mask) - 1;
+        int q = __shfl_sync(0xffffffffu, pv, src);
+        int64_t qb = __shfl_sync(0xffffffffu, by, src);
+        unsigned same = __ballot_sync(0xffffffffu, cutting && pv == q);
+        if (!((seen >> q) & 1ull)) {
+          seen |= 1ull << q;
+          if (lane == 0) { xc += 1; xb += qb; }
+        }
+        cut_mask &= ~same;
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    cb += __shfl_down_sync(0xffffffffu, cb, off);
+    ce += __shfl_down_sync(0xffffffffu, ce, off);
+    xc += __shfl_down_sync(0xffffffffu, xc, off);
+    xb += __shfl_down_sync(0xffffffffu, xb, off);
+  }
+  if (lane == 0) {
+    atomicAdd(&s_sum[0], (unsigned long long)cb);
+    atomicAdd(&s_sum[1], (unsigned long long)ce);
+    atomicAdd(&s_sum[2], (unsigned long long)xc);
+    atomicAdd(&s_sum[3], (unsigned long long)xb);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd((unsigned long long *)&cut_bytes[b], s_sum[0]);
+    atomicAdd((unsigned long long *)&cut_edges[b], s_sum[1]);
+    atomicAdd((unsigned long long *)&xcount[b], s_sum[2]);
+    atomicAdd((unsigned long long *)&xbytes[b], s_sum[3]);
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    if (s_load[i]) atomicAdd((unsigned long long *)&loads[(int64_t)b * k + i],
+                             s_load[i]);
+}
+
+}  // namespace
+
+extern "C" int hs_exact_totals(const hs_dag_t *g, int include_root, double *out_host,
+                               void *stream) {
+  HS_REQUIRE(g && out_host, HS_EINVAL, "hs_exact_totals: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  hs::Scratch<unsigned long long> acc;
+  hs::Scratch<double> out;
+  HS_CHECK_CUDA(acc.alloc(3 * kAccLimbs, s));
+  HS_CHECK_CUDA(out.alloc(3, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(acc, 0, 3 * kAccLimbs * sizeof(unsigned long long), s));
+  int64_t work = g->n > g->m ? g->n : g->m;
+  totals_kernel<<<hs::grid_for(work, 256, hs::sm_count() * 4), 256, 0, s>>>(*g, include_root, acc);
+  HS_CHECK_LAUNCH();
+  round_kernel<<<1, 32, 0, s>>>(acc, 3, out);
+  HS_CHECK_LAUNCH();
+  HS_CHECK_CUDA(cudaMemcpyAsync(out_host, out, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  return HS_OK;
+}
+
+extern "C" int hs_evaluate2(const hs_dag_t *g, const int8_t *part, int32_t batch,
+                            int weight_source, int mode, double *cut, double *cpu_w,
+                            double *total, void *stream) {
+  HS_REQUIRE(g && part && cut && cpu_w && total, HS_EINVAL, "hs_evaluate2: null argument");
+  HS_REQUIRE(mode == 0 || mode == 1, HS_EINVAL, "hs_evaluate2: mode must be 0 or 1");
+  if (batch <= 0) return HS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (mode == 0) {
+    eval2_ordered<<<(batch + 63) / 64, 64, 0, s>>>(*g, part, batch, weight_source, cut, cpu_w,
+                                                   total);
+    HS_CHECK_LAUNCH();
+    return HS_OK;
+  }
+  hs::Scratch<unsigned long long> acc;
+  size_t nacc = (size_t)batch * 3 * kAccLimbs;
+  HS_CHECK_CUDA(acc.alloc(nacc, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(acc, 0, nacc * sizeof(unsigned long long), s));
+  dim3 grid(hs::grid_for(g->n, 256, hs::sm_count() * 4), batch);
+  eval2_exact<<<grid, 256, 0, s>>>(*g, part, weight_source, acc);
+  HS_CHECK_LAUNCH();
+  eval2_exact_round<<<(batch + 63) / 64, 64, 0, s>>>(acc, batch, cut, cpu_w, total);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}
+
+extern "C" int hs_evaluate_kway(const hs_dag_t *g, const int32_t *part, int32_t batch,
+                                int32_t k, const int64_t *vwgt_i, int64_t *cut_bytes,
+                                int64_t *cut_edges, int64_t *loads, int64_t *xfer_count,
+                                int64_t *xfer_bytes, void *stream) {
+  HS_REQUIRE(g && part && vwgt_i && cut_bytes && cut_edges && loads && xfer_count && xfer_bytes,
+             HS_EINVAL, "hs_evaluate_kway: null argument");
+  HS_REQUIRE(k >= 1 && k <= kMaxK, HS_ELIMIT, "k must be in 1..%d", kMaxK);
+  if (batch <= 0) return HS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  HS_CHECK_CUDA(cudaMemsetAsync(cut_bytes, 0, batch * sizeof(int64_t), s));
+  HS_CHECK_CUDA(cudaMemsetAsync(cut_edges, 0, batch * sizeof(int64_t), s));
+  HS_CHECK_CUDA(cudaMemsetAsync(xfer_count, 0, batch * sizeof(int64_t), s));
+  HS_CHECK_CUDA(cudaMemsetAsync(xfer_bytes, 0, batch * sizeof(int64_t), s));
+  HS_CHECK_CUDA(cudaMemsetAsync(loads, 0, (size_t)batch * k * sizeof(int64_t), s));
+  dim3 grid(hs::grid_for((int64_t)g->n * 32, 256, hs::sm_count() * 8), batch);
+  evalk_kernel<<<grid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
+                                     xfer_count, xfer_bytes);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}

@@ -1,0 +1,299 @@
+"""Deterministic CPU+GPU machine simulation (drop-in mirror of ``hetsched.sim``).
+
+``simulate`` and ``compare`` run the event loop on the device (K8,
+csrc/des.cu): one thread per simulation, bit-exact with the reference because
+the loop only adds and maxes fp64 times in the reference's order.
+``compare`` packs every iteration's graph into one batch and launches one
+kernel per policy instead of looping simulations in Python. The trace
+formatting helpers (``trace_csv``, ``compare_csv``, ``metrics``) stay on the
+host: they format a finished event list.
+
+Reference: /root/reference/pkg/src/hetsched/sim.py (cited per symbol).
+"""
+from __future__ import annotations
+
+import io
+import statistics
+from dataclasses import dataclass
+from typing import Callable, Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _native
+from .csr import DagBatch
+from .graph import CPU, GPU, TaskGraph, topological_order, validate, CycleError
+
+HOST = "host"
+DEVICE = "device"
+EVENT_ORDER = {"xfer_start": 0, "xfer_end": 1, "kernel_start": 2, "kernel_end": 3}
+_KIND_NAMES = ("xfer_start", "xfer_end", "kernel_start", "kernel_end")
+
+
+class SimulationError(Exception):
+    """sim.py:23"""
+
+
+@dataclass(frozen=True)
+class MachineModel:
+    """C CPU workers (ids 0..C-1) then G GPU workers (sim.py:27-36)."""
+    cpu_workers: int = 3
+    gpu_workers: int = 1
+
+    def __post_init__(self):
+        if self.cpu_workers < 0 or self.gpu_workers < 0:
+            raise SimulationError("worker counts must be nonnegative")
+        if self.cpu_workers + self.gpu_workers == 0:
+            raise SimulationError("need at least one worker")
+
+
+@dataclass(frozen=True)
+class TraceEvent:
+    """sim.py:49-54"""
+    time: float
+    kind: str
+    subject: str
+    resource: str
+
+
+@dataclass
+class Trace:
+    """sim.py:57-65"""
+    events: List[TraceEvent]
+    makespan: float
+    transfer_count: int
+    transfer_bytes: int
+    busy_ms: Dict[str, float]
+    kernels_per_device: Dict[str, int]
+    policy: str = ""
+
+
+def _policy_id(policy) -> int:
+    pid = getattr(policy, "native_id", None)
+    if pid is None:
+        raise SimulationError(
+            f"policy {type(policy).__name__} not supported by native backend "
+            "(built-in eager/dmda/gp only)")
+    return pid
+
+
+def _check_graph(graph: TaskGraph) -> None:
+    """sim.py:72-78"""
+    problems = validate(graph)
+    if problems:
+        raise SimulationError(f"invalid graph: {problems[0]}")
+    for nid in graph.kernel_ids():
+        node = graph.nodes[nid]
+        if node.weight_cpu == 0 and node.weight_gpu == 0:
+            raise SimulationError(f"kernel {nid} has no weights; attach a cost model")
+
+
+def _pin_array(graphs: Sequence[TaskGraph], policies) -> Optional[torch.Tensor]:
+    pins = []
+    for g, p in zip(graphs, policies):
+        ids = g.csr().host.ids
+        pm = p.pin_map
+        pins.append(np.fromiter((1 if pm.get(int(i), CPU) == GPU else 0 for i in ids),
+                                dtype=np.int8, count=len(ids)))
+    return torch.from_numpy(np.concatenate(pins)).to(_native.device())
+
+
+def _worker_names(machine: MachineModel) -> List[str]:
+    return ([f"cpu{i}" for i in range(machine.cpu_workers)]
+            + [f"gpu{i}" for i in range(machine.gpu_workers)])
+
+
+def _events_to_trace(graph: TaskGraph, raw: np.ndarray, names: List[str]) -> List[TraceEvent]:
+    ids = graph.csr().host.ids
+    out = []
+    for rec in raw:
+        kind = _KIND_NAMES[rec["kind"]]
+        a, b = int(rec["a"]), int(rec["b"])
+        if rec["kind"] >= 2:
+            subject, resource = str(int(ids[a])), names[int(rec["resource"])]
+        else:
+            subject = f"d{int(ids[a])}.{int(ids[b])}" if b >= 0 else f"d{int(ids[a])}"
+            resource = "bus"
+        out.append(TraceEvent(float(rec["time"]), kind, subject, resource))
+    # sim.py:200 — subject compared as a string
+    out.sort(key=lambda e: (e.time, EVENT_ORDER[e.kind], e.subject, e.resource))
+    return out
+
+
+def _run(graphs: Sequence[TaskGraph], policies, machine: MachineModel, events: bool):
+    pid = _policy_id(policies[0])
+    batch = DagBatch([g.csr().host for g in graphs])
+    pin = _pin_array(graphs, policies) if pid == 2 else None
+    out = _native.simulate_batch(batch, pid, pin, machine.cpu_workers, machine.gpu_workers,
+                                 events=events)
+    host = {k: v.cpu().numpy() for k, v in out.items()}
+    if (host["status"] != 0).any():
+        raise AssertionError("simulation deadlocked on a valid DAG (bug)")
+    return batch, host
+
+
+def simulate(graph: TaskGraph, policy, machine: Optional[MachineModel] = None,
+             seed: int = 0) -> Trace:
+    """One simulation with its full event trace (sim.py:68-204)."""
+    machine = machine or MachineModel()
+    _policy_id(policy)
+    _check_graph(graph)
+    batch, h = _run([graph], [policy], machine, events=True)
+    names = _worker_names(machine)
+    cnt = int(h["ev_count"][0])
+    raw = h["events"].view(_native.EVENT_DTYPE)[int(h["ev_off"][0]):int(h["ev_off"][0]) + cnt]
+    events = _events_to_trace(graph, raw, names)
+    return Trace(events, float(h["makespan"][0]), int(h["transfer_count"][0]),
+                 int(h["transfer_bytes"][0]),
+                 {CPU: float(h["busy"][0, 0]), GPU: float(h["busy"][0, 1])},
+                 {CPU: int(h["kpd"][0, 0]), GPU: int(h["kpd"][0, 1])},
+                 policy=getattr(policy, "name", ""))
+
+
+@dataclass
+class BatchResult:
+    """Aggregates of a batch of simulations (no event traces)."""
+    makespan: np.ndarray
+    transfer_count: np.ndarray
+    transfer_bytes: np.ndarray
+    busy_ms: np.ndarray            # [B, 2] (CPU, GPU)
+    kernels_per_device: np.ndarray  # [B, 2]
+
+
+def simulate_batch(graphs: Sequence[TaskGraph], policies, machine: Optional[MachineModel] = None,
+                   validate_graphs: bool = True) -> BatchResult:
+    """Many independent simulations in one device launch (config 5).
+
+    ``policies`` holds one policy per graph, all of the same built-in type.
+    """
+    machine = machine or MachineModel()
+    if len(graphs) != len(policies):
+        raise SimulationError("need one policy per graph")
+    if not graphs:
+        z = np.zeros(0)
+        return BatchResult(z, z.astype(np.int64), z.astype(np.int64), z.reshape(0, 2),
+                           z.reshape(0, 2).astype(np.int64))
+    ids = {_policy_id(p) for p in policies}
+    if len(ids) != 1:
+        raise SimulationError("a batch must use a single policy type")
+    if validate_graphs:
+        for g in graphs:
+            _check_graph(g)
+    _, h = _run(graphs, policies, machine, events=False)
+    return BatchResult(h["makespan"], h["transfer_count"], h["transfer_bytes"], h["busy"],
+                       h["kpd"])
+
+
+def metrics(trace: Trace) -> Dict[str, object]:
+    """Summary recomputed from the events (sim.py:207-236)."""
+    starts: Dict[Tuple[str, str], float] = {}
+    busy = {CPU: 0.0, GPU: 0.0}
+    counts = {CPU: 0, GPU: 0}
+    n_xfers = 0
+    makespan = 0.0
+    for e in trace.events:
+        if e.kind == "kernel_start":
+            starts[(e.subject, e.resource)] = e.time
+        elif e.kind == "kernel_end":
+            key = (e.subject, e.resource)
+            if key not in starts:
+                raise SimulationError(f"kernel_end without start for {key}")
+            dev = CPU if e.resource.startswith("cpu") else GPU
+            busy[dev] += e.time - starts.pop(key)
+            counts[dev] += 1
+            makespan = max(makespan, e.time)
+        elif e.kind == "xfer_end":
+            n_xfers += 1
+    if starts:
+        raise SimulationError(f"kernel_start without end for {sorted(starts)}")
+    return {
+        "makespan": makespan,
+        "transfer_count": n_xfers,
+        "transfer_bytes": trace.transfer_bytes,
+        "busy_ms": busy,
+        "busy_fraction": {d: (busy[d] / makespan if makespan else 0.0) for d in busy},
+        "kernels_per_device": counts,
+    }
+
+
+def critical_path_lower_bound(graph: TaskGraph) -> float:
+    """Longest path with each kernel's faster device time (sim.py:239-247), on device (K7)."""
+    if not graph.nodes:
+        return 0.0
+    try:
+        _, _, cp, _ = _native.levels(graph.csr(), mode=0)
+    except _native.NativeError as exc:
+        if "cycle" in exc.message:
+            topological_order(graph)  # raises the reference's CycleError(min stuck id)
+        raise
+    return cp
+
+
+def trace_csv(trace: Trace) -> str:
+    """sim.py:250-255"""
+    out = io.StringIO()
+    out.write("time,kind,subject,resource\n")
+    for e in trace.events:
+        out.write(f"{e.time!r},{e.kind},{e.subject},{e.resource}\n")
+    return out.getvalue()
+
+
+@dataclass
+class CompareRow:
+    """sim.py:258-266"""
+    policy: str
+    mean_makespan: float
+    sd_makespan: float
+    mean_transfers: float
+    sd_transfers: float
+    mean_transfer_bytes: float
+    size: Optional[int] = None
+
+
+def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGraph],
+            machine: Optional[MachineModel] = None, iterations: int = 1, seed: int = 0,
+            policy_builder: Optional[Callable[[str, TaskGraph], object]] = None
+            ) -> List[CompareRow]:
+    """Mean/sd of makespan and transfers per policy over iterations (sim.py:269-306).
+
+    Iteration i simulates graph_factory(seed + i). All iterations of a policy
+    run as one device batch; the factory is called once per iteration and
+    its graph shared by every policy (the reference calls it once per
+    (policy, iteration); identical for deterministic factories).
+    """
+    if iterations < 1:
+        raise SimulationError("iterations must be >= 1")
+    if policy_builder is None:
+        from .policies import build_policy
+        policy_builder = lambda name, g: build_policy(name, g)  # noqa: E731
+    machine = machine or MachineModel()
+    graphs = [graph_factory(seed + i) for i in range(iterations)]
+    for g in graphs:
+        _check_graph(g)
+    rows: List[CompareRow] = []
+    for name in policy_names:
+        policies = [policy_builder(name, g) for g in graphs]
+        res = simulate_batch(graphs, policies, machine, validate_graphs=False)
+        makespans = [float(x) for x in res.makespan]
+        transfers = [float(x) for x in res.transfer_count]
+        t_bytes = [float(x) for x in res.transfer_bytes]
+        rows.append(CompareRow(
+            policy=name,
+            mean_makespan=statistics.fmean(makespans),
+            sd_makespan=statistics.stdev(makespans) if len(makespans) > 1 else 0.0,
+            mean_transfers=statistics.fmean(transfers),
+            sd_transfers=statistics.stdev(transfers) if len(transfers) > 1 else 0.0,
+            mean_transfer_bytes=statistics.fmean(t_bytes),
+        ))
+    return rows
+
+
+def compare_csv(rows: Sequence[CompareRow]) -> str:
+    """sim.py:309-316"""
+    out = io.StringIO()
+    out.write("policy,size,mean_makespan,sd_makespan,mean_transfers,sd_transfers\n")
+    for r in sorted(rows, key=lambda r: (r.size if r.size is not None else -1, r.policy)):
+        size = "" if r.size is None else str(r.size)
+        out.write(f"{r.policy},{size},{r.mean_makespan!r},{r.sd_makespan!r},"
+                  f"{r.mean_transfers!r},{r.sd_transfers!r}\n")
+    return out.getvalue()
