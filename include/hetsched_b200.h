@@ -94,9 +94,10 @@ typedef struct hs_ugraph {
     const int64_t *xadj;     /* [n+1] */
     const int32_t *adjncy;   /* [nnz] */
     const double *adjwgt;    /* [nnz] fp64 edge weights (exact 2-way path) */
-    const int64_t *adjwgt_i; /* [nnz] integer edge weights (k-way path) */
+    const int32_t *adjwgt_i; /* [nnz] integer edge weights (k-way path) */
     const double *vwgt;      /* [n]  fp64 vertex weights (exact 2-way path) */
-    const int64_t *vwgt_i;   /* [n]  integer vertex weights (k-way path) */
+    const int32_t *vwgt_i;   /* [n]  integer vertex weights (k-way path);
+                                total must be < 2^31 */
 } hs_ugraph_t;
 
 /* ---- status / library ------------------------------------------------ */
@@ -210,8 +211,11 @@ int hs_brute2(int32_t n, const double *weights, double r_cpu, double tol,
  * graph, projection and boundary refinement per level. Balance: for every
  * part p, |w_p/total - tpwgts[p]| <= tol (SURVEY App. B k-way
  * generalisation of partition.py:72). tpwgts_host: [k] host fractions.
- * part: [n] int32 output. stats_host (optional, 8 entries): cut, levels,
- * coarsest n, max |w_p/total - t_p| * 1e9, feasible, passes, -, -. */
+ * part: [n] int32 output. stats_host (optional, 8 entries): cut (integer,
+ * each undirected edge once), levels, coarsest n, max |w_p/total - t_p| *
+ * 1e9, feasible, refinement passes, internal weight divisor, 0.
+ * If the total edge weight reaches 2^30 the partitioner works on weights
+ * divided by a common factor (min 1); the reported cut uses the originals. */
 int hs_partition_kway(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host,
                       double tol, uint64_t seed, int32_t *part, int64_t *stats_host,
                       void *stream);
@@ -221,8 +225,8 @@ int hs_partition_kway(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host
  * position) adjacent to every predecessor and successor, adjwgt_i from
  * edge_w_i (out order), vwgt_i copied from node_w_i (node index space).
  * xadj/adjncy/adjwgt_i/vwgt_i are caller buffers sized (n-1)+1 / 2m. */
-int hs_symmetrize(const hs_dag_t *g, const int64_t *edge_w_i, const int64_t *node_w_i,
-                  int64_t *xadj, int32_t *adjncy, int64_t *adjwgt_i, int64_t *vwgt_i,
+int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *node_w_i,
+                  int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i,
                   int64_t *nnz_host, void *stream);
 
 /* Device generator of the layered fan-in DAG family of configs 2 and 4:

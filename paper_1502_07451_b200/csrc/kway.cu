@@ -1,0 +1,1399 @@
+// K1/K3/K4/K5/K6 — multilevel k-way partitioning of the weighted task DAG.
+//
+// The paper hands its DAG to METIS; the reference ships
+// a 2-way FM heuristic instead (partition.py:137-295) and lists k > 2 as a
+// non-goal. This file is the B200-native METIS role for graphs far beyond
+// FM's O(n^2) reach:
+//   K1 symmetrize  DAG (in+out CSR) -> undirected kernel graph (root dropped,
+//                  the graph emit_metis exports, graphio.py:285-304)
+//   K3 matching    heavy-edge matching by locally-dominant edges: every
+//                  unmatched vertex points at its best unmatched neighbour
+//                  (weight, then a symmetric per-round hash, then id); mutual
+//                  pointers match. A few rounds per level.
+//   K4 contraction coarse ids by a scan over pair leaders; coarse adjacency
+//                  = union of the pair's lists mapped through cmap, self
+//                  loops dropped, parallel edges merged in a per-vertex
+//                  shared-memory hash table (warp, CTA or global-memory
+//                  table by list length), written into padded slots so one
+//                  pass suffices.
+//   K5 initial     many randomized BFS-order streaming (LDG) k-way starts on
+//                  the coarsest graph, one warp each, plus greedy refinement;
+//                  best (feasible, cut) wins.
+//   K6 refinement  per level on the way up: parallel label-propagation
+//                  moves with a Jet-style afterburner (a move survives only
+//                  if it still gains assuming every higher-priority
+//                  neighbouring move happened), then deterministic
+//                  hash-thinned rebalancing if a part leaves its bound.
+// Every reduction is integer and every tie breaks on ids/hashes, so the
+// result is a pure function of (graph, k, targets, tol, seed) even though
+// adjacency order inside coarse lists is not fixed.
+//
+// Balance (SURVEY App. B k-way generalisation of partition.py:72):
+// |w_p / total - t_p| <= tol for every part p.
+#include "common.cuh"
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <vector>
+#include <algorithm>
+
+int hs_widen32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
+
+namespace {
+
+constexpr int kMaxParts = 64;
+
+struct G {
+  int32_t n;
+  int64_t cap;  // adjacency slots (padded)
+  int64_t *xbeg;
+  int32_t *deg;
+  int32_t *adj;
+  int32_t *wgt;
+  int32_t *vw;
+};
+
+__device__ __forceinline__ uint32_t mix32(uint64_t x) {
+  x ^= x >> 33;
+  x *= 0xff51afd7ed558ccdull;
+  x ^= x >> 33;
+  x *= 0xc4ceb9fe1a85ec53ull;
+  x ^= x >> 33;
+  return (uint32_t)x;
+}
+
+__device__ __forceinline__ uint32_t edge_hash(int a, int b, uint64_t salt) {
+  uint32_t lo = (uint32_t)min(a, b), hi = (uint32_t)max(a, b);
+  return mix32(salt ^ ((uint64_t)lo << 32 | hi));
+}
+
+__device__ __forceinline__ int warp_id_global() {
+  return (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+}
+__device__ __forceinline__ int warps_total() { return (int)(((int64_t)gridDim.x * blockDim.x) >> 5); }
+
+// ------------------------------------------------------------------ K1 ---
+__global__ void sym_degree(hs_dag_t g, int32_t *deg) {
+  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
+    if (v == g.root) continue;
+    const int lane = threadIdx.x & 31;
+    int cnt = 0;
+    for (int64_t j = g.in_ptr[v] + lane; j < g.in_ptr[v + 1]; j += 32) cnt += g.in_src[j] != g.root;
+    for (int off = 16; off; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
+    if (lane == 0) {
+      int kv = v < g.root ? v : v - 1;
+      deg[kv] = cnt + (int)(g.out_ptr[v + 1] - g.out_ptr[v]);
+    }
+  }
+}
+
+__global__ void sym_fill(hs_dag_t g, const int32_t *ew, const int32_t *nw, const int64_t *xadj,
+                         int32_t *adj, int32_t *wgt, int32_t *vw) {
+  const int lane = threadIdx.x & 31;
+  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
+    if (v == g.root) continue;
+    const int kv = v < g.root ? v : v - 1;
+    int64_t pos = xadj[kv];
+    if (lane == 0) vw[kv] = nw[v];
+    for (int64_t b = g.in_ptr[v]; b < g.in_ptr[v + 1]; b += 32) {
+      int64_t j = b + lane;
+      int u = -1;
+      if (j < g.in_ptr[v + 1]) u = g.in_src[j];
+      bool keep = u >= 0 && u != g.root;
+      unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (keep) {
+        int64_t at = pos + __popc(m & ((1u << lane) - 1));
+        adj[at] = u < g.root ? u : u - 1;
+        wgt[at] = ew[g.in_eid[j]];
+      }
+      pos += __popc(m);
+    }
+    const int64_t o0 = g.out_ptr[v], o1 = g.out_ptr[v + 1];
+    for (int64_t j = o0 + lane; j < o1; j += 32) {
+      int u = g.out_dst[j];
+      adj[pos + (j - o0)] = u < g.root ? u : u - 1;
+      wgt[pos + (j - o0)] = ew[j];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ K3 ---
+__global__ void deg_from_xadj(const int64_t *xadj, int n, int32_t *deg) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    deg[i] = (int32_t)(xadj[i + 1] - xadj[i]);
+}
+
+// Edge rating w^2 / (c(u) c(v)) ("expansion*2"): prefers heavy edges between
+// light vertices, which keeps coarse vertex weights even.
+__device__ __forceinline__ float rating(int w, int32_t a, int32_t b) {
+  return (float)w * (float)w / ((float)a * (float)b);
+}
+
+// prop[u]: best unmatched neighbour (or -1); fav[u]: best neighbour overall.
+__global__ void match_propose(G g, const int32_t *match, int32_t *prop, int32_t *fav,
+                              uint64_t salt, int32_t max_vw) {
+  const int lane = threadIdx.x & 31;
+  for (int u = warp_id_global(); u < g.n; u += warps_total()) {
+    if (match[u] >= 0) {
+      if (lane == 0) { prop[u] = -1; if (fav) fav[u] = -1; }
+      continue;
+    }
+    const int64_t b = g.xbeg[u];
+    const int d = g.deg[u];
+    const int32_t vu = g.vw[u];
+    float br = -1.f, fr = -1.f;
+    int bv = -1, fv = -1;
+    uint32_t bh = 0, fh = 0;
+    for (int j = lane; j < d; j += 32) {
+      int v = g.adj[b + j];
+      if (v == u) continue;
+      int32_t vv = g.vw[v];
+      if (vu + vv > max_vw) continue;
+      float r = rating(g.wgt[b + j], vu, vv);
+      uint32_t h = edge_hash(u, v, salt);
+      if (r > fr || (r == fr && (h > fh || (h == fh && v < fv)))) { fr = r; fh = h; fv = v; }
+      if (match[v] >= 0) continue;
+      if (r > br || (r == br && (h > bh || (h == bh && v < bv)))) { br = r; bh = h; bv = v; }
+    }
+    for (int off = 16; off; off >>= 1) {
+      float orr = __shfl_down_sync(0xffffffffu, br, off);
+      uint32_t oh = __shfl_down_sync(0xffffffffu, bh, off);
+      int ov = __shfl_down_sync(0xffffffffu, bv, off);
+      if (ov >= 0 && (bv < 0 || orr > br || (orr == br && (oh > bh || (oh == bh && ov < bv))))) {
+        br = orr; bh = oh; bv = ov;
+      }
+      orr = __shfl_down_sync(0xffffffffu, fr, off);
+      oh = __shfl_down_sync(0xffffffffu, fh, off);
+      ov = __shfl_down_sync(0xffffffffu, fv, off);
+      if (ov >= 0 && (fv < 0 || orr > fr || (orr == fr && (oh > fh || (oh == fh && ov < fv))))) {
+        fr = orr; fh = oh; fv = ov;
+      }
+    }
+    if (lane == 0) { prop[u] = bv; if (fav) fav[u] = fv; }
+  }
+}
+
+// Two-hop ("leaf") matching: unmatched vertices that share a favourite
+// neighbour are paired in (favourite, id) order.
+__global__ void twohop_keys(int n, const int32_t *match, const int32_t *fav, uint64_t *keys,
+                           int32_t *count) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x)
+    if (match[u] < 0 && fav[u] >= 0)
+      keys[atomicAdd(count, 1)] = ((uint64_t)(uint32_t)fav[u] << 32) | (uint64_t)u;
+}
+
+__global__ void twohop_heads(const uint64_t *keys, int cnt, int32_t *head) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x)
+    head[i] = (i == 0 || (keys[i - 1] >> 32) != (keys[i] >> 32)) ? (int32_t)i : 0;
+}
+
+// start[i] = first index of i's run (inclusive max-scan of head indices)
+__global__ void twohop_pair(const uint64_t *keys, const int32_t *start, int cnt, const int32_t *vw,
+                            int32_t max_vw, int32_t *match) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (((i - start[i]) & 1) || i + 1 >= cnt || (keys[i + 1] >> 32) != (keys[i] >> 32)) continue;
+    int a = (int)(uint32_t)keys[i], b = (int)(uint32_t)keys[i + 1];
+    if (vw[a] + vw[b] > max_vw) continue;
+    match[a] = b;
+    match[b] = a;
+  }
+}
+
+__global__ void match_accept(int n, int32_t *match, const int32_t *prop, int32_t *nmatched) {
+  int local = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    int v = prop[u];
+    if (match[u] < 0 && v >= 0 && prop[v] == (int)u) { match[u] = v; ++local; }
+  }
+  for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(nmatched, local);
+}
+
+// ------------------------------------------------------------------ K4 ---
+__global__ void leader_flags(int n, const int32_t *match, int32_t *flag) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    int m = match[u];
+    flag[u] = (m < 0 || m >= (int)u) ? 1 : 0;
+  }
+}
+
+__global__ void build_cmap(G g, const int32_t *match, const int32_t *cid, int32_t *cmap,
+                           int32_t *mem0, int32_t *mem1, int32_t *vw_c, int64_t *ub) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < g.n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    int m = match[u];
+    int partner = (m < 0) ? (int)u : m;
+    int lead = min((int)u, partner);
+    int c = cid[lead];
+    cmap[u] = c;
+    if (lead == (int)u) {
+      mem0[c] = (int)u;
+      mem1[c] = partner != (int)u ? partner : -1;
+      vw_c[c] = g.vw[u] + (partner != (int)u ? g.vw[partner] : 0);
+      ub[c] = (int64_t)g.deg[u] + (partner != (int)u ? g.deg[partner] : 0);
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t slot_hash(int key, uint32_t mask) {
+  return ((uint32_t)key * 0x9E3779B1u) & mask;
+}
+
+// warp per coarse vertex, table of pow2 >= 2*ub slots in shared memory
+constexpr int kWarpSlots = 1024;  // per warp
+constexpr int kContractWarps = 4;
+
+__global__ void __launch_bounds__(kContractWarps * 32)
+contract_warp(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1,
+              const int64_t *ub, int nc, G c) {
+  __shared__ int32_t keys[kContractWarps][kWarpSlots];
+  __shared__ int32_t vals[kContractWarps][kWarpSlots];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  int32_t *K = keys[wl], *V = vals[wl];
+  for (int cv = warp_id_global(); cv < nc; cv += warps_total()) {
+    const int64_t u_b = ub[cv];
+    if (u_b * 2 > kWarpSlots) continue;  // handled by the CTA / global paths
+    uint32_t size = 32;
+    while (size < 2 * u_b) size <<= 1;
+    const uint32_t mask = size - 1;
+    for (uint32_t s = lane; s < size; s += 32) { K[s] = -1; V[s] = 0; }
+    __syncwarp();
+    for (int t = 0; t < 2; ++t) {
+      int x = t == 0 ? mem0[cv] : mem1[cv];
+      if (x < 0) continue;
+      const int64_t b = g.xbeg[x];
+      const int d = g.deg[x];
+      for (int j = lane; j < d; j += 32) {
+        int key = cmap[g.adj[b + j]];
+        if (key == cv) continue;
+        int w = g.wgt[b + j];
+        uint32_t s = slot_hash(key, mask);
+        while (true) {
+          int prev = atomicCAS(&K[s], -1, key);
+          if (prev == -1 || prev == key) { atomicAdd(&V[s], w); break; }
+          s = (s + 1) & mask;
+        }
+      }
+    }
+    __syncwarp();
+    const int64_t base = c.xbeg[cv];
+    int cnt = 0;
+    for (uint32_t s0 = 0; s0 < size; s0 += 32) {
+      uint32_t s = s0 + lane;
+      int key = s < size ? K[s] : -1;
+      unsigned m = __ballot_sync(0xffffffffu, key >= 0);
+      if (key >= 0) {
+        int64_t at = base + cnt + __popc(m & ((1u << lane) - 1));
+        c.adj[at] = key;
+        c.wgt[at] = V[s];
+      }
+      cnt += __popc(m);
+    }
+    if (lane == 0) c.deg[cv] = cnt;
+    __syncwarp();
+  }
+}
+
+// CTA per (long) coarse vertex; table in dynamic shared memory or, when
+// `gtab` is set, in global scratch at 2*xbeg (2*ub slots available there).
+__global__ void contract_block(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1,
+                               const int64_t *ub, const int32_t *list, int nlist, G c,
+                               int32_t *gkeys, int32_t *gvals, int smem_slots) {
+  extern __shared__ int32_t sm[];
+  __shared__ int s_cnt;
+  for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
+    const int cv = list[li];
+    const int64_t u_b = ub[cv];
+    int32_t *K, *V;
+    uint64_t size;
+    if (gkeys) {
+      size = (uint64_t)(2 * u_b);
+      K = gkeys + 2 * c.xbeg[cv];
+      V = gvals + 2 * c.xbeg[cv];
+    } else {
+      size = 32;
+      while (size < (uint64_t)(2 * u_b)) size <<= 1;
+      K = sm;
+      V = sm + smem_slots;
+    }
+    const bool pow2 = (size & (size - 1)) == 0;
+    for (uint64_t s = threadIdx.x; s < size; s += blockDim.x) { K[s] = -1; V[s] = 0; }
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (int t = 0; t < 2; ++t) {
+      int x = t == 0 ? mem0[cv] : mem1[cv];
+      if (x < 0) continue;
+      const int64_t b = g.xbeg[x];
+      const int d = g.deg[x];
+      for (int j = threadIdx.x; j < d; j += blockDim.x) {
+        int key = cmap[g.adj[b + j]];
+        if (key == cv) continue;
+        int w = g.wgt[b + j];
+        uint64_t s = pow2 ? (uint64_t)slot_hash(key, (uint32_t)(size - 1))
+                          : ((uint64_t)((uint32_t)key * 0x9E3779B1u)) % size;
+        while (true) {
+          int prev = atomicCAS(&K[s], -1, key);
+          if (prev == -1 || prev == key) { atomicAdd(&V[s], w); break; }
+          s = s + 1 == size ? 0 : s + 1;
+        }
+      }
+    }
+    __syncthreads();
+    const int64_t base = c.xbeg[cv];
+    for (uint64_t s = threadIdx.x; s < size; s += blockDim.x) {
+      int key = K[s];
+      if (key >= 0) {
+        int at = atomicAdd(&s_cnt, 1);
+        c.adj[base + at] = key;
+        c.wgt[base + at] = V[s];
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) c.deg[cv] = s_cnt;
+    __syncthreads();
+  }
+}
+
+__global__ void classify_long(const int64_t *ub, int nc, int64_t lo, int64_t hi, int32_t *list,
+                              int32_t *count) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (ub[i] * 2 > lo && ub[i] * 2 <= hi) list[atomicAdd(count, 1)] = (int)i;
+}
+
+// ------------------------------------------------------------------ K5 ---
+// One warp per trial on the coarsest graph: BFS order from a hashed start,
+// streaming LDG assignment, then greedy single-vertex refinement passes.
+struct InitArgs {
+  G g;
+  int k;
+  const int64_t *hi;  // [k] max part weight
+  const int64_t *lo;  // [k] min part weight
+  uint64_t seed;
+  int trials;
+  int8_t *parts;      // [trials][n]
+  int32_t *order;     // [trials][n] scratch
+  int8_t *seen;       // [trials][n] scratch
+  int64_t *cut;       // [trials]
+  int32_t *infeas;    // [trials]
+};
+
+constexpr int kInitWarps = 4;
+
+__global__ void __launch_bounds__(kInitWarps * 32) initial_kernel(InitArgs A) {
+  __shared__ int32_t conn_s[kInitWarps][kMaxParts];
+  __shared__ int64_t pw_s[kInitWarps][kMaxParts];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int trial = blockIdx.x * kInitWarps + wl;
+  if (trial >= A.trials) return;
+  const G &g = A.g;
+  const int n = g.n, k = A.k;
+  int8_t *part = A.parts + (int64_t)trial * n;
+  int32_t *ord = A.order + (int64_t)trial * n;
+  int8_t *seen = A.seen + (int64_t)trial * n;
+  int32_t *conn = conn_s[wl];
+  int64_t *pw = pw_s[wl];
+  for (int i = lane; i < n; i += 32) { seen[i] = 0; part[i] = -1; }
+  for (int p = lane; p < k; p += 32) pw[p] = 0;
+  __syncwarp();
+  // BFS order; restarts at hashed unvisited vertices (scan from a hashed offset)
+  int head = 0, tail = 0;
+  int scan_pos = (int)(mix32(A.seed * 7919 + trial) % (uint32_t)n);
+  int scanned = 0;
+  while (tail < n) {
+    if (head == tail) {  // new component root
+      while (seen[scan_pos]) { scan_pos = scan_pos + 1 == n ? 0 : scan_pos + 1; ++scanned; }
+      if (lane == 0) { seen[scan_pos] = 1; ord[tail] = scan_pos; }
+      __syncwarp();
+      ++tail;
+    }
+    int v = ord[head++];
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    for (int j0 = 0; j0 < d; j0 += 32) {
+      int j = j0 + lane;
+      int u = j < d ? g.adj[b + j] : -1;
+      bool fresh = u >= 0 && !seen[u];
+      // de-duplicate within the batch: only the first lane holding u claims it
+      unsigned same = __match_any_sync(0xffffffffu, u);
+      bool first = fresh && (__ffs(same) - 1 == lane);
+      unsigned m = __ballot_sync(0xffffffffu, first);
+      if (first) {
+        seen[u] = 1;
+        ord[tail + __popc(m & ((1u << lane) - 1))] = u;
+      }
+      tail += __popc(m);
+      __syncwarp();
+    }
+  }
+  // streaming LDG assignment in BFS order
+  for (int idx = 0; idx < n; ++idx) {
+    const int v = ord[idx];
+    for (int p = lane; p < k; p += 32) conn[p] = 0;
+    __syncwarp();
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    for (int j = lane; j < d; j += 32) {
+      int p = part[g.adj[b + j]];
+      if (p >= 0) atomicAdd(&conn[p], g.wgt[b + j]);
+    }
+    __syncwarp();
+    // score = conn * (1 - pw/hi); lane p evaluates part p (k <= 64: two rounds)
+    double best = -1.0;
+    int bp = -1;
+    for (int p = lane; p < k; p += 32) {
+      int64_t after = pw[p] + g.vw[v];
+      if (after > A.hi[p]) continue;
+      double fill = (double)pw[p] / (double)A.hi[p];
+      double s = (double)conn[p] * (1.0 - fill) + (1.0 - fill) * 1e-9;
+      if (s > best || (s == best && p < bp)) { best = s; bp = p; }
+    }
+    for (int off = 16; off; off >>= 1) {
+      double ob = __shfl_down_sync(0xffffffffu, best, off);
+      int op = __shfl_down_sync(0xffffffffu, bp, off);
+      if (op >= 0 && (bp < 0 || ob > best || (ob == best && op < bp))) { best = ob; bp = op; }
+    }
+    bp = __shfl_sync(0xffffffffu, bp, 0);
+    if (bp < 0) {  // nothing fits: least relatively loaded part
+      double lf = 1e300;
+      for (int p = 0; p < k; ++p) {
+        double f = (double)pw[p] / (double)A.hi[p];
+        if (f < lf) { lf = f; bp = p; }
+      }
+    }
+    if (lane == 0) { part[v] = (int8_t)bp; pw[bp] += g.vw[v]; }
+    __syncwarp();
+  }
+  // greedy refinement passes (sequential per vertex, warp-parallel adjacency)
+  for (int pass = 0; pass < 4; ++pass) {
+    int moved = 0;
+    for (int idx = 0; idx < n; ++idx) {
+      const int v = ord[idx];
+      for (int p = lane; p < k; p += 32) conn[p] = 0;
+      __syncwarp();
+      const int64_t b = g.xbeg[v];
+      const int d = g.deg[v];
+      for (int j = lane; j < d; j += 32) atomicAdd(&conn[part[g.adj[b + j]]], g.wgt[b + j]);
+      __syncwarp();
+      const int own = part[v];
+      const int32_t vwv = g.vw[v];
+      int bg = 0, bp = -1;
+      for (int p = lane; p < k; p += 32) {
+        if (p == own) continue;
+        if (pw[p] + vwv > A.hi[p] || pw[own] - vwv < A.lo[own]) continue;
+        int gain = conn[p] - conn[own];
+        if (gain > bg || (gain == bg && bp >= 0 && p < bp)) { bg = gain; bp = p; }
+      }
+      for (int off = 16; off; off >>= 1) {
+        int og = __shfl_down_sync(0xffffffffu, bg, off);
+        int op = __shfl_down_sync(0xffffffffu, bp, off);
+        if (op >= 0 && (bp < 0 || og > bg || (og == bg && op < bp))) { bg = og; bp = op; }
+      }
+      bp = __shfl_sync(0xffffffffu, bp, 0);
+      bg = __shfl_sync(0xffffffffu, bg, 0);
+      if (bp >= 0 && bg > 0) {
+        if (lane == 0) { part[v] = (int8_t)bp; pw[bp] += vwv; pw[own] -= vwv; }
+        ++moved;
+      }
+      __syncwarp();
+    }
+    if (!moved) break;
+  }
+  // cut (each undirected edge counted twice) and feasibility
+  int64_t cut2 = 0;
+  for (int v = 0; v < n; ++v) {
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    const int pv = part[v];
+    for (int j = lane; j < d; j += 32)
+      if (part[g.adj[b + j]] != pv) cut2 += g.wgt[b + j];
+  }
+  for (int off = 16; off; off >>= 1) cut2 += __shfl_down_sync(0xffffffffu, cut2, off);
+  if (lane == 0) {
+    int bad = 0;
+    for (int p = 0; p < k; ++p) bad += (pw[p] > A.hi[p] || pw[p] < A.lo[p]);
+    A.cut[trial] = cut2 / 2;
+    A.infeas[trial] = bad;
+  }
+}
+
+__global__ void pick_best(const int64_t *cut, const int32_t *infeas, int trials, int32_t *best) {
+  if (threadIdx.x || blockIdx.x) return;
+  int b = 0;
+  for (int t = 1; t < trials; ++t) {
+    bool better = (infeas[t] != 0) != (infeas[b] != 0) ? infeas[t] == 0 : cut[t] < cut[b];
+    if (better) b = t;
+  }
+  *best = b;
+}
+
+// ------------------------------------------------------------------ K6 ---
+__global__ void project(int n, const int32_t *cmap, const int32_t *cpart, int32_t *part) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    part[i] = cpart[cmap[i]];
+}
+
+__global__ void part_weights(int n, const int32_t *vw, const int32_t *part, int k, int64_t *pw) {
+  __shared__ unsigned long long s[kMaxParts];
+  for (int p = threadIdx.x; p < k; p += blockDim.x) s[p] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&s[part[i]], (unsigned long long)vw[i]);
+  __syncthreads();
+  for (int p = threadIdx.x; p < k; p += blockDim.x)
+    if (s[p]) atomicAdd((unsigned long long *)&pw[p], s[p]);
+}
+
+constexpr int kRefWarps = 8;
+
+// Candidate move per vertex: best strictly positive gain into a part that can
+// take it (ties -> smaller part id). Only boundary vertices move.
+__global__ void __launch_bounds__(kRefWarps * 32)
+refine_candidates(G g, const int32_t *part, int k, const int64_t *pw, const int64_t *hi,
+                  const int64_t *lo, int32_t *cand, int32_t *cgain) {
+  __shared__ int32_t conn_s[kRefWarps][kMaxParts];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  int32_t *conn = conn_s[wl];
+  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
+    for (int p = lane; p < k; p += 32) conn[p] = 0;
+    __syncwarp();
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    const int own = part[v];
+    bool boundary = false;
+    for (int j = lane; j < d; j += 32) {
+      int p = part[g.adj[b + j]];
+      boundary |= p != own;
+      atomicAdd(&conn[p], g.wgt[b + j]);
+    }
+    boundary = __any_sync(0xffffffffu, boundary);
+    __syncwarp();
+    int bg = 0, bp = -1;
+    if (boundary) {
+      const int32_t vwv = g.vw[v];
+      const bool can_leave = pw[own] - vwv >= lo[own];
+      for (int p = lane; p < k; p += 32) {
+        if (p == own || !can_leave || pw[p] + vwv > hi[p]) continue;
+        int gain = conn[p] - conn[own];
+        if (gain > bg || (gain == bg && bp >= 0 && p < bp)) { bg = gain; bp = p; }
+      }
+      for (int off = 16; off; off >>= 1) {
+        int og = __shfl_down_sync(0xffffffffu, bg, off);
+        int op = __shfl_down_sync(0xffffffffu, bp, off);
+        if (op >= 0 && (bp < 0 || og > bg || (og == bg && op < bp))) { bg = og; bp = op; }
+      }
+    }
+    if (lane == 0) {
+      cand[v] = (bp >= 0 && bg > 0) ? bp : -1;
+      cgain[v] = bg;
+    }
+    __syncwarp();
+  }
+}
+
+// Jet-style afterburner: re-evaluate each candidate assuming every
+// higher-priority (gain, then smaller id) neighbouring candidate moved.
+// Rejected candidates get cand = -1.
+__global__ void refine_afterburner(G g, const int32_t *part, const int32_t *cand_in,
+                                   const int32_t *cgain, int32_t *cand_out) {
+  const int lane = threadIdx.x & 31;
+  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
+    const int dest = cand_in[v];
+    if (dest < 0) {
+      if (lane == 0) cand_out[v] = -1;
+      continue;
+    }
+    const int own = part[v];
+    const int gv = cgain[v];
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    int delta = 0;
+    for (int j = lane; j < d; j += 32) {
+      int u = g.adj[b + j];
+      int pu = part[u];
+      int cu = cand_in[u];
+      if (cu >= 0) {
+        int gu = cgain[u];
+        if (gu > gv || (gu == gv && u < v)) pu = cu;
+      }
+      int w = g.wgt[b + j];
+      delta += (pu == dest ? w : 0) - (pu == own ? w : 0);
+    }
+    for (int off = 16; off; off >>= 1) delta += __shfl_down_sync(0xffffffffu, delta, off);
+    if (lane == 0) cand_out[v] = delta > 0 ? dest : -1;
+  }
+}
+
+// Rebalance candidates: every vertex of an over-full part proposes its best
+// (max gain, possibly negative) part still below its target.
+__global__ void __launch_bounds__(kRefWarps * 32)
+rebalance_candidates(G g, const int32_t *part, int k, const int64_t *pw, const int64_t *hi,
+                     const int64_t *target, int32_t *cand) {
+  __shared__ int32_t conn_s[kRefWarps][kMaxParts];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  int32_t *conn = conn_s[wl];
+  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
+    const int own = part[v];
+    if (pw[own] <= hi[own]) {
+      if (lane == 0) cand[v] = -1;
+      continue;
+    }
+    for (int p = lane; p < k; p += 32) conn[p] = 0;
+    __syncwarp();
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    for (int j = lane; j < d; j += 32) atomicAdd(&conn[part[g.adj[b + j]]], g.wgt[b + j]);
+    __syncwarp();
+    int bg = INT_MIN, bp = -1;
+    for (int p = lane; p < k; p += 32) {
+      if (p == own || pw[p] >= target[p]) continue;
+      int gain = conn[p] - conn[own];
+      if (bp < 0 || gain > bg || (gain == bg && p < bp)) { bg = gain; bp = p; }
+    }
+    for (int off = 16; off; off >>= 1) {
+      int og = __shfl_down_sync(0xffffffffu, bg, off);
+      int op = __shfl_down_sync(0xffffffffu, bp, off);
+      if (op >= 0 && (bp < 0 || og > bg || (og == bg && op < bp))) { bg = og; bp = op; }
+    }
+    if (lane == 0) cand[v] = bp;
+    __syncwarp();
+  }
+}
+
+// flows[p] = weight leaving p, flows[k + q] = weight entering q (planned moves)
+__global__ void move_flows(int n, const int32_t *vw, const int32_t *part, const int32_t *cand,
+                           int k, int64_t *flows, int32_t *nmoves) {
+  __shared__ unsigned long long s[2 * kMaxParts];
+  __shared__ int s_n;
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) s[p] = 0;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
+  int local = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int dest = cand[v];
+    if (dest >= 0) {
+      atomicAdd(&s[part[v]], (unsigned long long)vw[v]);
+      atomicAdd(&s[k + dest], (unsigned long long)vw[v]);
+      ++local;
+    }
+  }
+  if (local) atomicAdd(&s_n, local);
+  __syncthreads();
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x)
+    if (s[p]) atomicAdd((unsigned long long *)&flows[p], s[p]);
+  if (threadIdx.x == 0 && s_n) atomicAdd(nmoves, s_n);
+}
+
+// Applies planned moves, each kept with probability p_out[own] * p_in[dest]
+// decided by a hash of (salt, v) — deterministic thinning that keeps the
+// expected inflow of every part within its room.
+__global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, const double *prob,
+                              int k, uint64_t salt, int32_t *part, int64_t *pw) {
+  __shared__ long long s[kMaxParts];
+  for (int p = threadIdx.x; p < k; p += blockDim.x) s[p] = 0;
+  __syncthreads();
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int dest = cand[v];
+    if (dest < 0) continue;
+    int own = part[v];
+    double pr = prob[own] * prob[k + dest];
+    if (pr < 1.0 && (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
+      continue;
+    part[v] = dest;
+    atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
+    atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < k; p += blockDim.x)
+    if (s[p]) atomicAdd((unsigned long long *)&pw[p], (unsigned long long)s[p]);
+}
+
+__global__ void cut_kernel(G g, const int32_t *part, unsigned long long *cut2) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long local = 0;
+  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
+    const int pv = part[v];
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    for (int j = lane; j < d; j += 32)
+      if (part[g.adj[b + j]] != pv) local += (unsigned long long)g.wgt[b + j];
+  }
+  for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+  if (lane == 0 && local) atomicAdd(cut2, local);
+}
+
+__global__ void scale_weights(int64_t nnz, const int32_t *in, int32_t *out, int64_t div) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nnz;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t w = in[i] / div;
+    out[i] = (int32_t)(w < 1 ? 1 : w);
+  }
+}
+
+// Initial "range" trial: contiguous id ranges by cumulative weight. Coarse
+// ids follow the smallest fine id they contain, so on a task DAG (ids in
+// creation/topological order) this is a layer-band partition.
+__global__ void range_parts(int n, const int64_t *prefix, const int32_t *vw, const double *cum,
+                            int k, int64_t total, int32_t *part) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    double mid = ((double)prefix[v] + 0.5 * (double)vw[v]) / (double)total;
+    int p = 0;
+    while (p < k - 1 && mid >= cum[p + 1]) ++p;
+    part[v] = p;
+  }
+}
+
+__global__ void int8_to_int32(const int8_t *in, int n, int32_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+__global__ void seg_bounds(int n, const int64_t *xbeg, const int32_t *deg, int64_t *b, int64_t *e) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    b[i] = xbeg[i];
+    e[i] = xbeg[i] + deg[i];
+  }
+}
+
+// ------------------------------------------------------------ host side ---
+struct Level {
+  G g;
+  int32_t *cmap = nullptr;  // fine -> coarse of the NEXT level (set when coarsened)
+  bool own_adj = true, own_wgt = true, own_xbeg_vw = true;
+};
+
+template <typename T>
+cudaError_t dalloc(T **p, size_t count, cudaStream_t s) {
+  return cudaMallocAsync((void **)p, (count ? count : 1) * sizeof(T), s);
+}
+
+int warp_grid(int64_t items, int warps_per_block) {
+  int64_t g = (items + warps_per_block - 1) / warps_per_block;
+  int64_t maxg = (int64_t)hs::sm_count() * 64;
+  if (g > maxg) g = maxg;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <typename T>
+int exclusive_scan(const T *in, T *out, int64_t n, cudaStream_t s) {
+  size_t tb = 0;
+  HS_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, out, n, s));
+  hs::Scratch<char> tmp;
+  HS_CHECK_CUDA(tmp.alloc(tb, s));
+  HS_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, s));
+  hs::count_launch(1);
+  return HS_OK;
+}
+
+struct PhaseTimer {
+  bool on;
+  cudaStream_t s;
+  std::vector<std::pair<const char *, cudaEvent_t>> ev;
+  PhaseTimer(cudaStream_t st) : s(st) { on = getenv("HS_KWAY_TRACE") != nullptr; }
+  void mark(const char *name) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.emplace_back(name, e);
+  }
+  ~PhaseTimer() {
+    if (!on || ev.empty()) return;
+    cudaEventSynchronize(ev.back().second);
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1].second, ev[i].second);
+      fprintf(stderr, "[kway] %-28s %8.3f ms\n", ev[i].first, ms);
+    }
+    for (auto &x : ev) cudaEventDestroy(x.second);
+  }
+};
+
+// Host-side helper that owns the per-call device state.
+struct Kway {
+  cudaStream_t s;
+  int k;
+  double tol;
+  uint64_t seed, salt;
+  int64_t total_vw = 0;
+  std::vector<int64_t> hi, lo, target;
+  std::vector<double> cum;
+  int64_t *d_hi = nullptr, *d_lo = nullptr, *d_target = nullptr, *d_pw = nullptr,
+          *d_flows = nullptr;
+  double *d_prob = nullptr, *d_cum = nullptr;
+  int32_t *counter = nullptr;
+  std::vector<Level> levels;
+  PhaseTimer timer;
+  Kway(cudaStream_t st) : s(st), timer(st) {}
+
+  int read_pw(std::vector<int64_t> &pw) {
+    pw.resize(k);
+    HS_CHECK_CUDA(cudaMemcpyAsync(pw.data(), d_pw, k * 8, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    return HS_OK;
+  }
+
+  int weights(const G &g, const int32_t *part) {
+    HS_CHECK_CUDA(cudaMemsetAsync(d_pw, 0, k * sizeof(int64_t), s));
+    part_weights<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw, part, k, d_pw);
+    HS_CHECK_LAUNCH();
+    return HS_OK;
+  }
+
+  // plans in `cand` -> thinned application; returns moves planned
+  int apply_plan(const G &g, const int32_t *cand, int32_t *part, bool rebalance,
+                 uint64_t salt2, int32_t *nplanned) {
+    HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
+    HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), s));
+    move_flows<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw, part, cand, k,
+                                                                         d_flows, counter);
+    HS_CHECK_LAUNCH();
+    std::vector<int64_t> fl(2 * k), pw;
+    HS_CHECK_CUDA(cudaMemcpyAsync(fl.data(), d_flows, 2 * k * 8, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(nplanned, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    int rc = read_pw(pw);
+    if (rc) return rc;
+    if (*nplanned == 0) return HS_OK;
+    std::vector<double> prob(2 * k, 1.0);
+    for (int p = 0; p < k; ++p) {
+      const int64_t out = fl[p], in = fl[k + p];
+      if (rebalance) {
+        if (out > 0) prob[p] = std::min(1.0, (double)(pw[p] - target[p]) / (double)out);
+        if (in > 0) prob[k + p] = std::min(1.0, (double)(target[p] - pw[p]) / (double)in);
+      } else {
+        // keep the expected post-move weight inside [lo, hi]
+        const double room_in = (double)(hi[p] - pw[p]) + 0.0 * out;
+        if (in > 0 && (double)in > room_in) prob[k + p] = std::max(0.0, room_in / (double)in);
+        const double room_out = (double)(pw[p] - lo[p]);
+        if (out > 0 && (double)out > room_out) prob[p] = std::max(0.0, room_out / (double)out);
+      }
+      prob[p] = std::max(0.0, prob[p]);
+      prob[k + p] = std::max(0.0, prob[k + p]);
+    }
+    HS_CHECK_CUDA(cudaMemcpyAsync(d_prob, prob.data(), 2 * k * 8, cudaMemcpyHostToDevice, s));
+    apply_thinned<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
+        g.n, g.vw, cand, d_prob, k, salt2, part, d_pw);
+    HS_CHECK_LAUNCH();
+    return HS_OK;
+  }
+
+  int rebalance(const G &g, int32_t *part, int32_t *cand, uint64_t salt2) {
+    for (int rb = 0; rb < 24; ++rb) {
+      std::vector<int64_t> pw;
+      int rc = read_pw(pw);
+      if (rc) return rc;
+      bool over = false;
+      for (int p = 0; p < k; ++p) over |= pw[p] > hi[p];
+      if (!over) return HS_OK;
+      rebalance_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(
+          g, part, k, d_pw, d_hi, d_target, cand);
+      HS_CHECK_LAUNCH();
+      int32_t planned = 0;
+      rc = apply_plan(g, cand, part, true, salt2 + rb * 7919, &planned);
+      if (rc) return rc;
+      if (!planned) return HS_OK;
+    }
+    return HS_OK;
+  }
+
+  int refine(const G &g, int32_t *part, uint64_t salt2, int64_t *passes) {
+    int32_t *cand, *cgain, *cand2;
+    HS_CHECK_CUDA(dalloc(&cand, g.n, s));
+    HS_CHECK_CUDA(dalloc(&cgain, g.n, s));
+    HS_CHECK_CUDA(dalloc(&cand2, g.n, s));
+    int rc = weights(g, part);
+    if (rc) return rc;
+    rc = rebalance(g, part, cand, salt2 ^ 0xabcdefull);
+    if (rc) return rc;
+    for (int pass = 0; pass < 10; ++pass) {
+      refine_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(g, part, k, d_pw, d_hi,
+                                                                            d_lo, cand, cgain);
+      HS_CHECK_LAUNCH();
+      refine_afterburner<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, cand, cgain, cand2);
+      HS_CHECK_LAUNCH();
+      int32_t planned = 0;
+      rc = apply_plan(g, cand2, part, false, salt2 + pass * 104729, &planned);
+      if (rc) return rc;
+      ++*passes;
+      if ((int64_t)planned * 1000 <= g.n) break;  // < 0.1% of vertices want to move
+    }
+    rc = rebalance(g, part, cand, salt2 ^ 0x5555ull);
+    cudaFreeAsync(cand, s);
+    cudaFreeAsync(cgain, s);
+    cudaFreeAsync(cand2, s);
+    return rc;
+  }
+
+  int64_t cut_of(const G &g, const int32_t *part) {
+    unsigned long long *c2, h = 0;
+    if (dalloc(&c2, 1, s) != cudaSuccess) return -1;
+    cudaMemsetAsync(c2, 0, 8, s);
+    cut_kernel<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, c2);
+    hs::count_launch();
+    cudaMemcpyAsync(&h, c2, 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFreeAsync(c2, s);
+    return (int64_t)(h / 2);
+  }
+
+  bool feasible(const std::vector<int64_t> &pw) const {
+    for (int p = 0; p < k; ++p)
+      if (pw[p] > hi[p] || pw[p] < lo[p]) return false;
+    return true;
+  }
+
+  int coarsen_once(bool *stop) {
+    Level &F = levels.back();
+    const int n = F.g.n;
+    const int lvl = (int)levels.size();
+    const int32_t max_vw = (int32_t)std::max<int64_t>(1, total_vw / (4ll * k));
+    int32_t *match, *prop, *fav, *flag, *cid;
+    HS_CHECK_CUDA(dalloc(&match, n, s));
+    HS_CHECK_CUDA(dalloc(&prop, n, s));
+    HS_CHECK_CUDA(dalloc(&fav, n, s));
+    HS_CHECK_CUDA(dalloc(&flag, n + 1, s));
+    HS_CHECK_CUDA(dalloc(&cid, n + 1, s));
+    HS_CHECK_CUDA(cudaMemsetAsync(match, 0xff, n * sizeof(int32_t), s));
+    const int rounds = 3;
+    for (int round = 0; round < rounds; ++round) {
+      match_propose<<<warp_grid(n, 8), 256, 0, s>>>(F.g, match, prop,
+                                                      round == rounds - 1 ? fav : nullptr,
+                                                      salt + (uint64_t)lvl * 131 + round, max_vw);
+      HS_CHECK_LAUNCH();
+      match_accept<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, prop, counter);
+      HS_CHECK_LAUNCH();
+    }
+    {  // two-hop pairing of leftovers that share a favourite neighbour
+      uint64_t *keys, *keys2;
+      int32_t *head, *start;
+      HS_CHECK_CUDA(dalloc(&keys, n, s));
+      HS_CHECK_CUDA(dalloc(&keys2, n, s));
+      HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), s));
+      twohop_keys<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, fav, keys, counter);
+      HS_CHECK_LAUNCH();
+      int32_t cnt = 0;
+      HS_CHECK_CUDA(cudaMemcpyAsync(&cnt, counter, sizeof cnt, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      if (cnt > 1) {
+        size_t tb = 0;
+        HS_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, cnt, 0, 64, s));
+        {
+          hs::Scratch<char> tmp;
+          HS_CHECK_CUDA(tmp.alloc(tb, s));
+          HS_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, keys, keys2, cnt, 0, 64, s));
+        }
+        HS_CHECK_CUDA(dalloc(&head, cnt, s));
+        HS_CHECK_CUDA(dalloc(&start, cnt, s));
+        twohop_heads<<<hs::grid_for(cnt, 256), 256, 0, s>>>(keys2, cnt, head);
+        HS_CHECK_LAUNCH();
+        tb = 0;
+        HS_CHECK_CUDA(cub::DeviceScan::InclusiveScan(nullptr, tb, head, start, cub::Max(), cnt, s));
+        {
+          hs::Scratch<char> tmp;
+          HS_CHECK_CUDA(tmp.alloc(tb, s));
+          HS_CHECK_CUDA(cub::DeviceScan::InclusiveScan(tmp.p, tb, head, start, cub::Max(), cnt, s));
+        }
+        twohop_pair<<<hs::grid_for(cnt, 256), 256, 0, s>>>(keys2, start, cnt, F.g.vw, max_vw, match);
+        HS_CHECK_LAUNCH();
+        hs::count_launch(2);
+        cudaFreeAsync(head, s);
+        cudaFreeAsync(start, s);
+      }
+      cudaFreeAsync(keys, s);
+      cudaFreeAsync(keys2, s);
+    }
+    leader_flags<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, flag);
+    HS_CHECK_LAUNCH();
+    HS_CHECK_CUDA(cudaMemsetAsync(flag + n, 0, sizeof(int32_t), s));
+    int rc = exclusive_scan<int32_t>(flag, cid, n + 1, s);
+    if (rc) return rc;
+    int32_t nc = 0;
+    HS_CHECK_CUDA(cudaMemcpyAsync(&nc, cid + n, sizeof nc, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (nc > (int64_t)n * 92 / 100) {  // matching stalled: stop coarsening here
+      cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
+      cudaFreeAsync(flag, s); cudaFreeAsync(cid, s);
+      *stop = true;
+      return HS_OK;
+    }
+    Level C;
+    C.g.n = nc;
+    int32_t *mem0, *mem1;
+    int64_t *ub;
+    HS_CHECK_CUDA(dalloc(&F.cmap, n, s));
+    HS_CHECK_CUDA(dalloc(&mem0, nc, s));
+    HS_CHECK_CUDA(dalloc(&mem1, nc, s));
+    HS_CHECK_CUDA(dalloc(&ub, nc + 1, s));
+    HS_CHECK_CUDA(dalloc(&C.g.vw, nc, s));
+    HS_CHECK_CUDA(dalloc(&C.g.deg, nc, s));
+    HS_CHECK_CUDA(dalloc(&C.g.xbeg, nc + 1, s));
+    build_cmap<<<hs::grid_for(n, 256), 256, 0, s>>>(F.g, match, cid, F.cmap, mem0, mem1, C.g.vw, ub);
+    HS_CHECK_LAUNCH();
+    HS_CHECK_CUDA(cudaMemsetAsync(ub + nc, 0, sizeof(int64_t), s));
+    rc = exclusive_scan<int64_t>(ub, C.g.xbeg, nc + 1, s);
+    if (rc) return rc;
+    int64_t capc = 0;
+    HS_CHECK_CUDA(cudaMemcpyAsync(&capc, C.g.xbeg + nc, sizeof capc, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    C.g.cap = capc;
+    HS_CHECK_CUDA(dalloc(&C.g.adj, capc, s));
+    HS_CHECK_CUDA(dalloc(&C.g.wgt, capc, s));
+    contract_warp<<<warp_grid(nc, kContractWarps), kContractWarps * 32, 0, s>>>(
+        F.g, F.cmap, mem0, mem1, ub, nc, C.g);
+    HS_CHECK_LAUNCH();
+    const int smem_slots = 8192;
+    int32_t *list;
+    HS_CHECK_CUDA(dalloc(&list, nc, s));
+    int32_t cnt[2] = {0, 0};
+    HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, 2 * sizeof(int32_t), s));
+    classify_long<<<hs::grid_for(nc, 256), 256, 0, s>>>(ub, nc, kWarpSlots, smem_slots, list, counter);
+    HS_CHECK_LAUNCH();
+    HS_CHECK_CUDA(cudaMemcpyAsync(cnt, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (cnt[0]) {
+      size_t smem = 2 * smem_slots * sizeof(int32_t);
+      cudaFuncSetAttribute(contract_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      contract_block<<<std::min(cnt[0], hs::sm_count() * 2), 512, smem, s>>>(
+          F.g, F.cmap, mem0, mem1, ub, list, cnt[0], C.g, nullptr, nullptr, smem_slots);
+      HS_CHECK_LAUNCH();
+    }
+    HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), s));
+    classify_long<<<hs::grid_for(nc, 256), 256, 0, s>>>(ub, nc, smem_slots, INT64_MAX / 4, list,
+                                                        counter);
+    HS_CHECK_LAUNCH();
+    HS_CHECK_CUDA(cudaMemcpyAsync(cnt + 1, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (cnt[1]) {
+      int32_t *gk, *gv;
+      HS_CHECK_CUDA(dalloc(&gk, 2 * capc, s));
+      HS_CHECK_CUDA(dalloc(&gv, 2 * capc, s));
+      contract_block<<<std::min(cnt[1], hs::sm_count() * 2), 1024, 0, s>>>(
+          F.g, F.cmap, mem0, mem1, ub, list, cnt[1], C.g, gk, gv, 0);
+      HS_CHECK_LAUNCH();
+      cudaFreeAsync(gk, s);
+      cudaFreeAsync(gv, s);
+    }
+    cudaFreeAsync(list, s);
+    cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
+    cudaFreeAsync(flag, s); cudaFreeAsync(cid, s); cudaFreeAsync(mem0, s);
+    cudaFreeAsync(mem1, s); cudaFreeAsync(ub, s);
+    levels.push_back(C);
+    return HS_OK;
+  }
+
+  // Sorts every adjacency list of g (deterministic order for the initial trials).
+  int sort_lists(Level &Lv) {
+    G &g = Lv.g;
+    int64_t *b, *e;
+    int32_t *adj2, *wgt2;
+    HS_CHECK_CUDA(dalloc(&b, g.n, s));
+    HS_CHECK_CUDA(dalloc(&e, g.n, s));
+    HS_CHECK_CUDA(dalloc(&adj2, g.cap, s));
+    HS_CHECK_CUDA(dalloc(&wgt2, g.cap, s));
+    seg_bounds<<<hs::grid_for(g.n, 256), 256, 0, s>>>(g.n, g.xbeg, g.deg, b, e);
+    HS_CHECK_LAUNCH();
+    size_t tb = 0;
+    HS_CHECK_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, g.adj, adj2, g.wgt, wgt2,
+                                                      g.cap, g.n, b, e, s));
+    {
+      hs::Scratch<char> tmp;
+      HS_CHECK_CUDA(tmp.alloc(tb, s));
+      HS_CHECK_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, g.adj, adj2, g.wgt, wgt2,
+                                                        g.cap, g.n, b, e, s));
+    }
+    hs::count_launch(2);
+    // padding slots are not part of any segment: copy only the sorted ranges
+    // back by swapping the buffers (unsorted padding stays garbage, never read)
+    if (Lv.own_adj) cudaFreeAsync(g.adj, s);
+    if (Lv.own_wgt) cudaFreeAsync(g.wgt, s);
+    g.adj = adj2;
+    g.wgt = wgt2;
+    Lv.own_adj = Lv.own_wgt = true;
+    cudaFreeAsync(b, s);
+    cudaFreeAsync(e, s);
+    return HS_OK;
+  }
+
+  int initial(int32_t **out_part) {
+    Level &Cst = levels.back();
+    G &g = Cst.g;
+    const int nc = g.n;
+    int32_t *best;
+    HS_CHECK_CUDA(dalloc(&best, nc, s));
+    // trial 0: id-range bands
+    {
+      int64_t *vw64, *prefix;
+      HS_CHECK_CUDA(dalloc(&vw64, nc + 1, s));
+      HS_CHECK_CUDA(dalloc(&prefix, nc + 1, s));
+      int rc = hs_widen32(g.vw, vw64, nc, s);
+      if (rc) return rc;
+      rc = exclusive_scan<int64_t>(vw64, prefix, nc, s);
+      if (rc) return rc;
+      range_parts<<<hs::grid_for(nc, 256), 256, 0, s>>>(nc, prefix, g.vw, d_cum, k, total_vw, best);
+      HS_CHECK_LAUNCH();
+      cudaFreeAsync(vw64, s);
+      cudaFreeAsync(prefix, s);
+    }
+    int64_t best_cut = cut_of(g, best);
+    std::vector<int64_t> pw;
+    int rc = weights(g, best);
+    if (rc) return rc;
+    rc = read_pw(pw);
+    if (rc) return rc;
+    bool best_feas = feasible(pw);
+    // warp trials (BFS-order LDG + greedy refinement) on small coarsest graphs
+    if (nc <= 32768) {
+      rc = sort_lists(Cst);  // trials depend on list order: make it canonical
+      if (rc) return rc;
+      const int trials = nc <= 8192 ? 256 : 64;
+      InitArgs IA;
+      IA.g = g; IA.k = k; IA.hi = d_hi; IA.lo = d_lo; IA.seed = seed; IA.trials = trials;
+      int32_t *bt;
+      HS_CHECK_CUDA(dalloc(&IA.parts, (int64_t)trials * nc, s));
+      HS_CHECK_CUDA(dalloc(&IA.order, (int64_t)trials * nc, s));
+      HS_CHECK_CUDA(dalloc(&IA.seen, (int64_t)trials * nc, s));
+      HS_CHECK_CUDA(dalloc(&IA.cut, trials, s));
+      HS_CHECK_CUDA(dalloc(&IA.infeas, trials, s));
+      HS_CHECK_CUDA(dalloc(&bt, 1, s));
+      initial_kernel<<<(trials + kInitWarps - 1) / kInitWarps, kInitWarps * 32, 0, s>>>(IA);
+      HS_CHECK_LAUNCH();
+      pick_best<<<1, 1, 0, s>>>(IA.cut, IA.infeas, trials, bt);
+      HS_CHECK_LAUNCH();
+      int32_t bti = 0, binf = 0;
+      int64_t bcut = 0;
+      HS_CHECK_CUDA(cudaMemcpyAsync(&bti, bt, 4, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      HS_CHECK_CUDA(cudaMemcpyAsync(&bcut, IA.cut + bti, 8, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaMemcpyAsync(&binf, IA.infeas + bti, 4, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      bool tf = binf == 0;
+      if ((tf && !best_feas) || (tf == best_feas && bcut < best_cut)) {
+        int8_to_int32<<<hs::grid_for(nc, 256), 256, 0, s>>>(IA.parts + (int64_t)bti * nc, nc, best);
+        HS_CHECK_LAUNCH();
+      }
+      cudaFreeAsync(IA.parts, s); cudaFreeAsync(IA.order, s); cudaFreeAsync(IA.seen, s);
+      cudaFreeAsync(IA.cut, s); cudaFreeAsync(IA.infeas, s); cudaFreeAsync(bt, s);
+    }
+    *out_part = best;
+    return HS_OK;
+  }
+};
+
+}  // namespace
+
+extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *node_w_i,
+                             int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i,
+                             int64_t *nnz_host, void *stream) {
+  HS_REQUIRE(g && edge_w_i && node_w_i && xadj && adjncy && adjwgt_i && vwgt_i, HS_EINVAL,
+             "hs_symmetrize: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nk = g->n - 1;
+  hs::Scratch<int32_t> deg;
+  hs::Scratch<int64_t> deg64;
+  HS_CHECK_CUDA(deg.alloc(nk + 1, s));
+  HS_CHECK_CUDA(deg64.alloc(nk + 1, s));
+  sym_degree<<<warp_grid(g->n, 8), 256, 0, s>>>(*g, deg);
+  HS_CHECK_LAUNCH();
+  HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nk, 0, sizeof(int64_t), s));
+  int rc = hs_widen32(deg, deg64, nk, s);
+  if (rc) return rc;
+  rc = exclusive_scan<int64_t>(deg64, xadj, nk + 1, s);
+  if (rc) return rc;
+  sym_fill<<<warp_grid(g->n, 8), 256, 0, s>>>(*g, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i,
+                                               vwgt_i);
+  HS_CHECK_LAUNCH();
+  if (nnz_host) {
+    HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nk, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  return HS_OK;
+}
+
+namespace {
+__global__ void widen_kernel(const int32_t *in, int64_t *out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+}  // namespace
+
+int hs_widen32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s) {
+  if (n <= 0) return HS_OK;
+  widen_kernel<<<hs::grid_for(n, 256), 256, 0, s>>>(in, out, n);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}
+
+extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double *tpwgts_host,
+                                 double tol, uint64_t seed, int32_t *part_out,
+                                 int64_t *stats_host, void *stream) {
+  HS_REQUIRE(ug && tpwgts_host && part_out, HS_EINVAL, "hs_partition_kway: null argument");
+  HS_REQUIRE(k >= 1 && k <= kMaxParts, HS_ELIMIT, "k must be in 1..%d", kMaxParts);
+  HS_REQUIRE(ug->n >= 1, HS_EINVAL, "empty graph");
+  HS_REQUIRE(ug->adjwgt_i && ug->vwgt_i, HS_EINVAL, "k-way path needs integer weights");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n0 = ug->n;
+  const int64_t nnz0 = ug->nnz;
+  Kway K(s);
+  K.k = k;
+  K.tol = tol;
+  K.seed = seed;
+  K.salt = seed * 0x9E3779B97F4A7C15ull + 0x1234567ull;
+  K.timer.mark("start");
+
+  // ---- totals and the int32 weight guard ----
+  int64_t *tot_dev;
+  HS_CHECK_CUDA(dalloc(&tot_dev, 2, s));
+  int64_t tot[2] = {0, 0};
+  {
+    size_t tb = 0, tb2 = 0;
+    HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, ug->adjwgt_i, tot_dev, nnz0, s));
+    HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, ug->vwgt_i, tot_dev + 1, n0, s));
+    hs::Scratch<char> tmp;
+    HS_CHECK_CUDA(tmp.alloc(std::max(tb, tb2), s));
+    HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, ug->adjwgt_i, tot_dev, nnz0, s));
+    HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb2, ug->vwgt_i, tot_dev + 1, n0, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(tot, tot_dev, sizeof tot, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    hs::count_launch(2);
+  }
+  cudaFreeAsync(tot_dev, s);
+  HS_REQUIRE(tot[1] > 0 && tot[1] < (1ll << 31), HS_ELIMIT,
+             "total vertex weight must be in 1..2^31-1 (got %lld)", (long long)tot[1]);
+  K.total_vw = tot[1];
+
+  Level L0;
+  L0.own_adj = false;
+  L0.own_xbeg_vw = false;
+  L0.g.n = n0;
+  L0.g.cap = nnz0;
+  L0.g.xbeg = const_cast<int64_t *>(ug->xadj);
+  L0.g.adj = const_cast<int32_t *>(ug->adjncy);
+  L0.g.vw = const_cast<int32_t *>(ug->vwgt_i);
+  HS_CHECK_CUDA(dalloc(&L0.g.deg, n0, s));
+  deg_from_xadj<<<hs::grid_for(n0, 256), 256, 0, s>>>(ug->xadj, n0, L0.g.deg);
+  HS_CHECK_LAUNCH();
+  int64_t div = 1;
+  if (tot[0] >= (1ll << 30)) div = (tot[0] >> 30) + 1;
+  if (div > 1) {
+    HS_CHECK_CUDA(dalloc(&L0.g.wgt, nnz0, s));
+    scale_weights<<<hs::grid_for(nnz0, 256), 256, 0, s>>>(nnz0, ug->adjwgt_i, L0.g.wgt, div);
+    HS_CHECK_LAUNCH();
+  } else {
+    L0.g.wgt = const_cast<int32_t *>(ug->adjwgt_i);
+    L0.own_wgt = false;
+  }
+  K.levels.push_back(L0);
+
+  // ---- balance bounds ----
+  K.hi.resize(k); K.lo.resize(k); K.target.resize(k); K.cum.assign(k + 1, 0.0);
+  for (int p = 0; p < k; ++p) {
+    double t = tpwgts_host[p];
+    K.hi[p] = (int64_t)floor((t + tol) * (double)K.total_vw);
+    double l = (t - tol) * (double)K.total_vw;
+    K.lo[p] = l <= 0 ? 0 : (int64_t)ceil(l);
+    K.target[p] = (int64_t)llround(t * (double)K.total_vw);
+    K.cum[p + 1] = K.cum[p] + t;
+  }
+  HS_CHECK_CUDA(dalloc(&K.d_hi, k, s));
+  HS_CHECK_CUDA(dalloc(&K.d_lo, k, s));
+  HS_CHECK_CUDA(dalloc(&K.d_target, k, s));
+  HS_CHECK_CUDA(dalloc(&K.d_pw, k, s));
+  HS_CHECK_CUDA(dalloc(&K.d_flows, 2 * k, s));
+  HS_CHECK_CUDA(dalloc(&K.d_prob, 2 * k, s));
+  HS_CHECK_CUDA(dalloc(&K.d_cum, k + 1, s));
+  HS_CHECK_CUDA(dalloc(&K.counter, 4, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(K.d_hi, K.hi.data(), k * 8, cudaMemcpyHostToDevice, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(K.d_lo, K.lo.data(), k * 8, cudaMemcpyHostToDevice, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(K.d_target, K.target.data(), k * 8, cudaMemcpyHostToDevice, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(K.d_cum, K.cum.data(), (k + 1) * 8, cudaMemcpyHostToDevice, s));
+  K.timer.mark("setup");
+
+  // ---- coarsening ----
+  const int coarse_target = std::max(64 * k, 1024);
+  bool stop = false;
+  while (!stop && K.levels.back().g.n > coarse_target && (int)K.levels.size() < 40) {
+    int rc = K.coarsen_once(&stop);
+    if (rc) return rc;
+    K.timer.mark("coarsen level");
+  }
+
+  // ---- initial partition ----
+  int32_t *cur = nullptr;
+  int rc = K.initial(&cur);
+  if (rc) return rc;
+  K.timer.mark("initial partition");
+  const int coarsest_n = K.levels.back().g.n;
+
+  // ---- uncoarsening + refinement ----
+  int64_t passes = 0;
+  for (int li = (int)K.levels.size() - 1; li >= 0; --li) {
+    Level &Lv = K.levels[li];
+    if (li != (int)K.levels.size() - 1) {
+      int32_t *pf = li == 0 ? part_out : nullptr;
+      if (!pf) HS_CHECK_CUDA(dalloc(&pf, Lv.g.n, s));
+      project<<<hs::grid_for(Lv.g.n, 256), 256, 0, s>>>(Lv.g.n, Lv.cmap, cur, pf);
+      HS_CHECK_LAUNCH();
+      cudaFreeAsync(cur, s);
+      cur = pf;
+    }
+    rc = K.refine(Lv.g, cur, K.salt ^ ((uint64_t)li << 40), &passes);
+    if (rc) return rc;
+    K.timer.mark("refine level");
+  }
+  if (cur != part_out) {  // single-level case: the coarsest graph is the input
+    HS_CHECK_CUDA(cudaMemcpyAsync(part_out, cur, n0 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    cudaFreeAsync(cur, s);
+  }
+
+  // ---- statistics (cut with the caller's unscaled weights) ----
+  G g0 = K.levels[0].g;  // the caller's arrays and unscaled weights
+  g0.adj = const_cast<int32_t *>(ug->adjncy);
+  g0.wgt = const_cast<int32_t *>(ug->adjwgt_i);
+  int64_t cut = K.cut_of(g0, part_out);
+  std::vector<int64_t> pw;
+  rc = K.weights(g0, part_out);
+  if (rc) return rc;
+  rc = K.read_pw(pw);
+  if (rc) return rc;
+  K.timer.mark("stats");
+  double maxdev = 0;
+  for (int p = 0; p < k; ++p)
+    maxdev = std::max(maxdev, fabs((double)pw[p] / (double)K.total_vw - tpwgts_host[p]));
+  if (stats_host) {
+    stats_host[0] = cut;
+    stats_host[1] = (int64_t)K.levels.size();
+    stats_host[2] = coarsest_n;
+    stats_host[3] = (int64_t)llround(maxdev * 1e9);
+    stats_host[4] = maxdev <= tol ? 1 : 0;
+    stats_host[5] = passes;
+    stats_host[6] = div;
+    stats_host[7] = 0;
+  }
+  for (size_t i = 0; i < K.levels.size(); ++i) {
+    Level &Lv = K.levels[i];
+    if (Lv.cmap) cudaFreeAsync(Lv.cmap, s);
+    cudaFreeAsync(Lv.g.deg, s);
+    if (Lv.own_adj) cudaFreeAsync(Lv.g.adj, s);
+    if (Lv.own_wgt) cudaFreeAsync(Lv.g.wgt, s);
+    if (Lv.own_xbeg_vw) { cudaFreeAsync(Lv.g.xbeg, s); cudaFreeAsync(Lv.g.vw, s); }
+  }
+  cudaFreeAsync(K.d_hi, s); cudaFreeAsync(K.d_lo, s); cudaFreeAsync(K.d_target, s);
+  cudaFreeAsync(K.d_pw, s); cudaFreeAsync(K.d_flows, s); cudaFreeAsync(K.d_prob, s);
+  cudaFreeAsync(K.d_cum, s); cudaFreeAsync(K.counter, s);
+  return HS_OK;
+}

@@ -1,0 +1,153 @@
+"""CSR-native entry points for graphs beyond the object model (configs 2-4).
+
+* ``layered_dag``      — device generator of the layered fan-in DAG family
+                         (100k/1M, 10M/100M) straight into a ``DagCSR``.
+* ``integer_weights``  — METIS integerisation of fp64 weights
+                         (graphio.py:272-274: ×100, round half up, min 1).
+* ``symmetrize``       — K1: DAG -> undirected kernel graph (root dropped).
+* ``partition_kway``   — K3-K6 multilevel k-way partitioner.
+* ``evaluate_batch``   — K2 integer cut / load / transfer volume for many
+                         k-way assignments of one DAG.
+* ``levels`` / ``level_order`` / ``critical_path`` — K7 on a ``DagCSR``.
+
+These are additive to the reference API (which stops at 2-way).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+from .costs import SyntheticCostModel, TransferModel
+from .csr import DagCSR
+
+
+class UGraph:
+    """Undirected integer-weighted kernel graph on the device (hs_ugraph_t)."""
+
+    def __init__(self, xadj, adjncy, adjwgt, vwgt):
+        self.xadj, self.adjncy, self.adjwgt, self.vwgt = xadj, adjncy, adjwgt, vwgt
+        self.n = int(vwgt.numel())
+        self.nnz = int(adjncy.numel())
+        self._struct = None
+
+    def struct(self):
+        if self._struct is None:
+            p = _native.ptr
+            self._struct = _native.HsUGraph(self.n, self.nnz, p(self.xadj), p(self.adjncy), None,
+                                            p(self.adjwgt), None, p(self.vwgt))
+        return self._struct
+
+
+def layered_dag(n_kernels: int, m_inter: int, seed: int = 0, kind: str = "MA", size: int = 512,
+                model=None) -> DagCSR:
+    """Layered fan-in DAG generated on the device (see csrc/gen.cu for the family).
+
+    Node weights come from ``model`` (default ``SyntheticCostModel``) for
+    (kind, size); every edge carries one size² fp32 matrix (graph.py:195).
+    """
+    dev = _native.device()
+    model = model or SyntheticCostModel()
+    n_nodes, m = _native.layered_sizes(n_kernels, m_inter)
+    out_ptr = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+    in_ptr = torch.empty(n_nodes + 1, dtype=torch.int64, device=dev)
+    out_dst = torch.empty(m, dtype=torch.int32, device=dev)
+    in_src = torch.empty(m, dtype=torch.int32, device=dev)
+    in_eid = torch.empty(m, dtype=torch.int32, device=dev)
+    layer_of = torch.empty(n_nodes, dtype=torch.int32, device=dev)
+    _native.layered_generate(n_kernels, m_inter, seed, out_ptr, out_dst, in_ptr, in_src, in_eid,
+                             layer_of)
+    wc = model.kernel_time(kind, size, "CPU")
+    wg = model.kernel_time(kind, size, "GPU")
+    w_cpu = torch.full((n_nodes,), wc, dtype=torch.float64, device=dev)
+    w_gpu = torch.full((n_nodes,), wg, dtype=torch.float64, device=dev)
+    w_cpu[0] = 0.0
+    w_gpu[0] = 0.0
+    payload = size * size * 4
+    nbytes = torch.full((m,), payload, dtype=torch.int64, device=dev)
+    w_xfer = torch.full((m,), model.transfer_time(payload), dtype=torch.float64, device=dev)
+    csr = DagCSR(n_nodes, m, 0, out_ptr, out_dst, in_ptr, in_src, in_eid, w_cpu, w_gpu, w_xfer,
+                 nbytes, ids=None, host=None)
+    csr.layer_of = layer_of
+    return csr
+
+
+def integer_weights(w: torch.Tensor, scale: int = 100) -> torch.Tensor:
+    """``_scaled`` (graphio.py:272-274) elementwise: max(1, floor(w*scale + 0.5)), int32."""
+    return torch.clamp(torch.floor(w * scale + 0.5), min=1).to(torch.int32)
+
+
+def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,
+               node_w_i: Optional[torch.Tensor] = None) -> UGraph:
+    """K1 on the device; default weights are the integerised w_xfer / w_gpu."""
+    dev = csr.device
+    if edge_w_i is None:
+        edge_w_i = integer_weights(csr.w_xfer)
+    if node_w_i is None:
+        node_w_i = integer_weights(csr.w_gpu)
+    nk = csr.n - 1
+    xadj = torch.empty(nk + 1, dtype=torch.int64, device=dev)
+    nnz_cap = 2 * csr.m
+    adjncy = torch.empty(nnz_cap, dtype=torch.int32, device=dev)
+    adjwgt = torch.empty(nnz_cap, dtype=torch.int32, device=dev)
+    vwgt = torch.empty(nk, dtype=torch.int32, device=dev)
+    nnz = _native.symmetrize(csr, edge_w_i.contiguous(), node_w_i.contiguous(), xadj, adjncy,
+                             adjwgt, vwgt)
+    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz], vwgt)
+
+
+@dataclass
+class KwayResult:
+    part: torch.Tensor        # int32 [n] (kernel positions)
+    cut: int                  # integer cut, each undirected edge once
+    levels: int
+    coarsest: int
+    max_deviation: float      # max_p |w_p/total - t_p|
+    feasible: bool
+    refine_passes: int
+
+
+def partition_kway(graph, k: int, tpwgts: Optional[Sequence[float]] = None, tol: float = 0.03,
+                   seed: int = 0, out: Optional[torch.Tensor] = None) -> KwayResult:
+    """Multilevel k-way partition (K3-K6) of a ``UGraph`` or ``DagCSR``.
+
+    Balance: |w_p/total - t_p| <= tol for every part (the k-way
+    generalisation of partition.py:72); default targets are uniform 1/k.
+    """
+    ug = graph if isinstance(graph, UGraph) else symmetrize(graph)
+    if tpwgts is None:
+        tpwgts = [1.0 / k] * k
+    if len(tpwgts) != k:
+        raise ValueError("need one target fraction per part")
+    part = out if out is not None else torch.empty(ug.n, dtype=torch.int32, device=ug.xadj.device)
+    st = _native.partition_kway(ug, k, tpwgts, tol, seed, part)
+    return KwayResult(part, st[0], st[1], st[2], st[3] / 1e9, bool(st[4]), st[5])
+
+
+def evaluate_batch(csr: DagCSR, parts: torch.Tensor, k: int,
+                   node_w_i: Optional[torch.Tensor] = None) -> Dict[str, torch.Tensor]:
+    """K2 for B k-way assignments (int32 [B, n], node index space incl. root)."""
+    if node_w_i is None:
+        node_w_i = integer_weights(csr.w_gpu).to(torch.int64)
+    if parts.dim() == 1:
+        parts = parts.unsqueeze(0)
+    return _native.evaluate_kway(csr, parts.contiguous(), k, node_w_i.contiguous())
+
+
+def kernel_to_node_parts(csr: DagCSR, kpart: torch.Tensor) -> torch.Tensor:
+    """Kernel-position part array -> node-index part array (root gets part 0)."""
+    r = csr.root
+    return torch.cat([kpart[:r], kpart.new_zeros(1), kpart[r:]]).contiguous()
+
+
+def levels(csr: DagCSR, mode: int = 0):
+    """Longest-path level per node and the critical path (K7)."""
+    return _native.levels(csr, mode)
+
+
+def level_order(csr: DagCSR) -> torch.Tensor:
+    lv, _, _, nl = _native.levels(csr, 0)
+    return _native.level_order(csr, lv, nl)

@@ -1,0 +1,98 @@
+"""Config 2/4 path on the device: generator, symmetrize, k-way partition, k-way evaluate,
+levels — checked against the CPU oracle restatements."""
+import numpy as np
+import pytest
+import torch
+
+from paper_1502_07451_b200 import kway
+from oracle import hetsched_oracle as O
+from oracle import layered_oracle as LO
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("n,m,seed", [(50, 300, 0), (400, 4000, 3), (2000, 20000, 7)])
+def test_generator_matches_oracle(n, m, seed):
+    csr = kway.layered_dag(n, m, seed)
+    preds, edges, layer = LO.generate(n, m, seed)
+    src = np.repeat(np.arange(csr.n), np.diff(csr.out_ptr.cpu().numpy()))
+    dst = csr.out_dst.cpu().numpy()
+    assert list(zip(src.tolist(), dst.tolist())) == edges
+    in_ptr = csr.in_ptr.cpu().numpy()
+    in_src = csr.in_src.cpu().numpy()
+    for v in range(csr.n):
+        assert in_src[in_ptr[v]:in_ptr[v + 1]].tolist() == preds[v]
+    in_eid = csr.in_eid.cpu().numpy()
+    assert (dst[in_eid] == np.repeat(np.arange(csr.n), np.diff(in_ptr))).all()
+    assert (src[in_eid] == in_src).all()
+    lay = csr.layer_of.cpu().numpy()
+    assert all(lay[v] == layer[v] for v in range(1, n + 1))
+
+
+def _host_graph(csr):
+    src = np.repeat(np.arange(csr.n), np.diff(csr.out_ptr.cpu().numpy()))
+    return src, csr.out_dst.cpu().numpy(), csr.bytes.cpu().numpy()
+
+
+def test_symmetrize_adjacency_sets():
+    csr = kway.layered_dag(3000, 30000, 1)
+    ug = kway.symmetrize(csr)
+    src, dst, _ = _host_graph(csr)
+    keep = (src != 0) & (dst != 0)
+    want = {}
+    for u, v in zip(src[keep] - 1, dst[keep] - 1):
+        want.setdefault(u, []).append(v)
+        want.setdefault(v, []).append(u)
+    xadj = ug.xadj.cpu().numpy()
+    adj = ug.adjncy.cpu().numpy()
+    assert ug.nnz == 2 * keep.sum()
+    for v in range(ug.n):
+        assert sorted(adj[xadj[v]:xadj[v + 1]].tolist()) == sorted(want.get(v, []))
+
+
+@pytest.mark.parametrize("n,m,k", [(5000, 50000, 2), (20000, 200000, 8), (100000, 1000000, 8)])
+def test_kway_valid_balanced_deterministic(n, m, k):
+    csr = kway.layered_dag(n, m, 0)
+    ug = kway.symmetrize(csr)
+    r1 = kway.partition_kway(ug, k, tol=0.03, seed=5)
+    r2 = kway.partition_kway(ug, k, tol=0.03, seed=5)
+    p1 = r1.part.cpu().numpy()
+    assert (p1 == r2.part.cpu().numpy()).all(), "not deterministic"
+    assert p1.min() >= 0 and p1.max() < k
+    assert r1.feasible and r1.max_deviation <= 0.03
+    # integer cut from the partitioner == K2 on the directed DAG == oracle
+    nodep = kway.kernel_to_node_parts(csr, r1.part)
+    ev = kway.evaluate_batch(csr, nodep.unsqueeze(0), k,
+                             node_w_i=kway.integer_weights(csr.w_gpu).to(torch.int64))
+    src, dst, nb = _host_graph(csr)
+    ew = kway.integer_weights(csr.w_xfer).cpu().numpy()
+    np_ = nodep.cpu().numpy()
+    cut_w = int(ew[(src != 0) & (dst != 0) & (np_[src] != np_[dst])].sum())
+    assert r1.cut == cut_w
+    vw = kway.integer_weights(csr.w_gpu).cpu().numpy()
+    ref = O.evaluate_kway(csr.n, 0, src.tolist(), dst.tolist(), nb.tolist(), np_.tolist(), k, vw)
+    for key in ("cut_bytes", "cut_edges", "xfer_count", "xfer_bytes"):
+        assert int(ev[key][0]) == ref[key], key
+    assert ev["loads"][0].cpu().tolist() == ref["loads"]
+    # quality: clearly better than a random balanced assignment
+    rnd = np.random.default_rng(0).integers(0, k, size=ug.n)
+    nodes_r = np.concatenate([[0], rnd])
+    rand_cut = int(ew[(src != 0) & (dst != 0) & (nodes_r[src] != nodes_r[dst])].sum())
+    assert r1.cut < rand_cut
+
+
+def test_levels_and_critical_path_match_oracle():
+    csr = kway.layered_dag(3000, 20000, 2)
+    lv, finish, cp, nl = kway.levels(csr)
+    src, dst, _ = _host_graph(csr)
+    nodes = [[i, "MA", 512, float(csr.w_cpu[i]), float(csr.w_gpu[i])] for i in range(csr.n)]
+    wx = csr.w_xfer.cpu().numpy()
+    spec = {"root": 0, "nodes": nodes,
+            "edges": [[int(u), int(v), 0, float(w)] for u, v, w in zip(src, dst, wx)]}
+    g = O.OGraph(spec)
+    assert cp == O.critical_path(g)
+    want = O.levels(g)
+    got = lv.cpu().numpy()
+    assert all(got[i] == want[i] for i in range(csr.n))
+    order = kway.level_order(csr).cpu().numpy().tolist()
+    assert order == O.level_order(g)
