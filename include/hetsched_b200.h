@@ -106,6 +106,14 @@ const char *hs_version(void);
 /* Number of launches of this library's kernels since load (evidence for the
  * bench's gpu_launches field). */
 int64_t hs_launch_count(void);
+/* Live kernel profiling: when enabled, designated launches are bracketed by
+ * CUDA events on their stream and booked as (launches, device ms,
+ * algorithmic bytes) per kernel name. hs_profile_report writes
+ * "name,launches,ms,bytes\n" lines (synchronises the pending events) and
+ * returns the full text length. */
+void hs_profile_enable(int on);
+void hs_profile_reset(void);
+int hs_profile_report(char *buf, int len);
 
 /* ---- K0 exact sums (fsum) --------------------------------------------
  * Replaces math.fsum in total_weights (graph.py:327-332) and

@@ -273,3 +273,31 @@ def layered_generate(n_kernels, m_inter, seed, out_ptr, out_dst, in_ptr, in_src,
     check(fn(n_kernels, m_inter, ctypes.c_uint64(seed & (2**64 - 1)), ptr(out_ptr),
              ptr(out_dst), ptr(in_ptr), ptr(in_src), ptr(in_eid), ptr(layer_of),
              stream_ptr()))
+
+
+# ---------------------------------------------------------------- profiling --
+_lib.hs_profile_enable.argtypes = [ctypes.c_int]
+_lib.hs_profile_enable.restype = None
+_lib.hs_profile_reset.restype = None
+_lib.hs_profile_report.argtypes = [ctypes.c_char_p, ctypes.c_int]
+_lib.hs_profile_report.restype = ctypes.c_int
+
+
+def profile_enable(on: bool = True) -> None:
+    _lib.hs_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    _lib.hs_profile_reset()
+
+
+def profile_report() -> dict:
+    """{kernel: {"launches", "ms", "bytes"}} accumulated since the last reset."""
+    size = _lib.hs_profile_report(None, 0)
+    buf = ctypes.create_string_buffer(size + 1)
+    _lib.hs_profile_report(buf, size + 1)
+    out = {}
+    for line in buf.value.decode().splitlines():
+        name, launches, ms, nbytes = line.split(",")
+        out[name] = {"launches": int(launches), "ms": float(ms), "bytes": float(nbytes)}
+    return out

@@ -2,6 +2,10 @@
 // version, scratch-pool configuration.
 #include "common.cuh"
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
 #include <string.h>
 
 namespace hs {
@@ -52,7 +56,65 @@ int iota32(int32_t *out, int64_t n, cudaStream_t s) {
   return HS_OK;
 }
 
+struct ProfEntry {
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+  int64_t launches = 0;
+  double ms = 0, bytes = 0;
+};
+static std::mutex g_prof_mu;
+static std::map<std::string, ProfEntry> g_prof;
+static std::atomic<int> g_prof_on{0};
+
+bool prof_enabled() { return g_prof_on.load(std::memory_order_relaxed) != 0; }
+
+void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b, double bytes) {
+  std::lock_guard<std::mutex> lk(g_prof_mu);
+  ProfEntry &e = g_prof[name];
+  e.pending.emplace_back(a, b);
+  e.launches += 1;
+  e.bytes += bytes;
+}
+
+static void prof_drain() {
+  for (auto &kv : g_prof) {
+    for (auto &ab : kv.second.pending) {
+      cudaEventSynchronize(ab.second);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ab.first, ab.second);
+      kv.second.ms += ms;
+      cudaEventDestroy(ab.first);
+      cudaEventDestroy(ab.second);
+    }
+    kv.second.pending.clear();
+  }
+}
+
 }  // namespace hs
+
+extern "C" void hs_profile_enable(int on) { hs::g_prof_on.store(on ? 1 : 0); }
+
+extern "C" void hs_profile_reset(void) {
+  std::lock_guard<std::mutex> lk(hs::g_prof_mu);
+  hs::prof_drain();
+  hs::g_prof.clear();
+}
+
+extern "C" int hs_profile_report(char *buf, int len) {
+  std::lock_guard<std::mutex> lk(hs::g_prof_mu);
+  hs::prof_drain();
+  std::string out;
+  char line[256];
+  for (auto &kv : hs::g_prof) {
+    snprintf(line, sizeof line, "%s,%lld,%.6f,%.0f\n", kv.first.c_str(),
+             (long long)kv.second.launches, kv.second.ms, kv.second.bytes);
+    out += line;
+  }
+  if (buf && len > 0) {
+    strncpy(buf, out.c_str(), (size_t)len - 1);
+    buf[len - 1] = 0;
+  }
+  return (int)out.size();
+}
 
 extern "C" const char *hs_last_error(void) { return hs::g_err; }
 extern "C" const char *hs_version(void) { return "hetsched_b200 0.1.0 sm_100a"; }

@@ -70,4 +70,29 @@ int iota32(int32_t *out, int64_t n, cudaStream_t s);
 // Number of SMs of the current device (cached).
 int sm_count();
 
+// ---- live kernel profiling (hs_profile_*) --------------------------------
+// When enabled, Prof brackets one launch with CUDA events on its stream and
+// books (launches, device ms, algorithmic bytes) under the kernel's name.
+bool prof_enabled();
+void prof_record(const char *name, cudaEvent_t a, cudaEvent_t b, double bytes);
+struct Prof {
+  const char *name;
+  cudaStream_t s;
+  double bytes;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Prof(const char *n, cudaStream_t st, double by) : name(n), s(st), bytes(by) {
+    if (prof_enabled()) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~Prof() {
+    if (a) {
+      cudaEventRecord(b, s);
+      prof_record(name, a, b, bytes);
+    }
+  }
+};
+
 }  // namespace hs

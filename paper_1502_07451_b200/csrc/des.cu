@@ -312,7 +312,11 @@ extern "C" int hs_simulate_batch(const hs_dag_batch_t *g, int policy, const int8
   A.ev = ev; A.ev_off = ev_off; A.ev_count = ev_count;
   A.pending = pending; A.qnext = qnext; A.ready = ready; A.arr = arr;
   const int block = 64;
-  des_kernel<<<(g->batch + block - 1) / block, block, 0, s>>>(A);
+  {
+    // every graph's CSR + weights read once, scratch state initialised once
+    hs::Prof P("des", s, 40.0 * N + 36.0 * M);
+    des_kernel<<<(g->batch + block - 1) / block, block, 0, s>>>(A);
+  }
   HS_CHECK_LAUNCH();
   return HS_OK;
 }

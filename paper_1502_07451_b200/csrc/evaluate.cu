@@ -254,8 +254,13 @@ extern "C" int hs_evaluate_kway(const hs_dag_t *g, const int32_t *part, int32_t 
   HS_CHECK_CUDA(cudaMemsetAsync(xfer_bytes, 0, batch * sizeof(int64_t), s));
   HS_CHECK_CUDA(cudaMemsetAsync(loads, 0, (size_t)batch * k * sizeof(int64_t), s));
   dim3 grid(hs::grid_for((int64_t)g->n * 32, 256, hs::sm_count() * 8), batch);
-  evalk_kernel<<<grid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
-                                     xfer_count, xfer_bytes);
+  {
+    // per assignment: out_ptr, out_dst, bytes, part[dst] gather, part[src], vwgt
+    hs::Prof P("evaluate_kway", s, (double)batch * (8.0 * (g->n + 1) + 4.0 * g->m + 8.0 * g->m +
+                                                    4.0 * g->m + 4.0 * g->n + 8.0 * g->n));
+    evalk_kernel<<<grid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
+                                       xfer_count, xfer_bytes);
+  }
   HS_CHECK_LAUNCH();
   return HS_OK;
 }

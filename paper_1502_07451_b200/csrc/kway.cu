@@ -47,6 +47,7 @@ constexpr int kMaxParts = 64;
 struct G {
   int32_t n;
   int64_t cap;  // adjacency slots (padded)
+  int64_t nnz;  // live adjacency entries
   int64_t *xbeg;
   int32_t *deg;
   int32_t *adj;
@@ -920,10 +921,16 @@ struct Kway {
     rc = rebalance(g, part, cand, salt2 ^ 0xabcdefull);
     if (rc) return rc;
     for (int pass = 0; pass < 10; ++pass) {
-      refine_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(g, part, k, d_pw, d_hi,
-                                                                            d_lo, cand, cgain);
+      {
+        hs::Prof P("refine_candidates", s, 28.0 * g.n + 12.0 * g.nnz);
+        refine_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(
+            g, part, k, d_pw, d_hi, d_lo, cand, cgain);
+      }
       HS_CHECK_LAUNCH();
-      refine_afterburner<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, cand, cgain, cand2);
+      {
+        hs::Prof P("refine_afterburner", s, 12.0 * g.n);
+        refine_afterburner<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, cand, cgain, cand2);
+      }
       HS_CHECK_LAUNCH();
       int32_t planned = 0;
       rc = apply_plan(g, cand2, part, false, salt2 + pass * 104729, &planned);
@@ -942,7 +949,10 @@ struct Kway {
     unsigned long long *c2, h = 0;
     if (dalloc(&c2, 1, s) != cudaSuccess) return -1;
     cudaMemsetAsync(c2, 0, 8, s);
-    cut_kernel<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, c2);
+    {
+      hs::Prof P("cut", s, 16.0 * g.n + 12.0 * g.nnz);
+      cut_kernel<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, c2);
+    }
     hs::count_launch();
     cudaMemcpyAsync(&h, c2, 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
@@ -970,9 +980,14 @@ struct Kway {
     HS_CHECK_CUDA(cudaMemsetAsync(match, 0xff, n * sizeof(int32_t), s));
     const int rounds = 3;
     for (int round = 0; round < rounds; ++round) {
-      match_propose<<<warp_grid(n, 8), 256, 0, s>>>(F.g, match, prop,
-                                                      round == rounds - 1 ? fav : nullptr,
-                                                      salt + (uint64_t)lvl * 131 + round, max_vw);
+      {
+        // round 0 scans every list; later rounds only unmatched vertices (N-bytes bound)
+        hs::Prof P(round == 0 ? "match_propose_r0" : "match_propose_rN", s,
+                   round == 0 ? 28.0 * n + 16.0 * F.g.nnz : 28.0 * n);
+        match_propose<<<warp_grid(n, 8), 256, 0, s>>>(F.g, match, prop,
+                                                        round == rounds - 1 ? fav : nullptr,
+                                                        salt + (uint64_t)lvl * 131 + round, max_vw);
+      }
       HS_CHECK_LAUNCH();
       match_accept<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, prop, counter);
       HS_CHECK_LAUNCH();
@@ -1052,6 +1067,12 @@ struct Kway {
     C.g.cap = capc;
     HS_CHECK_CUDA(dalloc(&C.g.adj, capc, s));
     HS_CHECK_CUDA(dalloc(&C.g.wgt, capc, s));
+    cudaEvent_t ct0 = nullptr, ct1 = nullptr;
+    if (hs::prof_enabled()) {
+      cudaEventCreate(&ct0);
+      cudaEventCreate(&ct1);
+      cudaEventRecord(ct0, s);
+    }
     contract_warp<<<warp_grid(nc, kContractWarps), kContractWarps * 32, 0, s>>>(
         F.g, F.cmap, mem0, mem1, ub, nc, C.g);
     HS_CHECK_LAUNCH();
@@ -1087,6 +1108,23 @@ struct Kway {
       cudaFreeAsync(gk, s);
       cudaFreeAsync(gv, s);
     }
+    if (ct0) cudaEventRecord(ct1, s);
+    {  // live adjacency entries of the coarse level
+      int64_t *dsum;
+      HS_CHECK_CUDA(dalloc(&dsum, 1, s));
+      size_t tb = 0;
+      HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, C.g.deg, dsum, nc, s));
+      hs::Scratch<char> tmp;
+      HS_CHECK_CUDA(tmp.alloc(tb, s));
+      HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, C.g.deg, dsum, nc, s));
+      HS_CHECK_CUDA(cudaMemcpyAsync(&C.g.nnz, dsum, 8, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      cudaFreeAsync(dsum, s);
+      hs::count_launch(1);
+    }
+    if (ct0)
+      hs::prof_record("contract", ct0, ct1,
+                      28.0 * nc + 12.0 * n + 12.0 * F.g.nnz + 8.0 * C.g.nnz);
     cudaFreeAsync(list, s);
     cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
     cudaFreeAsync(flag, s); cudaFreeAsync(cid, s); cudaFreeAsync(mem0, s);
@@ -1206,6 +1244,7 @@ extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const i
   hs::Scratch<int64_t> deg64;
   HS_CHECK_CUDA(deg.alloc(nk + 1, s));
   HS_CHECK_CUDA(deg64.alloc(nk + 1, s));
+  hs::Prof P("symmetrize", s, 32.0 * g->n + 36.0 * g->m);
   sym_degree<<<warp_grid(g->n, 8), 256, 0, s>>>(*g, deg);
   HS_CHECK_LAUNCH();
   HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nk, 0, sizeof(int64_t), s));
@@ -1281,6 +1320,7 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   L0.own_xbeg_vw = false;
   L0.g.n = n0;
   L0.g.cap = nnz0;
+  L0.g.nnz = nnz0;
   L0.g.xbeg = const_cast<int64_t *>(ug->xadj);
   L0.g.adj = const_cast<int32_t *>(ug->adjncy);
   L0.g.vw = const_cast<int32_t *>(ug->vwgt_i);

@@ -139,7 +139,12 @@ extern "C" int hs_levels(const hs_dag_t *g, int mode, int32_t *level, double *fi
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   void *args[] = {&A};
-  HS_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)levels_kernel, grid, block, args, 0, s));
+  {
+    // in-CSR + pred finish/level gathers + weights + finish/level writes + out-CSR
+    hs::Prof P("levels", s, 16.0 * n + 8.0 * n + 4.0 * g->m + 12.0 * g->m + 16.0 * n + 12.0 * n +
+                                4.0 * g->m);
+    HS_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)levels_kernel, grid, block, args, 0, s));
+  }
   HS_CHECK_LAUNCH();
   if (cp_host || n_levels_host) {
     int32_t h[8];
