@@ -37,12 +37,14 @@
 #include <cub/device/device_segmented_sort.cuh>
 #include <vector>
 #include <algorithm>
+#include <cuda_profiler_api.h>
 
 int hs_widen32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
 
 namespace {
 
 constexpr int kMaxParts = 64;
+using part_t = int8_t;  // part ids (k <= 64) as bytes: 4x less gather traffic
 
 struct G {
   int32_t n;
@@ -67,6 +69,19 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
 __device__ __forceinline__ uint32_t edge_hash(int a, int b, uint64_t salt) {
   uint32_t lo = (uint32_t)min(a, b), hi = (uint32_t)max(a, b);
   return mix32(salt ^ ((uint64_t)lo << 32 | hi));
+}
+
+// 32-bit symmetric edge hash (lowbias32 of a mix of both ends and the salt):
+// cheap enough for the per-edge inner loop of the matching proposals.
+__device__ __forceinline__ uint32_t edge_hash32(int a, int b, uint32_t salt) {
+  uint32_t lo = (uint32_t)min(a, b), hi = (uint32_t)max(a, b);
+  uint32_t x = lo * 0x9E3779B1u ^ (hi + salt) * 0x85EBCA77u;
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
 }
 
 __device__ __forceinline__ int warp_id_global() {
@@ -132,58 +147,24 @@ __device__ __forceinline__ float rating(int w, int32_t a, int32_t b) {
   return (float)w * (float)w / ((float)a * (float)b);
 }
 
-// prop[u]: best unmatched neighbour (or -1); fav[u]: best neighbour overall.
-__global__ void match_propose(G g, const int32_t *match, int32_t *prop, int32_t *fav,
-                              uint64_t salt, int32_t max_vw) {
-  const int lane = threadIdx.x & 31;
-  for (int u = warp_id_global(); u < g.n; u += warps_total()) {
-    if (match[u] >= 0) {
-      if (lane == 0) { prop[u] = -1; if (fav) fav[u] = -1; }
-      continue;
-    }
-    const int64_t b = g.xbeg[u];
-    const int d = g.deg[u];
-    const int32_t vu = g.vw[u];
-    float br = -1.f, fr = -1.f;
-    int bv = -1, fv = -1;
-    uint32_t bh = 0, fh = 0;
-    for (int j = lane; j < d; j += 32) {
-      int v = g.adj[b + j];
-      if (v == u) continue;
-      int32_t vv = g.vw[v];
-      if (vu + vv > max_vw) continue;
-      float r = rating(g.wgt[b + j], vu, vv);
-      uint32_t h = edge_hash(u, v, salt);
-      if (r > fr || (r == fr && (h > fh || (h == fh && v < fv)))) { fr = r; fh = h; fv = v; }
-      if (match[v] >= 0) continue;
-      if (r > br || (r == br && (h > bh || (h == bh && v < bv)))) { br = r; bh = h; bv = v; }
-    }
-    for (int off = 16; off; off >>= 1) {
-      float orr = __shfl_down_sync(0xffffffffu, br, off);
-      uint32_t oh = __shfl_down_sync(0xffffffffu, bh, off);
-      int ov = __shfl_down_sync(0xffffffffu, bv, off);
-      if (ov >= 0 && (bv < 0 || orr > br || (orr == br && (oh > bh || (oh == bh && ov < bv))))) {
-        br = orr; bh = oh; bv = ov;
-      }
-      orr = __shfl_down_sync(0xffffffffu, fr, off);
-      oh = __shfl_down_sync(0xffffffffu, fh, off);
-      ov = __shfl_down_sync(0xffffffffu, fv, off);
-      if (ov >= 0 && (fv < 0 || orr > fr || (orr == fr && (oh > fh || (oh == fh && ov < fv))))) {
-        fr = orr; fh = oh; fv = ov;
-      }
-    }
-    if (lane == 0) { prop[u] = bv; if (fav) fav[u] = fv; }
-  }
-}
-
 // Two-hop ("leaf") matching: unmatched vertices that share a favourite
 // neighbour are paired in (favourite, id) order.
 __global__ void twohop_keys(int n, const int32_t *match, const int32_t *fav, uint64_t *keys,
                            int32_t *count) {
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
-       u += (int64_t)gridDim.x * blockDim.x)
-    if (match[u] < 0 && fav[u] >= 0)
-      keys[atomicAdd(count, 1)] = ((uint64_t)(uint32_t)fav[u] << 32) | (uint64_t)u;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t u = base + threadIdx.x;
+    const bool take = u < n && match[u] < 0 && fav[u] >= 0;
+    const uint64_t key = take ? ((uint64_t)(uint32_t)fav[u] << 32) | (uint64_t)u : 0;
+    // warp-aggregated append (one atomic per warp, not per vertex)
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int at = 0;
+    if (lane == leader) at = atomicAdd(count, __popc(m));
+    at = __shfl_sync(0xffffffffu, at, leader);
+    if (take) keys[at + __popc(m & ((1u << lane) - 1))] = key;
+  }
 }
 
 __global__ void twohop_heads(const uint64_t *keys, int cnt, int32_t *head) {
@@ -205,12 +186,17 @@ __global__ void twohop_pair(const uint64_t *keys, const int32_t *start, int cnt,
   }
 }
 
-__global__ void match_accept(int n, int32_t *match, const int32_t *prop, int32_t *nmatched) {
+__global__ void match_accept(int n, int32_t *match, const int32_t *prop, uint32_t *mw,
+                             int32_t *nmatched) {
   int local = 0;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
        u += (int64_t)gridDim.x * blockDim.x) {
     int v = prop[u];
-    if (match[u] < 0 && v >= 0 && prop[v] == (int)u) { match[u] = v; ++local; }
+    if (match[u] < 0 && v >= 0 && prop[v] == (int)u) {
+      match[u] = v;
+      mw[u] |= 0x80000000u;
+      ++local;
+    }
   }
   for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(nmatched, local);
@@ -305,10 +291,11 @@ contract_warp(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1
 // CTA per (long) coarse vertex; table in dynamic shared memory or, when
 // `gtab` is set, in global scratch at 2*xbeg (2*ub slots available there).
 __global__ void contract_block(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1,
-                               const int64_t *ub, const int32_t *list, int nlist, G c,
+                               const int64_t *ub, const int32_t *list, const int32_t *nlistp, G c,
                                int32_t *gkeys, int32_t *gvals, int smem_slots) {
   extern __shared__ int32_t sm[];
   __shared__ int s_cnt;
+  const int nlist = *nlistp;
   for (int li = blockIdx.x; li < nlist; li += gridDim.x) {
     const int cv = list[li];
     const int64_t u_b = ub[cv];
@@ -362,11 +349,21 @@ __global__ void contract_block(G g, const int32_t *cmap, const int32_t *mem0, co
   }
 }
 
-__global__ void classify_long(const int64_t *ub, int nc, int64_t lo, int64_t hi, int32_t *list,
-                              int32_t *count) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nc;
-       i += (int64_t)gridDim.x * blockDim.x)
-    if (ub[i] * 2 > lo && ub[i] * 2 <= hi) list[atomicAdd(count, 1)] = (int)i;
+__global__ void classify_long(const int64_t *ub, const int32_t *ncp, int64_t lo, int64_t hi,
+                              int32_t *list, int32_t *count) {
+  const int nc = *ncp;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nc; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const bool take = i < nc && ub[i] * 2 > lo && ub[i] * 2 <= hi;
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int at = 0;
+    if (lane == leader) at = atomicAdd(count, __popc(m));
+    at = __shfl_sync(0xffffffffu, at, leader);
+    if (take) list[at + __popc(m & ((1u << lane) - 1))] = (int)i;
+  }
 }
 
 // ------------------------------------------------------------------ K5 ---
@@ -536,13 +533,13 @@ __global__ void pick_best(const int64_t *cut, const int32_t *infeas, int trials,
 }
 
 // ------------------------------------------------------------------ K6 ---
-__global__ void project(int n, const int32_t *cmap, const int32_t *cpart, int32_t *part) {
+__global__ void project(int n, const int32_t *cmap, const part_t *cpart, part_t *part) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     part[i] = cpart[cmap[i]];
 }
 
-__global__ void part_weights(int n, const int32_t *vw, const int32_t *part, int k, int64_t *pw) {
+__global__ void part_weights(int n, const int32_t *vw, const part_t *part, int k, int64_t *pw) {
   __shared__ unsigned long long s[kMaxParts];
   for (int p = threadIdx.x; p < k; p += blockDim.x) s[p] = 0;
   __syncthreads();
@@ -556,95 +553,25 @@ __global__ void part_weights(int n, const int32_t *vw, const int32_t *part, int 
 
 constexpr int kRefWarps = 8;
 
-// Candidate move per vertex: best strictly positive gain into a part that can
-// take it (ties -> smaller part id). Only boundary vertices move.
-__global__ void __launch_bounds__(kRefWarps * 32)
-refine_candidates(G g, const int32_t *part, int k, const int64_t *pw, const int64_t *hi,
-                  const int64_t *lo, int32_t *cand, int32_t *cgain) {
-  __shared__ int32_t conn_s[kRefWarps][kMaxParts];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  int32_t *conn = conn_s[wl];
-  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
-    for (int p = lane; p < k; p += 32) conn[p] = 0;
-    __syncwarp();
-    const int64_t b = g.xbeg[v];
-    const int d = g.deg[v];
-    const int own = part[v];
-    bool boundary = false;
-    for (int j = lane; j < d; j += 32) {
-      int p = part[g.adj[b + j]];
-      boundary |= p != own;
-      atomicAdd(&conn[p], g.wgt[b + j]);
-    }
-    boundary = __any_sync(0xffffffffu, boundary);
-    __syncwarp();
-    int bg = 0, bp = -1;
-    if (boundary) {
-      const int32_t vwv = g.vw[v];
-      const bool can_leave = pw[own] - vwv >= lo[own];
-      for (int p = lane; p < k; p += 32) {
-        if (p == own || !can_leave || pw[p] + vwv > hi[p]) continue;
-        int gain = conn[p] - conn[own];
-        if (gain > bg || (gain == bg && bp >= 0 && p < bp)) { bg = gain; bp = p; }
-      }
-      for (int off = 16; off; off >>= 1) {
-        int og = __shfl_down_sync(0xffffffffu, bg, off);
-        int op = __shfl_down_sync(0xffffffffu, bp, off);
-        if (op >= 0 && (bp < 0 || og > bg || (og == bg && op < bp))) { bg = og; bp = op; }
-      }
-    }
-    if (lane == 0) {
-      cand[v] = (bp >= 0 && bg > 0) ? bp : -1;
-      cgain[v] = bg;
-    }
-    __syncwarp();
-  }
-}
-
-// Jet-style afterburner: re-evaluate each candidate assuming every
-// higher-priority (gain, then smaller id) neighbouring candidate moved.
-// Rejected candidates get cand = -1.
-__global__ void refine_afterburner(G g, const int32_t *part, const int32_t *cand_in,
-                                   const int32_t *cgain, int32_t *cand_out) {
-  const int lane = threadIdx.x & 31;
-  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
-    const int dest = cand_in[v];
-    if (dest < 0) {
-      if (lane == 0) cand_out[v] = -1;
-      continue;
-    }
-    const int own = part[v];
-    const int gv = cgain[v];
-    const int64_t b = g.xbeg[v];
-    const int d = g.deg[v];
-    int delta = 0;
-    for (int j = lane; j < d; j += 32) {
-      int u = g.adj[b + j];
-      int pu = part[u];
-      int cu = cand_in[u];
-      if (cu >= 0) {
-        int gu = cgain[u];
-        if (gu > gv || (gu == gv && u < v)) pu = cu;
-      }
-      int w = g.wgt[b + j];
-      delta += (pu == dest ? w : 0) - (pu == own ? w : 0);
-    }
-    for (int off = 16; off; off >>= 1) delta += __shfl_down_sync(0xffffffffu, delta, off);
-    if (lane == 0) cand_out[v] = delta > 0 ? dest : -1;
-  }
-}
-
 // Rebalance candidates: every vertex of an over-full part proposes its best
 // (max gain, possibly negative) part still below its target.
 __global__ void __launch_bounds__(kRefWarps * 32)
-rebalance_candidates(G g, const int32_t *part, int k, const int64_t *pw, const int64_t *hi,
-                     const int64_t *target, int32_t *cand) {
+rebalance_candidates(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
+                     const int64_t *target, int32_t *cand, const int32_t *run) {
+  if (run && !*run) return;
   __shared__ int32_t conn_s[kRefWarps][kMaxParts];
+  __shared__ int64_t s_pw[kMaxParts], s_hi[kMaxParts], s_t[kMaxParts];
+  for (int p = threadIdx.x; p < k; p += blockDim.x) {
+    s_pw[p] = pw[p];
+    s_hi[p] = hi[p];
+    s_t[p] = target[p];
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   int32_t *conn = conn_s[wl];
   for (int v = warp_id_global(); v < g.n; v += warps_total()) {
     const int own = part[v];
-    if (pw[own] <= hi[own]) {
+    if (s_pw[own] <= s_hi[own]) {
       if (lane == 0) cand[v] = -1;
       continue;
     }
@@ -656,7 +583,7 @@ rebalance_candidates(G g, const int32_t *part, int k, const int64_t *pw, const i
     __syncwarp();
     int bg = INT_MIN, bp = -1;
     for (int p = lane; p < k; p += 32) {
-      if (p == own || pw[p] >= target[p]) continue;
+      if (p == own || s_pw[p] >= s_t[p]) continue;
       int gain = conn[p] - conn[own];
       if (bp < 0 || gain > bg || (gain == bg && p < bp)) { bg = gain; bp = p; }
     }
@@ -671,8 +598,9 @@ rebalance_candidates(G g, const int32_t *part, int k, const int64_t *pw, const i
 }
 
 // flows[p] = weight leaving p, flows[k + q] = weight entering q (planned moves)
-__global__ void move_flows(int n, const int32_t *vw, const int32_t *part, const int32_t *cand,
-                           int k, int64_t *flows, int32_t *nmoves) {
+__global__ void move_flows(int n, const int32_t *vw, const part_t *part, const int32_t *cand,
+                           int k, int64_t *flows, int32_t *nmoves, const int32_t *run) {
+  if (run && !*run) return;
   __shared__ unsigned long long s[2 * kMaxParts];
   __shared__ int s_n;
   for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) s[p] = 0;
@@ -699,16 +627,20 @@ __global__ void move_flows(int n, const int32_t *vw, const int32_t *part, const 
 // decided by a hash of (salt, v) — deterministic thinning that keeps the
 // expected inflow of every part within its room.
 __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, const double *prob,
-                              int k, uint64_t salt, int32_t *part, int64_t *pw) {
+                              int k, uint64_t salt, part_t *part, int64_t *pw,
+                              const int32_t *run) {
+  if (run && !*run) return;
   __shared__ long long s[kMaxParts];
+  __shared__ double s_prob[2 * kMaxParts];
   for (int p = threadIdx.x; p < k; p += blockDim.x) s[p] = 0;
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) s_prob[p] = prob[p];
   __syncthreads();
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     int dest = cand[v];
     if (dest < 0) continue;
     int own = part[v];
-    double pr = prob[own] * prob[k + dest];
+    double pr = s_prob[own] * s_prob[k + dest];
     if (pr < 1.0 && (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
       continue;
     part[v] = dest;
@@ -718,20 +650,6 @@ __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, con
   __syncthreads();
   for (int p = threadIdx.x; p < k; p += blockDim.x)
     if (s[p]) atomicAdd((unsigned long long *)&pw[p], (unsigned long long)s[p]);
-}
-
-__global__ void cut_kernel(G g, const int32_t *part, unsigned long long *cut2) {
-  const int lane = threadIdx.x & 31;
-  unsigned long long local = 0;
-  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
-    const int pv = part[v];
-    const int64_t b = g.xbeg[v];
-    const int d = g.deg[v];
-    for (int j = lane; j < d; j += 32)
-      if (part[g.adj[b + j]] != pv) local += (unsigned long long)g.wgt[b + j];
-  }
-  for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
-  if (lane == 0 && local) atomicAdd(cut2, local);
 }
 
 __global__ void scale_weights(int64_t nnz, const int32_t *in, int32_t *out, int64_t div) {
@@ -746,7 +664,7 @@ __global__ void scale_weights(int64_t nnz, const int32_t *in, int32_t *out, int6
 // ids follow the smallest fine id they contain, so on a task DAG (ids in
 // creation/topological order) this is a layer-band partition.
 __global__ void range_parts(int n, const int64_t *prefix, const int32_t *vw, const double *cum,
-                            int k, int64_t total, int32_t *part) {
+                            int k, int64_t total, part_t *part) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     double mid = ((double)prefix[v] + 0.5 * (double)vw[v]) / (double)total;
@@ -769,6 +687,8 @@ __global__ void seg_bounds(int n, const int64_t *xbeg, const int32_t *deg, int64
     e[i] = xbeg[i] + deg[i];
   }
 }
+
+#include "kway_team.cuh"
 
 // ------------------------------------------------------------ host side ---
 struct Level {
@@ -837,9 +757,15 @@ struct Kway {
           *d_flows = nullptr;
   double *d_prob = nullptr, *d_cum = nullptr;
   int32_t *counter = nullptr;
+  int32_t *ctl = nullptr;   // device control block (see CTL_* in kway_team.cuh)
+  int64_t *d_nnz = nullptr, *h_nnz = nullptr;
+  bool prev_nnz_pending = false;
   std::vector<Level> levels;
   PhaseTimer timer;
-  Kway(cudaStream_t st) : s(st), timer(st) {}
+  int passes_big = 4, passes_small = 8;
+  Kway(cudaStream_t st) : s(st), timer(st) {
+    if (const char *e = getenv("HS_KWAY_PASSES")) passes_big = std::max(1, atoi(e));
+  }
 
   int read_pw(std::vector<int64_t> &pw) {
     pw.resize(k);
@@ -848,7 +774,7 @@ struct Kway {
     return HS_OK;
   }
 
-  int weights(const G &g, const int32_t *part) {
+  int weights(const G &g, const part_t *part) {
     HS_CHECK_CUDA(cudaMemsetAsync(d_pw, 0, k * sizeof(int64_t), s));
     part_weights<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw, part, k, d_pw);
     HS_CHECK_LAUNCH();
@@ -856,102 +782,93 @@ struct Kway {
   }
 
   // plans in `cand` -> thinned application; returns moves planned
-  int apply_plan(const G &g, const int32_t *cand, int32_t *part, bool rebalance,
-                 uint64_t salt2, int32_t *nplanned) {
-    HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
-    HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), s));
-    move_flows<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw, part, cand, k,
-                                                                         d_flows, counter);
-    HS_CHECK_LAUNCH();
-    std::vector<int64_t> fl(2 * k), pw;
-    HS_CHECK_CUDA(cudaMemcpyAsync(fl.data(), d_flows, 2 * k * 8, cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaMemcpyAsync(nplanned, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    int rc = read_pw(pw);
-    if (rc) return rc;
-    if (*nplanned == 0) return HS_OK;
-    std::vector<double> prob(2 * k, 1.0);
-    for (int p = 0; p < k; ++p) {
-      const int64_t out = fl[p], in = fl[k + p];
-      if (rebalance) {
-        if (out > 0) prob[p] = std::min(1.0, (double)(pw[p] - target[p]) / (double)out);
-        if (in > 0) prob[k + p] = std::min(1.0, (double)(target[p] - pw[p]) / (double)in);
-      } else {
-        // keep the expected post-move weight inside [lo, hi]
-        const double room_in = (double)(hi[p] - pw[p]) + 0.0 * out;
-        if (in > 0 && (double)in > room_in) prob[k + p] = std::max(0.0, room_in / (double)in);
-        const double room_out = (double)(pw[p] - lo[p]);
-        if (out > 0 && (double)out > room_out) prob[p] = std::max(0.0, room_out / (double)out);
-      }
-      prob[p] = std::max(0.0, prob[p]);
-      prob[k + p] = std::max(0.0, prob[k + p]);
-    }
-    HS_CHECK_CUDA(cudaMemcpyAsync(d_prob, prob.data(), 2 * k * 8, cudaMemcpyHostToDevice, s));
-    apply_thinned<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
-        g.n, g.vw, cand, d_prob, k, salt2, part, d_pw);
-    HS_CHECK_LAUNCH();
-    return HS_OK;
+  static int team_grid(int64_t n, int T) {
+    int64_t g = (n * T + kTeamBlock - 1) / kTeamBlock;
+    int64_t maxg = (int64_t)hs::sm_count() * 32;
+    return (int)std::max<int64_t>(1, std::min(g, maxg));
   }
 
-  int rebalance(const G &g, int32_t *part, int32_t *cand, uint64_t salt2) {
-    for (int rb = 0; rb < 24; ++rb) {
-      std::vector<int64_t> pw;
-      int rc = read_pw(pw);
-      if (rc) return rc;
-      bool over = false;
-      for (int p = 0; p < k; ++p) over |= pw[p] > hi[p];
-      if (!over) return HS_OK;
-      rebalance_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(
-          g, part, k, d_pw, d_hi, d_target, cand);
+  // Up to `rounds` rebalancing rounds, each gated on the device by "some part
+  // is above its bound" — no host round trip.
+  int rebalance(const G &g, part_t *part, int32_t *cand, uint64_t salt2, int rounds) {
+    const int grid = hs::grid_for(g.n, 256, hs::sm_count() * 4);
+    for (int rb = 0; rb < rounds; ++rb) {
+      balance_check<<<1, 32, 0, s>>>(k, d_pw, d_hi, ctl);
       HS_CHECK_LAUNCH();
-      int32_t planned = 0;
-      rc = apply_plan(g, cand, part, true, salt2 + rb * 7919, &planned);
-      if (rc) return rc;
-      if (!planned) return HS_OK;
+      rebalance_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(
+          g, part, k, d_pw, d_hi, d_target, cand, ctl + CTL_OVER);
+      HS_CHECK_LAUNCH();
+      HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
+      HS_CHECK_CUDA(cudaMemsetAsync(ctl + CTL_NCONF, 0, sizeof(int32_t), s));
+      move_flows<<<grid, 256, 0, s>>>(g.n, g.vw, part, cand, k, d_flows, ctl + CTL_NCONF,
+                                      ctl + CTL_OVER);
+      HS_CHECK_LAUNCH();
+      plan_kernel<<<1, kMaxParts, 0, s>>>(k, g.n, 1, d_flows, d_pw, d_hi, d_lo, d_target, d_prob,
+                                          ctl);
+      HS_CHECK_LAUNCH();
+      apply_thinned<<<grid, 256, 0, s>>>(g.n, g.vw, cand, d_prob, k, salt2 + rb * 7919, part, d_pw,
+                                         ctl + CTL_APPLY);
+      HS_CHECK_LAUNCH();
     }
     return HS_OK;
   }
 
-  int refine(const G &g, int32_t *part, uint64_t salt2, int64_t *passes) {
-    int32_t *cand, *cgain, *cand2;
+  // K6 on one level: fixed pass budget, convergence decided on the device.
+  int refine(const G &g, part_t *part, uint64_t salt2) {
+    int32_t *cand, *list, *conf;
+    uint32_t *st;
     HS_CHECK_CUDA(dalloc(&cand, g.n, s));
-    HS_CHECK_CUDA(dalloc(&cgain, g.n, s));
-    HS_CHECK_CUDA(dalloc(&cand2, g.n, s));
+    HS_CHECK_CUDA(dalloc(&st, g.n, s));
+    HS_CHECK_CUDA(dalloc(&list, g.n, s));
+    HS_CHECK_CUDA(dalloc(&conf, g.n, s));
     int rc = weights(g, part);
     if (rc) return rc;
-    rc = rebalance(g, part, cand, salt2 ^ 0xabcdefull);
+    rc = rebalance(g, part, cand, salt2 ^ 0xabcdefull, 3);
     if (rc) return rc;
-    for (int pass = 0; pass < 10; ++pass) {
+    const int T = team_for(g);
+    const int tgrid = team_grid(g.n, T);
+    const int max_passes = g.nnz > (4ll << 20) ? passes_big : passes_small;
+    const int32_t one = 1;
+    HS_CHECK_CUDA(cudaMemcpyAsync(ctl + CTL_ACTIVE, &one, sizeof one, cudaMemcpyHostToDevice, s));
+    for (int pass = 0; pass < max_passes; ++pass) {
+      HS_CHECK_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int32_t), s));  // list count, nconf
+      HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
       {
         hs::Prof P("refine_candidates", s, 28.0 * g.n + 12.0 * g.nnz);
-        refine_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(
-            g, part, k, d_pw, d_hi, d_lo, cand, cgain);
+        HS_TEAM_DISPATCH(T, refine_cand_t, tgrid, g, part, k, d_pw, d_hi, d_lo, st, list,
+                         ctl + CTL_COUNT, ctl + CTL_ACTIVE);
       }
       HS_CHECK_LAUNCH();
       {
-        hs::Prof P("refine_afterburner", s, 12.0 * g.n);
-        refine_afterburner<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, cand, cgain, cand2);
+        hs::Prof P("refine_afterburner", s, 4.0 * g.n);  // lower bound: list-sized reads
+        HS_TEAM_DISPATCH(T, afterburner_t, tgrid, g, st, list, ctl + CTL_COUNT, k, conf, d_flows,
+                         ctl + CTL_NCONF, ctl + CTL_ACTIVE);
       }
       HS_CHECK_LAUNCH();
-      int32_t planned = 0;
-      rc = apply_plan(g, cand2, part, false, salt2 + pass * 104729, &planned);
-      if (rc) return rc;
-      ++*passes;
-      if ((int64_t)planned * 1000 <= g.n) break;  // < 0.1% of vertices want to move
+      plan_kernel<<<1, kMaxParts, 0, s>>>(k, g.n, 0, d_flows, d_pw, d_hi, d_lo, d_target, d_prob,
+                                          ctl);
+      HS_CHECK_LAUNCH();
+      apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
+          list, ctl + CTL_COUNT, conf, g.vw, d_prob, k, salt2 + pass * 104729, part, d_pw,
+          ctl + CTL_APPLY);
+      HS_CHECK_LAUNCH();
     }
-    rc = rebalance(g, part, cand, salt2 ^ 0x5555ull);
+    rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8);
     cudaFreeAsync(cand, s);
-    cudaFreeAsync(cgain, s);
-    cudaFreeAsync(cand2, s);
+    cudaFreeAsync(st, s);
+    cudaFreeAsync(list, s);
+    cudaFreeAsync(conf, s);
     return rc;
   }
 
-  int64_t cut_of(const G &g, const int32_t *part) {
+  int64_t cut_of(const G &g, const part_t *part) {
     unsigned long long *c2, h = 0;
     if (dalloc(&c2, 1, s) != cudaSuccess) return -1;
     cudaMemsetAsync(c2, 0, 8, s);
     {
       hs::Prof P("cut", s, 16.0 * g.n + 12.0 * g.nnz);
-      cut_kernel<<<warp_grid(g.n, 8), 256, 0, s>>>(g, part, c2);
+      const int T = team_for(g);
+      HS_TEAM_DISPATCH(T, cut_t, team_grid(g.n, T), g, part, c2);
     }
     hs::count_launch();
     cudaMemcpyAsync(&h, c2, 8, cudaMemcpyDeviceToHost, s);
@@ -966,44 +883,59 @@ struct Kway {
     return true;
   }
 
+  // One coarsening level: heavy-edge matching rounds, two-hop pairing,
+  // contraction. Two host round trips: the two-hop list size (CUB sorts take
+  // host counts) and the coarse vertex count (stop test, next sizes).
   int coarsen_once(bool *stop) {
     Level &F = levels.back();
     const int n = F.g.n;
     const int lvl = (int)levels.size();
     const int32_t max_vw = (int32_t)std::max<int64_t>(1, total_vw / (4ll * k));
     int32_t *match, *prop, *fav, *flag, *cid;
+    uint32_t *mw;  // vertex weight | matched bit, gathered once per neighbour
     HS_CHECK_CUDA(dalloc(&match, n, s));
     HS_CHECK_CUDA(dalloc(&prop, n, s));
     HS_CHECK_CUDA(dalloc(&fav, n, s));
     HS_CHECK_CUDA(dalloc(&flag, n + 1, s));
     HS_CHECK_CUDA(dalloc(&cid, n + 1, s));
+    HS_CHECK_CUDA(dalloc(&mw, n, s));
     HS_CHECK_CUDA(cudaMemsetAsync(match, 0xff, n * sizeof(int32_t), s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(mw, F.g.vw, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     const int rounds = 3;
+    const int T = team_for(F.g);
     for (int round = 0; round < rounds; ++round) {
       {
         // round 0 scans every list; later rounds only unmatched vertices (N-bytes bound)
         hs::Prof P(round == 0 ? "match_propose_r0" : "match_propose_rN", s,
-                   round == 0 ? 28.0 * n + 16.0 * F.g.nnz : 28.0 * n);
-        match_propose<<<warp_grid(n, 8), 256, 0, s>>>(F.g, match, prop,
-                                                        round == rounds - 1 ? fav : nullptr,
-                                                        salt + (uint64_t)lvl * 131 + round, max_vw);
+                   round == 0 ? 20.0 * n + 12.0 * F.g.nnz : 20.0 * n);
+        HS_TEAM_DISPATCH(T, propose_t, team_grid(n, T), F.g, mw, prop,
+                         round == rounds - 1 ? fav : nullptr, salt + (uint64_t)lvl * 131 + round,
+                         max_vw);
       }
       HS_CHECK_LAUNCH();
-      match_accept<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, prop, counter);
+      match_accept<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, prop, mw, ctl + 6);
       HS_CHECK_LAUNCH();
     }
+    cudaFreeAsync(mw, s);
     {  // two-hop pairing of leftovers that share a favourite neighbour
       uint64_t *keys, *keys2;
-      int32_t *head, *start;
       HS_CHECK_CUDA(dalloc(&keys, n, s));
       HS_CHECK_CUDA(dalloc(&keys2, n, s));
-      HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), s));
-      twohop_keys<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, fav, keys, counter);
+      HS_CHECK_CUDA(cudaMemsetAsync(ctl + 7, 0, sizeof(int32_t), s));
+      twohop_keys<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, fav, keys, ctl + 7);
       HS_CHECK_LAUNCH();
       int32_t cnt = 0;
-      HS_CHECK_CUDA(cudaMemcpyAsync(&cnt, counter, sizeof cnt, cudaMemcpyDeviceToHost, s));
-      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      HS_CHECK_CUDA(cudaMemcpyAsync(&cnt, ctl + 7, sizeof cnt, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));  // host round trip 1
+      if (prev_nnz_pending) {  // the previous level's live adjacency count has landed
+        levels.back().g.nnz = *h_nnz;
+        prev_nnz_pending = false;
+      }
+      if (timer.on)
+        fprintf(stderr, "[kway] level %d: n=%d nnz=%lld avg_deg=%.1f team=%d twohop=%d\n", lvl - 1, n,
+                (long long)F.g.nnz, n ? (double)F.g.nnz / n : 0.0, T, cnt);
       if (cnt > 1) {
+        int32_t *head, *start;
         size_t tb = 0;
         HS_CHECK_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, keys, keys2, cnt, 0, 64, s));
         {
@@ -1038,7 +970,7 @@ struct Kway {
     if (rc) return rc;
     int32_t nc = 0;
     HS_CHECK_CUDA(cudaMemcpyAsync(&nc, cid + n, sizeof nc, cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));  // host round trip 2
     if (nc > (int64_t)n * 92 / 100) {  // matching stalled: stop coarsening here
       cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
       cudaFreeAsync(flag, s); cudaFreeAsync(cid, s);
@@ -1061,75 +993,78 @@ struct Kway {
     HS_CHECK_CUDA(cudaMemsetAsync(ub + nc, 0, sizeof(int64_t), s));
     rc = exclusive_scan<int64_t>(ub, C.g.xbeg, nc + 1, s);
     if (rc) return rc;
-    int64_t capc = 0;
-    HS_CHECK_CUDA(cudaMemcpyAsync(&capc, C.g.xbeg + nc, sizeof capc, cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    // sum(ub) = live fine entries <= fine capacity: allocate without a round trip
+    const int64_t capc = F.g.cap;
     C.g.cap = capc;
+    C.g.nnz = capc;  // refined below (asynchronously) to the live count
     HS_CHECK_CUDA(dalloc(&C.g.adj, capc, s));
     HS_CHECK_CUDA(dalloc(&C.g.wgt, capc, s));
-    cudaEvent_t ct0 = nullptr, ct1 = nullptr;
-    if (hs::prof_enabled()) {
-      cudaEventCreate(&ct0);
-      cudaEventCreate(&ct1);
-      cudaEventRecord(ct0, s);
+    {
+      hs::Prof P("contract_warp", s, 28.0 * nc + 12.0 * n + 12.0 * F.g.nnz);
+      contract_warp<<<warp_grid(nc, kContractWarps), kContractWarps * 32, 0, s>>>(
+          F.g, F.cmap, mem0, mem1, ub, nc, C.g);
     }
-    contract_warp<<<warp_grid(nc, kContractWarps), kContractWarps * 32, 0, s>>>(
-        F.g, F.cmap, mem0, mem1, ub, nc, C.g);
     HS_CHECK_LAUNCH();
+    // long lists: CTA with a shared-memory table, then global-memory tables;
+    // list sizes stay on the device, the CTA kernels read them there
     const int smem_slots = 8192;
-    int32_t *list;
+    int32_t *list, *ncd;
     HS_CHECK_CUDA(dalloc(&list, nc, s));
-    int32_t cnt[2] = {0, 0};
-    HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, 2 * sizeof(int32_t), s));
-    classify_long<<<hs::grid_for(nc, 256), 256, 0, s>>>(ub, nc, kWarpSlots, smem_slots, list, counter);
+    HS_CHECK_CUDA(dalloc(&ncd, 1, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(ncd, cid + n, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    HS_CHECK_CUDA(cudaMemsetAsync(ctl + 8, 0, 2 * sizeof(int32_t), s));
+    classify_long<<<hs::grid_for(nc, 256), 256, 0, s>>>(ub, ncd, kWarpSlots, smem_slots, list,
+                                                        ctl + 8);
     HS_CHECK_LAUNCH();
-    HS_CHECK_CUDA(cudaMemcpyAsync(cnt, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaStreamSynchronize(s));
-    if (cnt[0]) {
+    {
       size_t smem = 2 * smem_slots * sizeof(int32_t);
       cudaFuncSetAttribute(contract_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      contract_block<<<std::min(cnt[0], hs::sm_count() * 2), 512, smem, s>>>(
-          F.g, F.cmap, mem0, mem1, ub, list, cnt[0], C.g, nullptr, nullptr, smem_slots);
-      HS_CHECK_LAUNCH();
+      hs::Prof P("contract_block_smem", s, 0.0);
+      contract_block<<<hs::sm_count() * 2, 512, smem, s>>>(F.g, F.cmap, mem0, mem1, ub, list,
+                                                          ctl + 8, C.g, nullptr, nullptr,
+                                                          smem_slots);
     }
-    HS_CHECK_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), s));
-    classify_long<<<hs::grid_for(nc, 256), 256, 0, s>>>(ub, nc, smem_slots, INT64_MAX / 4, list,
-                                                        counter);
     HS_CHECK_LAUNCH();
-    HS_CHECK_CUDA(cudaMemcpyAsync(cnt + 1, counter, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaStreamSynchronize(s));
-    if (cnt[1]) {
+    int32_t *list2;
+    HS_CHECK_CUDA(dalloc(&list2, nc, s));
+    classify_long<<<hs::grid_for(nc, 256), 256, 0, s>>>(ub, ncd, smem_slots, INT64_MAX / 4, list2,
+                                                        ctl + 9);
+    HS_CHECK_LAUNCH();
+    {
       int32_t *gk, *gv;
       HS_CHECK_CUDA(dalloc(&gk, 2 * capc, s));
       HS_CHECK_CUDA(dalloc(&gv, 2 * capc, s));
-      contract_block<<<std::min(cnt[1], hs::sm_count() * 2), 1024, 0, s>>>(
-          F.g, F.cmap, mem0, mem1, ub, list, cnt[1], C.g, gk, gv, 0);
-      HS_CHECK_LAUNCH();
+      hs::Prof P("contract_block_global", s, 0.0);
+      contract_block<<<hs::sm_count() * 2, 1024, 0, s>>>(F.g, F.cmap, mem0, mem1, ub, list2,
+                                                         ctl + 9, C.g, gk, gv, 0);
       cudaFreeAsync(gk, s);
       cudaFreeAsync(gv, s);
     }
-    if (ct0) cudaEventRecord(ct1, s);
-    {  // live adjacency entries of the coarse level
-      int64_t *dsum;
-      HS_CHECK_CUDA(dalloc(&dsum, 1, s));
+    HS_CHECK_LAUNCH();
+    {  // live adjacency entries of the coarse level, read at the next round trip
       size_t tb = 0;
-      HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, C.g.deg, dsum, nc, s));
+      HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, C.g.deg, d_nnz, nc, s));
       hs::Scratch<char> tmp;
       HS_CHECK_CUDA(tmp.alloc(tb, s));
-      HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, C.g.deg, dsum, nc, s));
-      HS_CHECK_CUDA(cudaMemcpyAsync(&C.g.nnz, dsum, 8, cudaMemcpyDeviceToHost, s));
-      HS_CHECK_CUDA(cudaStreamSynchronize(s));
-      cudaFreeAsync(dsum, s);
+      HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, C.g.deg, d_nnz, nc, s));
+      HS_CHECK_CUDA(cudaMemcpyAsync(h_nnz, d_nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      prev_nnz_pending = true;
       hs::count_launch(1);
     }
-    if (ct0)
-      hs::prof_record("contract", ct0, ct1,
-                      28.0 * nc + 12.0 * n + 12.0 * F.g.nnz + 8.0 * C.g.nnz);
-    cudaFreeAsync(list, s);
+    cudaFreeAsync(list, s); cudaFreeAsync(list2, s); cudaFreeAsync(ncd, s);
     cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
     cudaFreeAsync(flag, s); cudaFreeAsync(cid, s); cudaFreeAsync(mem0, s);
     cudaFreeAsync(mem1, s); cudaFreeAsync(ub, s);
     levels.push_back(C);
+    return HS_OK;
+  }
+
+  // Lands the last pending live-entry count (after the final coarsening level).
+  int settle_nnz() {
+    if (!prev_nnz_pending) return HS_OK;
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    levels.back().g.nnz = *h_nnz;
+    prev_nnz_pending = false;
     return HS_OK;
   }
 
@@ -1166,11 +1101,11 @@ struct Kway {
     return HS_OK;
   }
 
-  int initial(int32_t **out_part) {
+  int initial(part_t **out_part) {
     Level &Cst = levels.back();
     G &g = Cst.g;
     const int nc = g.n;
-    int32_t *best;
+    part_t *best;
     HS_CHECK_CUDA(dalloc(&best, nc, s));
     // trial 0: id-range bands
     {
@@ -1220,8 +1155,8 @@ struct Kway {
       HS_CHECK_CUDA(cudaStreamSynchronize(s));
       bool tf = binf == 0;
       if ((tf && !best_feas) || (tf == best_feas && bcut < best_cut)) {
-        int8_to_int32<<<hs::grid_for(nc, 256), 256, 0, s>>>(IA.parts + (int64_t)bti * nc, nc, best);
-        HS_CHECK_LAUNCH();
+        HS_CHECK_CUDA(cudaMemcpyAsync(best, IA.parts + (int64_t)bti * nc, nc,
+                                      cudaMemcpyDeviceToDevice, s));
       }
       cudaFreeAsync(IA.parts, s); cudaFreeAsync(IA.order, s); cudaFreeAsync(IA.seen, s);
       cudaFreeAsync(IA.cut, s); cudaFreeAsync(IA.infeas, s); cudaFreeAsync(bt, s);
@@ -1357,6 +1292,10 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   HS_CHECK_CUDA(dalloc(&K.d_prob, 2 * k, s));
   HS_CHECK_CUDA(dalloc(&K.d_cum, k + 1, s));
   HS_CHECK_CUDA(dalloc(&K.counter, 4, s));
+  HS_CHECK_CUDA(dalloc(&K.ctl, 16, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(K.ctl, 0, 16 * sizeof(int32_t), s));
+  HS_CHECK_CUDA(dalloc(&K.d_nnz, 1, s));
+  HS_CHECK_CUDA(cudaMallocHost((void **)&K.h_nnz, sizeof(int64_t)));
   HS_CHECK_CUDA(cudaMemcpyAsync(K.d_hi, K.hi.data(), k * 8, cudaMemcpyHostToDevice, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(K.d_lo, K.lo.data(), k * 8, cudaMemcpyHostToDevice, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(K.d_target, K.target.data(), k * 8, cudaMemcpyHostToDevice, s));
@@ -1366,54 +1305,81 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   // ---- coarsening ----
   const int coarse_target = std::max(64 * k, 1024);
   bool stop = false;
+  // Coarsening also stops once the coarse graph turns dense (average degree
+  // above max_deg): on random-like DAGs the edge count stops shrinking while
+  // every further level costs a full pass over ~all edges.
+  // Default: 1.5x the finest level's average degree (edges no longer shrink
+  // with the vertices, so matching has no locality left to exploit).
+  const double deg0 = n0 ? (double)nnz0 / (double)n0 : 0.0;
+  double max_deg = std::max(16.0, 1.5 * deg0);
+  if (const char *e = getenv("HS_KWAY_MAXDEG")) max_deg = atof(e);
   while (!stop && K.levels.back().g.n > coarse_target && (int)K.levels.size() < 40) {
+    if (K.levels.size() > 1) {
+      int rc0 = K.settle_nnz();
+      if (rc0) return rc0;
+      const G &cg = K.levels.back().g;
+      if ((double)cg.nnz > max_deg * (double)cg.n) break;
+    }
+    const bool ncu_win = K.levels.size() == 1 && getenv("HS_NCU_COARSEN0") != nullptr;
+    if (ncu_win) cudaProfilerStart();
     int rc = K.coarsen_once(&stop);
+    if (ncu_win) cudaProfilerStop();
     if (rc) return rc;
     K.timer.mark("coarsen level");
   }
 
+  {
+    int rc = K.settle_nnz();
+    if (rc) return rc;
+  }
   // ---- initial partition ----
-  int32_t *cur = nullptr;
+  part_t *cur = nullptr;
   int rc = K.initial(&cur);
   if (rc) return rc;
   K.timer.mark("initial partition");
   const int coarsest_n = K.levels.back().g.n;
 
   // ---- uncoarsening + refinement ----
-  int64_t passes = 0;
   for (int li = (int)K.levels.size() - 1; li >= 0; --li) {
     Level &Lv = K.levels[li];
     if (li != (int)K.levels.size() - 1) {
-      int32_t *pf = li == 0 ? part_out : nullptr;
-      if (!pf) HS_CHECK_CUDA(dalloc(&pf, Lv.g.n, s));
+      part_t *pf;
+      HS_CHECK_CUDA(dalloc(&pf, Lv.g.n, s));
       project<<<hs::grid_for(Lv.g.n, 256), 256, 0, s>>>(Lv.g.n, Lv.cmap, cur, pf);
       HS_CHECK_LAUNCH();
       cudaFreeAsync(cur, s);
       cur = pf;
     }
-    rc = K.refine(Lv.g, cur, K.salt ^ ((uint64_t)li << 40), &passes);
+    // HS_NCU_LEVEL0=1: open the profiler window around the finest level only
+    const bool ncu_win = li == 0 && getenv("HS_NCU_LEVEL0") != nullptr;
+    if (ncu_win) cudaProfilerStart();
+    rc = K.refine(Lv.g, cur, K.salt ^ ((uint64_t)li << 40));
+    if (ncu_win) cudaProfilerStop();
     if (rc) return rc;
     K.timer.mark("refine level");
   }
-  if (cur != part_out) {  // single-level case: the coarsest graph is the input
-    HS_CHECK_CUDA(cudaMemcpyAsync(part_out, cur, n0 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    cudaFreeAsync(cur, s);
-  }
+  int8_to_int32<<<hs::grid_for(n0, 256), 256, 0, s>>>(cur, n0, part_out);
+  HS_CHECK_LAUNCH();
 
   // ---- statistics (cut with the caller's unscaled weights) ----
   G g0 = K.levels[0].g;  // the caller's arrays and unscaled weights
   g0.adj = const_cast<int32_t *>(ug->adjncy);
   g0.wgt = const_cast<int32_t *>(ug->adjwgt_i);
-  int64_t cut = K.cut_of(g0, part_out);
+  int64_t cut = K.cut_of(g0, cur);
   std::vector<int64_t> pw;
-  rc = K.weights(g0, part_out);
+  rc = K.weights(g0, cur);
   if (rc) return rc;
   rc = K.read_pw(pw);
   if (rc) return rc;
+  cudaFreeAsync(cur, s);
   K.timer.mark("stats");
   double maxdev = 0;
   for (int p = 0; p < k; ++p)
     maxdev = std::max(maxdev, fabs((double)pw[p] / (double)K.total_vw - tpwgts_host[p]));
+  int32_t ctl_h[16];
+  HS_CHECK_CUDA(cudaMemcpyAsync(ctl_h, K.ctl, sizeof ctl_h, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  const int64_t passes = ctl_h[CTL_PASSES];
   if (stats_host) {
     stats_host[0] = cut;
     stats_host[1] = (int64_t)K.levels.size();
@@ -1435,5 +1401,7 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   cudaFreeAsync(K.d_hi, s); cudaFreeAsync(K.d_lo, s); cudaFreeAsync(K.d_target, s);
   cudaFreeAsync(K.d_pw, s); cudaFreeAsync(K.d_flows, s); cudaFreeAsync(K.d_prob, s);
   cudaFreeAsync(K.d_cum, s); cudaFreeAsync(K.counter, s);
+  cudaFreeAsync(K.ctl, s); cudaFreeAsync(K.d_nnz, s);
+  cudaFreeHost(K.h_nnz);
   return HS_OK;
 }
