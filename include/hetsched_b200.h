@@ -232,10 +232,12 @@ int hs_partition_kway(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host
  * hs_partition_kway (K1): root and root edges dropped, vertex v (kernel
  * position) adjacent to every predecessor and successor, adjwgt_i from
  * edge_w_i (out order), vwgt_i copied from node_w_i (node index space).
+ * edge_w_i_in (optional) holds the same weights in in-order (the DAG's CSC
+ * copy of the edge attribute); without it they are gathered via in_eid.
  * xadj/adjncy/adjwgt_i/vwgt_i are caller buffers sized (n-1)+1 / 2m. */
-int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *node_w_i,
-                  int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i,
-                  int64_t *nnz_host, void *stream);
+int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *edge_w_i_in,
+                  const int32_t *node_w_i, int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i,
+                  int32_t *vwgt_i, int64_t *nnz_host, void *stream);
 
 /* Device generator of the layered fan-in DAG family of configs 2 and 4:
  * n kernels over ceil(sqrt(n)) layers, m inter-kernel edges spread as evenly

@@ -90,46 +90,56 @@ __device__ __forceinline__ int warp_id_global() {
 __device__ __forceinline__ int warps_total() { return (int)(((int64_t)gridDim.x * blockDim.x) >> 5); }
 
 // ------------------------------------------------------------------ K1 ---
+// Position of the root in v's ascending in-list, or -1 (a DAG has at most
+// one root edge per node).
+__device__ __forceinline__ int64_t root_slot(const hs_dag_t &g, int v) {
+  int64_t lo = g.in_ptr[v], hi = g.in_ptr[v + 1];
+  while (lo < hi) {  // lower_bound(root)
+    int64_t mid = (lo + hi) >> 1;
+    if (g.in_src[mid] < g.root) lo = mid + 1; else hi = mid;
+  }
+  return (lo < g.in_ptr[v + 1] && g.in_src[lo] == g.root) ? lo : -1;
+}
+
 __global__ void sym_degree(hs_dag_t g, int32_t *deg) {
-  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n;
+       v += (int64_t)gridDim.x * blockDim.x) {
     if (v == g.root) continue;
-    const int lane = threadIdx.x & 31;
-    int cnt = 0;
-    for (int64_t j = g.in_ptr[v] + lane; j < g.in_ptr[v + 1]; j += 32) cnt += g.in_src[j] != g.root;
-    for (int off = 16; off; off >>= 1) cnt += __shfl_down_sync(0xffffffffu, cnt, off);
-    if (lane == 0) {
-      int kv = v < g.root ? v : v - 1;
-      deg[kv] = cnt + (int)(g.out_ptr[v + 1] - g.out_ptr[v]);
-    }
+    const int kv = v < g.root ? (int)v : (int)v - 1;
+    deg[kv] = (int)(g.in_ptr[v + 1] - g.in_ptr[v]) - (root_slot(g, (int)v) >= 0 ? 1 : 0) +
+              (int)(g.out_ptr[v + 1] - g.out_ptr[v]);
   }
 }
 
-__global__ void sym_fill(hs_dag_t g, const int32_t *ew, const int32_t *nw, const int64_t *xadj,
-                         int32_t *adj, int32_t *wgt, int32_t *vw) {
-  const int lane = threadIdx.x & 31;
-  for (int v = warp_id_global(); v < g.n; v += warps_total()) {
-    if (v == g.root) continue;
+// Team of 8 lanes per vertex: in-neighbours (root dropped) then
+// out-neighbours. ew_in (in-order weights) avoids a random gather through
+// in_eid when the caller has it; otherwise the weight is gathered.
+__global__ void sym_fill(hs_dag_t g, const int32_t *ew, const int32_t *ew_in, const int32_t *nw,
+                         const int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw) {
+  constexpr int T = 8;
+  const int lane = (threadIdx.x & 31) % T;
+  const int64_t step = (int64_t)warps_total() * (32 / T);
+  for (int64_t vb = (int64_t)warp_id_global() * (32 / T); vb < g.n; vb += step) {
+    const int v = (int)(vb + (threadIdx.x & 31) / T);
+    if (v >= g.n || v == g.root) continue;
     const int kv = v < g.root ? v : v - 1;
-    int64_t pos = xadj[kv];
+    const int64_t pos = xadj[kv];
     if (lane == 0) vw[kv] = nw[v];
-    for (int64_t b = g.in_ptr[v]; b < g.in_ptr[v + 1]; b += 32) {
-      int64_t j = b + lane;
-      int u = -1;
-      if (j < g.in_ptr[v + 1]) u = g.in_src[j];
-      bool keep = u >= 0 && u != g.root;
-      unsigned m = __ballot_sync(0xffffffffu, keep);
-      if (keep) {
-        int64_t at = pos + __popc(m & ((1u << lane) - 1));
-        adj[at] = u < g.root ? u : u - 1;
-        wgt[at] = ew[g.in_eid[j]];
-      }
-      pos += __popc(m);
+    const int64_t i0 = g.in_ptr[v], i1 = g.in_ptr[v + 1];
+    const int64_t rs = root_slot(g, v);
+    for (int64_t j = i0 + lane; j < i1; j += T) {
+      if (j == rs) continue;
+      const int u = g.in_src[j];
+      const int64_t at = pos + (j - i0) - (rs >= 0 && j > rs ? 1 : 0);
+      adj[at] = u < g.root ? u : u - 1;
+      wgt[at] = ew_in ? ew_in[j] : ew[g.in_eid[j]];
     }
+    const int64_t opos = pos + (i1 - i0) - (rs >= 0 ? 1 : 0);
     const int64_t o0 = g.out_ptr[v], o1 = g.out_ptr[v + 1];
-    for (int64_t j = o0 + lane; j < o1; j += 32) {
-      int u = g.out_dst[j];
-      adj[pos + (j - o0)] = u < g.root ? u : u - 1;
-      wgt[pos + (j - o0)] = ew[j];
+    for (int64_t j = o0 + lane; j < o1; j += T) {
+      const int u = g.out_dst[j];
+      adj[opos + (j - o0)] = u < g.root ? u : u - 1;
+      wgt[opos + (j - o0)] = ew[j];
     }
   }
 }
@@ -195,11 +205,10 @@ __global__ void match_accept(int n, int32_t *match, const int32_t *prop, uint32_
     if (match[u] < 0 && v >= 0 && prop[v] == (int)u) {
       match[u] = v;
       mw[u] |= 0x80000000u;
-      ++local;
     }
   }
-  for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
-  if ((threadIdx.x & 31) == 0 && local) atomicAdd(nmatched, local);
+  (void)local;
+  (void)nmatched;
 }
 
 // ------------------------------------------------------------------ K4 ---
@@ -234,8 +243,8 @@ __device__ __forceinline__ uint32_t slot_hash(int key, uint32_t mask) {
 }
 
 // warp per coarse vertex, table of pow2 >= 2*ub slots in shared memory
-constexpr int kWarpSlots = 1024;  // per warp
-constexpr int kContractWarps = 4;
+constexpr int kWarpSlots = 256;  // per warp: lists up to 128 entries (level 0 is ~40)
+constexpr int kContractWarps = 8;
 
 __global__ void __launch_bounds__(kContractWarps * 32)
 contract_warp(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1,
@@ -539,13 +548,23 @@ __global__ void project(int n, const int32_t *cmap, const part_t *cpart, part_t 
     part[i] = cpart[cmap[i]];
 }
 
+// Per-part weight sums: one warp-wide __reduce_add per part per 32 vertices
+// (shared-memory atomics here serialised: neighbouring ids share a part).
 __global__ void part_weights(int n, const int32_t *vw, const part_t *part, int k, int64_t *pw) {
   __shared__ unsigned long long s[kMaxParts];
   for (int p = threadIdx.x; p < k; p += blockDim.x) s[p] = 0;
   __syncthreads();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&s[part[i]], (unsigned long long)vw[i]);
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const int p = i < n ? part[i] : -1;
+    const unsigned w = i < n ? (unsigned)vw[i] : 0u;  // 32 x vw < 2^31
+    for (int q = 0; q < k; ++q) {
+      const unsigned sum = __reduce_add_sync(0xffffffffu, p == q ? w : 0u);
+      if (lane == 0 && sum) atomicAdd(&s[q], (unsigned long long)sum);
+    }
+  }
   __syncthreads();
   for (int p = threadIdx.x; p < k; p += blockDim.x)
     if (s[p]) atomicAdd((unsigned long long *)&pw[p], s[p]);
@@ -690,6 +709,20 @@ __global__ void seg_bounds(int n, const int64_t *xbeg, const int32_t *deg, int64
 
 #include "kway_team.cuh"
 
+// max over vertices of the weighted degree (saturating at 2^30)
+__global__ void max_wdeg_kernel(G g, int32_t *out) {
+  int local = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    int64_t sum = 0;
+    const int64_t b = g.xbeg[v];
+    for (int j = 0; j < g.deg[v] && sum < (1 << 30); ++j) sum += g.wgt[b + j];
+    local = max(local, (int)(sum < (1 << 30) ? sum : (1 << 30)));
+  }
+  for (int off = 16; off; off >>= 1) local = max(local, __shfl_down_sync(0xffffffffu, local, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, local);
+}
+
 // ------------------------------------------------------------ host side ---
 struct Level {
   G g;
@@ -828,6 +861,18 @@ struct Kway {
     const int T = team_for(g);
     const int tgrid = team_grid(g.n, T);
     const int max_passes = g.nnz > (4ll << 20) ? passes_big : passes_small;
+    // 16-bit packed connectivity counters are exact iff every vertex's
+    // weighted degree stays below 2^16 on this level
+    bool pack16 = false;
+    {
+      HS_CHECK_CUDA(cudaMemsetAsync(ctl + 12, 0, sizeof(int32_t), s));
+      max_wdeg_kernel<<<hs::grid_for(g.n, 256, hs::sm_count() * 8), 256, 0, s>>>(g, ctl + 12);
+      HS_CHECK_LAUNCH();
+      int32_t mx = 0;
+      HS_CHECK_CUDA(cudaMemcpyAsync(&mx, ctl + 12, sizeof mx, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      pack16 = mx < 65536;
+    }
     const int32_t one = 1;
     HS_CHECK_CUDA(cudaMemcpyAsync(ctl + CTL_ACTIVE, &one, sizeof one, cudaMemcpyHostToDevice, s));
     for (int pass = 0; pass < max_passes; ++pass) {
@@ -835,8 +880,8 @@ struct Kway {
       HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
       {
         hs::Prof P("refine_candidates", s, 28.0 * g.n + 12.0 * g.nnz);
-        HS_TEAM_DISPATCH(T, refine_cand_t, tgrid, g, part, k, d_pw, d_hi, d_lo, st, list,
-                         ctl + CTL_COUNT, ctl + CTL_ACTIVE);
+        HS_REFINE_DISPATCH(T, k, pack16, tgrid, g, part, k, d_pw, d_hi, d_lo, st, list,
+                           ctl + CTL_COUNT, ctl + CTL_ACTIVE);
       }
       HS_CHECK_LAUNCH();
       {
@@ -1031,14 +1076,12 @@ struct Kway {
                                                         ctl + 9);
     HS_CHECK_LAUNCH();
     {
-      int32_t *gk, *gv;
-      HS_CHECK_CUDA(dalloc(&gk, 2 * capc, s));
-      HS_CHECK_CUDA(dalloc(&gv, 2 * capc, s));
+      int32_t *gk = nullptr, *gv = nullptr;
+      int rc2 = global_tables(2 * capc, &gk, &gv);
+      if (rc2) return rc2;
       hs::Prof P("contract_block_global", s, 0.0);
       contract_block<<<hs::sm_count() * 2, 1024, 0, s>>>(F.g, F.cmap, mem0, mem1, ub, list2,
                                                          ctl + 9, C.g, gk, gv, 0);
-      cudaFreeAsync(gk, s);
-      cudaFreeAsync(gv, s);
     }
     HS_CHECK_LAUNCH();
     {  // live adjacency entries of the coarse level, read at the next round trip
@@ -1056,6 +1099,25 @@ struct Kway {
     cudaFreeAsync(flag, s); cudaFreeAsync(cid, s); cudaFreeAsync(mem0, s);
     cudaFreeAsync(mem1, s); cudaFreeAsync(ub, s);
     levels.push_back(C);
+    return HS_OK;
+  }
+
+  // Grow-only device scratch for the global-memory hash tables of the
+  // longest lists (kept across calls: re-reserving GBs per call stalls).
+  int global_tables(int64_t slots, int32_t **keys, int32_t **vals) {
+    static int32_t *gk = nullptr, *gv = nullptr;
+    static int64_t have = 0;
+    if (slots > have) {
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      if (gk) cudaFree(gk);
+      if (gv) cudaFree(gv);
+      gk = gv = nullptr;
+      HS_CHECK_CUDA(cudaMalloc((void **)&gk, slots * sizeof(int32_t)));
+      HS_CHECK_CUDA(cudaMalloc((void **)&gv, slots * sizeof(int32_t)));
+      have = slots;
+    }
+    *keys = gk;
+    *vals = gv;
     return HS_OK;
   }
 
@@ -1168,9 +1230,10 @@ struct Kway {
 
 }  // namespace
 
-extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *node_w_i,
-                             int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i,
-                             int64_t *nnz_host, void *stream) {
+extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i,
+                             const int32_t *edge_w_i_in, const int32_t *node_w_i, int64_t *xadj,
+                             int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int64_t *nnz_host,
+                             void *stream) {
   HS_REQUIRE(g && edge_w_i && node_w_i && xadj && adjncy && adjwgt_i && vwgt_i, HS_EINVAL,
              "hs_symmetrize: null argument");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1179,16 +1242,17 @@ extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const i
   hs::Scratch<int64_t> deg64;
   HS_CHECK_CUDA(deg.alloc(nk + 1, s));
   HS_CHECK_CUDA(deg64.alloc(nk + 1, s));
-  hs::Prof P("symmetrize", s, 32.0 * g->n + 36.0 * g->m);
-  sym_degree<<<warp_grid(g->n, 8), 256, 0, s>>>(*g, deg);
+  // in/out pointers, in_src/out_dst, weights (in + out order), adj+wgt writes
+  hs::Prof P("symmetrize", s, 32.0 * g->n + 32.0 * g->m);
+  sym_degree<<<hs::grid_for(g->n, 256), 256, 0, s>>>(*g, deg);
   HS_CHECK_LAUNCH();
   HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nk, 0, sizeof(int64_t), s));
   int rc = hs_widen32(deg, deg64, nk, s);
   if (rc) return rc;
   rc = exclusive_scan<int64_t>(deg64, xadj, nk + 1, s);
   if (rc) return rc;
-  sym_fill<<<warp_grid(g->n, 8), 256, 0, s>>>(*g, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i,
-                                               vwgt_i);
+  sym_fill<<<std::max(1, std::min(hs::sm_count() * 32, (g->n * 8 + 255) / 256)), 256, 0, s>>>(
+      *g, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i);
   HS_CHECK_LAUNCH();
   if (nnz_host) {
     HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nk, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1293,9 +1357,13 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   HS_CHECK_CUDA(dalloc(&K.d_cum, k + 1, s));
   HS_CHECK_CUDA(dalloc(&K.counter, 4, s));
   HS_CHECK_CUDA(dalloc(&K.ctl, 16, s));
-  HS_CHECK_CUDA(cudaMemsetAsync(K.ctl, 0, 16 * sizeof(int32_t), s));
+  HS_CHECK_CUDA(cudaMemsetAsync(K.ctl, 0, 16 * sizeof(int32_t), s));  // ctl[12]: max wdeg
   HS_CHECK_CUDA(dalloc(&K.d_nnz, 1, s));
-  HS_CHECK_CUDA(cudaMallocHost((void **)&K.h_nnz, sizeof(int64_t)));
+  {  // one pinned word for the whole process (cudaFreeHost would sync the device)
+    static int64_t *pinned = nullptr;
+    if (!pinned) HS_CHECK_CUDA(cudaMallocHost((void **)&pinned, sizeof(int64_t)));
+    K.h_nnz = pinned;
+  }
   HS_CHECK_CUDA(cudaMemcpyAsync(K.d_hi, K.hi.data(), k * 8, cudaMemcpyHostToDevice, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(K.d_lo, K.lo.data(), k * 8, cudaMemcpyHostToDevice, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(K.d_target, K.target.data(), k * 8, cudaMemcpyHostToDevice, s));
@@ -1402,6 +1470,6 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   cudaFreeAsync(K.d_pw, s); cudaFreeAsync(K.d_flows, s); cudaFreeAsync(K.d_prob, s);
   cudaFreeAsync(K.d_cum, s); cudaFreeAsync(K.counter, s);
   cudaFreeAsync(K.ctl, s); cudaFreeAsync(K.d_nnz, s);
-  cudaFreeHost(K.h_nnz);
+
   return HS_OK;
 }

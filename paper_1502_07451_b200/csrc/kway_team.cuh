@@ -51,6 +51,35 @@ __device__ __forceinline__ void warp_append(bool take, int value, int32_t *list,
 }
 
 constexpr int kTeamBlock = 256;
+constexpr int kAppendBuf = 256;  // per-warp staging slots for list appends
+
+// Per-warp staged append: entries gather in shared memory and are flushed to
+// the global list with one atomic per ~kAppendBuf entries (a global atomic
+// per warp-iteration made the list counter an L2 hotspot).
+struct WarpAppender {
+  int32_t *buf;  // kAppendBuf slots of this warp
+  int n = 0;     // warp-uniform fill level
+  __device__ void push(bool take, int value, int32_t *list, int32_t *count) {
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    if (n + 32 > kAppendBuf) flush(list, count);
+    if (take) buf[n + __popc(m & ((1u << lane) - 1))] = value;
+    n += __popc(m);
+    __syncwarp();
+  }
+  __device__ void flush(int32_t *list, int32_t *count) {
+    if (!n) return;
+    const int lane = threadIdx.x & 31;
+    __syncwarp();
+    int base = 0;
+    if (lane == 0) base = atomicAdd(count, n);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int i = lane; i < n; i += 32) list[base + i] = buf[i];
+    n = 0;
+    __syncwarp();
+  }
+};
 
 // Per-vertex refinement state packed in one word so the afterburner gathers
 // 4 bytes per neighbour: part (bits 0-6), candidate part + 1 (bits 7-13, 0 =
@@ -65,59 +94,116 @@ __device__ __forceinline__ int st_gain(uint32_t s) { return (int)(s >> 14); }
 
 // Candidate move per vertex (K6): best strictly positive gain into a part that
 // can take it; candidates are appended to `list`.
-template <int T>
+// KR > 0: per-part connectivity lives in KR registers per lane (k <= KR),
+// summed across the team with xor shuffles — no shared-memory atomics (those
+// serialised whenever a vertex's neighbours share a part, the common case).
+// KR == 0: shared-memory accumulators for larger k.
+template <int T, int KR>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, uint32_t *st, int32_t *list, int32_t *count, const int32_t *run) {
   if (run && !*run) return;
-  __shared__ int32_t conn_s[kTeamBlock / T][kMaxParts];
+  __shared__ int32_t conn_s[KR > 0 ? 1 : kTeamBlock / T][kMaxParts];
   // part weights and bounds are read for every vertex: keep them on chip
   // (global reads of these few lines made one L2 slice the bottleneck)
   __shared__ int64_t s_pw[kMaxParts], s_hi[kMaxParts], s_lo[kMaxParts];
+  __shared__ int32_t s_app[kTeamBlock / 32][kAppendBuf];
   for (int p = threadIdx.x; p < k; p += blockDim.x) {
     s_pw[p] = pw[p];
     s_hi[p] = hi[p];
     s_lo[p] = lo[p];
   }
   __syncthreads();
+  WarpAppender app{s_app[threadIdx.x >> 5]};
   const int lane = team_lane<T>();
-  int32_t *conn = conn_s[threadIdx.x / T];
   const int64_t step = (int64_t)warps_total() * (32 / T);
   for (int64_t vb = (int64_t)warp_id_global() * (32 / T); vb < g.n; vb += step) {
     const int v = (int)(vb + (threadIdx.x & 31) / T);
     const bool valid = v < g.n;
-    for (int p = lane; p < k; p += T) conn[p] = 0;
-    __syncwarp();
-    int own = 0, bnd = 0;
+    int own = 0, bnd = 0, bg = 0, bp = -1;
+    int32_t vwv = 0;
+    int64_t b = 0;
+    int d = 0;
     if (valid) {
       own = part[v];
-      const int64_t b = g.xbeg[v];
-      const int d = g.deg[v];
+      vwv = g.vw[v];
+      b = g.xbeg[v];
+      d = g.deg[v];
+    }
+    if constexpr (KR > 0) {
+      // PK = 2: two 16-bit counters per register (host guarantees every
+      // vertex's weighted degree < 2^16 on this level); PK = 1: 32-bit.
+      constexpr int PK = KR == 8 ? 2 : 1;
+      constexpr int NR = KR / PK;
+      uint32_t c[NR];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) c[i] = 0;
+      // 4 neighbours per lane in flight: independent adj loads, then gathers
+      for (int j0 = lane; j0 < d; j0 += 4 * T) {
+        int u[4], w[4], p[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j0 + q * T;
+          u[q] = j < d ? __ldg(g.adj + b + j) : -1;
+          w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : own;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          bnd |= p[q] != own;
+          const int idx = PK == 2 ? (p[q] >> 1) : p[q];
+          const uint32_t val = PK == 2 ? ((uint32_t)w[q] << ((p[q] & 1) << 4)) : (uint32_t)w[q];
+#pragma unroll
+          for (int i = 0; i < NR; ++i) c[i] += (idx == i) ? val : 0u;
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < NR; ++i)
+        for (int off = T / 2; off; off >>= 1) c[i] += __shfl_xor_sync(0xffffffffu, c[i], off, T);
+      bnd = team_or<T>(bnd);
+      // lane q of the team evaluates parts q, q+T, ... (T >= 8 >= k for KR = 8)
+      auto conn_of = [&](int p) -> int {
+        uint32_t r = 0;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) r = ((PK == 2 ? (p >> 1) : p) == i) ? c[i] : r;
+        return PK == 2 ? (int)((r >> ((p & 1) << 4)) & 0xffffu) : (int)r;
+      };
+      if (valid && bnd && s_pw[own] - vwv >= s_lo[own]) {
+        const int cown = conn_of(own);
+        for (int pp = lane; pp < k; pp += T) {
+          if (pp == own || s_pw[pp] + vwv > s_hi[pp]) continue;
+          const int gain = conn_of(pp) - cown;
+          if (gain > bg || (gain == bg && bp >= 0 && pp < bp)) { bg = gain; bp = pp; }
+        }
+      }
+      team_argmax<T>(bg, bp);
+    } else {
+      int32_t *conn = conn_s[threadIdx.x / T];
+      for (int p = lane; p < k; p += T) conn[p] = 0;
+      __syncwarp();
       for (int j = lane; j < d; j += T) {
         int p = part[g.adj[b + j]];
         bnd |= p != own;
         atomicAdd(&conn[p], g.wgt[b + j]);
       }
-    }
-    __syncwarp();
-    bnd = team_or<T>(bnd);
-    int bg = 0, bp = -1;
-    if (valid && bnd) {
-      const int32_t vwv = g.vw[v];
-      if (s_pw[own] - vwv >= s_lo[own])
+      __syncwarp();
+      bnd = team_or<T>(bnd);
+      if (valid && bnd && s_pw[own] - vwv >= s_lo[own])
         for (int p = lane; p < k; p += T) {
           if (p == own || s_pw[p] + vwv > s_hi[p]) continue;
           int gain = conn[p] - conn[own];
           if (gain > bg || (gain == bg && bp >= 0 && p < bp)) { bg = gain; bp = p; }
         }
+      team_argmax<T>(bg, bp);
+      __syncwarp();
     }
-    team_argmax<T>(bg, bp);
     const bool writer = valid && lane == 0;
     const int c = (bp >= 0 && bg > 0) ? bp : -1;
     if (writer) st[v] = pack_state(own, c, bg);
-    warp_append(writer && c >= 0, v, list, count);
-    __syncwarp();
+    app.push(writer && c >= 0, v, list, count);
   }
+  app.flush(list, count);
 }
 
 // Jet-style afterburner over the candidate list: a move survives only if it
@@ -150,17 +236,28 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
       const int gv = st_gain(sv);
       const int64_t b = g.xbeg[v];
       const int d = g.deg[v];
-      for (int j = lane; j < d; j += T) {
-        int u = g.adj[b + j];
-        const uint32_t su = st[u];
-        int pu = st_part(su);
-        int cu = st_cand(su);
-        if (cu >= 0) {
-          int gu = st_gain(su);
-          if (gu > gv || (gu == gv && u < v)) pu = cu;
+      for (int j0 = lane; j0 < d; j0 += 4 * T) {
+        int u[4], w[4];
+        uint32_t su[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int j = j0 + q * T;
+          u[q] = j < d ? __ldg(g.adj + b + j) : -1;
+          w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
         }
-        int w = g.wgt[b + j];
-        delta += (pu == dest ? w : 0) - (pu == own ? w : 0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) su[q] = u[q] >= 0 ? __ldg(st + u[q]) : 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (u[q] < 0) continue;
+          int pu = st_part(su[q]);
+          const int cu = st_cand(su[q]);
+          if (cu >= 0) {
+            const int gu = st_gain(su[q]);
+            if (gu > gv || (gu == gv && u[q] < v)) pu = cu;
+          }
+          delta += (pu == dest ? w[q] : 0) - (pu == own ? w[q] : 0);
+        }
       }
     }
     delta = team_sum<T>(delta);
@@ -231,19 +328,32 @@ propose_t(G g, const uint32_t *mw, int32_t *prop, int32_t *fav, uint64_t salt,
       const int64_t b = g.xbeg[u];
       const int d = g.deg[u];
       const int32_t vu = (int32_t)(mw[u] & 0x7fffffffu);
-      for (int j = lane; j < d; j += T) {
-        int v = g.adj[b + j];
-        if (v == u) continue;
-        const uint32_t wv = mw[v];
+      for (int j0 = lane; j0 < d; j0 += 2 * T) {
+        int vq[2], wq[2];
+        uint32_t mq[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int j = j0 + q * T;
+          vq[q] = j < d ? __ldg(g.adj + b + j) : -1;
+          wq[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) mq[q] = vq[q] >= 0 ? __ldg(mw + vq[q]) : 0x80000000u;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+        const int v = vq[q];
+        if (v < 0 || v == u) continue;
+        const uint32_t wv = mq[q];
         const int32_t vv = (int32_t)(wv & 0x7fffffffu);
         if (vu + vv > max_vw) continue;
-        float r = rating(g.wgt[b + j], vu, vv);
+        float r = rating(wq[q], vu, vv);
         uint32_t h = edge_hash32(u, v, (uint32_t)salt);
         if (fav && (r > fr || (r == fr && (h > fh || (h == fh && v < fv))))) {
           fr = r; fh = h; fv = v;
         }
         if (wv >> 31) continue;  // already matched
         if (r > br || (r == br && (h > bh || (h == bh && v < bv)))) { br = r; bh = h; bv = v; }
+        }
       }
     }
     for (int off = T / 2; off; off >>= 1) {
@@ -290,6 +400,24 @@ inline int team_for(const G &g) {
   const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
   return avg <= 24.0 ? 8 : (avg <= 64.0 ? 16 : 32);
 }
+
+// refine_cand_t<T, KR>: KR = 8 / 16 register accumulators, 0 = shared memory
+#define HS_REFINE_DISPATCH(T_, K_, PACK16_, GRID, ...)                          \
+  do {                                                                           \
+    if ((K_) <= 8 && (PACK16_)) {                                                \
+      if ((T_) == 8) refine_cand_t<8, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);        \
+      else if ((T_) == 16) refine_cand_t<16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else refine_cand_t<32, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);                 \
+    } else if ((K_) <= 16) {                                                     \
+      if ((T_) == 8) refine_cand_t<8, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);       \
+      else if ((T_) == 16) refine_cand_t<16, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);\
+      else refine_cand_t<32, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);                \
+    } else {                                                                     \
+      if ((T_) == 8) refine_cand_t<8, 0><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);        \
+      else if ((T_) == 16) refine_cand_t<16, 0><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else refine_cand_t<32, 0><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);                 \
+    }                                                                            \
+  } while (0)
 
 #define HS_TEAM_DISPATCH(T_, KERNEL, GRID, ...)                                  \
   do {                                                                           \

@@ -75,14 +75,24 @@ def layered_dag(n_kernels: int, m_inter: int, seed: int = 0, kind: str = "MA", s
     return csr
 
 
+def in_order(csr: DagCSR, edge_attr: torch.Tensor) -> torch.Tensor:
+    """CSC copy of a per-edge attribute (in-order), for ``symmetrize``."""
+    return edge_attr[csr.in_eid.long()].contiguous()
+
+
 def integer_weights(w: torch.Tensor, scale: int = 100) -> torch.Tensor:
     """``_scaled`` (graphio.py:272-274) elementwise: max(1, floor(w*scale + 0.5)), int32."""
     return torch.clamp(torch.floor(w * scale + 0.5), min=1).to(torch.int32)
 
 
 def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,
-               node_w_i: Optional[torch.Tensor] = None) -> UGraph:
-    """K1 on the device; default weights are the integerised w_xfer / w_gpu."""
+               node_w_i: Optional[torch.Tensor] = None,
+               edge_w_i_in: Optional[torch.Tensor] = None) -> UGraph:
+    """K1 on the device; default weights are the integerised w_xfer / w_gpu.
+
+    ``edge_w_i_in`` is the same edge weight in in-order (CSC copy,
+    ``edge_w_i[csr.in_eid]``); passing it saves a random gather.
+    """
     dev = csr.device
     if edge_w_i is None:
         edge_w_i = integer_weights(csr.w_xfer)
@@ -95,7 +105,8 @@ def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,
     adjwgt = torch.empty(nnz_cap, dtype=torch.int32, device=dev)
     vwgt = torch.empty(nk, dtype=torch.int32, device=dev)
     nnz = _native.symmetrize(csr, edge_w_i.contiguous(), node_w_i.contiguous(), xadj, adjncy,
-                             adjwgt, vwgt)
+                             adjwgt, vwgt,
+                             edge_w_i_in.contiguous() if edge_w_i_in is not None else None)
     return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz], vwgt)
 
 

@@ -7,7 +7,7 @@ sys.path.insert(0, %r)
 from paper_1502_07451_b200 import kway
 csr = kway.layered_dag(10_000_000, 100_000_000, 0)
 ew, nw = kway.integer_weights(csr.w_xfer), kway.integer_weights(csr.w_gpu)
-ug = kway.symmetrize(csr, ew, nw)
+ug = kway.symmetrize(csr, ew, nw, kway.in_order(csr, ew))
 for _ in range(2): r = kway.partition_kway(ug, 8, seed=0)
 torch.cuda.synchronize()
 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
