@@ -253,6 +253,22 @@ int hs_layered_generate(int64_t n_kernels, int64_t m_inter, uint64_t seed,
                         int32_t *in_src, int32_t *in_eid, int32_t *layer_of,
                         void *stream);
 
+/* ---- K9 tiled-Cholesky execution (fp64) ------------------------------------
+ * No reference counterpart (the reference simulates this DAG, sim.py:135-164).
+ * hs_chol_pack: row-major n x n <-> tiles of b x b (b = 512), tile (i, j),
+ * i >= j, contiguous row-major at tiles + (i*T + j)*b*b; unpacking zeroes the
+ * strictly upper part of the diagonal tiles.
+ * hs_chol_execute: runs the task DAG (gen.cholesky_tasks order; kind 0
+ * POTRF, 1 TRSM, 2 SYRK, 3 GEMM; tile coordinates ti/tj/tk; successor CSR;
+ * in-degree) as one persistent kernel of grid_ctas CTAs (0 = one per SM).
+ * dinv: T*4 inverted 128x128 diagonal blocks (scratch, T*4*128*128 doubles).
+ * *fail_host != 0 if a pivot was not positive (matrix not SPD). */
+int hs_chol_pack(double *A, int32_t n, int32_t b, double *tiles, int32_t to_tiles, void *stream);
+int hs_chol_execute(double *tiles, double *dinv, int32_t T, int32_t n_tasks, const int8_t *kind,
+                    const int16_t *ti, const int16_t *tj, const int16_t *tk,
+                    const int64_t *succ_ptr, const int32_t *succ, const int32_t *indeg,
+                    int32_t grid_ctas, int32_t *fail_host, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

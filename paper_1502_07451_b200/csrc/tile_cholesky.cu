@@ -1,0 +1,437 @@
+// K9 — execution of the tiled-Cholesky task DAG on one B200 (fp64).
+//
+// No reference counterpart: the reference only *simulates* these kernels
+// (sim.py:135-164 with kernel_time from a calibration table). This is the
+// "execution of the partitioned DAG" leg of the hot path (SURVEY §8(a) last
+// row, App. D): the task DAG of gen.cholesky_tasks runs as ONE persistent
+// kernel per GPU; every CTA pulls work items from device-side ready queues,
+// and a finishing task releases its successors by atomic dependency counters.
+//
+// Layout: the matrix is stored as tiles of b x b (b = 512) doubles, tile
+// (i, j) (i >= j) contiguous and row-major at tiles + (i*T + j)*b*b.
+//
+// Work items (all dense math on DMMA, mma.sync m16n8k8 f64 — fp64 has no
+// tcgen05 kind; DMMA and DFMA both peak at ~37 TF/s measured on this part):
+//   GEMM(i,j,k)  16 items: 128x128 block of A_ij -= A_ik A_jk^T (K = 512)
+//   SYRK(i,k)    10 items: lower 128x128 blocks of A_ii -= A_ik A_ik^T
+//   TRSM(i,k)     4 items: a 128-row block of A_ik <- A_ik L_kk^-T, by block
+//                          columns: R = A - X L^T (GEMM), X = R Dinv^T (GEMM)
+//   POTRF(k)      1 item : blocked Cholesky of A_kk by 128-column blocks
+//                          (GEMM updates, 128x128 diagonal factor + inverse
+//                          in shared memory, panel X = A Dinv^T), keeping
+//                          the 4 inverted diagonal blocks Dinv[k] for TRSM.
+// Data produced inside the kernel is read with L1-bypassing loads (cp.async.cg
+// / ld.cg): L1 is not coherent across SMs.
+#include "common.cuh"
+#include <vector>
+
+namespace {
+
+constexpr int B = 512;        // tile size
+constexpr int BB = 128;       // block size of the MMA engine
+constexpr int KC = 16;        // k chunk per pipeline stage
+constexpr int STAGES = 3;
+constexpr int THREADS = 256;  // 8 warps: 2 (M) x 4 (N), warp tile 64 x 32
+constexpr int STAGE_DBL = 2 * BB * KC;                 // A + B doubles per stage
+constexpr int SMEM_GEMM = STAGES * STAGE_DBL * 8;      // 96 KB
+constexpr int SMEM_DIAG = BB * BB * 8;                 // 128 KB (diagonal block)
+constexpr int SMEM_BYTES = SMEM_DIAG > SMEM_GEMM ? SMEM_DIAG : SMEM_GEMM;
+
+enum { K_POTRF = 0, K_TRSM = 1, K_SYRK = 2, K_GEMM = 3 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+// element (r, k) of a [BB][KC] stage block; XOR swizzle of k bits 2-3 by
+// r & 3 makes every fragment load hit 16 distinct bank pairs (2 wavefronts)
+__device__ __forceinline__ int sw(int r, int k) { return r * KC + (k ^ ((r & 3) << 2)); }
+
+__device__ __forceinline__ void dmma(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+// Loads k columns [k0, k0+KC) of 128 rows of A (ld lda) and of B into a stage.
+__device__ __forceinline__ void load_stage(double *st, const double *A, int lda, const double *Bm,
+                                           int ldb, int k0) {
+  double *As = st, *Bs = st + BB * KC;
+  // 128 rows x 16 doubles = 1024 16-byte chunks per operand; 4 per thread
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = threadIdx.x + q * THREADS;
+    const int r = c >> 3, kk = (c & 7) * 2;
+    cp_async16(As + sw(r, kk), A + (size_t)r * lda + k0 + kk);
+    cp_async16(Bs + sw(r, kk), Bm + (size_t)r * ldb + k0 + kk);
+  }
+}
+
+// C[128x128] (ld ldc) = (mode 0) C - A B^T  |  (mode 1) A B^T, K % 16 == 0.
+// A, B: pointers to row 0 of the 128-row operand blocks. K may be 0 (no-op
+// for mode 0). Ends with __syncthreads (safe to overwrite A/B/C after).
+__device__ void mma_block(double *smem, const double *A, int lda, const double *Bm, int ldb,
+                          int K, double *C, int ldc, int mode) {
+  if (K == 0 && mode == 0) return;  // nothing to subtract
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+  double acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
+  const int nk = K / KC;
+  // prologue
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(smem + s * STAGE_DBL, A, lda, Bm, ldb, s * KC);
+    cp_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    // prefetch chunk kc + STAGES - 1 into the slot consumed at kc - 1
+    const int nx = kc + STAGES - 1;
+    if (nx < nk) load_stage(smem + (nx % STAGES) * STAGE_DBL, A, lda, Bm, ldb, nx * KC);
+    cp_commit();
+    const double *As = smem + (kc % STAGES) * STAGE_DBL, *Bs = As + BB * KC;
+#pragma unroll
+    for (int ks = 0; ks < KC; ks += 8) {
+      double a[4][4], b[4][2];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int r = wm + mt * 16 + gid;
+        a[mt][0] = As[sw(r, ks + tig)];
+        a[mt][1] = As[sw(r + 8, ks + tig)];
+        a[mt][2] = As[sw(r, ks + tig + 4)];
+        a[mt][3] = As[sw(r + 8, ks + tig + 4)];
+      }
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int r = wn + nt * 8 + gid;
+        b[nt][0] = Bs[sw(r, ks + tig)];
+        b[nt][1] = Bs[sw(r, ks + tig + 4)];
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], a[mt], b[nt]);
+    }
+  }
+  cp_wait<0>();
+  __syncthreads();  // every read of A/B done before C (possibly aliasing A) is written
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = wm + mt * 16 + gid + 8 * h, c = wn + nt * 8 + 2 * tig;
+        double *p = C + (size_t)r * ldc + c;
+        double2 v;
+        if (mode == 0) {
+          double2 o = __ldcg((const double2 *)p);
+          v.x = o.x - acc[mt][nt][2 * h];
+          v.y = o.y - acc[mt][nt][2 * h + 1];
+        } else {
+          v.x = acc[mt][nt][2 * h];
+          v.y = acc[mt][nt][2 * h + 1];
+        }
+        __stcg((double2 *)p, v);
+      }
+  __syncthreads();
+}
+
+// 128x128 diagonal block: in-place Cholesky (lower) in shared memory, write L
+// back, then Dinv = L^-1 (lower) column by column (thread c owns column c,
+// right-looking substitution over a private array).
+__device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *fail) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < BB * BB; e += THREADS) sm[e] = __ldcg(D + (size_t)(e / BB) * ldd + e % BB);
+  __syncthreads();
+  for (int j = 0; j < BB; ++j) {
+    if (tid == 0) {
+      double d = sm[j * BB + j];
+      if (!(d > 0.0)) { *fail = 1; d = 1.0; }
+      sm[j * BB + j] = sqrt(d);
+    }
+    __syncthreads();
+    const double djj = sm[j * BB + j];
+    for (int i = j + 1 + tid; i < BB; i += THREADS) sm[i * BB + j] /= djj;
+    __syncthreads();
+    // trailing update of the lower triangle, rows i > j, cols j < l <= i
+    const int rows = BB - j - 1;
+    for (int e = tid; e < rows * rows; e += THREADS) {
+      const int i = j + 1 + e / rows, l = j + 1 + e % rows;
+      if (l <= i) sm[i * BB + l] -= sm[i * BB + j] * sm[l * BB + j];
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < BB * BB; e += THREADS) {
+    const int i = e / BB, l = e % BB;
+    __stcg(D + (size_t)i * ldd + l, l <= i ? sm[e] : 0.0);
+  }
+  // inverse: column c of X with L X = I
+  if (tid < BB) {
+    const int c = tid;
+    double x[BB];
+#pragma unroll 1
+    for (int r = 0; r < BB; ++r) x[r] = 0.0;
+    x[c] = 1.0;
+#pragma unroll 1
+    for (int m = c; m < BB; ++m) {
+      const double xm = x[m] / sm[m * BB + m];
+      x[m] = xm;
+#pragma unroll 1
+      for (int r = m + 1; r < BB; ++r) x[r] -= sm[r * BB + m] * xm;
+    }
+#pragma unroll 1
+    for (int r = 0; r < BB; ++r) __stcg(Dinv + (size_t)r * BB + c, x[r]);
+  }
+  __syncthreads();
+}
+
+struct Task {
+  int8_t kind;
+  int16_t i, j, k;
+};
+
+struct ExecArgs {
+  double *tiles;     // T*T tiles (lower used)
+  double *dinv;      // T * 4 * 128*128 inverted diagonal blocks
+  int T;
+  int n_tasks;
+  const int8_t *kind;
+  const int16_t *ti, *tj, *tk;
+  const int64_t *succ_ptr;
+  const int32_t *succ;
+  int32_t *pending;     // [n_tasks] unmet dependencies
+  int32_t *items_left;  // [n_tasks]
+  // two queues: 0 urgent (panel critical path), 1 normal
+  int64_t *q[2];
+  unsigned long long *head, *tail;  // [2] each
+  unsigned long long *done;         // finished items
+  unsigned long long total_items;
+  int *fail;
+};
+
+__device__ __forceinline__ int n_items_of(int kind) {
+  return kind == K_POTRF ? 1 : kind == K_TRSM ? 4 : kind == K_SYRK ? 10 : 16;
+}
+
+__device__ __forceinline__ int urgent(const ExecArgs &E, int t) {
+  const int kd = E.kind[t];
+  return kd == K_POTRF || kd == K_TRSM || E.tj[t] == E.tk[t] + 1;
+}
+
+__device__ void push_task(const ExecArgs &E, int t) {
+  const int qi = urgent(E, t) ? 0 : 1;
+  const int n = n_items_of(E.kind[t]);
+  const unsigned long long pos = atomicAdd(&E.tail[qi], (unsigned long long)n);
+  for (int it = 0; it < n; ++it)
+    atomicExch((unsigned long long *)&E.q[qi][pos + it], (unsigned long long)(((int64_t)t << 8) | it));
+}
+
+__device__ double *tile(const ExecArgs &E, int i, int j) {
+  return E.tiles + ((size_t)i * E.T + j) * (size_t)B * B;
+}
+
+__device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
+  const int kd = E.kind[t], i = E.ti[t], j = E.tj[t], k = E.tk[t];
+  if (kd == K_GEMM) {
+    const int rb = it >> 2, cb = it & 3;
+    mma_block(smem, tile(E, i, k) + (size_t)rb * BB * B, B, tile(E, j, k) + (size_t)cb * BB * B, B,
+              B, tile(E, i, j) + (size_t)rb * BB * B + cb * BB, B, 0);
+  } else if (kd == K_SYRK) {
+    // lower blocks (rb, cb), rb >= cb, enumerated row by row
+    int rb = 0, rem = it;
+    while (rem > rb) { rem -= rb + 1; ++rb; }
+    const int cb = rem;
+    mma_block(smem, tile(E, i, k) + (size_t)rb * BB * B, B, tile(E, i, k) + (size_t)cb * BB * B, B,
+              B, tile(E, i, i) + (size_t)rb * BB * B + cb * BB, B, 0);
+  } else if (kd == K_TRSM) {
+    // row block rb of A_ik: X = A L_kk^-T by block columns
+    const int rb = it;
+    double *Aik = tile(E, i, k) + (size_t)rb * BB * B;
+    const double *Lkk = tile(E, k, k);
+    for (int cb = 0; cb < B / BB; ++cb) {
+      // R = A[:, cb] - X[:, :cb] L[cb, :cb]^T
+      mma_block(smem, Aik, B, Lkk + (size_t)cb * BB * B, B, cb * BB, Aik + cb * BB, B, 0);
+      // X[:, cb] = R Dinv_cb^T (in place)
+      mma_block(smem, Aik + cb * BB, B, E.dinv + ((size_t)k * 4 + cb) * BB * BB, BB, BB,
+                Aik + cb * BB, B, 1);
+    }
+  } else {  // POTRF(k): blocked by 128 columns
+    double *Akk = tile(E, k, k);
+    for (int cb = 0; cb < B / BB; ++cb) {
+      for (int rb = cb; rb < B / BB; ++rb)  // A[rb, cb] -= L[rb, :cb] L[cb, :cb]^T
+        mma_block(smem, Akk + (size_t)rb * BB * B, B, Akk + (size_t)cb * BB * B, B, cb * BB,
+                  Akk + (size_t)rb * BB * B + cb * BB, B, 0);
+      double *dinv = E.dinv + ((size_t)k * 4 + cb) * BB * BB;
+      diag_factor(smem, Akk + (size_t)cb * BB * B + cb * BB, B, dinv, E.fail);
+      for (int rb = cb + 1; rb < B / BB; ++rb)  // panel: X = A Dinv^T
+        mma_block(smem, Akk + (size_t)rb * BB * B + cb * BB, B, dinv, BB, BB,
+                  Akk + (size_t)rb * BB * B + cb * BB, B, 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ long long s_item;
+  while (true) {
+    if (threadIdx.x == 0) {
+      long long got = -1;
+      int spins = 0;
+      while (got < 0) {
+        for (int qi = 0; qi < 2 && got < 0; ++qi) {
+          unsigned long long h = *(volatile unsigned long long *)&E.head[qi];
+          unsigned long long tl = *(volatile unsigned long long *)&E.tail[qi];
+          if (h < tl && atomicCAS(&E.head[qi], h, h + 1) == h) {
+            volatile long long *slot = (volatile long long *)&E.q[qi][h];
+            long long v;
+            while ((v = *slot) < 0) __nanosleep(20);
+            got = v;
+          }
+        }
+        if (got < 0) {
+          if (*(volatile unsigned long long *)E.done >= E.total_items) { got = -2; break; }
+          __nanosleep(spins < 64 ? 32 : 256);
+          ++spins;
+        }
+      }
+      s_item = got;
+    }
+    __syncthreads();
+    const long long item = s_item;
+    __syncthreads();
+    if (item == -2) break;
+    const int t = (int)(item >> 8), it = (int)(item & 0xff);
+    run_item(E, smem, t, it);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (atomicSub(&E.items_left[t], 1) == 1) {  // task complete: release successors
+        __threadfence();
+        for (int64_t e = E.succ_ptr[t]; e < E.succ_ptr[t + 1]; ++e) {
+          const int s = E.succ[e];
+          if (atomicSub(&E.pending[s], 1) == 1) push_task(E, s);
+        }
+      }
+      atomicAdd(E.done, 1ull);
+    }
+  }
+}
+
+// tiled <-> row-major conversion (lower tiles only); blockIdx.y = tile
+__global__ void pack_kernel(double *A, int n, int T, double *tiles, int to_tiles) {
+  const int tl = blockIdx.y;
+  int ti = 0;
+  while ((ti + 1) * (ti + 2) / 2 <= tl) ++ti;
+  const int tj = tl - ti * (ti + 1) / 2;
+  double *tp = tiles + ((size_t)ti * T + tj) * B * B;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B * B; e += gridDim.x * blockDim.x) {
+    const int r = e / B, c = e % B;
+    const size_t gi = (size_t)(ti * B + r) * n + (tj * B + c);
+    if (to_tiles)
+      tp[e] = A[gi];
+    else
+      A[gi] = (ti == tj && c > r) ? 0.0 : tp[e];
+  }
+}
+
+}  // namespace
+
+extern "C" int hs_chol_pack(double *A, int32_t n, int32_t b, double *tiles, int32_t to_tiles,
+                            void *stream) {
+  HS_REQUIRE(b == B && n % B == 0, HS_EINVAL, "tile size must be %d and divide n", B);
+  const int T = n / B;
+  cudaStream_t s = (cudaStream_t)stream;
+  pack_kernel<<<dim3(16, T * (T + 1) / 2), 256, 0, s>>>(A, n, T, tiles, to_tiles);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}
+
+extern "C" int hs_chol_execute(double *tiles, double *dinv, int32_t T, int32_t n_tasks,
+                               const int8_t *kind, const int16_t *ti, const int16_t *tj,
+                               const int16_t *tk, const int64_t *succ_ptr, const int32_t *succ,
+                               const int32_t *indeg, int32_t grid_ctas, int32_t *fail_host,
+                               void *stream) {
+  HS_REQUIRE(tiles && dinv && kind && succ_ptr && indeg, HS_EINVAL, "hs_chol_execute: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  // host copies of the small task table to size the queues and seed them
+  std::vector<int8_t> hk(n_tasks);
+  std::vector<int32_t> hin(n_tasks);
+  std::vector<int16_t> hj(n_tasks), hkk(n_tasks);
+  HS_CHECK_CUDA(cudaMemcpyAsync(hk.data(), kind, n_tasks, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(hin.data(), indeg, n_tasks * 4, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(hj.data(), tj, n_tasks * 2, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(hkk.data(), tk, n_tasks * 2, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  auto items = [](int kd) { return kd == K_POTRF ? 1 : kd == K_TRSM ? 4 : kd == K_SYRK ? 10 : 16; };
+  unsigned long long cap[2] = {0, 0}, total = 0;
+  std::vector<int64_t> q0, q1;  // seeds (tasks ready at start)
+  std::vector<int32_t> left(n_tasks);
+  for (int t = 0; t < n_tasks; ++t) {
+    const int n = items(hk[t]);
+    left[t] = n;
+    const int qi = (hk[t] == K_POTRF || hk[t] == K_TRSM || hj[t] == hkk[t] + 1) ? 0 : 1;
+    cap[qi] += n;
+    total += n;
+    if (hin[t] == 0)
+      for (int it = 0; it < n; ++it) (qi ? q1 : q0).push_back(((int64_t)t << 8) | it);
+  }
+  hs::Scratch<int64_t> qa, qb;
+  hs::Scratch<int32_t> pending, items_left, fail;
+  hs::Scratch<unsigned long long> ctr;
+  HS_CHECK_CUDA(qa.alloc(cap[0], s));
+  HS_CHECK_CUDA(qb.alloc(cap[1], s));
+  HS_CHECK_CUDA(pending.alloc(n_tasks, s));
+  HS_CHECK_CUDA(items_left.alloc(n_tasks, s));
+  HS_CHECK_CUDA(fail.alloc(1, s));
+  HS_CHECK_CUDA(ctr.alloc(5, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(qa, 0xff, cap[0] * 8, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(qb, 0xff, cap[1] * 8, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(pending, indeg, n_tasks * 4, cudaMemcpyDeviceToDevice, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(items_left, left.data(), n_tasks * 4, cudaMemcpyHostToDevice, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(fail, 0, 4, s));
+  unsigned long long c0[5] = {0, 0, q0.size(), q1.size(), 0};  // head[2], tail[2], done
+  HS_CHECK_CUDA(cudaMemcpyAsync(ctr, c0, sizeof c0, cudaMemcpyHostToDevice, s));
+  if (!q0.empty())
+    HS_CHECK_CUDA(cudaMemcpyAsync(qa, q0.data(), q0.size() * 8, cudaMemcpyHostToDevice, s));
+  if (!q1.empty())
+    HS_CHECK_CUDA(cudaMemcpyAsync(qb, q1.data(), q1.size() * 8, cudaMemcpyHostToDevice, s));
+  ExecArgs E;
+  E.tiles = tiles; E.dinv = dinv; E.T = T; E.n_tasks = n_tasks;
+  E.kind = kind; E.ti = ti; E.tj = tj; E.tk = tk; E.succ_ptr = succ_ptr; E.succ = succ;
+  E.pending = pending; E.items_left = items_left;
+  E.q[0] = qa; E.q[1] = qb;
+  E.head = ctr.p; E.tail = ctr.p + 2; E.done = ctr.p + 4;
+  E.total_items = total;
+  E.fail = fail;
+  HS_CHECK_CUDA(cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     SMEM_BYTES));
+  const int grid = grid_ctas > 0 ? grid_ctas : hs::sm_count();
+  {
+    hs::Prof P("cholesky_exec", s, 0.0);
+    exec_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(E);
+  }
+  HS_CHECK_LAUNCH();
+  if (fail_host) {
+    HS_CHECK_CUDA(cudaMemcpyAsync(fail_host, fail, 4, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  return HS_OK;
+}
