@@ -9,7 +9,10 @@ ranks; with --gpus N every rank partitions its own 10M DAG: replicas, weak
 scaling). The DAG (~2.4 GB of CSR) is far larger than L2 (126 MB), so no L2
 flush is needed between steps.
 
-Also reported (``extra``): the config-2 100k/1M partition and k-way evaluate,
+Also reported: ``cholesky`` — the metric's second half, config 3 (tiled
+Cholesky n=32768, b=512, 45,760 tasks) executed on this GPU, GFLOP/s against
+the measured fp64 DMMA ceiling; ``extra``: the config-2 100k/1M partition and
+k-way evaluate,
 K7 levels/critical path on the 10M DAG, and the config-5 policy sweep
 (4096 simulations x eager/dmda/gp, bit-exact with the reference's means).
 
@@ -46,6 +49,7 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs")
+    ap.add_argument("--no-cholesky", action="store_true", help="skip the config-3 Cholesky block")
     ap.add_argument("--profile-json", default=None,
                     help="optional path: dump the per-kernel live profile")
     return ap.parse_args()
@@ -60,7 +64,7 @@ def dist_env():
 
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
-    """nvidia-smi sampled every 200 ms during the timed region."""
+    """nvidia-smi sampled every 50 ms during the timed region."""
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
@@ -75,7 +79,7 @@ class ClockSampler:
             self.out = open(self.path, "w")
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=self.out, stderr=subprocess.DEVNULL)
         except (OSError, FileNotFoundError):
             self.proc = None
@@ -325,8 +329,13 @@ def run_ours(args):
 
     # ---- secondary configs ----
     extra = {}
+    chol = None
     if not args.no_extra and rank == 0:
         extra = secondary(csr, args)
+    if rank == 0 and not args.no_cholesky:
+        del csr
+        torch.cuda.empty_cache()
+        chol = cholesky_block(args, dev)
 
     cpu = None
     if rank == 0 and world == 1:
@@ -358,11 +367,78 @@ def run_ours(args):
             "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "cpu_baseline": cpu,
+            "cholesky": chol,
             "extra": extra,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+FP64_PEAK_TFLOPS = 37.0  # DMMA ceiling measured on this pool's B200 by tools/fp64_peak.cu
+
+
+def cholesky_block(args, dev):
+    """Config 3: tiled Cholesky n=32768, b=512 (45,760 tasks) on this GPU."""
+    import numpy as np
+    import torch
+    from paper_1502_07451_b200.cholesky import TiledCholesky, spd_matrix
+    n = 32768
+    A = spd_matrix(n, seed=0, device=dev)
+    c = TiledCholesky(n, device=dev)
+    c.load(A)
+    c.run()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        c.load(A)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        c.run()
+        b.record()
+        torch.cuda.synchronize()
+        times.append(a.elapsed_time(b))
+    ms = statistics.fmean(times)
+    L = c.result()
+    resid = ((L @ L.T - A).abs().max() / A.abs().max()).item()
+    gflops = c.flops / ms / 1e6
+    # e2e: matrix from pinned host memory, factor back to host
+    hostA = A.cpu().pin_memory()
+    hostL = torch.empty_like(hostA).pin_memory()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    dA = hostA.to(dev, non_blocking=True)
+    c.load(dA)
+    c.run()
+    hostL.copy_(c.result(), non_blocking=True)
+    b.record()
+    torch.cuda.synchronize()
+    e2e_ms = a.elapsed_time(b)
+    del L, A, dA
+    torch.cuda.empty_cache()
+    # host LAPACK point (numerics oracle, not the reference): bounded n=8192
+    import time as _t
+    hn = 8192
+    R = np.random.default_rng(0).standard_normal((hn, hn))
+    H = R @ R.T + hn * np.eye(hn)
+    t0 = _t.perf_counter()
+    np.linalg.cholesky(H)
+    host_s = _t.perf_counter() - t0
+    return {
+        "metric": "partitioned Cholesky GFLOP/s (n=32768, b=512, 45,760 tasks, 1 GPU)",
+        "value": gflops, "unit": "GFLOP/s", "ms": ms, "residual": resid,
+        "roofline": {"kernel": "cholesky_exec (persistent DAG executor)", "bound": "tensor",
+                     "achieved": gflops / 1e3, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": gflops / 1e3 / FP64_PEAK_TFLOPS,
+                     "peak_source": "fp64 DMMA ceiling measured by tools/fp64_peak.cu (MEASURED_PEAKS "
+                                    "has no fp64 entry)"},
+        "e2e": {"value": c.flops / e2e_ms / 1e6, "unit": "GFLOP/s", "ms": e2e_ms,
+                "h2d_bytes_per_step": n * n * 8, "d2h_bytes_per_step": n * n * 8},
+        "cpu_point": {"value": hn ** 3 / 3 / host_s / 1e9, "unit": "GFLOP/s", "kind": "numpy LAPACK",
+                      "cores": os.cpu_count(), "sample": f"numpy.linalg.cholesky n={hn} fp64 "
+                      "(numerics oracle; the reference only simulates this DAG)"},
+    }
 
 
 def secondary(csr10m, args):

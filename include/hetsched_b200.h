@@ -268,6 +268,15 @@ int hs_chol_execute(double *tiles, double *dinv, int32_t T, int32_t n_tasks, con
                     const int16_t *ti, const int16_t *tj, const int16_t *tk,
                     const int64_t *succ_ptr, const int32_t *succ, const int32_t *indeg,
                     int32_t grid_ctas, int32_t *fail_host, void *stream);
+/* Same, with optional device counters (16 x u64, zeroed by the caller):
+ * [2*kind] SM cycles spent in items of that kind, [2*kind+1] items run,
+ * [8..10] POTRF phases (block updates, 128x128 diagonal factor+inverse,
+ * panel solve). */
+int hs_chol_execute_stats(double *tiles, double *dinv, int32_t T, int32_t n_tasks,
+                          const int8_t *kind, const int16_t *ti, const int16_t *tj,
+                          const int16_t *tk, const int64_t *succ_ptr, const int32_t *succ,
+                          const int32_t *indeg, int32_t grid_ctas, int32_t *fail_host,
+                          unsigned long long *stats, void *stream);
 
 #ifdef __cplusplus
 }

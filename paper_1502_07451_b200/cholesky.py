@@ -26,8 +26,8 @@ TILE = 512
 
 _P = ctypes.c_void_p
 _pack = _native._proto("hs_chol_pack", _P, ctypes.c_int32, ctypes.c_int32, _P, ctypes.c_int32, _P)
-_exec = _native._proto("hs_chol_execute", _P, _P, ctypes.c_int32, ctypes.c_int32, _P, _P, _P, _P,
-                       _P, _P, _P, ctypes.c_int32, _P, _P)
+_exec = _native._proto("hs_chol_execute_stats", _P, _P, ctypes.c_int32, ctypes.c_int32, _P, _P, _P,
+                       _P, _P, _P, _P, ctypes.c_int32, _P, _P, _P)
 
 
 @dataclass
@@ -87,15 +87,15 @@ class TiledCholesky:
         _native.check(_pack(_native.ptr(A), self.n, TILE, _native.ptr(self.tiles), 1,
                             _native.stream_ptr()))
 
-    def run(self) -> None:
-        """Execute the DAG in place on the loaded tiles."""
+    def run(self, stats: Optional[torch.Tensor] = None) -> None:
+        """Execute the DAG in place on the loaded tiles (optional u64[16] cycle stats)."""
         tb = self.table
         fail = ctypes.c_int32(0)
         _native.check(_exec(_native.ptr(self.tiles), _native.ptr(self.dinv), self.T, tb.n_tasks,
                             _native.ptr(tb.kind), _native.ptr(tb.ti), _native.ptr(tb.tj),
                             _native.ptr(tb.tk), _native.ptr(tb.succ_ptr), _native.ptr(tb.succ),
                             _native.ptr(tb.indeg), self.grid_ctas, ctypes.byref(fail),
-                            _native.stream_ptr()))
+                            _native.ptr(stats), _native.stream_ptr()))
         if fail.value:
             raise ValueError("matrix is not positive definite")
 

@@ -34,7 +34,7 @@ constexpr int STAGES = 3;
 constexpr int THREADS = 256;  // 8 warps: 2 (M) x 4 (N), warp tile 64 x 32
 constexpr int STAGE_DBL = 2 * BB * KC;                 // A + B doubles per stage
 constexpr int SMEM_GEMM = STAGES * STAGE_DBL * 8;      // 96 KB
-constexpr int SMEM_DIAG = BB * BB * 8;                 // 128 KB (diagonal block)
+constexpr int SMEM_DIAG = (BB * BB + 3 * 32 * 32) * 8;  // 152 KB (diagonal block + scratch)
 constexpr int SMEM_BYTES = SMEM_DIAG > SMEM_GEMM ? SMEM_DIAG : SMEM_GEMM;
 
 enum { K_POTRF = 0, K_TRSM = 1, K_SYRK = 2, K_GEMM = 3 };
@@ -154,28 +154,62 @@ __device__ void mma_block(double *smem, const double *A, int lda, const double *
   __syncthreads();
 }
 
-// 128x128 diagonal block: in-place Cholesky (lower) in shared memory, write L
-// back, then Dinv = L^-1 (lower) column by column (thread c owns column c,
-// right-looking substitution over a private array).
+// 128x128 diagonal block, blocked by 32 columns, in shared memory:
+//  A) Cholesky: per 32-block one warp factors the diagonal 32x32, one thread
+//     per row solves the panel below, all threads apply the trailing update;
+//  B) Dinv = L^-1: warp s inverts diagonal 32x32 block s (lane = column), then
+//     off-diagonal 32x32 blocks by increasing distance d = bi - bj:
+//     Linv[bi][bj] = -Linv[bi][bi] * sum_{m=bj}^{bi-1} L[bi][m] Linv[m][bj].
+// L goes back to D (zeros above the diagonal), Dinv to global (128x128).
+constexpr int DIAG_SCRATCH = 3 * 32 * 32;  // doubles after the 128x128 block
 __device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *fail) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double *scr = sm + BB * BB;
   for (int e = tid; e < BB * BB; e += THREADS) sm[e] = __ldcg(D + (size_t)(e / BB) * ldd + e % BB);
   __syncthreads();
-  for (int j = 0; j < BB; ++j) {
-    if (tid == 0) {
-      double d = sm[j * BB + j];
-      if (!(d > 0.0)) { *fail = 1; d = 1.0; }
-      sm[j * BB + j] = sqrt(d);
+  for (int s = 0; s < 4; ++s) {
+    const int o = 32 * s;
+    if (warp == 0) {
+      for (int j = 0; j < 32; ++j) {
+        if (lane == j) {
+          double d = sm[(o + j) * BB + o + j];
+          if (!(d > 0.0)) { *fail = 1; d = 1.0; }
+          sm[(o + j) * BB + o + j] = sqrt(d);
+        }
+        __syncwarp();
+        const double djj = sm[(o + j) * BB + o + j];
+        if (lane > j) sm[(o + lane) * BB + o + j] /= djj;
+        __syncwarp();
+        if (lane > j) {
+          const double lij = sm[(o + lane) * BB + o + j];
+          for (int l = j + 1; l <= lane; ++l)
+            sm[(o + lane) * BB + o + l] -= lij * sm[(o + l) * BB + o + j];
+        }
+        __syncwarp();
+      }
     }
     __syncthreads();
-    const double djj = sm[j * BB + j];
-    for (int i = j + 1 + tid; i < BB; i += THREADS) sm[i * BB + j] /= djj;
+    const int R = BB - o - 32;
+    if (tid < R) {  // panel row r: x L_ss^T = row
+      double *row = sm + (o + 32 + tid) * BB + o;
+      for (int c = 0; c < 32; ++c) {
+        double v = row[c];
+        const double *lc = sm + (o + c) * BB + o;
+        for (int m = 0; m < c; ++m) v -= row[m] * lc[m];
+        row[c] = v / lc[c];
+      }
+    }
     __syncthreads();
-    // trailing update of the lower triangle, rows i > j, cols j < l <= i
-    const int rows = BB - j - 1;
-    for (int e = tid; e < rows * rows; e += THREADS) {
-      const int i = j + 1 + e / rows, l = j + 1 + e % rows;
-      if (l <= i) sm[i * BB + l] -= sm[i * BB + j] * sm[l * BB + j];
+    if (R > 0) {  // trailing update of the lower triangle
+      const int ti = tid >> 4, tj = tid & 15;
+      for (int i = o + 32 + ti; i < BB; i += 16)
+        for (int j = o + 32 + tj; j <= i; j += 16) {
+          const double *ri = sm + i * BB + o, *rj = sm + j * BB + o;
+          double acc = 0.0;
+#pragma unroll 8
+          for (int m = 0; m < 32; ++m) acc += ri[m] * rj[m];
+          sm[i * BB + j] -= acc;
+        }
     }
     __syncthreads();
   }
@@ -183,24 +217,58 @@ __device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *f
     const int i = e / BB, l = e % BB;
     __stcg(D + (size_t)i * ldd + l, l <= i ? sm[e] : 0.0);
   }
-  // inverse: column c of X with L X = I
-  if (tid < BB) {
-    const int c = tid;
-    double x[BB];
-#pragma unroll 1
-    for (int r = 0; r < BB; ++r) x[r] = 0.0;
-    x[c] = 1.0;
-#pragma unroll 1
-    for (int m = c; m < BB; ++m) {
-      const double xm = x[m] / sm[m * BB + m];
-      x[m] = xm;
-#pragma unroll 1
-      for (int r = m + 1; r < BB; ++r) x[r] -= sm[r * BB + m] * xm;
+  // B1: diagonal blocks of the inverse (warp s, lane = column)
+  if (warp < 4) {
+    const int o = 32 * warp, c = lane;
+    double x[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) x[r] = 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      if (r < c) continue;
+      double v = (r == c) ? 1.0 : 0.0;
+      const double *lr = sm + (o + r) * BB + o;
+#pragma unroll
+      for (int m = 0; m < r; ++m)
+        if (m >= c) v -= lr[m] * x[m];
+      x[r] = v / lr[r];
     }
-#pragma unroll 1
-    for (int r = 0; r < BB; ++r) __stcg(Dinv + (size_t)r * BB + c, x[r]);
+#pragma unroll
+    for (int r = 0; r < 32; ++r) __stcg(Dinv + (size_t)(o + r) * BB + o + c, x[r]);
   }
+  // zero the strictly upper 32x32 blocks
+  for (int e = tid; e < BB * BB; e += THREADS) {
+    const int i = e / BB, l = e % BB;
+    if ((l >> 5) > (i >> 5)) __stcg(Dinv + e, 0.0);
+  }
+  __threadfence_block();
   __syncthreads();
+  // B2: off-diagonal blocks by distance
+  for (int d = 1; d < 4; ++d) {
+    const int nb = 4 - d;
+    // T_b = sum_{m = bj*32}^{bi*32 - 1} L[bi*32 + r][m] Linv[m][bj*32 + c]
+    for (int e = tid; e < nb * 1024; e += THREADS) {
+      const int b = e >> 10, r = (e >> 5) & 31, c = e & 31;
+      const int bj = b, bi = b + d;
+      const double *lr = sm + (bi * 32 + r) * BB;
+      double acc = 0.0;
+      for (int m = bj * 32; m < bi * 32; ++m)
+        acc += lr[m] * __ldcg(Dinv + (size_t)m * BB + bj * 32 + c);
+      scr[e] = acc;
+    }
+    __syncthreads();
+    // Linv[bi][bj] = -Linv[bi][bi] T_b   (Linv[bi][bi] lower: q <= r)
+    for (int e = tid; e < nb * 1024; e += THREADS) {
+      const int b = e >> 10, r = (e >> 5) & 31, c = e & 31;
+      const int bj = b, bi = b + d;
+      double acc = 0.0;
+      for (int q = 0; q <= r; ++q)
+        acc += __ldcg(Dinv + (size_t)(bi * 32 + r) * BB + bi * 32 + q) * scr[(b << 10) + q * 32 + c];
+      __stcg(Dinv + (size_t)(bi * 32 + r) * BB + bj * 32 + c, -acc);
+    }
+    __threadfence_block();
+    __syncthreads();
+  }
 }
 
 struct Task {
@@ -225,6 +293,7 @@ struct ExecArgs {
   unsigned long long *done;         // finished items
   unsigned long long total_items;
   int *fail;
+  unsigned long long *stats;  // optional: [kind*2] cycles, [kind*2+1] items; [8..13] POTRF phases; [14] idle
 };
 
 __device__ __forceinline__ int n_items_of(int kind) {
@@ -246,6 +315,10 @@ __device__ void push_task(const ExecArgs &E, int t) {
 
 __device__ double *tile(const ExecArgs &E, int i, int j) {
   return E.tiles + ((size_t)i * E.T + j) * (size_t)B * B;
+}
+
+__device__ __forceinline__ void stat_add(const ExecArgs &E, int idx, unsigned long long v) {
+  if (E.stats && threadIdx.x == 0) atomicAdd(&E.stats[idx], v);
 }
 
 __device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
@@ -276,14 +349,21 @@ __device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
   } else {  // POTRF(k): blocked by 128 columns
     double *Akk = tile(E, k, k);
     for (int cb = 0; cb < B / BB; ++cb) {
+      long long c0 = clock64();
       for (int rb = cb; rb < B / BB; ++rb)  // A[rb, cb] -= L[rb, :cb] L[cb, :cb]^T
         mma_block(smem, Akk + (size_t)rb * BB * B, B, Akk + (size_t)cb * BB * B, B, cb * BB,
                   Akk + (size_t)rb * BB * B + cb * BB, B, 0);
+      long long c1 = clock64();
       double *dinv = E.dinv + ((size_t)k * 4 + cb) * BB * BB;
       diag_factor(smem, Akk + (size_t)cb * BB * B + cb * BB, B, dinv, E.fail);
+      long long c2 = clock64();
       for (int rb = cb + 1; rb < B / BB; ++rb)  // panel: X = A Dinv^T
         mma_block(smem, Akk + (size_t)rb * BB * B + cb * BB, B, dinv, BB, BB,
                   Akk + (size_t)rb * BB * B + cb * BB, B, 1);
+      long long c3 = clock64();
+      stat_add(E, 8, c1 - c0);
+      stat_add(E, 9, c2 - c1);
+      stat_add(E, 10, c3 - c2);
     }
   }
 }
@@ -319,7 +399,10 @@ __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
     __syncthreads();
     if (item == -2) break;
     const int t = (int)(item >> 8), it = (int)(item & 0xff);
+    const long long c0 = clock64();
     run_item(E, smem, t, it);
+    stat_add(E, E.kind[t] * 2, clock64() - c0);
+    stat_add(E, E.kind[t] * 2 + 1, 1);
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -369,6 +452,15 @@ extern "C" int hs_chol_execute(double *tiles, double *dinv, int32_t T, int32_t n
                                const int16_t *tk, const int64_t *succ_ptr, const int32_t *succ,
                                const int32_t *indeg, int32_t grid_ctas, int32_t *fail_host,
                                void *stream) {
+  return hs_chol_execute_stats(tiles, dinv, T, n_tasks, kind, ti, tj, tk, succ_ptr, succ, indeg,
+                               grid_ctas, fail_host, nullptr, stream);
+}
+
+extern "C" int hs_chol_execute_stats(double *tiles, double *dinv, int32_t T, int32_t n_tasks,
+                                     const int8_t *kind, const int16_t *ti, const int16_t *tj,
+                                     const int16_t *tk, const int64_t *succ_ptr,
+                                     const int32_t *succ, const int32_t *indeg, int32_t grid_ctas,
+                                     int32_t *fail_host, unsigned long long *stats, void *stream) {
   HS_REQUIRE(tiles && dinv && kind && succ_ptr && indeg, HS_EINVAL, "hs_chol_execute: null argument");
   cudaStream_t s = (cudaStream_t)stream;
   // host copies of the small task table to size the queues and seed them
@@ -421,6 +513,7 @@ extern "C" int hs_chol_execute(double *tiles, double *dinv, int32_t T, int32_t n
   E.head = ctr.p; E.tail = ctr.p + 2; E.done = ctr.p + 4;
   E.total_items = total;
   E.fail = fail;
+  E.stats = stats;
   HS_CHECK_CUDA(cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SMEM_BYTES));
   const int grid = grid_ctas > 0 ? grid_ctas : hs::sm_count();

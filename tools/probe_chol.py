@@ -12,6 +12,15 @@ for n in [int(x) for x in sys.argv[1:]]:
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(); c.run(); b.record(); torch.cuda.synchronize()
         ts.append(a.elapsed_time(b))
+    st = torch.zeros(16, dtype=torch.int64, device="cuda")
+    c.load(A); c.run(st); torch.cuda.synchronize()
+    st = st.cpu().tolist()
+    ghz = 1.965e6  # cycles per ms
+    names = ["POTRF", "TRSM", "SYRK", "GEMM"]
+    print("  per item us:", {names[i]: round(st[2*i] / max(1, st[2*i+1]) / ghz * 1e3, 1) for i in range(4)},
+          "items:", {names[i]: st[2*i+1] for i in range(4)},
+          "POTRF phases us/call:", [round(x / max(1, st[1]) / ghz * 1e3, 1) for x in st[8:11]],
+          "busy CTA-ms:", round(sum(st[0:8:2]) / ghz, 1), flush=True)
     L = c.result()
     res = ((L @ L.T - A).abs().max() / A.abs().max()).item()
     t = min(ts)
