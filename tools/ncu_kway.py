@@ -7,7 +7,8 @@ from paper_1502_07451_b200 import kway
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
 csr = kway.layered_dag(n, 10 * n, 0)
-ug = kway.symmetrize(csr)
+ew = kway.integer_weights(csr.w_xfer)
+ug = kway.symmetrize(csr, ew, kway.integer_weights(csr.w_gpu), kway.in_order(csr, ew))
 r = kway.partition_kway(ug, 8, tol=0.03, seed=0)
 torch.cuda.synchronize()
 print("cut", r.cut, "levels", r.levels, "passes", r.refine_passes)
