@@ -278,6 +278,47 @@ int hs_chol_execute_stats(double *tiles, double *dinv, int32_t T, int32_t n_task
                           const int32_t *indeg, int32_t grid_ctas, int32_t *fail_host,
                           unsigned long long *stats, void *stream);
 
+/* Partitioned execution over nranks GPUs (or nranks executors on one GPU):
+ * rank r runs the tasks with owner[t] == r. When a task's last work item
+ * finishes, its CTA stores the task's output tile (and Dinv[k] for POTRF)
+ * into tiles[q]/dinv[q] of every rank q owning a successor — one copy per
+ * (producer, destination), the k-node generalisation of the simulator's
+ * item dedup (sim.py:86-89,141-144) — then appends the task id to q's inbox
+ * ring (system-scope atomics). Idle CTAs drain their own inbox and release
+ * local successors. All pointers are device pointers valid on the calling
+ * rank's device: peers' buffers are CUDA-IPC mappings (hs_ipc_*) or, for
+ * loopback executors, plain pointers on the same device.
+ * inbox[r]: n_tasks int64 filled with -1; ctl[r]: 2 uint64 zeroed
+ * (tail, head). copies_dev (optional, device u64, caller-zeroed) counts the
+ * tiles this rank sent. fail_host != NULL makes the call synchronous (status
+ * check); pass NULL when several executors must be launched concurrently. */
+typedef struct hs_chol_peers {
+    int32_t rank, nranks;               /* nranks <= 8 */
+    const int8_t *owner;                /* [n_tasks] */
+    double *tiles[8];
+    double *dinv[8];
+    long long *inbox[8];
+    unsigned long long *ctl[8];
+} hs_chol_peers_t;
+
+int hs_chol_execute_part(double *tiles, double *dinv, int32_t T, int32_t n_tasks,
+                         const int8_t *kind, const int16_t *ti, const int16_t *tj,
+                         const int16_t *tk, const int64_t *succ_ptr, const int32_t *succ,
+                         const int32_t *indeg, const hs_chol_peers_t *peers, int32_t grid_ctas,
+                         int32_t *fail_host, unsigned long long *stats,
+                         unsigned long long *copies_dev, void *stream);
+
+/* CUDA IPC plumbing for one-process-per-GPU runs (64-byte opaque handles).
+ * Shared buffers must be whole allocations (hs_ipc_alloc): a handle names an
+ * allocation base. The executor's watchdog returns HS_EDEADLOCK instead of
+ * spinning forever if a peer never delivers a dependency. */
+int hs_ipc_alloc(int64_t bytes, void **dev_ptr);
+int hs_ipc_free(void *dev_ptr);
+int hs_memset_async(void *dev_ptr, int32_t byte_value, int64_t bytes, void *stream);
+int hs_ipc_handle(void *dev_ptr, char *handle64);
+int hs_ipc_open(const char *handle64, void **dev_ptr);
+int hs_ipc_close(void *dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

@@ -38,6 +38,7 @@ constexpr int SMEM_DIAG = (BB * BB + 3 * 32 * 32) * 8;  // 152 KB (diagonal bloc
 constexpr int SMEM_BYTES = SMEM_DIAG > SMEM_GEMM ? SMEM_DIAG : SMEM_GEMM;
 
 enum { K_POTRF = 0, K_TRSM = 1, K_SYRK = 2, K_GEMM = 3 };
+constexpr int kMaxRanks = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -294,6 +295,19 @@ struct ExecArgs {
   unsigned long long total_items;
   int *fail;
   unsigned long long *stats;  // optional: [kind*2] cycles, [kind*2+1] items; [8..13] POTRF phases; [14] idle
+  // partitioned execution (nranks > 1): tasks owned by other ranks are
+  // completed there; their output tiles arrive by peer stores and their ids
+  // through this rank's inbox ring
+  int rank, nranks;
+  const int8_t *owner;
+  double *peer_tiles[kMaxRanks];
+  double *peer_dinv[kMaxRanks];
+  long long *peer_inbox[kMaxRanks];
+  unsigned long long *peer_inbox_tail[kMaxRanks];
+  long long *inbox;                 // own ring (= peer_inbox[rank])
+  unsigned long long *inbox_tail;   // own (= peer_inbox_tail[rank])
+  unsigned long long *inbox_head;   // own, local claims
+  unsigned long long *copies;       // tiles sent (evidence: = K2 transfer count)
 };
 
 __device__ __forceinline__ int n_items_of(int kind) {
@@ -368,9 +382,42 @@ __device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
   }
 }
 
+// releases the local successors of task t (any rank's task) — thread 0 only
+__device__ void release_local(const ExecArgs &E, int t) {
+  for (int64_t e = E.succ_ptr[t]; e < E.succ_ptr[t + 1]; ++e) {
+    const int s = E.succ[e];
+    if (E.nranks > 1 && E.owner[s] != E.rank) continue;
+    if (atomicSub(&E.pending[s], 1) == 1) push_task(E, s);
+  }
+}
+
+// output tile of task t: GEMM (i,j), SYRK (i,i), TRSM (i,k), POTRF (k,k)
+__device__ __forceinline__ size_t out_tile_offset(const ExecArgs &E, int t) {
+  const int kd = E.kind[t], i = E.ti[t], j = E.tj[t], k = E.tk[t];
+  const int r = kd == K_POTRF ? k : i;
+  const int c = kd == K_GEMM ? j : (kd == K_SYRK ? i : k);
+  return ((size_t)r * E.T + c) * (size_t)B * B;
+}
+
+// all threads: copy t's output (and Dinv[k] for POTRF) into rank q's buffers
+__device__ void send_output(const ExecArgs &E, int t, int q) {
+  const size_t off = out_tile_offset(E, t);
+  const double2 *src = (const double2 *)(E.tiles + off);
+  double2 *dst = (double2 *)(E.peer_tiles[q] + off);
+  for (int e = threadIdx.x; e < B * B / 2; e += THREADS) dst[e] = __ldcg(src + e);
+  if (E.kind[t] == K_POTRF) {
+    const size_t doff = (size_t)E.tk[t] * 4 * BB * BB;
+    const double2 *ds = (const double2 *)(E.dinv + doff);
+    double2 *dd = (double2 *)(E.peer_dinv[q] + doff);
+    for (int e = threadIdx.x; e < 4 * BB * BB / 2; e += THREADS) dd[e] = __ldcg(ds + e);
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
   extern __shared__ __align__(16) double smem[];
   __shared__ long long s_item;
+  __shared__ int s_last;
+  __shared__ unsigned s_mask;
   while (true) {
     if (threadIdx.x == 0) {
       long long got = -1;
@@ -386,10 +433,31 @@ __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
             got = v;
           }
         }
+        if (got < 0 && E.nranks > 1) {  // remote completions: release local successors
+          unsigned long long h = *(volatile unsigned long long *)E.inbox_head;
+          unsigned long long tl = *(volatile unsigned long long *)E.inbox_tail;
+          if (h < tl && atomicCAS(E.inbox_head, h, h + 1) == h) {
+            volatile long long *slot = (volatile long long *)&E.inbox[h];
+            long long v;
+            int w = 0;
+            while ((v = *slot) < 0 && ++w < (1 << 28)) __nanosleep(20);
+            if (v < 0) { atomicMax(E.fail, 2); continue; }
+            __threadfence_system();  // acquire: the peer's tile stores precede its post
+            release_local(E, (int)v);
+            continue;
+          }
+        }
         if (got < 0) {
           if (*(volatile unsigned long long *)E.done >= E.total_items) { got = -2; break; }
+          if (*(volatile int *)E.fail >= 2) { got = -2; break; }  // another CTA gave up
           __nanosleep(spins < 64 ? 32 : 256);
-          ++spins;
+          // watchdog: ~30 s without any work means a lost dependency (e.g. a
+          // peer that never posts) — fail loudly instead of hanging the GPU
+          if (++spins > (1 << 27)) {
+            atomicMax(E.fail, 2);
+            got = -2;
+            break;
+          }
         }
       }
       s_item = got;
@@ -406,15 +474,35 @@ __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (atomicSub(&E.items_left[t], 1) == 1) {  // task complete: release successors
+      const int last = atomicSub(&E.items_left[t], 1) == 1;
+      unsigned mask = 0;
+      if (last) {  // task complete: release successors, collect remote owners
         __threadfence();
-        for (int64_t e = E.succ_ptr[t]; e < E.succ_ptr[t + 1]; ++e) {
-          const int s = E.succ[e];
-          if (atomicSub(&E.pending[s], 1) == 1) push_task(E, s);
-        }
+        release_local(E, t);
+        if (E.nranks > 1)
+          for (int64_t e = E.succ_ptr[t]; e < E.succ_ptr[t + 1]; ++e) {
+            const int q = E.owner[E.succ[e]];
+            if (q != E.rank) mask |= 1u << q;
+          }
       }
-      atomicAdd(E.done, 1ull);
+      s_last = last;
+      s_mask = mask;
     }
+    __syncthreads();
+    if (s_mask) {  // one copy per (producer, destination rank), then post
+      for (int q = 0; q < E.nranks; ++q)
+        if ((s_mask >> q) & 1u) send_output(E, t, q);
+      __threadfence_system();
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int q = 0; q < E.nranks; ++q)
+          if ((s_mask >> q) & 1u) {
+            const unsigned long long pos = atomicAdd_system(E.peer_inbox_tail[q], 1ull);
+            atomicExch_system((unsigned long long *)&E.peer_inbox[q][pos], (unsigned long long)t);
+            atomicAdd(E.copies, 1ull);
+          }
+    }
+    if (threadIdx.x == 0) atomicAdd(E.done, 1ull);
   }
 }
 
@@ -461,24 +549,44 @@ extern "C" int hs_chol_execute_stats(double *tiles, double *dinv, int32_t T, int
                                      const int16_t *tk, const int64_t *succ_ptr,
                                      const int32_t *succ, const int32_t *indeg, int32_t grid_ctas,
                                      int32_t *fail_host, unsigned long long *stats, void *stream) {
+  return hs_chol_execute_part(tiles, dinv, T, n_tasks, kind, ti, tj, tk, succ_ptr, succ, indeg,
+                              nullptr, grid_ctas, fail_host, stats, nullptr, stream);
+}
+
+extern "C" int hs_chol_execute_part(double *tiles, double *dinv, int32_t T, int32_t n_tasks,
+                                    const int8_t *kind, const int16_t *ti, const int16_t *tj,
+                                    const int16_t *tk, const int64_t *succ_ptr,
+                                    const int32_t *succ, const int32_t *indeg,
+                                    const hs_chol_peers_t *peers, int32_t grid_ctas,
+                                    int32_t *fail_host, unsigned long long *stats,
+                                    unsigned long long *copies_dev, void *stream) {
   HS_REQUIRE(tiles && dinv && kind && succ_ptr && indeg, HS_EINVAL, "hs_chol_execute: null argument");
+  const int nranks = peers ? peers->nranks : 1;
+  const int rank = peers ? peers->rank : 0;
+  HS_REQUIRE(nranks >= 1 && nranks <= kMaxRanks && rank >= 0 && rank < nranks, HS_ELIMIT,
+             "ranks must be 1..%d", kMaxRanks);
+  HS_REQUIRE(nranks == 1 || (peers->owner && peers->inbox[rank] && peers->ctl[rank]), HS_EINVAL,
+             "partitioned execution needs owner, inbox and ctl buffers");
   cudaStream_t s = (cudaStream_t)stream;
   // host copies of the small task table to size the queues and seed them
-  std::vector<int8_t> hk(n_tasks);
+  std::vector<int8_t> hk(n_tasks), hown(n_tasks, 0);
   std::vector<int32_t> hin(n_tasks);
   std::vector<int16_t> hj(n_tasks), hkk(n_tasks);
   HS_CHECK_CUDA(cudaMemcpyAsync(hk.data(), kind, n_tasks, cudaMemcpyDeviceToHost, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(hin.data(), indeg, n_tasks * 4, cudaMemcpyDeviceToHost, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(hj.data(), tj, n_tasks * 2, cudaMemcpyDeviceToHost, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(hkk.data(), tk, n_tasks * 2, cudaMemcpyDeviceToHost, s));
+  if (nranks > 1)
+    HS_CHECK_CUDA(cudaMemcpyAsync(hown.data(), peers->owner, n_tasks, cudaMemcpyDeviceToHost, s));
   HS_CHECK_CUDA(cudaStreamSynchronize(s));
   auto items = [](int kd) { return kd == K_POTRF ? 1 : kd == K_TRSM ? 4 : kd == K_SYRK ? 10 : 16; };
-  unsigned long long cap[2] = {0, 0}, total = 0;
-  std::vector<int64_t> q0, q1;  // seeds (tasks ready at start)
+  unsigned long long cap[2] = {1, 1}, total = 0;
+  std::vector<int64_t> q0, q1;  // seeds (owned tasks ready at start)
   std::vector<int32_t> left(n_tasks);
   for (int t = 0; t < n_tasks; ++t) {
     const int n = items(hk[t]);
     left[t] = n;
+    if (hown[t] != rank) continue;
     const int qi = (hk[t] == K_POTRF || hk[t] == K_TRSM || hj[t] == hkk[t] + 1) ? 0 : 1;
     cap[qi] += n;
     total += n;
@@ -493,27 +601,44 @@ extern "C" int hs_chol_execute_stats(double *tiles, double *dinv, int32_t T, int
   HS_CHECK_CUDA(pending.alloc(n_tasks, s));
   HS_CHECK_CUDA(items_left.alloc(n_tasks, s));
   HS_CHECK_CUDA(fail.alloc(1, s));
-  HS_CHECK_CUDA(ctr.alloc(5, s));
+  HS_CHECK_CUDA(ctr.alloc(8, s));
   HS_CHECK_CUDA(cudaMemsetAsync(qa, 0xff, cap[0] * 8, s));
   HS_CHECK_CUDA(cudaMemsetAsync(qb, 0xff, cap[1] * 8, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(pending, indeg, n_tasks * 4, cudaMemcpyDeviceToDevice, s));
   HS_CHECK_CUDA(cudaMemcpyAsync(items_left, left.data(), n_tasks * 4, cudaMemcpyHostToDevice, s));
   HS_CHECK_CUDA(cudaMemsetAsync(fail, 0, 4, s));
-  unsigned long long c0[5] = {0, 0, q0.size(), q1.size(), 0};  // head[2], tail[2], done
+  // head[2], tail[2], done, copies, -, -
+  unsigned long long c0[8] = {0, 0, q0.size(), q1.size(), 0, 0, 0, 0};
   HS_CHECK_CUDA(cudaMemcpyAsync(ctr, c0, sizeof c0, cudaMemcpyHostToDevice, s));
   if (!q0.empty())
     HS_CHECK_CUDA(cudaMemcpyAsync(qa, q0.data(), q0.size() * 8, cudaMemcpyHostToDevice, s));
   if (!q1.empty())
     HS_CHECK_CUDA(cudaMemcpyAsync(qb, q1.data(), q1.size() * 8, cudaMemcpyHostToDevice, s));
   ExecArgs E;
+  memset(&E, 0, sizeof E);
   E.tiles = tiles; E.dinv = dinv; E.T = T; E.n_tasks = n_tasks;
   E.kind = kind; E.ti = ti; E.tj = tj; E.tk = tk; E.succ_ptr = succ_ptr; E.succ = succ;
   E.pending = pending; E.items_left = items_left;
   E.q[0] = qa; E.q[1] = qb;
   E.head = ctr.p; E.tail = ctr.p + 2; E.done = ctr.p + 4;
+  E.copies = copies_dev ? copies_dev : ctr.p + 5;
   E.total_items = total;
   E.fail = fail;
   E.stats = stats;
+  E.rank = rank;
+  E.nranks = nranks;
+  if (nranks > 1) {
+    E.owner = peers->owner;
+    for (int q = 0; q < nranks; ++q) {
+      E.peer_tiles[q] = peers->tiles[q];
+      E.peer_dinv[q] = peers->dinv[q];
+      E.peer_inbox[q] = peers->inbox[q];
+      E.peer_inbox_tail[q] = peers->ctl[q];
+    }
+    E.inbox = peers->inbox[rank];
+    E.inbox_tail = peers->ctl[rank];
+    E.inbox_head = peers->ctl[rank] + 1;
+  }
   HS_CHECK_CUDA(cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      SMEM_BYTES));
   const int grid = grid_ctas > 0 ? grid_ctas : hs::sm_count();
@@ -522,9 +647,49 @@ extern "C" int hs_chol_execute_stats(double *tiles, double *dinv, int32_t T, int
     exec_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(E);
   }
   HS_CHECK_LAUNCH();
-  if (fail_host) {
-    HS_CHECK_CUDA(cudaMemcpyAsync(fail_host, fail, 4, cudaMemcpyDeviceToHost, s));
+  if (fail_host) {  // synchronous only when the caller asks for the status
+    int32_t f = 0;
+    HS_CHECK_CUDA(cudaMemcpyAsync(&f, fail, 4, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    *fail_host = f;
+    HS_REQUIRE(f < 2, HS_EDEADLOCK, "partitioned execution lost a dependency (watchdog)");
   }
+  return HS_OK;
+}
+
+// IPC-shareable buffers are separate cudaMalloc allocations: a handle refers
+// to an allocation's base, so sub-allocations (e.g. from a caching allocator)
+// cannot be shared by pointer.
+extern "C" int hs_ipc_alloc(int64_t bytes, void **dev_ptr) {
+  HS_CHECK_CUDA(cudaMalloc(dev_ptr, bytes > 0 ? bytes : 1));
+  return HS_OK;
+}
+
+extern "C" int hs_ipc_free(void *dev_ptr) {
+  HS_CHECK_CUDA(cudaFree(dev_ptr));
+  return HS_OK;
+}
+
+extern "C" int hs_memset_async(void *dev_ptr, int32_t byte_value, int64_t bytes, void *stream) {
+  HS_CHECK_CUDA(cudaMemsetAsync(dev_ptr, byte_value, bytes, (cudaStream_t)stream));
+  return HS_OK;
+}
+
+extern "C" int hs_ipc_handle(void *dev_ptr, char *handle64) {
+  cudaIpcMemHandle_t h;
+  HS_CHECK_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+  memcpy(handle64, &h, sizeof h);
+  return HS_OK;
+}
+
+extern "C" int hs_ipc_open(const char *handle64, void **dev_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof h);
+  HS_CHECK_CUDA(cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return HS_OK;
+}
+
+extern "C" int hs_ipc_close(void *dev_ptr) {
+  HS_CHECK_CUDA(cudaIpcCloseMemHandle(dev_ptr));
   return HS_OK;
 }
