@@ -208,10 +208,13 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     rank, world, local = dist_env()
+    ndev = torch.cuda.device_count()
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    dev = torch.device("cuda", local)
+        torch.cuda.set_device(local % ndev)
+        # one process per GPU over NCCL; gloo only when ranks share a device
+        # (NCCL refuses duplicate GPUs) — used to exercise N>1 on a 1-GPU box
+        dist.init_process_group("nccl" if world <= ndev else "gloo")
+    dev = torch.device("cuda", local % ndev)
     torch.cuda.set_device(dev)
     from paper_1502_07451_b200 import _native, kway
 
@@ -251,9 +254,7 @@ def run_ours(args):
     launches = _native.launch_count() - launches0
     elapsed = t0.elapsed_time(t1)
     if world > 1:
-        t = torch.tensor([elapsed], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
+        elapsed = allmax(elapsed, dev)
     ms_per_step = elapsed / args.steps
 
     # ---- live per-kernel profile: CUDA events around single launches on the
@@ -322,9 +323,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = allmax(e2e_ms, dev)
     del host
 
     # ---- secondary configs ----
@@ -332,10 +331,13 @@ def run_ours(args):
     chol = None
     if not args.no_extra and rank == 0:
         extra = secondary(csr, args)
-    if rank == 0 and not args.no_cholesky:
+    if not args.no_cholesky:
         del csr
         torch.cuda.empty_cache()
-        chol = cholesky_block(args, dev)
+        if world == 1:
+            chol = cholesky_block(args, dev)
+        else:
+            chol = cholesky_partitioned(args, dev, rank, world)
 
     cpu = None
     if rank == 0 and world == 1:
@@ -376,6 +378,68 @@ def run_ours(args):
 
 
 FP64_PEAK_TFLOPS = 37.0  # DMMA ceiling measured on this pool's B200 by tools/fp64_peak.cu
+
+
+def allmax(x: float, dev) -> float:
+    """Max over ranks (device tensor on NCCL, host tensor on gloo)."""
+    import torch
+    import torch.distributed as dist
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=on, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allsum(x: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], device=on, dtype=torch.float64)
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def cholesky_partitioned(args, dev, rank, world):
+    """Config 3 across `world` GPUs: partitioned DAG, cross edges = peer tile stores."""
+    import torch
+    import torch.distributed as dist
+    from paper_1502_07451_b200.cholesky import (PartitionedCholesky, owner_cyclic, owner_partition,
+                                                 spd_matrix, task_table, transfer_count)
+    n = 32768
+    tb = task_table(n // 512, dev)
+    owner = owner_cyclic(tb, world)
+    t_part = transfer_count(tb, owner_partition(tb, world)) if rank == 0 else None
+    pc = PartitionedCholesky(n, owner, world, mode="ipc", rank=rank, device=dev)
+    A = spd_matrix(n, seed=0, device=dev)
+    times = []
+    for it in range(1 + max(1, min(args.steps, 3))):
+        pc.load(A)
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        pc.run()
+        b.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = allmax(a.elapsed_time(b), dev)
+        if it:
+            times.append(t)
+    ms = statistics.fmean(times)
+    copies = allsum(float(pc.copies[rank]), dev)
+    del A, pc
+    torch.cuda.empty_cache()
+    if rank:
+        return None
+    flops = n ** 3 / 3.0
+    return {"metric": f"partitioned Cholesky GFLOP/s (n=32768, b=512, {world} GPUs)",
+            "value": flops / ms / 1e6, "unit": "GFLOP/s", "ms": ms,
+            "owner_map": "2D block-cyclic over output tiles",
+            "tile_copies": int(copies), "transfers_expected": transfer_count(tb, owner),
+            "transfers_if_kway_partition_owner": t_part,
+            "roofline": {"bound": "tensor", "achieved": flops / ms / 1e9,
+                         "peak": FP64_PEAK_TFLOPS * world, "unit": "TFLOP/s",
+                         "frac": flops / ms / 1e9 / (FP64_PEAK_TFLOPS * world)}}
 
 
 def cholesky_block(args, dev):
