@@ -505,6 +505,79 @@ def cholesky_block(args, dev):
     }
 
 
+REF_CFG5 = {  # reference compare(), seeds 0..4095, MA-1024 38/75, MachineModel(3,1)
+    "eager": (29.18461795232863, 23.15234375),
+    "dmda": (32.08542565885587, 12.678466796875),
+    "gp": (31.596276731658286, 11.28271484375),
+}
+
+
+def policy_sweep(iterations: int = 4096):
+    """Config 5: 4096 x (generate_random_dag(38, 75, MA, 1024), gp/eager/dmda)."""
+    import time as _t
+    import torch
+    import paper_1502_07451_b200 as H
+    from paper_1502_07451_b200.sim import MachineModel, simulate_batch
+    from paper_1502_07451_b200.policies import EagerPolicy, DmdaPolicy, gp_build_batch
+    model = H.SyntheticCostModel()
+    t0 = _t.perf_counter()
+    graphs = [H.attach_weights(H.generate_random_dag(38, 75, "MA", 1024, seed=i), model)
+              for i in range(iterations)]
+    for g in graphs:
+        g.csr()  # lower to device CSR once
+    host_prep = _t.perf_counter() - t0
+    machine = MachineModel(3, 1)
+    out = {"iterations": iterations, "host_graph_prep_s": host_prep}
+    torch.cuda.synchronize()
+    t1 = _t.perf_counter()
+    gp = gp_build_batch(graphs)
+    torch.cuda.synchronize()
+    out["gp_partitions_s"] = _t.perf_counter() - t1
+    sims = 0
+    dev_ms = 0.0
+    exact = True
+    for name, pols in (("eager", [EagerPolicy()] * iterations),
+                       ("dmda", [DmdaPolicy()] * iterations), ("gp", gp)):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = simulate_batch(graphs, pols, machine, validate_graphs=False)
+        b.record()
+        torch.cuda.synchronize()
+        dev_ms += a.elapsed_time(b)
+        sims += iterations
+        mk = statistics.fmean([float(x) for x in res.makespan])
+        tr = statistics.fmean([float(x) for x in res.transfer_count])
+        out[f"{name}_mean_makespan"] = mk
+        out[f"{name}_mean_transfers"] = tr
+        if iterations == 4096:
+            exact &= (mk, tr) == REF_CFG5[name]
+    out["simulate_calls_ms"] = dev_ms  # public API incl. host batch packing
+    # device-only: one packed batch, K8 launch per policy timed with events
+    from paper_1502_07451_b200 import _native
+    from paper_1502_07451_b200.csr import DagBatch
+    from paper_1502_07451_b200.sim import _pin_array
+    batch = DagBatch([g.csr().host for g in graphs])
+    pin = _pin_array(graphs, gp)
+    kern_ms = 0.0
+    for pid, p in ((0, None), (1, None), (2, pin)):
+        _native.simulate_batch(batch, pid, p, 3, 1)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _native.simulate_batch(batch, pid, p, 3, 1)
+        b.record()
+        torch.cuda.synchronize()
+        kern_ms += a.elapsed_time(b)
+    out["des_kernel_ms_3x4096"] = kern_ms
+    out["simulations_per_s"] = sims / (kern_ms / 1e3)
+    out["simulations_per_s_public_api"] = sims / (dev_ms / 1e3)
+    out["sweep_s_incl_gp_partitions"] = out["gp_partitions_s"] + dev_ms / 1e3
+    if iterations == 4096:
+        out["matches_reference_means_bit_exact"] = exact
+    out["reference_cpu_s"] = 80.0  # SURVEY §3C probe: reference compare(), 1 core (not re-timed)
+    return out
+
+
 def secondary(csr10m, args):
     """Config 2, K7 on config 4, config 5 — reported beside the headline."""
     import torch
@@ -540,6 +613,7 @@ def secondary(csr10m, args):
     out["cfg2_evaluate_64_assignments_ms"] = ms
     out["cfg2_transfer_count"] = int(e["xfer_count"][0])
     out["cfg2_transfer_bytes"] = int(e["xfer_bytes"][0])
+    out["cfg5_policy_sweep"] = policy_sweep(4096)
     return out
 
 

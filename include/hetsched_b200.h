@@ -121,6 +121,8 @@ int hs_profile_report(char *buf, int len);
  * sums of w_cpu, w_gpu over nodes (root skipped unless include_root) and
  * of w_xfer over all edges. Synchronous. */
 int hs_exact_totals(const hs_dag_t *g, int include_root, double *out_host, void *stream);
+/* Per graph of a batch: out[3b..3b+2] (device) = fsum of w_cpu, w_gpu, w_xfer. */
+int hs_exact_totals_batch(const hs_dag_batch_t *g, int include_root, double *out, void *stream);
 
 /* ---- K2 evaluate -------------------------------------------------------
  * Replaces partition.evaluate / _finish (partition.py:60-84) for `batch`
@@ -203,6 +205,20 @@ int hs_fm2(const hs_ugraph_t *g, const double *edge_w_sorted,
            const double *weights, double r_cpu, double tol,
            const int32_t *orders, int32_t n_orders, const int8_t *start,
            int8_t *assign, double *cut, double *err, void *stream);
+
+/* Batched hs_fm2 for G independent graphs (config 5's gp policy builds): one
+ * CTA per (graph, start order). Arrays are concatenated: node_off/adj_off/
+ * edge_off [G+1] give each graph's slice of the kernel-indexed arrays
+ * (weights, assignment rows), of adjncy/adjwgt and of the edge list; xadj
+ * holds n_g + 1 LOCAL offsets per graph; orders/assign are [G][R][n_g] at
+ * R * node_off[g]; cut/err/status are [G][R]. r_cpu: [G] device. */
+int hs_fm2_batch(int32_t G, const int64_t *node_off, const int64_t *adj_off,
+                 const int64_t *edge_off, int64_t total_nodes, int32_t max_n,
+                 const int64_t *xadj, const int32_t *adjncy, const double *adjwgt,
+                 const double *edge_w, const int32_t *edge_u, const int32_t *edge_v,
+                 const double *weights, const double *r_cpu, double tol,
+                 const int32_t *orders, int32_t n_orders, int8_t *assign, double *cut,
+                 double *err, int32_t *status, void *stream);
 
 /* Exhaustive 2-way oracle (brute_force_partition, partition.py:87-134) on
  * the device for n <= 30 (the Python API keeps the reference's limit of 20).

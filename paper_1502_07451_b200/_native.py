@@ -301,3 +301,31 @@ def profile_report() -> dict:
         name, launches, ms, nbytes = line.split(",")
         out[name] = {"launches": int(launches), "ms": float(ms), "bytes": float(nbytes)}
     return out
+
+
+_fm2_batch = _opt("hs_fm2_batch", _i32, _P, _P, _P, _i64, _i32, _P, _P, _P, _P, _P, _P, _P, _P, _f64,
+                  _P, _i32, _P, _P, _P, _P, _P)
+_exact_totals_batch = _opt("hs_exact_totals_batch", _P, ctypes.c_int, _P, _P)
+
+
+def fm2_batch(tb, weights, r_cpu, tol, orders, n_orders):
+    """Batched exact 2-way partitioner; returns (assign int8 flat, cut [G,R], err [G,R], status)."""
+    fn = _need(_fm2_batch, "hs_fm2_batch")
+    dev = weights.device
+    G = tb.G
+    assign = torch.empty(n_orders * tb.total_nodes, dtype=torch.int8, device=dev)
+    cut = torch.empty(G, n_orders, dtype=torch.float64, device=dev)
+    err = torch.empty(G, n_orders, dtype=torch.float64, device=dev)
+    status = torch.zeros(G, n_orders, dtype=torch.int32, device=dev)
+    check(fn(G, ptr(tb.node_off), ptr(tb.adj_off), ptr(tb.edge_off), tb.total_nodes, tb.max_n,
+             ptr(tb.xadj), ptr(tb.adjncy), ptr(tb.adjwgt), ptr(tb.edge_w), ptr(tb.edge_u),
+             ptr(tb.edge_v), ptr(weights), ptr(r_cpu), float(tol), ptr(orders), n_orders,
+             ptr(assign), ptr(cut), ptr(err), ptr(status), stream_ptr()))
+    return assign, cut, err, status
+
+
+def exact_totals_batch(batch, include_root: bool) -> torch.Tensor:
+    fn = _need(_exact_totals_batch, "hs_exact_totals_batch")
+    out = torch.empty(batch.batch, 3, dtype=torch.float64, device=batch.device)
+    check(fn(ctypes.byref(batch.struct()), int(include_root), ptr(out), stream_ptr()))
+    return out

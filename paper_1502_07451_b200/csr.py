@@ -218,3 +218,42 @@ class DagBatch:
                 p(self.out_dst), p(self.in_ptr), p(self.in_src), p(self.in_eid),
                 p(self.w_cpu), p(self.w_gpu), p(self.w_xfer), p(self.bytes))
         return self._struct
+
+
+class TwoWayBatch:
+    """Many TwoWayGraphs concatenated (hs_fm2_batch layout)."""
+
+    def __init__(self, hosts: Sequence[HostDag], device=None):
+        dev = device or _native.device()
+        self.G = len(hosts)
+        xadj, adjncy, adjwgt, eu, ev, ew = [], [], [], [], [], []
+        node_off, adj_off, edge_off = [0], [0], [0]
+        for h in hosts:
+            n = h.n - 1
+            keep = (h.src != h.root) & (h.dst != h.root)
+            kp = lambda a: np.where(a < h.root, a, a - 1).astype(np.int32)  # noqa: E731
+            u, v, w = kp(h.src[keep]), kp(h.dst[keep]), h.w_xfer[keep]
+            ne = len(u)
+            node = np.concatenate([u, v])
+            nbr = np.concatenate([v, u])
+            pos = np.concatenate([np.arange(ne), np.arange(ne)])
+            order = np.lexsort((pos, node))
+            xadj.append(_csr_ptr(node, n))
+            adjncy.append(nbr[order].astype(np.int32))
+            adjwgt.append(np.concatenate([w, w])[order])
+            eu.append(u), ev.append(v), ew.append(w)
+            node_off.append(node_off[-1] + n)
+            adj_off.append(adj_off[-1] + 2 * ne)
+            edge_off.append(edge_off[-1] + ne)
+        t = lambda xs, dt: torch.from_numpy(  # noqa: E731
+            np.ascontiguousarray(np.concatenate(xs) if xs else np.zeros(0, dt), dtype=dt)).to(dev)
+        self.node_off_h = np.array(node_off, dtype=np.int64)
+        self.node_off = t([self.node_off_h], np.int64)
+        self.adj_off = t([np.array(adj_off, dtype=np.int64)], np.int64)
+        self.edge_off = t([np.array(edge_off, dtype=np.int64)], np.int64)
+        self.xadj = t(xadj, np.int64)
+        self.adjncy = t(adjncy, np.int32)
+        self.adjwgt = t(adjwgt, np.float64)
+        self.edge_u, self.edge_v, self.edge_w = t(eu, np.int32), t(ev, np.int32), t(ew, np.float64)
+        self.total_nodes = int(node_off[-1])
+        self.max_n = int(max(np.diff(self.node_off_h))) if self.G else 0

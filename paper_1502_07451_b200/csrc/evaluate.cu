@@ -264,3 +264,42 @@ extern "C" int hs_evaluate_kway(const hs_dag_t *g, const int32_t *part, int32_t 
   HS_CHECK_LAUNCH();
   return HS_OK;
 }
+
+namespace {
+// one block per graph of a batch: exact (fsum) totals of w_cpu, w_gpu over the
+// graph's non-root nodes (include_root = 0) and of w_xfer over its edges
+__global__ void totals_batch_kernel(hs_dag_batch_t g, int include_root, double *out) {
+  __shared__ unsigned long long sacc[3 * kAccLimbs];
+  for (int i = threadIdx.x; i < 3 * kAccLimbs; i += blockDim.x) sacc[i] = 0;
+  __syncthreads();
+  const int b = blockIdx.x;
+  const int64_t n0 = g.node_off[b], n1 = g.node_off[b + 1];
+  const int64_t e0 = g.edge_off[b], e1 = g.edge_off[b + 1];
+  const int root = g.root[b];
+  for (int64_t v = n0 + threadIdx.x; v < n1; v += blockDim.x) {
+    if (!include_root && v - n0 == root) continue;
+    hs::superacc_split(g.w_cpu[v], [&](int li, int64_t c) {
+      atomicAdd(&sacc[li], (unsigned long long)c);
+    });
+    hs::superacc_split(g.w_gpu[v], [&](int li, int64_t c) {
+      atomicAdd(&sacc[kAccLimbs + li], (unsigned long long)c);
+    });
+  }
+  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+    hs::superacc_split(g.w_xfer[e], [&](int li, int64_t c) {
+      atomicAdd(&sacc[2 * kAccLimbs + li], (unsigned long long)c);
+    });
+  __syncthreads();
+  if (threadIdx.x < 3)
+    out[3 * b + threadIdx.x] = hs::superacc_round((const int64_t *)(sacc + threadIdx.x * kAccLimbs));
+}
+}  // namespace
+
+extern "C" int hs_exact_totals_batch(const hs_dag_batch_t *g, int include_root, double *out,
+                                     void *stream) {
+  HS_REQUIRE(g && out, HS_EINVAL, "hs_exact_totals_batch: null argument");
+  if (g->batch == 0) return HS_OK;
+  totals_batch_kernel<<<g->batch, 128, 0, (cudaStream_t)stream>>>(*g, include_root, out);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}

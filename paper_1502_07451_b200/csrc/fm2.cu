@@ -118,11 +118,10 @@ __device__ __forceinline__ bool key_less(bool ia, double ca, bool ib, double cb)
   return ca < cb;
 }
 
-__global__ void __launch_bounds__(kThreads) fm2_kernel(FmArgs A) {
+__device__ void fm2_body(const FmArgs &A, const int o) {
   __shared__ Best sbuf[32];
   __shared__ double s_total, s_cpu, s_err, s_cut;
   __shared__ int s_flag;
-  const int o = blockIdx.x;
   const int n = A.n;
   int8_t *asg = A.assign + (int64_t)o * n;
   int8_t *work = A.work + (int64_t)o * n;
@@ -276,6 +275,46 @@ __global__ void __launch_bounds__(kThreads) fm2_kernel(FmArgs A) {
   }
 }
 
+__global__ void __launch_bounds__(kThreads) fm2_kernel(FmArgs A) { fm2_body(A, blockIdx.x); }
+
+// Batched: blockIdx.y = graph, blockIdx.x = start order. Per-graph arrays are
+// concatenated; xadj holds n_g + 1 local offsets per graph.
+struct FmBatch {
+  FmArgs base;
+  const int64_t *node_off, *adj_off, *edge_off;
+  const double *r;
+  int R;
+};
+
+__global__ void __launch_bounds__(kThreads) fm2_batch_kernel(FmBatch Bt) {
+  const int g = blockIdx.y;
+  FmArgs A = Bt.base;
+  const int64_t n0 = Bt.node_off[g];
+  const int n = (int)(Bt.node_off[g + 1] - n0);
+  const int64_t a0 = Bt.adj_off[g], e0 = Bt.edge_off[g];
+  A.n = n;
+  A.xadj = Bt.base.xadj + n0 + g;
+  A.adjncy = Bt.base.adjncy + a0;
+  A.adjwgt = Bt.base.adjwgt + a0;
+  A.ew = Bt.base.ew + e0;
+  A.eu = Bt.base.eu + e0;
+  A.ev = Bt.base.ev + e0;
+  A.ne = Bt.edge_off[g + 1] - e0;
+  A.w = Bt.base.w + n0;
+  A.r = Bt.r[g];
+  const int64_t so = (int64_t)Bt.R * n0;
+  A.orders = Bt.base.orders + so;
+  A.assign = Bt.base.assign + so;
+  A.work = Bt.base.work + so;
+  A.locked = Bt.base.locked + so;
+  A.gain = Bt.base.gain + so;
+  A.trail = Bt.base.trail + so;
+  A.cut_out = Bt.base.cut_out + (int64_t)g * Bt.R;
+  A.err_out = Bt.base.err_out + (int64_t)g * Bt.R;
+  A.status = Bt.base.status + (int64_t)g * Bt.R;
+  if (n > 0) fm2_body(A, blockIdx.x);
+}
+
 // ---- brute_force_partition (partition.py:87-134) ----
 // Mask bit (n-1-k) set = kernel k on GPU; ascending mask = lexicographic
 // order, so "first minimum" = smallest mask among equal keys.
@@ -424,5 +463,42 @@ extern "C" int hs_brute2(int32_t n, const double *weights, double r_cpu, double 
   HS_REQUIRE(!h[2], HS_EPARTITION, "zero total node weight; attach weights first");
   *mask_host = h[0];
   *feasible_host = (int32_t)h[1];
+  return HS_OK;
+}
+
+extern "C" int hs_fm2_batch(int32_t G, const int64_t *node_off, const int64_t *adj_off,
+                            const int64_t *edge_off, int64_t total_nodes, int32_t max_n,
+                            const int64_t *xadj, const int32_t *adjncy, const double *adjwgt,
+                            const double *edge_w, const int32_t *edge_u, const int32_t *edge_v,
+                            const double *weights, const double *r_cpu, double tol,
+                            const int32_t *orders, int32_t n_orders, int8_t *assign, double *cut,
+                            double *err, int32_t *status, void *stream) {
+  HS_REQUIRE(G >= 0 && n_orders > 0, HS_EINVAL, "hs_fm2_batch: bad sizes");
+  if (G == 0) return HS_OK;
+  HS_REQUIRE(G <= 65535, HS_ELIMIT, "at most 65535 graphs per batch");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t cells = (int64_t)n_orders * total_nodes;
+  hs::Scratch<int8_t> work, locked;
+  hs::Scratch<double> gain;
+  hs::Scratch<int32_t> trail;
+  HS_CHECK_CUDA(work.alloc(cells, s));
+  HS_CHECK_CUDA(locked.alloc(cells, s));
+  HS_CHECK_CUDA(gain.alloc(cells, s));
+  HS_CHECK_CUDA(trail.alloc(cells, s));
+  FmBatch Bt;
+  memset(&Bt, 0, sizeof Bt);
+  Bt.base.xadj = xadj; Bt.base.adjncy = adjncy; Bt.base.adjwgt = adjwgt;
+  Bt.base.ew = edge_w; Bt.base.eu = edge_u; Bt.base.ev = edge_v;
+  Bt.base.w = weights; Bt.base.tol = tol; Bt.base.orders = orders; Bt.base.start = nullptr;
+  Bt.base.assign = assign; Bt.base.cut_out = cut; Bt.base.err_out = err; Bt.base.status = status;
+  Bt.base.work = work; Bt.base.locked = locked; Bt.base.gain = gain; Bt.base.trail = trail;
+  Bt.node_off = node_off; Bt.adj_off = adj_off; Bt.edge_off = edge_off; Bt.r = r_cpu;
+  Bt.R = n_orders;
+  const int threads = max_n >= 4096 ? kThreads : (max_n >= 512 ? 256 : (max_n >= 64 ? 64 : 32));
+  {
+    hs::Prof P("fm2_batch", s, 0.0);
+    fm2_batch_kernel<<<dim3(n_orders, G), threads, 0, s>>>(Bt);
+  }
+  HS_CHECK_LAUNCH();
   return HS_OK;
 }

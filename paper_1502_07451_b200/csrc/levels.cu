@@ -48,7 +48,13 @@ struct LevelArgs {
   int32_t *processed; // [1]
 };
 
+constexpr int kStage = 2048;  // frontier entries staged per block and level
+
 __global__ void levels_kernel(LevelArgs A) {
+  __shared__ int32_t s_buf[kStage];
+  __shared__ int s_n, s_base;
+  if (threadIdx.x == 0) s_n = 0;
+  __syncthreads();
   GridBarrier bar{A.bar, A.bar + 1};
   const hs_dag_t &g = A.g;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -67,7 +73,9 @@ __global__ void levels_kernel(LevelArgs A) {
     const int32_t ncur = __ldcg(&A.counts[cur]);
     if (ncur == 0) break;
     if (tid == 0) A.counts[(it + 2) % 3] = 0;
-    for (int64_t i = tid; i < ncur; i += stride) {
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ncur; base += stride) {
+      const int64_t i = base + threadIdx.x;
+      if (i >= ncur) continue;
       const int v = __ldcg(&A.front[cur][i]);
       double reach = 0.0;
       int lv = 0;
@@ -90,8 +98,22 @@ __global__ void levels_kernel(LevelArgs A) {
       ++done;
       for (int64_t e = g.out_ptr[v]; e < g.out_ptr[v + 1]; ++e) {
         int s = g.out_dst[e];
-        if (atomicSub(&A.indeg[s], 1) == 1) A.front[nxt][atomicAdd(&A.counts[nxt], 1)] = s;
+        if (atomicSub(&A.indeg[s], 1) == 1) {
+          // block-local staging: one global atomic per flush, not per node
+          int at = atomicAdd(&s_n, 1);
+          if (at < kStage) s_buf[at] = s;
+          else A.front[nxt][atomicAdd(&A.counts[nxt], 1)] = s;  // overflow: direct
+        }
       }
+    }
+    __syncthreads();
+    {
+      const int cnt = s_n < kStage ? s_n : kStage;
+      if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&A.counts[nxt], cnt);
+      __syncthreads();
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) A.front[nxt][s_base + i] = s_buf[i];
+      __syncthreads();
+      if (threadIdx.x == 0) s_n = 0;
     }
     bar.sync(gridDim.x);
   }

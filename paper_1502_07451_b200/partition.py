@@ -213,3 +213,75 @@ def partition_heuristic(graph: TaskGraph, targets: PartitionTargets,
         if best is None or key < best[0]:
             best = (key, k)
     return _finish(graph, _assignment_dict(csr, assign[best[1]]), targets, source, tol)
+
+
+_ORDER_CACHE: Dict[Tuple[int, int, int], np.ndarray] = {}
+
+
+def _shuffles(n: int, config: PartitionConfig) -> np.ndarray:
+    """The restart permutations depend only on (n, seed, restarts): cached."""
+    key = (n, config.seed, config.restarts)
+    if key not in _ORDER_CACHE:
+        out = np.empty((config.restarts, n), dtype=np.int32)
+        for r in range(config.restarts):
+            perm = list(range(n))
+            random.Random(config.seed * 1_000_003 + r).shuffle(perm)
+            out[r] = perm
+        _ORDER_CACHE[key] = out
+    return _ORDER_CACHE[key]
+
+
+def partition_heuristic_batch(graphs: Sequence[TaskGraph], targets: Sequence[PartitionTargets],
+                              config: Optional[PartitionConfig] = None) -> List[Dict[int, str]]:
+    """``partition_heuristic`` for many graphs in one launch; returns the assignments.
+
+    Same semantics per graph (partition.py:258-295): degenerate targets
+    short-circuit, otherwise 1 + restarts start orders refined by FM on the
+    device (one CTA per graph x order), winner by (not feasible, cut, err, lex).
+    """
+    from .csr import TwoWayBatch
+    config = config or PartitionConfig()
+    source, tol = config.node_weight_source, config.imbalance_tolerance
+    out: List[Optional[Dict[int, str]]] = [None] * len(graphs)
+    work = []
+    for gi, (g, t) in enumerate(zip(graphs, targets)):
+        ids = g.kernel_ids()
+        if not ids:
+            raise PartitionError("graph has no non-root kernels")
+        w = np.array([_node_weight(g.nodes[i], source) for i in ids], dtype=np.float64)
+        if not np.any(w):
+            raise PartitionError("zero total node weight; attach weights first")
+        if t.r_cpu == 0.0 or t.r_cpu == 1.0:
+            side = GPU if t.r_cpu == 0.0 else CPU
+            out[gi] = {i: side for i in ids}
+        else:
+            work.append((gi, g, t, w))
+    if not work:
+        return out
+    R = config.restarts + 1
+    tb = TwoWayBatch([g.csr().host for _, g, _, _ in work])
+    orders = []
+    for _, g, _, w in work:
+        o = np.empty((R, len(w)), dtype=np.int32)
+        o[0] = np.argsort(-w, kind="stable")
+        o[1:] = _shuffles(len(w), config)
+        orders.append(o.reshape(-1))
+    dev = tb.xadj.device
+    weights = torch.from_numpy(np.concatenate([w for *_, w in work])).to(dev)
+    r = torch.tensor([t.r_cpu for _, _, t, _ in work], dtype=torch.float64, device=dev)
+    ordt = torch.from_numpy(np.concatenate(orders)).to(dev)
+    assign, cut, err, status = _native.fm2_batch(tb, weights, r, tol, ordt, R)
+    if bool((status != 0).any()):
+        raise PartitionError("zero total node weight; attach weights first")
+    assign, cut, err = assign.cpu().numpy(), cut.cpu().numpy(), err.cpu().numpy()
+    for b, (gi, g, _, w) in enumerate(work):
+        n = len(w)
+        rows = assign[R * tb.node_off_h[b]: R * tb.node_off_h[b] + R * n].reshape(R, n)
+        best = None
+        for k in range(R):
+            key = (not bool(err[b, k] <= tol), float(cut[b, k]), float(err[b, k]),
+                   tuple(rows[k].tolist()))
+            if best is None or key < best[0]:
+                best = (key, k)
+        out[gi] = _assignment_dict(g.csr(), rows[best[1]])
+    return out

@@ -263,6 +263,7 @@ def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGrap
     """
     if iterations < 1:
         raise SimulationError("iterations must be >= 1")
+    batched_gp = policy_builder is None
     if policy_builder is None:
         from .policies import build_policy
         policy_builder = lambda name, g: build_policy(name, g)  # noqa: E731
@@ -272,7 +273,11 @@ def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGrap
         _check_graph(g)
     rows: List[CompareRow] = []
     for name in policy_names:
-        policies = [policy_builder(name, g) for g in graphs]
+        if name == "gp" and batched_gp:  # all gp decisions in one device launch
+            from .policies import gp_build_batch
+            policies = gp_build_batch(graphs)
+        else:
+            policies = [policy_builder(name, g) for g in graphs]
         res = simulate_batch(graphs, policies, machine, validate_graphs=False)
         makespans = [float(x) for x in res.makespan]
         transfers = [float(x) for x in res.transfer_count]

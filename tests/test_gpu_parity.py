@@ -188,3 +188,14 @@ def test_random_graphs_against_oracle():
             tr = simulate(g, GraphPartitionPolicy(pin) if pin else H.build_policy(pol, g))
             ref = O.simulate(og, pol, pin)
             assert tr.makespan == ref["makespan"] and tr.transfer_count == ref["transfer_count"]
+
+
+def test_batched_partition_equals_single():
+    from paper_1502_07451_b200.partition import partition_heuristic_batch
+    from paper_1502_07451_b200.costs import workload_ratio_batch
+    graphs = [random_weighted_graph(s, max_kernels=18) for s in range(300, 340)]
+    targets = workload_ratio_batch(graphs)
+    assert [t.r_cpu for t in targets] == [H.workload_ratio(g).r_cpu for g in graphs]
+    batch = partition_heuristic_batch(graphs, targets)
+    for g, t, a in zip(graphs, targets, batch):
+        assert a == partition_heuristic(g, t).assignment
