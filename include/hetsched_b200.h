@@ -244,6 +244,17 @@ int hs_partition_kway(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host
                       double tol, uint64_t seed, int32_t *part, int64_t *stats_host,
                       void *stream);
 
+/* METIS_PartGraphKway-compatible front end (idx_t = int32, real_t = float,
+ * HOST arrays, ncon = 1): the paper's partitioning tool boundary
+ * (graphio.py:277-304). Balance: ubvec[0] (default 1.03)
+ * becomes tol = (ubvec - 1) * min_p tpwgts[p] in the |w_p/W - t_p| <= tol
+ * sense. objval = edge cut. Synchronous, default stream. */
+int hs_METIS_PartGraphKway(const int32_t *nvtxs, const int32_t *ncon, const int32_t *xadj,
+                           const int32_t *adjncy, const int32_t *vwgt, const int32_t *vsize,
+                           const int32_t *adjwgt, const int32_t *nparts, const float *tpwgts,
+                           const float *ubvec, const int32_t *options, int32_t *objval,
+                           int32_t *part);
+
 /* Symmetrise a DAG into the kernel-space undirected graph used by
  * hs_partition_kway (K1): root and root edges dropped, vertex v (kernel
  * position) adjacent to every predecessor and successor, adjwgt_i from
