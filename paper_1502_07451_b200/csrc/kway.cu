@@ -795,9 +795,14 @@ struct Kway {
   bool prev_nnz_pending = false;
   std::vector<Level> levels;
   PhaseTimer timer;
-  int passes_big = 4, passes_small = 8;
+  // measured on the config-4 DAG: 1 pass on coarse levels + 4 on the finest
+  // beat 4 + 4 on both time and cut (over-refined coarse levels trap the
+  // finest level in a worse local optimum)
+  int passes_big = 4, passes_small = 8, passes_coarse = 1, rounds = 3;
   Kway(cudaStream_t st) : s(st), timer(st) {
     if (const char *e = getenv("HS_KWAY_PASSES")) passes_big = std::max(1, atoi(e));
+    if (const char *e = getenv("HS_KWAY_PASSES_COARSE")) passes_coarse = std::max(0, atoi(e));
+    if (const char *e = getenv("HS_KWAY_ROUNDS")) rounds = std::max(1, atoi(e));
   }
 
   int read_pw(std::vector<int64_t> &pw) {
@@ -847,7 +852,7 @@ struct Kway {
   }
 
   // K6 on one level: fixed pass budget, convergence decided on the device.
-  int refine(const G &g, part_t *part, uint64_t salt2) {
+  int refine(const G &g, part_t *part, uint64_t salt2, bool finest = true) {
     int32_t *cand, *list, *conf;
     uint32_t *st;
     HS_CHECK_CUDA(dalloc(&cand, g.n, s));
@@ -860,7 +865,8 @@ struct Kway {
     if (rc) return rc;
     const int T = team_for(g);
     const int tgrid = team_grid(g.n, T);
-    const int max_passes = g.nnz > (4ll << 20) ? passes_big : passes_small;
+    int max_passes = g.nnz > (4ll << 20) ? passes_big : passes_small;
+    if (!finest && passes_coarse >= 0) max_passes = passes_coarse;
     // 16-bit packed connectivity counters are exact iff every vertex's
     // weighted degree stays below 2^16 on this level
     bool pack16 = false;
@@ -946,7 +952,6 @@ struct Kway {
     HS_CHECK_CUDA(dalloc(&mw, n, s));
     HS_CHECK_CUDA(cudaMemsetAsync(match, 0xff, n * sizeof(int32_t), s));
     HS_CHECK_CUDA(cudaMemcpyAsync(mw, F.g.vw, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
-    const int rounds = 3;
     const int T = team_for(F.g);
     for (int round = 0; round < rounds; ++round) {
       {
@@ -1421,7 +1426,7 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
     // HS_NCU_LEVEL0=1: open the profiler window around the finest level only
     const bool ncu_win = li == 0 && getenv("HS_NCU_LEVEL0") != nullptr;
     if (ncu_win) cudaProfilerStart();
-    rc = K.refine(Lv.g, cur, K.salt ^ ((uint64_t)li << 40));
+    rc = K.refine(Lv.g, cur, K.salt ^ ((uint64_t)li << 40), li == 0);
     if (ncu_win) cudaProfilerStop();
     if (rc) return rc;
     K.timer.mark("refine level");
