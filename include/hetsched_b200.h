@@ -98,6 +98,9 @@ typedef struct hs_ugraph {
     const double *vwgt;      /* [n]  fp64 vertex weights (exact 2-way path) */
     const int32_t *vwgt_i;   /* [n]  integer vertex weights (k-way path);
                                 total must be < 2^31 */
+    const int32_t *twin;     /* [nnz] optional: position of the reverse entry
+                                (u in v's list <-> v in u's list); enables the
+                                ghost-part refinement on the finest level */
 } hs_ugraph_t;
 
 /* ---- status / library ------------------------------------------------ */
@@ -261,10 +264,11 @@ int hs_METIS_PartGraphKway(const int32_t *nvtxs, const int32_t *ncon, const int3
  * edge_w_i (out order), vwgt_i copied from node_w_i (node index space).
  * edge_w_i_in (optional) holds the same weights in in-order (the DAG's CSC
  * copy of the edge attribute); without it they are gathered via in_eid.
+ * twin (optional, [2m] int32) receives each entry's reverse-entry position. 
  * xadj/adjncy/adjwgt_i/vwgt_i are caller buffers sized (n-1)+1 / 2m. */
 int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *edge_w_i_in,
                   const int32_t *node_w_i, int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i,
-                  int32_t *vwgt_i, int64_t *nnz_host, void *stream);
+                  int32_t *vwgt_i, int32_t *twin, int64_t *nnz_host, void *stream);
 
 /* Device generator of the layered fan-in DAG family of configs 2 and 4:
  * n kernels over ceil(sqrt(n)) layers, m inter-kernel edges spread as evenly

@@ -55,7 +55,7 @@ class HsDagBatch(ctypes.Structure):
 class HsUGraph(ctypes.Structure):
     _fields_ = [("n", _i32), ("nnz", _i64), ("xadj", _c_void_p), ("adjncy", _c_void_p),
                 ("adjwgt", _c_void_p), ("adjwgt_i", _c_void_p),
-                ("vwgt", _c_void_p), ("vwgt_i", _c_void_p)]
+                ("vwgt", _c_void_p), ("vwgt_i", _c_void_p), ("twin", _c_void_p)]
 
 
 class HsEvent(ctypes.Structure):
@@ -95,7 +95,7 @@ def _opt(name, *argtypes):
 _fm2 = _opt("hs_fm2", _P, _P, _P, _P, _i64, _P, _f64, _f64, _P, _i32, _P, _P, _P, _P, _P)
 _brute2 = _opt("hs_brute2", _i32, _P, _f64, _f64, _P, _P, _P, _i64, _P, _P, _P)
 _partition_kway = _opt("hs_partition_kway", _P, _i32, _P, _f64, ctypes.c_uint64, _P, _P, _P)
-_symmetrize = _opt("hs_symmetrize", _P, _P, _P, _P, _P, _P, _P, _P, _P, _P)
+_symmetrize = _opt("hs_symmetrize", _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P)
 _layered_sizes = _opt("hs_layered_sizes", _i64, _i64, _P, _P)
 _layered_generate = _opt("hs_layered_generate", _i64, _i64, ctypes.c_uint64,
                          _P, _P, _P, _P, _P, _P, _P)
@@ -252,11 +252,12 @@ def partition_kway(ug, k: int, tpwgts, tol: float, seed: int, part: torch.Tensor
     return list(stats)
 
 
-def symmetrize(csr, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, edge_w_i_in=None) -> int:
+def symmetrize(csr, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, edge_w_i_in=None,
+               twin=None) -> int:
     fn = _need(_symmetrize, "hs_symmetrize")
     nnz = ctypes.c_int64(0)
     check(fn(ctypes.byref(csr.struct()), ptr(edge_w_i), ptr(edge_w_i_in), ptr(node_w_i), ptr(xadj),
-             ptr(adjncy), ptr(adjwgt_i), ptr(vwgt_i), ctypes.byref(nnz), stream_ptr()))
+             ptr(adjncy), ptr(adjwgt_i), ptr(vwgt_i), ptr(twin), ctypes.byref(nnz), stream_ptr()))
     return nnz.value
 
 

@@ -47,9 +47,10 @@ constexpr int kMaxParts = 64;
 using part_t = int8_t;  // part ids (k <= 64) as bytes: 4x less gather traffic
 
 struct G {
-  int32_t n;
-  int64_t cap;  // adjacency slots (padded)
-  int64_t nnz;  // live adjacency entries
+  int32_t n = 0;
+  int64_t cap = 0;  // adjacency slots (padded)
+  int64_t nnz = 0;  // live adjacency entries
+  const int32_t *twin = nullptr;  // reverse-entry positions (finest level only)
   int64_t *xbeg;
   int32_t *deg;
   int32_t *adj;
@@ -115,7 +116,8 @@ __global__ void sym_degree(hs_dag_t g, int32_t *deg) {
 // out-neighbours. ew_in (in-order weights) avoids a random gather through
 // in_eid when the caller has it; otherwise the weight is gathered.
 __global__ void sym_fill(hs_dag_t g, const int32_t *ew, const int32_t *ew_in, const int32_t *nw,
-                         const int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw) {
+                         const int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw,
+                         int32_t *twin) {
   constexpr int T = 8;
   const int lane = (threadIdx.x & 31) % T;
   const int64_t step = (int64_t)warps_total() * (32 / T);
@@ -131,8 +133,15 @@ __global__ void sym_fill(hs_dag_t g, const int32_t *ew, const int32_t *ew_in, co
       if (j == rs) continue;
       const int u = g.in_src[j];
       const int64_t at = pos + (j - i0) - (rs >= 0 && j > rs ? 1 : 0);
-      adj[at] = u < g.root ? u : u - 1;
+      const int ku = u < g.root ? u : u - 1;
+      adj[at] = ku;
       wgt[at] = ew_in ? ew_in[j] : ew[g.in_eid[j]];
+      if (twin) {  // the reverse entry is v in u's out-part: xadj[ku+1] - outdeg(u) + rank
+        const int64_t e = g.in_eid[j];
+        const int64_t tw = xadj[ku + 1] - g.out_ptr[u + 1] + e;
+        twin[at] = (int32_t)tw;
+        twin[tw] = (int32_t)at;
+      }
     }
     const int64_t opos = pos + (i1 - i0) - (rs >= 0 ? 1 : 0);
     const int64_t o0 = g.out_ptr[v], o1 = g.out_ptr[v + 1];
@@ -647,7 +656,8 @@ __global__ void move_flows(int n, const int32_t *vw, const part_t *part, const i
 // expected inflow of every part within its room.
 __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, const double *prob,
                               int k, uint64_t salt, part_t *part, int64_t *pw,
-                              const int32_t *run) {
+                              const int32_t *run, const int64_t *xbeg, const int32_t *deg,
+                              const int32_t *twin, part_t *gp) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -663,6 +673,8 @@ __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, con
     if (pr < 1.0 && (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
       continue;
     part[v] = dest;
+    if (gp)
+      for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
     atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
     atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
   }
@@ -708,6 +720,31 @@ __global__ void seg_bounds(int n, const int64_t *xbeg, const int32_t *deg, int64
 }
 
 #include "kway_team.cuh"
+
+__global__ void ghost_fill(int64_t nnz, const int32_t *adj, const part_t *part, part_t *gp) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (int64_t)gridDim.x * blockDim.x)
+    gp[j] = part[adj[j]];
+}
+
+// out[0] = min weight, out[1] = -max weight (both via atomicMin; the caller
+// initialises both words to 0x7f7f7f7f)
+__global__ void wrange_kernel(int64_t nnz, const int32_t *w, int32_t *out) {
+  int mn = INT_MAX, mx = INT_MIN;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    mn = min(mn, w[j]);
+    mx = max(mx, w[j]);
+  }
+  for (int off = 16; off; off >>= 1) {
+    mn = min(mn, __shfl_down_sync(0xffffffffu, mn, off));
+    mx = max(mx, __shfl_down_sync(0xffffffffu, mx, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&out[0], mn);
+    atomicMin(&out[1], -mx);
+  }
+}
 
 // max over vertices of the weighted degree (saturating at 2^30)
 __global__ void max_wdeg_kernel(G g, int32_t *out) {
@@ -791,6 +828,7 @@ struct Kway {
   double *d_prob = nullptr, *d_cum = nullptr;
   int32_t *counter = nullptr;
   int32_t *ctl = nullptr;   // device control block (see CTL_* in kway_team.cuh)
+  part_t *gp = nullptr;     // ghost parts of the level being refined (finest only)
   int64_t *d_nnz = nullptr, *h_nnz = nullptr;
   bool prev_nnz_pending = false;
   std::vector<Level> levels;
@@ -845,7 +883,7 @@ struct Kway {
                                           ctl);
       HS_CHECK_LAUNCH();
       apply_thinned<<<grid, 256, 0, s>>>(g.n, g.vw, cand, d_prob, k, salt2 + rb * 7919, part, d_pw,
-                                         ctl + CTL_APPLY);
+                                         ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
       HS_CHECK_LAUNCH();
     }
     return HS_OK;
@@ -861,6 +899,22 @@ struct Kway {
     HS_CHECK_CUDA(dalloc(&conf, g.n, s));
     int rc = weights(g, part);
     if (rc) return rc;
+    // finest level with twins: ghost copies of the neighbours' parts inside
+    // the adjacency stream (refinement reads 1 coalesced byte per entry)
+    int32_t wconst = 0;
+    if (finest && g.twin) {
+      HS_CHECK_CUDA(dalloc(&gp, g.nnz, s));
+      ghost_fill<<<hs::grid_for(g.nnz, 256), 256, 0, s>>>(g.nnz, g.adj, part, gp);
+      HS_CHECK_LAUNCH();
+      HS_CHECK_CUDA(cudaMemsetAsync(ctl + 13, 0x7f, 2 * sizeof(int32_t), s));
+      wrange_kernel<<<hs::grid_for(g.nnz, 256, hs::sm_count() * 8), 256, 0, s>>>(g.nnz, g.wgt,
+                                                                               ctl + 13);
+      HS_CHECK_LAUNCH();
+      int32_t mm[2];
+      HS_CHECK_CUDA(cudaMemcpyAsync(mm, ctl + 13, sizeof mm, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      if (mm[0] == -mm[1]) wconst = mm[0];  // every edge weight equal: skip the weight stream
+    }
     rc = rebalance(g, part, cand, salt2 ^ 0xabcdefull, 3);
     if (rc) return rc;
     const int T = team_for(g);
@@ -886,8 +940,9 @@ struct Kway {
       HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
       {
         hs::Prof P("refine_candidates", s, 28.0 * g.n + 12.0 * g.nnz);
-        HS_REFINE_DISPATCH(T, k, pack16, tgrid, g, part, k, d_pw, d_hi, d_lo, st, list,
-                           ctl + CTL_COUNT, ctl + CTL_ACTIVE);
+        const int TR = k <= 16 ? refine_team_for(g) : team_for(g);
+        HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, part, k, d_pw, d_hi, d_lo, st,
+                           list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst);
       }
       HS_CHECK_LAUNCH();
       {
@@ -901,10 +956,14 @@ struct Kway {
       HS_CHECK_LAUNCH();
       apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
           list, ctl + CTL_COUNT, conf, g.vw, d_prob, k, salt2 + pass * 104729, part, d_pw,
-          ctl + CTL_APPLY);
+          ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
       HS_CHECK_LAUNCH();
     }
     rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8);
+    if (gp) {
+      cudaFreeAsync(gp, s);
+      gp = nullptr;
+    }
     cudaFreeAsync(cand, s);
     cudaFreeAsync(st, s);
     cudaFreeAsync(list, s);
@@ -1162,6 +1221,7 @@ struct Kway {
     if (Lv.own_wgt) cudaFreeAsync(g.wgt, s);
     g.adj = adj2;
     g.wgt = wgt2;
+    g.twin = nullptr;  // positions moved: the reverse-entry index no longer applies
     Lv.own_adj = Lv.own_wgt = true;
     cudaFreeAsync(b, s);
     cudaFreeAsync(e, s);
@@ -1188,15 +1248,15 @@ struct Kway {
       cudaFreeAsync(vw64, s);
       cudaFreeAsync(prefix, s);
     }
-    int64_t best_cut = cut_of(g, best);
-    std::vector<int64_t> pw;
-    int rc = weights(g, best);
-    if (rc) return rc;
-    rc = read_pw(pw);
-    if (rc) return rc;
-    bool best_feas = feasible(pw);
     // warp trials (BFS-order LDG + greedy refinement) on small coarsest graphs
     if (nc <= 32768) {
+      const int64_t best_cut = cut_of(g, best);
+      std::vector<int64_t> pw;
+      int rc = weights(g, best);
+      if (rc) return rc;
+      rc = read_pw(pw);
+      if (rc) return rc;
+      const bool best_feas = feasible(pw);
       rc = sort_lists(Cst);  // trials depend on list order: make it canonical
       if (rc) return rc;
       const int trials = nc <= 8192 ? 256 : 64;
@@ -1237,8 +1297,9 @@ struct Kway {
 
 extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i,
                              const int32_t *edge_w_i_in, const int32_t *node_w_i, int64_t *xadj,
-                             int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int64_t *nnz_host,
-                             void *stream) {
+                             int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,
+                             int64_t *nnz_host, void *stream) {
+  HS_REQUIRE(!twin || 2 * g->m < (1ll << 31), HS_ELIMIT, "twin indices need < 2^31 entries");
   HS_REQUIRE(g && edge_w_i && node_w_i && xadj && adjncy && adjwgt_i && vwgt_i, HS_EINVAL,
              "hs_symmetrize: null argument");
   cudaStream_t s = (cudaStream_t)stream;
@@ -1257,7 +1318,7 @@ extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i,
   rc = exclusive_scan<int64_t>(deg64, xadj, nk + 1, s);
   if (rc) return rc;
   sym_fill<<<std::max(1, std::min(hs::sm_count() * 32, (g->n * 8 + 255) / 256)), 256, 0, s>>>(
-      *g, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i);
+      *g, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin);
   HS_CHECK_LAUNCH();
   if (nnz_host) {
     HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nk, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1327,6 +1388,7 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   L0.g.nnz = nnz0;
   L0.g.xbeg = const_cast<int64_t *>(ug->xadj);
   L0.g.adj = const_cast<int32_t *>(ug->adjncy);
+  L0.g.twin = ug->twin;
   L0.g.vw = const_cast<int32_t *>(ug->vwgt_i);
   HS_CHECK_CUDA(dalloc(&L0.g.deg, n0, s));
   deg_from_xadj<<<hs::grid_for(n0, 256), 256, 0, s>>>(ug->xadj, n0, L0.g.deg);

@@ -8,7 +8,7 @@
 #pragma once
 
 template <int T>
-__device__ __forceinline__ int team_lane() { return (threadIdx.x & 31) % T; }
+__device__ __forceinline__ int team_lane() { return T == 1 ? 0 : (threadIdx.x & 31) % T; }
 
 template <int T>
 __device__ __forceinline__ int team_sum(int x) {
@@ -101,9 +101,16 @@ __device__ __forceinline__ int st_gain(uint32_t s) { return (int)(s >> 14); }
 template <int T, int KR>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
-              const int64_t *lo, uint32_t *st, int32_t *list, int32_t *count, const int32_t *run) {
+              const int64_t *lo, uint32_t *st, int32_t *list, int32_t *count, const int32_t *run,
+              const part_t *gp, int32_t wconst) {
   if (run && !*run) return;
-  __shared__ int32_t conn_s[KR > 0 ? 1 : kTeamBlock / T][kMaxParts];
+  __shared__ int32_t conn_s[KR != 0 ? 1 : kTeamBlock / T][kMaxParts];
+  // KR < 0: per-lane private counters, [part][thread] so every lane hits its
+  // own bank; zeroed here and re-zeroed by the lanes that reduce them
+  __shared__ int32_t priv_s[KR < 0 ? -KR : 1][kTeamBlock];
+  if constexpr (KR < 0) {
+    for (int i = threadIdx.x; i < (-KR) * kTeamBlock; i += blockDim.x) (&priv_s[0][0])[i] = 0;
+  }
   // part weights and bounds are read for every vertex: keep them on chip
   // (global reads of these few lines made one L2 slice the bottleneck)
   __shared__ int64_t s_pw[kMaxParts], s_hi[kMaxParts], s_lo[kMaxParts];
@@ -130,7 +137,58 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       b = g.xbeg[v];
       d = g.deg[v];
     }
-    if constexpr (KR > 0) {
+    if constexpr (KR < 0) {
+      const int tcol = threadIdx.x, base_col = threadIdx.x - lane;
+      for (int j0 = lane; j0 < d; j0 += 4 * T) {
+        int w[4], p[4];
+        if (gp) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q * T;
+            p[q] = j < d ? (int)gp[b + j] : -1;
+            w[q] = j < d ? (wconst ? wconst : __ldg(g.wgt + b + j)) : 0;
+          }
+        } else {
+          int u[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q * T;
+            u[q] = j < d ? __ldg(g.adj + b + j) : -1;
+            w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (p[q] >= 0) {
+            bnd |= p[q] != own;
+            priv_s[p[q]][tcol] += w[q];
+          }
+      }
+      __syncwarp();
+      bnd = team_or<T>(bnd);
+      // every lane reads the own-part row (rotated columns: distinct banks)
+      int cown = 0;
+      for (int c = 0; c < T; ++c) cown += priv_s[own][base_col + ((c + lane) & (T - 1))];
+      __syncwarp();
+      // lane handles parts lane, lane + T, ...: team total, then re-zero
+      const bool can = valid && bnd && s_pw[own] - vwv >= s_lo[own];
+      for (int q = lane; q < k; q += T) {
+        int cq = 0;
+        for (int c = 0; c < T; ++c) {
+          const int col = base_col + ((c + lane) & (T - 1));
+          cq += priv_s[q][col];
+          priv_s[q][col] = 0;
+        }
+        if (can && q != own && s_pw[q] + vwv <= s_hi[q]) {
+          const int gain = cq - cown;
+          if (gain > bg) { bg = gain; bp = q; }  // ascending q: ties keep the smaller part
+        }
+      }
+      __syncwarp();
+      team_argmax<T>(bg, bp);
+    } else if constexpr (KR > 0) {
       // PK = 2: two 16-bit counters per register (host guarantees every
       // vertex's weighted degree < 2^16 on this level); PK = 1: 32-bit.
       constexpr int PK = KR == 8 ? 2 : 1;
@@ -140,15 +198,25 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       for (int i = 0; i < NR; ++i) c[i] = 0;
       // 4 neighbours per lane in flight: independent adj loads, then gathers
       for (int j0 = lane; j0 < d; j0 += 4 * T) {
-        int u[4], w[4], p[4];
+        int w[4], p[4];
+        if (gp) {  // ghost parts: one coalesced byte per entry, no gather
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int j = j0 + q * T;
-          u[q] = j < d ? __ldg(g.adj + b + j) : -1;
-          w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+          for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q * T;
+            p[q] = j < d ? (int)gp[b + j] : own;
+            w[q] = j < d ? (wconst ? wconst : __ldg(g.wgt + b + j)) : 0;
+          }
+        } else {
+          int u[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int j = j0 + q * T;
+            u[q] = j < d ? __ldg(g.adj + b + j) : -1;
+            w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : own;
         }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : own;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           bnd |= p[q] != own;
@@ -283,7 +351,9 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
 // prob[own] * prob[k + dest] (hash of (salt, v): deterministic thinning).
 __global__ void apply_list(const int32_t *list, const int32_t *count, const int32_t *conf,
                            const int32_t *vw, const double *prob, int k, uint64_t salt,
-                           part_t *part, int64_t *pw, const int32_t *run) {
+                           part_t *part, int64_t *pw, const int32_t *run,
+                           const int64_t *xbeg, const int32_t *deg, const int32_t *twin,
+                           part_t *gp) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -302,6 +372,8 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
         (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
       continue;
     part[v] = dest;
+    if (gp)  // keep the ghost copies in the neighbours' lists current
+      for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
     atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
     atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
   }
@@ -396,15 +468,44 @@ cut_t(G g, const part_t *part, unsigned long long *cut2) {
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(cut2, local);
 }
 
+// private shared-memory counters (default) vs register select chains
+inline bool refine_private() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("HS_KWAY_REGCONN");
+    v = (e && e[0] == '1') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 inline int team_for(const G &g) {
   const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
   return avg <= 24.0 ? 8 : (avg <= 64.0 ? 16 : 32);
 }
 
+// team size of the refinement candidate scan (private-counter path supports
+// 1/4/8/16/32); HS_KWAY_TREFINE overrides the fine-level choice for sweeps
+inline int refine_team_for(const G &g) {
+  const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
+  static int force = -2;
+  if (force == -2) {
+    const char *e = getenv("HS_KWAY_TREFINE");
+    force = e ? atoi(e) : 4;  // measured: 4 lanes per vertex beat 8 and 1 at degree ~20
+  }
+  if (avg <= 24.0 && force > 0) return force;
+  return team_for(g);
+}
+
 // refine_cand_t<T, KR>: KR = 8 / 16 register accumulators, 0 = shared memory
 #define HS_REFINE_DISPATCH(T_, K_, PACK16_, GRID, ...)                          \
   do {                                                                           \
-    if ((K_) <= 8 && (PACK16_)) {                                                \
+    if ((K_) <= 16 && refine_private()) {                                        \
+      if ((T_) == 1) refine_cand_t<1, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);      \
+      else if ((T_) == 4) refine_cand_t<4, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 8) refine_cand_t<8, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 16) refine_cand_t<16, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);\
+      else refine_cand_t<32, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);               \
+    } else if ((K_) <= 8 && (PACK16_)) {                                         \
       if ((T_) == 8) refine_cand_t<8, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);        \
       else if ((T_) == 16) refine_cand_t<16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
       else refine_cand_t<32, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);                 \

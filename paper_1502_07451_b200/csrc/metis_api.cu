@@ -55,6 +55,7 @@ extern "C" int hs_METIS_PartGraphKway(const int32_t *nvtxs, const int32_t *ncon,
   g.adjwgt_i = dw;
   g.vwgt = nullptr;
   g.vwgt_i = dv;
+  g.twin = nullptr;
   int64_t stats[8] = {0};
   int rc = hs_partition_kway(&g, k, tp.data(), tol, 0, dp, stats, s);
   if (rc) return rc;

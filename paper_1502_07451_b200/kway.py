@@ -14,6 +14,7 @@ These are additive to the reference API (which stops at 2-way).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Dict, Optional, Sequence
 
@@ -28,8 +29,9 @@ from .csr import DagCSR
 class UGraph:
     """Undirected integer-weighted kernel graph on the device (hs_ugraph_t)."""
 
-    def __init__(self, xadj, adjncy, adjwgt, vwgt):
+    def __init__(self, xadj, adjncy, adjwgt, vwgt, twin=None):
         self.xadj, self.adjncy, self.adjwgt, self.vwgt = xadj, adjncy, adjwgt, vwgt
+        self.twin = twin
         self.n = int(vwgt.numel())
         self.nnz = int(adjncy.numel())
         self._struct = None
@@ -38,7 +40,8 @@ class UGraph:
         if self._struct is None:
             p = _native.ptr
             self._struct = _native.HsUGraph(self.n, self.nnz, p(self.xadj), p(self.adjncy), None,
-                                            p(self.adjwgt), None, p(self.vwgt))
+                                            p(self.adjwgt), None, p(self.vwgt),
+                                            p(self.twin) if self.twin is not None else None)
         return self._struct
 
 
@@ -104,10 +107,15 @@ def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,
     adjncy = torch.empty(nnz_cap, dtype=torch.int32, device=dev)
     adjwgt = torch.empty(nnz_cap, dtype=torch.int32, device=dev)
     vwgt = torch.empty(nk, dtype=torch.int32, device=dev)
+    # reverse-entry index for ghost-part refinement: opt-in (its random scatter
+    # costs more in K1 than the ghost reads save in K6 on issue-bound passes)
+    want_twin = os.environ.get("HS_KWAY_GHOST") == "1" and nnz_cap < 2 ** 31
+    twin = torch.empty(nnz_cap, dtype=torch.int32, device=dev) if want_twin else None
     nnz = _native.symmetrize(csr, edge_w_i.contiguous(), node_w_i.contiguous(), xadj, adjncy,
                              adjwgt, vwgt,
-                             edge_w_i_in.contiguous() if edge_w_i_in is not None else None)
-    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz], vwgt)
+                             edge_w_i_in.contiguous() if edge_w_i_in is not None else None, twin)
+    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz], vwgt,
+                  twin[:nnz] if twin is not None else None)
 
 
 @dataclass
