@@ -257,12 +257,14 @@ constexpr int kContractWarps = 8;
 
 __global__ void __launch_bounds__(kContractWarps * 32)
 contract_warp(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1,
-              const int64_t *ub, int nc, G c) {
+              const int64_t *ub, int nc, G c, int stride) {
   __shared__ int32_t keys[kContractWarps][kWarpSlots];
   __shared__ int32_t vals[kContractWarps][kWarpSlots];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   int32_t *K = keys[wl], *V = vals[wl];
-  for (int cv = warp_id_global(); cv < nc; cv += warps_total()) {
+  // stride > 1: only every stride-th coarse vertex (merged-degree sampling)
+  for (int64_t ci = warp_id_global(); ci * stride < nc; ci += warps_total()) {
+    const int cv = (int)(ci * stride);
     const int64_t u_b = ub[cv];
     if (u_b * 2 > kWarpSlots) continue;  // handled by the CTA / global paths
     uint32_t size = 32;
@@ -303,6 +305,69 @@ contract_warp(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1
     }
     if (lane == 0) c.deg[cv] = cnt;
     __syncwarp();
+  }
+}
+
+// Merged / unmerged entry counts over the sampled coarse vertices.
+__global__ void sample_ratio(const int64_t *ub, const int32_t *deg_c, int nc, int stride,
+                             int64_t slots, unsigned long long *out) {
+  unsigned long long a = 0, b = 0;
+  for (int64_t ci = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; ci * stride < nc;
+       ci += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t cv = ci * stride;
+    if (ub[cv] * 2 > slots) continue;
+    a += (unsigned long long)deg_c[cv];
+    b += (unsigned long long)ub[cv];
+  }
+  for (int off = 16; off; off >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, off);
+    b += __shfl_down_sync(0xffffffffu, b, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&out[0], a);
+    atomicAdd(&out[1], b);
+  }
+}
+
+// Unmerged contraction (the level will be the coarsest): the pair's lists
+// mapped through cmap, self loops dropped, parallel edges kept. Refinement
+// gains, balance and cut are sums over entries, so they are identical on this
+// multigraph. Team of 8 lanes per coarse vertex, ballot-compacted stores.
+__global__ void contract_direct(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1,
+                                int nc, G c) {
+  constexpr int T = 8;
+  const int lane = (threadIdx.x & 31) % T, tw = (threadIdx.x & 31) / T;
+  const int64_t step = (int64_t)warps_total() * (32 / T);
+  for (int64_t vb = (int64_t)warp_id_global() * (32 / T); vb < nc; vb += step) {
+    const int cv = (int)(vb + tw);
+    const bool valid = cv < nc;
+    int64_t base = valid ? c.xbeg[cv] : 0;
+    int cnt = 0;
+    for (int t = 0; t < 2; ++t) {
+      const int x = valid ? (t == 0 ? mem0[cv] : mem1[cv]) : -1;
+      const int64_t b = x >= 0 ? g.xbeg[x] : 0;
+      const int d = x >= 0 ? g.deg[x] : 0;
+      // warp-uniform trip count: max over the 4 teams of this warp
+      int dm = d;
+      for (int off = 16; off >= T; off >>= 1) dm = max(dm, __shfl_xor_sync(0xffffffffu, dm, off));
+      for (int j0 = 0; j0 < dm; j0 += T) {
+        const int j = j0 + lane;
+        int key = -1, w = 0;
+        if (j < d) {
+          key = cmap[g.adj[b + j]];
+          w = g.wgt[b + j];
+        }
+        const bool keep = key >= 0 && key != cv;
+        const unsigned m = (__ballot_sync(0xffffffffu, keep) >> (tw * T)) & ((1u << T) - 1);
+        if (keep) {
+          const int64_t at = base + cnt + __popc(m & ((1u << lane) - 1));
+          c.adj[at] = key;
+          c.wgt[at] = w;
+        }
+        cnt += __popc(m);
+      }
+    }
+    if (valid && lane == 0) c.deg[cv] = cnt;
   }
 }
 
@@ -837,6 +902,7 @@ struct Kway {
   // beat 4 + 4 on both time and cut (over-refined coarse levels trap the
   // finest level in a worse local optimum)
   int passes_big = 4, passes_small = 8, passes_coarse = 1, rounds = 3;
+  double max_deg = 1e30;  // coarsening stop threshold (average degree)
   Kway(cudaStream_t st) : s(st), timer(st) {
     if (const char *e = getenv("HS_KWAY_PASSES")) passes_big = std::max(1, atoi(e));
     if (const char *e = getenv("HS_KWAY_PASSES_COARSE")) passes_coarse = std::max(0, atoi(e));
@@ -1108,10 +1174,38 @@ struct Kway {
     C.g.nnz = capc;  // refined below (asynchronously) to the live count
     HS_CHECK_CUDA(dalloc(&C.g.adj, capc, s));
     HS_CHECK_CUDA(dalloc(&C.g.wgt, capc, s));
+    // Will this coarse level be the last one (merged average degree above
+    // the stop threshold)? Estimate the merge ratio on a 1/64 sample.
+    bool direct = false;
+    if (nc >= 65536) {
+      const int S = 64;
+      contract_warp<<<warp_grid(nc / S + 1, kContractWarps), kContractWarps * 32, 0, s>>>(
+          F.g, F.cmap, mem0, mem1, ub, nc, C.g, S);
+      HS_CHECK_LAUNCH();
+      unsigned long long *sr;
+      HS_CHECK_CUDA(dalloc(&sr, 2, s));
+      HS_CHECK_CUDA(cudaMemsetAsync(sr, 0, 16, s));
+      sample_ratio<<<hs::grid_for(nc / S + 1, 256), 256, 0, s>>>(ub, C.g.deg, nc, S, kWarpSlots, sr);
+      HS_CHECK_LAUNCH();
+      unsigned long long hr[2] = {0, 0};
+      HS_CHECK_CUDA(cudaMemcpyAsync(hr, sr, 16, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      cudaFreeAsync(sr, s);
+      if (hr[1] > 0) {
+        const double merged_avg = (double)hr[0] / (double)hr[1] * (double)F.g.nnz / (double)nc;
+        direct = merged_avg > max_deg;
+      }
+    }
+    if (direct) {
+      hs::Prof P("contract_direct", s, 16.0 * nc + 12.0 * n + 12.0 * F.g.nnz + 8.0 * F.g.nnz);
+      contract_direct<<<std::max(1, std::min(hs::sm_count() * 32, (nc * 8 + 255) / 256)), 256, 0,
+                        s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
+      HS_CHECK_LAUNCH();
+    } else {
     {
       hs::Prof P("contract_warp", s, 28.0 * nc + 12.0 * n + 12.0 * F.g.nnz);
       contract_warp<<<warp_grid(nc, kContractWarps), kContractWarps * 32, 0, s>>>(
-          F.g, F.cmap, mem0, mem1, ub, nc, C.g);
+          F.g, F.cmap, mem0, mem1, ub, nc, C.g, 1);
     }
     HS_CHECK_LAUNCH();
     // long lists: CTA with a shared-memory table, then global-memory tables;
@@ -1148,6 +1242,8 @@ struct Kway {
                                                          ctl + 9, C.g, gk, gv, 0);
     }
     HS_CHECK_LAUNCH();
+    cudaFreeAsync(list, s); cudaFreeAsync(list2, s); cudaFreeAsync(ncd, s);
+    }
     {  // live adjacency entries of the coarse level, read at the next round trip
       size_t tb = 0;
       HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, C.g.deg, d_nnz, nc, s));
@@ -1158,7 +1254,6 @@ struct Kway {
       prev_nnz_pending = true;
       hs::count_launch(1);
     }
-    cudaFreeAsync(list, s); cudaFreeAsync(list2, s); cudaFreeAsync(ncd, s);
     cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
     cudaFreeAsync(flag, s); cudaFreeAsync(cid, s); cudaFreeAsync(mem0, s);
     cudaFreeAsync(mem1, s); cudaFreeAsync(ub, s);
@@ -1448,6 +1543,7 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   const double deg0 = n0 ? (double)nnz0 / (double)n0 : 0.0;
   double max_deg = std::max(16.0, 1.5 * deg0);
   if (const char *e = getenv("HS_KWAY_MAXDEG")) max_deg = atof(e);
+  K.max_deg = max_deg;
   while (!stop && K.levels.back().g.n > coarse_target && (int)K.levels.size() < 40) {
     if (K.levels.size() > 1) {
       int rc0 = K.settle_nnz();
