@@ -1,0 +1,88 @@
+"""N>1 host logic on CPU with torch.distributed gloo, world_size 2.
+
+The GPU data path cannot run here; what is shared by every rank and must agree
+is host logic: the DAG task table, the owner maps (2D block-cyclic and the
+partition-based one's contract), the expected transfer counts that the
+executors' copy counters are checked against, and bench.py's max/sum-over-
+ranks reductions.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1502_07451_b200.gen import cholesky_tasks
+
+KIND = {"POTRF": 0, "TRSM": 1, "SYRK": 2, "GEMM": 3}
+
+
+def _owner_cyclic(tasks, nranks):
+    pr = int(np.floor(np.sqrt(nranks)))
+    while nranks % pr:
+        pr -= 1
+    pc = nranks // pr
+    out = []
+    for kind, (i, j, k) in tasks:
+        kd = KIND[kind]
+        r = k if kd == 0 else i
+        c = j if kd == 3 else (i if kd == 2 else k)
+        out.append((r % pr) * pc + (c % pc))
+    return np.array(out, dtype=np.int8)
+
+
+def _transfers(deps, owner):
+    d = np.array(deps) - 1
+    po, co = owner[d[:, 0]], owner[d[:, 1]]
+    cross = po != co
+    return len(set(zip(d[cross, 0].tolist(), co[cross].tolist())))
+
+
+def _worker(rank, world, port, T, q):
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    tasks, deps = cholesky_tasks(T)
+    owner = _owner_cyclic(tasks, world)
+    # every rank derives the same owner map and transfer count
+    mine = torch.tensor([float(owner.astype(np.int64).sum()), float(_transfers(deps, owner))])
+    allv = [torch.zeros(2) for _ in range(world)]
+    dist.all_gather(allv, mine)
+    # work owned per rank (flops units b^3/3: POTRF 1, TRSM 3, SYRK 3, GEMM 6)
+    w = np.array([{0: 1, 1: 3, 2: 3, 3: 6}[KIND[k]] for k, _ in tasks])
+    load = torch.tensor([float(w[owner == rank].sum())])
+    loads = [torch.zeros(1) for _ in range(world)]
+    dist.all_gather(loads, load)
+    # bench.py's max-over-ranks of a per-rank time
+    t = torch.tensor([1.0 + rank])
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        q.put({"agree": all(torch.equal(allv[0], x) for x in allv),
+               "transfers": float(allv[0][1]), "loads": [float(x) for x in loads],
+               "total": float(w.sum()), "max_t": float(t)})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("T", [8, 16])
+def test_two_rank_owner_maps_agree_and_balance(T):
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, T, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert res["agree"]
+    assert res["max_t"] == 2.0
+    assert sum(res["loads"]) == res["total"]
+    assert max(res["loads"]) / (res["total"] / 2) < 1.2  # cyclic map balances work
+    tasks, deps = cholesky_tasks(T)
+    assert res["transfers"] == _transfers(deps, _owner_cyclic(tasks, 2)) > 0
