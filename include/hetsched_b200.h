@@ -269,6 +269,44 @@ int hs_METIS_PartGraphKway(const int32_t *nvtxs, const int32_t *ncon, const int3
 int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *edge_w_i_in,
                   const int32_t *node_w_i, int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i,
                   int32_t *vwgt_i, int32_t *twin, int64_t *nnz_host, void *stream);
+/* The rows of kernel positions [kv0, kv1) only (one rank's shard): xadj has
+ * kv1-kv0+1 entries starting at 0, adjncy holds GLOBAL kernel positions,
+ * vwgt_i[i] is the weight of kernel kv0+i. twin must be NULL unless the range
+ * is the whole graph. */
+int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1, const int32_t *edge_w_i,
+                        const int32_t *edge_w_i_in, const int32_t *node_w_i, int64_t *xadj,
+                        int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,
+                        int64_t *nnz_host, void *stream);
+
+/* ---- sharded k-way partition (config 4 at 2/4/8 GPUs) ---------------------
+ * One call per rank, all ranks concurrently (one process per GPU, or one host
+ * thread per rank in loopback mode on a single GPU). Rank r passes the rows
+ * of its contiguous vertex range [v0, v0 + g->n) (hs_symmetrize_range) with
+ * global neighbour ids. Ranks exchange through `arena[q]`: one whole device
+ * allocation per rank (hs_ipc_alloc; peers' arenas CUDA-IPC mapped, or plain
+ * pointers on one GPU), at least hs_kway_dist_arena_bytes(n_global) bytes,
+ * zeroed once before the group's first call (epochs persist across calls).
+ * Per-vertex state neighbours read (parts, refinement state, fine->coarse
+ * maps) is replicated by producer-side peer stores; sums/maxima go through an
+ * in-kernel all-reduce over the arenas (integer, rank order: bit-identical on
+ * every rank). part_out: [n_global] int32, the whole partition, on every
+ * rank. stats_host: as hs_partition_kway (global values). The result is a
+ * pure function of (graph, ranges, k, targets, tol, seed). A peer that never
+ * arrives makes the call fail with HS_EDEADLOCK after a 30 s watchdog. */
+typedef struct hs_dist {
+    int32_t rank, size;      /* size <= 8 */
+    void *arena[8];          /* arena of every rank, valid on this rank's device */
+    int64_t arena_bytes;
+    int32_t mode;            /* 0: one process per rank (in-kernel flag barriers);
+                                1: ranks are host threads of this process sharing
+                                one GPU (loopback: host barriers between phases) */
+} hs_dist_t;
+
+int64_t hs_kway_dist_arena_bytes(int32_t n_global);
+int hs_partition_kway_dist(const hs_ugraph_t *g_local, int32_t v0, int32_t n_global,
+                           const hs_dist_t *dist, int32_t k, const double *tpwgts_host,
+                           double tol, uint64_t seed, int32_t *part_out, int64_t *stats_host,
+                           void *stream);
 
 /* Device generator of the layered fan-in DAG family of configs 2 and 4:
  * n kernels over ceil(sqrt(n)) layers, m inter-kernel edges spread as evenly

@@ -58,6 +58,11 @@ class HsUGraph(ctypes.Structure):
                 ("vwgt", _c_void_p), ("vwgt_i", _c_void_p), ("twin", _c_void_p)]
 
 
+class HsDist(ctypes.Structure):
+    _fields_ = [("rank", _i32), ("size", _i32), ("arena", _c_void_p * 8), ("arena_bytes", _i64),
+                ("mode", _i32)]
+
+
 class HsEvent(ctypes.Structure):
     _fields_ = [("time", _f64), ("kind", _i32), ("a", _i32), ("b", _i32),
                 ("resource", _i32)]
@@ -96,6 +101,13 @@ _fm2 = _opt("hs_fm2", _P, _P, _P, _P, _i64, _P, _f64, _f64, _P, _i32, _P, _P, _P
 _brute2 = _opt("hs_brute2", _i32, _P, _f64, _f64, _P, _P, _P, _i64, _P, _P, _P)
 _partition_kway = _opt("hs_partition_kway", _P, _i32, _P, _f64, ctypes.c_uint64, _P, _P, _P)
 _symmetrize = _opt("hs_symmetrize", _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P)
+_symmetrize_range = _opt("hs_symmetrize_range", _P, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _P,
+                         _P, _P)
+_partition_kway_dist = _opt("hs_partition_kway_dist", _P, _i32, _i32, _P, _i32, _P, _f64,
+                            ctypes.c_uint64, _P, _P, _P)
+if hasattr(_lib, "hs_kway_dist_arena_bytes"):
+    _lib.hs_kway_dist_arena_bytes.restype = ctypes.c_int64
+    _lib.hs_kway_dist_arena_bytes.argtypes = [_i32]
 _layered_sizes = _opt("hs_layered_sizes", _i64, _i64, _P, _P)
 _layered_generate = _opt("hs_layered_generate", _i64, _i64, ctypes.c_uint64,
                          _P, _P, _P, _P, _P, _P, _P)
@@ -259,6 +271,31 @@ def symmetrize(csr, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, edge_w_i
     check(fn(ctypes.byref(csr.struct()), ptr(edge_w_i), ptr(edge_w_i_in), ptr(node_w_i), ptr(xadj),
              ptr(adjncy), ptr(adjwgt_i), ptr(vwgt_i), ptr(twin), ctypes.byref(nnz), stream_ptr()))
     return nnz.value
+
+
+def symmetrize_range(csr, kv0: int, kv1: int, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i,
+                     vwgt_i, edge_w_i_in=None) -> int:
+    fn = _need(_symmetrize_range, "hs_symmetrize_range")
+    nnz = ctypes.c_int64(0)
+    check(fn(ctypes.byref(csr.struct()), kv0, kv1, ptr(edge_w_i), ptr(edge_w_i_in),
+             ptr(node_w_i), ptr(xadj), ptr(adjncy), ptr(adjwgt_i), ptr(vwgt_i), None,
+             ctypes.byref(nnz), stream_ptr()))
+    return nnz.value
+
+
+def kway_dist_arena_bytes(n_global: int) -> int:
+    return int(_lib.hs_kway_dist_arena_bytes(n_global))
+
+
+def partition_kway_dist(ug, v0: int, n_global: int, dist: HsDist, k: int, tpwgts, tol: float,
+                        seed: int, part: torch.Tensor):
+    """One rank's call (blocks until every rank of the group has made its own)."""
+    fn = _need(_partition_kway_dist, "hs_partition_kway_dist")
+    tp = (ctypes.c_double * k)(*[float(x) for x in tpwgts])
+    stats = (ctypes.c_int64 * 8)()
+    check(fn(ctypes.byref(ug.struct()), v0, n_global, ctypes.byref(dist), k, tp, float(tol),
+             ctypes.c_uint64(seed & (2**64 - 1)), ptr(part), stats, stream_ptr()))
+    return list(stats)
 
 
 def layered_sizes(n_kernels: int, m_inter: int) -> Tuple[int, int]:

@@ -38,6 +38,11 @@
 #include <vector>
 #include <algorithm>
 #include <cuda_profiler_api.h>
+#include <mutex>
+#include <condition_variable>
+#include <chrono>
+#include <memory>
+#include "dist.cuh"
 
 int hs_widen32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
 
@@ -56,6 +61,7 @@ struct G {
   int32_t *adj;
   int32_t *wgt;
   int32_t *vw;
+  int32_t v0 = 0;  // global id of local vertex 0 (a rank's range when sharded)
 };
 
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
@@ -102,31 +108,35 @@ __device__ __forceinline__ int64_t root_slot(const hs_dag_t &g, int v) {
   return (lo < g.in_ptr[v + 1] && g.in_src[lo] == g.root) ? lo : -1;
 }
 
-__global__ void sym_degree(hs_dag_t g, int32_t *deg) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    if (v == g.root) continue;
-    const int kv = v < g.root ? (int)v : (int)v - 1;
-    deg[kv] = (int)(g.in_ptr[v + 1] - g.in_ptr[v]) - (root_slot(g, (int)v) >= 0 ? 1 : 0) +
-              (int)(g.out_ptr[v + 1] - g.out_ptr[v]);
+// Kernel positions [kv0, kv1) only (one rank's vertex range when sharded);
+// outputs are indexed kv - kv0.
+__device__ __forceinline__ int node_of(const hs_dag_t &g, int kv) { return kv < g.root ? kv : kv + 1; }
+
+__global__ void sym_degree(hs_dag_t g, int kv0, int kv1, int32_t *deg) {
+  for (int64_t kv = kv0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; kv < kv1;
+       kv += (int64_t)gridDim.x * blockDim.x) {
+    const int v = node_of(g, (int)kv);
+    deg[kv - kv0] = (int)(g.in_ptr[v + 1] - g.in_ptr[v]) - (root_slot(g, v) >= 0 ? 1 : 0) +
+                    (int)(g.out_ptr[v + 1] - g.out_ptr[v]);
   }
 }
 
 // Team of 8 lanes per vertex: in-neighbours (root dropped) then
 // out-neighbours. ew_in (in-order weights) avoids a random gather through
 // in_eid when the caller has it; otherwise the weight is gathered.
-__global__ void sym_fill(hs_dag_t g, const int32_t *ew, const int32_t *ew_in, const int32_t *nw,
-                         const int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw,
-                         int32_t *twin) {
+__global__ void sym_fill(hs_dag_t g, int kv0, int kv1, const int32_t *ew, const int32_t *ew_in,
+                         const int32_t *nw, const int64_t *xadj, int32_t *adj, int32_t *wgt,
+                         int32_t *vw, int32_t *twin) {
   constexpr int T = 8;
   const int lane = (threadIdx.x & 31) % T;
   const int64_t step = (int64_t)warps_total() * (32 / T);
-  for (int64_t vb = (int64_t)warp_id_global() * (32 / T); vb < g.n; vb += step) {
-    const int v = (int)(vb + (threadIdx.x & 31) / T);
-    if (v >= g.n || v == g.root) continue;
-    const int kv = v < g.root ? v : v - 1;
-    const int64_t pos = xadj[kv];
-    if (lane == 0) vw[kv] = nw[v];
+  for (int64_t vb = kv0 + (int64_t)warp_id_global() * (32 / T); vb < kv1; vb += step) {
+    const int kv = (int)(vb + (threadIdx.x & 31) / T);
+    if (kv >= kv1) continue;
+    const int v = node_of(g, kv);
+    const int li = kv - kv0;
+    const int64_t pos = xadj[li];
+    if (lane == 0) vw[li] = nw[v];
     const int64_t i0 = g.in_ptr[v], i1 = g.in_ptr[v + 1];
     const int64_t rs = root_slot(g, v);
     for (int64_t j = i0 + lane; j < i1; j += T) {
@@ -229,15 +239,17 @@ __global__ void leader_flags(int n, const int32_t *match, int32_t *flag) {
   }
 }
 
-__global__ void build_cmap(G g, const int32_t *match, const int32_t *cid, int32_t *cmap,
-                           int32_t *mem0, int32_t *mem1, int32_t *vw_c, int64_t *ub) {
+// cmap is replicated (global fine id -> global coarse id = coff + local cid)
+__global__ void build_cmap(G g, const int32_t *match, const int32_t *cid, int32_t coff,
+                           Rep<int32_t> cmap, int32_t *mem0, int32_t *mem1, int32_t *vw_c,
+                           int64_t *ub) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < g.n;
        u += (int64_t)gridDim.x * blockDim.x) {
     int m = match[u];
     int partner = (m < 0) ? (int)u : m;
     int lead = min((int)u, partner);
     int c = cid[lead];
-    cmap[u] = c;
+    cmap.put(g.v0 + u, coff + c);
     if (lead == (int)u) {
       mem0[c] = (int)u;
       mem1[c] = partner != (int)u ? partner : -1;
@@ -279,7 +291,7 @@ contract_warp(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1
       const int d = g.deg[x];
       for (int j = lane; j < d; j += 32) {
         int key = cmap[g.adj[b + j]];
-        if (key == cv) continue;
+        if (key == cv + c.v0) continue;
         int w = g.wgt[b + j];
         uint32_t s = slot_hash(key, mask);
         while (true) {
@@ -357,7 +369,7 @@ __global__ void contract_direct(G g, const int32_t *cmap, const int32_t *mem0, c
           key = cmap[g.adj[b + j]];
           w = g.wgt[b + j];
         }
-        const bool keep = key >= 0 && key != cv;
+        const bool keep = key >= 0 && key != cv + c.v0;
         const unsigned m = (__ballot_sync(0xffffffffu, keep) >> (tw * T)) & ((1u << T) - 1);
         if (keep) {
           const int64_t at = base + cnt + __popc(m & ((1u << lane) - 1));
@@ -405,7 +417,7 @@ __global__ void contract_block(G g, const int32_t *cmap, const int32_t *mem0, co
       const int d = g.deg[x];
       for (int j = threadIdx.x; j < d; j += blockDim.x) {
         int key = cmap[g.adj[b + j]];
-        if (key == cv) continue;
+        if (key == cv + c.v0) continue;
         int w = g.wgt[b + j];
         uint64_t s = pow2 ? (uint64_t)slot_hash(key, (uint32_t)(size - 1))
                           : ((uint64_t)((uint32_t)key * 0x9E3779B1u)) % size;
@@ -663,7 +675,7 @@ rebalance_candidates(G g, const part_t *part, int k, const int64_t *pw, const in
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   int32_t *conn = conn_s[wl];
   for (int v = warp_id_global(); v < g.n; v += warps_total()) {
-    const int own = part[v];
+    const int own = part[g.v0 + v];
     if (s_pw[own] <= s_hi[own]) {
       if (lane == 0) cand[v] = -1;
       continue;
@@ -720,9 +732,10 @@ __global__ void move_flows(int n, const int32_t *vw, const part_t *part, const i
 // decided by a hash of (salt, v) — deterministic thinning that keeps the
 // expected inflow of every part within its room.
 __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, const double *prob,
-                              int k, uint64_t salt, part_t *part, int64_t *pw,
-                              const int32_t *run, const int64_t *xbeg, const int32_t *deg,
-                              const int32_t *twin, part_t *gp) {
+                              int k, uint64_t salt, int32_t v0, const part_t *part,
+                              Rep<part_t> prep, int64_t *pw, const int32_t *run,
+                              const int64_t *xbeg, const int32_t *deg, const int32_t *twin,
+                              part_t *gp) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -733,11 +746,12 @@ __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, con
        v += (int64_t)gridDim.x * blockDim.x) {
     int dest = cand[v];
     if (dest < 0) continue;
-    int own = part[v];
+    int own = part[v0 + v];
     double pr = s_prob[own] * s_prob[k + dest];
-    if (pr < 1.0 && (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
+    const uint64_t gv = (uint64_t)(v0 + v);
+    if (pr < 1.0 && (double)mix32(salt ^ (gv * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
       continue;
-    part[v] = dest;
+    prep.put(v0 + v, (part_t)dest);
     if (gp)
       for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
     atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
@@ -759,14 +773,15 @@ __global__ void scale_weights(int64_t nnz, const int32_t *in, int32_t *out, int6
 // Initial "range" trial: contiguous id ranges by cumulative weight. Coarse
 // ids follow the smallest fine id they contain, so on a task DAG (ids in
 // creation/topological order) this is a layer-band partition.
-__global__ void range_parts(int n, const int64_t *prefix, const int32_t *vw, const double *cum,
-                            int k, int64_t total, part_t *part) {
+__global__ void range_parts(int n, const int64_t *prefix, int64_t woff, const int32_t *vw,
+                            const double *cum, int k, int64_t total, int32_t v0,
+                            Rep<part_t> part) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
-    double mid = ((double)prefix[v] + 0.5 * (double)vw[v]) / (double)total;
+    double mid = ((double)(prefix[v] + woff) + 0.5 * (double)vw[v]) / (double)total;
     int p = 0;
     while (p < k - 1 && mid >= cum[p + 1]) ++p;
-    part[v] = p;
+    part.put(v0 + v, (part_t)p);
   }
 }
 
@@ -827,10 +842,72 @@ __global__ void max_wdeg_kernel(G g, int32_t *out) {
 
 // ------------------------------------------------------------ host side ---
 struct Level {
-  G g;
-  int32_t *cmap = nullptr;  // fine -> coarse of the NEXT level (set when coarsened)
+  G g;                      // this rank's rows (all rows on one GPU)
+  int32_t n_glob = 0;       // vertices over all ranks
+  int64_t nnz_glob = 0;     // live adjacency entries over all ranks
+  int32_t *cmap = nullptr;  // global fine id -> global coarse id of the NEXT level
+                            // (this rank's replica; set when coarsened)
   bool own_adj = true, own_wgt = true, own_xbeg_vw = true;
 };
+
+// Loopback groups (ranks = host threads on one GPU) synchronise on the host:
+// a kernel spinning on a peer's flag inside one CUDA context can deadlock
+// against that peer's own launches (lazy kernel loading synchronises the
+// context), so there each all-reduce is post -> stream sync -> host barrier ->
+// reduce. One-process-per-GPU groups use the in-kernel flags.
+struct HostBarrier {
+  std::mutex mu;
+  std::condition_variable cv;
+  int count = 0;
+  uint64_t gen = 0;
+  bool wait(int P, double seconds) {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t g = gen;
+    if (++count == P) {
+      count = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    return cv.wait_for(lk, std::chrono::duration<double>(seconds), [&] { return gen != g; });
+  }
+};
+std::mutex g_hb_mu;
+std::vector<std::pair<void *, std::shared_ptr<HostBarrier>>> g_hbs;
+std::shared_ptr<HostBarrier> host_barrier_for(void *key) {
+  std::lock_guard<std::mutex> lk(g_hb_mu);
+  for (auto &e : g_hbs)
+    if (e.first == key) return e.second;
+  g_hbs.emplace_back(key, std::make_shared<HostBarrier>());
+  return g_hbs.back().second;
+}
+
+// Flags are never reset, so epochs continue across calls: a rank's last
+// epoch is the flag it wrote into its own arena (0 in a fresh arena).
+int load_epoch(const Dist &D, uint32_t *epoch, cudaStream_t s) {
+  HS_CHECK_CUDA(cudaMemcpyAsync(epoch, D.arena[D.rank] + 4 * D.rank, 4, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  return HS_OK;
+}
+
+// Loopback ranks share this process's default memory pool: a pool allowed to
+// reuse a block freed on another rank's stream would make this rank wait on
+// that stream — which may be parked in a barrier waiting for this rank.
+int no_cross_stream_pool_waits() {
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    int dev = 0;
+    cudaMemPool_t pool;
+    err = cudaGetDevice(&dev);
+    if (err == cudaSuccess) err = cudaDeviceGetDefaultMemPool(&pool, dev);
+    int zero = 0;
+    if (err == cudaSuccess)
+      err = cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+  });
+  HS_CHECK_CUDA(err);
+  return HS_OK;
+}
 
 template <typename T>
 cudaError_t dalloc(T **p, size_t count, cudaStream_t s) {
@@ -903,6 +980,114 @@ struct Kway {
   // finest level in a worse local optimum)
   int passes_big = 4, passes_small = 8, passes_coarse = 1, rounds = 3;
   double max_deg = 1e30;  // coarsening stop threshold (average degree)
+  Dist D;                         // P = 1: the whole graph on this GPU
+  std::shared_ptr<HostBarrier> hb;  // loopback groups
+  int64_t *d_dpw = nullptr;       // sharded: this rank's part-weight deltas
+  int64_t *d_arbuf = nullptr;     // sharded: staging for host all-reduces
+
+  // ---- sharding helpers (no-ops on one GPU) ----
+  // All-reduce of up to kArSlots values over the group; also a barrier.
+  int ar(std::initializer_list<ArSeg> segs, int line = __builtin_LINE()) {
+    if (!D.on()) return HS_OK;
+    ArArgs A;
+    static const char *wd = getenv("HS_DIST_WATCHDOG_S");
+    if (wd) A.timeout_ns = (uint64_t)(atof(wd) * 1e9);
+    static const bool trace = getenv("HS_DIST_TRACE") != nullptr;
+    if (trace) fprintf(stderr, "[dist] rank %d epoch %u line %d\n", D.rank, D.epoch + 1, line);
+    for (int r = 0; r < D.P; ++r) A.arena[r] = D.arena[r];
+    A.rank = D.rank;
+    A.P = D.P;
+    A.epoch = ++D.epoch;
+    int tot = 0;
+    for (const ArSeg &g : segs) {
+      HS_REQUIRE(A.nseg < 4, HS_EINVAL, "all-reduce: too many segments");
+      A.seg[A.nseg++] = g;
+      tot += g.n;
+    }
+    HS_REQUIRE(tot <= kArSlots, HS_EINVAL, "all-reduce: %d values > %d", tot, kArSlots);
+    if (!D.threads) {
+      ar_kernel<<<1, 256, 0, s>>>(A);
+      HS_CHECK_LAUNCH();
+      return HS_OK;
+    }
+    A.phase = 1;
+    ar_kernel<<<1, 256, 0, s>>>(A);
+    HS_CHECK_LAUNCH();
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    HS_REQUIRE(hb->wait(D.P, A.timeout_ns * 1e-9), HS_EDEADLOCK,
+               "k-way (sharded): a peer thread never reached barrier %u", A.epoch);
+    A.phase = 2;
+    ar_kernel<<<1, 256, 0, s>>>(A);
+    HS_CHECK_LAUNCH();
+    return HS_OK;
+  }
+  int barrier(int line = __builtin_LINE()) { return ar({}, line); }
+  static ArSeg seg64(int64_t *p, int n, int op = 0, int acc = 0, int64_t *out = nullptr) {
+    ArSeg g;
+    g.in = p; g.out = out ? out : p; g.n = n; g.is64 = 1; g.op = (int8_t)op; g.acc = (int8_t)acc;
+    return g;
+  }
+  static ArSeg seg32(int32_t *p, int n, int op = 0) {
+    ArSeg g;
+    g.in = p; g.out = p; g.n = n; g.is64 = 0; g.op = (int8_t)op;
+    return g;
+  }
+  // Host values in/out (synchronous); checks the watchdog.
+  int ar_host(int64_t *vals, int n, int op = 0, int line = __builtin_LINE()) {
+    if (!D.on()) return HS_OK;
+    HS_CHECK_CUDA(cudaMemcpyAsync(d_arbuf, vals, n * 8, cudaMemcpyHostToDevice, s));
+    int rc = ar({seg64(d_arbuf, n, op)}, line);
+    if (rc) return rc;
+    HS_CHECK_CUDA(cudaMemcpyAsync(vals, d_arbuf, n * 8, cudaMemcpyDeviceToHost, s));
+    return check_peers();
+  }
+  int check_peers() {
+    if (!D.on()) return HS_OK;
+    int32_t err = 0;
+    HS_CHECK_CUDA(cudaMemcpyAsync(&err, D.arena[D.rank] + 64, 4, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    HS_REQUIRE(err == 0, HS_EDEADLOCK, "k-way (sharded): a peer never reached a barrier");
+    return HS_OK;
+  }
+  // Sum over ranks of one host value; *before = sum over lower ranks.
+  int exscan_host(int64_t mine, int64_t *before, int64_t *total, int line = __builtin_LINE()) {
+    int64_t v[kMaxRanks] = {0};
+    v[D.rank] = mine;
+    int rc = ar_host(v, D.P, 0, line);
+    if (rc) return rc;
+    *before = 0;
+    *total = 0;
+    for (int r = 0; r < D.P; ++r) {
+      if (r < D.rank) *before += v[r];
+      *total += v[r];
+    }
+    return HS_OK;
+  }
+  // Replicated array of `count` elements: a private buffer on one GPU, the
+  // same offset of every rank's arena when sharded.
+  template <typename T>
+  int alloc_rep(Rep<T> &r, int64_t count) {
+    if (!D.on()) {
+      r.n = 1;
+      HS_CHECK_CUDA(dalloc(&r.p[0], count, s));
+      return HS_OK;
+    }
+    const int64_t bytes = ((std::max<int64_t>(count, 1) * (int64_t)sizeof(T)) + 255) & ~255ll;
+    HS_REQUIRE(D.bump + bytes <= D.arena_bytes, HS_ELIMIT,
+               "k-way (sharded): arena too small (%lld bytes needed beyond %lld)",
+               (long long)bytes, (long long)D.arena_bytes);
+    r.n = D.P;
+    for (int q = 0; q < D.P; ++q) r.p[q] = (T *)(D.arena[q] + D.bump);
+    D.bump += bytes;
+    return HS_OK;
+  }
+  template <typename T>
+  T *loc(const Rep<T> &r) const { return r.p[D.on() ? D.rank : 0]; }
+  template <typename T>
+  void free_rep(Rep<T> &r) {
+    if (!D.on() && r.p[0]) cudaFreeAsync(r.p[0], s);
+    r.p[0] = nullptr;
+  }
   Kway(cudaStream_t st) : s(st), timer(st) {
     if (const char *e = getenv("HS_KWAY_PASSES")) passes_big = std::max(1, atoi(e));
     if (const char *e = getenv("HS_KWAY_PASSES_COARSE")) passes_coarse = std::max(0, atoi(e));
@@ -916,11 +1101,13 @@ struct Kway {
     return HS_OK;
   }
 
+  // part: this rank's replica (global ids); sums this rank's vertices, then all ranks'
   int weights(const G &g, const part_t *part) {
     HS_CHECK_CUDA(cudaMemsetAsync(d_pw, 0, k * sizeof(int64_t), s));
-    part_weights<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw, part, k, d_pw);
+    part_weights<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw,
+                                                                           part + g.v0, k, d_pw);
     HS_CHECK_LAUNCH();
-    return HS_OK;
+    return ar({seg64(d_pw, k)});
   }
 
   // plans in `cand` -> thinned application; returns moves planned
@@ -932,45 +1119,65 @@ struct Kway {
 
   // Up to `rounds` rebalancing rounds, each gated on the device by "some part
   // is above its bound" — no host round trip.
-  int rebalance(const G &g, part_t *part, int32_t *cand, uint64_t salt2, int rounds) {
+  // Planned flows and move counts of all ranks (a no-op on one GPU).
+  int ar_flows() { return ar({seg64(d_flows, 2 * k), seg32(ctl + CTL_NCONF, 1)}); }
+  // Part-weight deltas of this rank's applied moves -> every rank's d_pw.
+  int64_t *apply_target() {
+    if (!D.on()) return d_pw;
+    cudaMemsetAsync(d_dpw, 0, k * sizeof(int64_t), s);
+    return d_dpw;
+  }
+  int ar_applied() { return D.on() ? ar({seg64(d_dpw, k, 0, 1, d_pw)}) : HS_OK; }
+
+  int rebalance(const G &g, const Rep<part_t> &part, int32_t *cand, uint64_t salt2, int rounds) {
     const int grid = hs::grid_for(g.n, 256, hs::sm_count() * 4);
+    const part_t *pl = loc(part);
     for (int rb = 0; rb < rounds; ++rb) {
       balance_check<<<1, 32, 0, s>>>(k, d_pw, d_hi, ctl);
       HS_CHECK_LAUNCH();
       rebalance_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(
-          g, part, k, d_pw, d_hi, d_target, cand, ctl + CTL_OVER);
+          g, pl, k, d_pw, d_hi, d_target, cand, ctl + CTL_OVER);
       HS_CHECK_LAUNCH();
       HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
       HS_CHECK_CUDA(cudaMemsetAsync(ctl + CTL_NCONF, 0, sizeof(int32_t), s));
-      move_flows<<<grid, 256, 0, s>>>(g.n, g.vw, part, cand, k, d_flows, ctl + CTL_NCONF,
+      move_flows<<<grid, 256, 0, s>>>(g.n, g.vw, pl + g.v0, cand, k, d_flows, ctl + CTL_NCONF,
                                       ctl + CTL_OVER);
       HS_CHECK_LAUNCH();
+      int rc = ar_flows();
+      if (rc) return rc;
       plan_kernel<<<1, kMaxParts, 0, s>>>(k, g.n, 1, d_flows, d_pw, d_hi, d_lo, d_target, d_prob,
                                           ctl);
       HS_CHECK_LAUNCH();
-      apply_thinned<<<grid, 256, 0, s>>>(g.n, g.vw, cand, d_prob, k, salt2 + rb * 7919, part, d_pw,
-                                         ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
+      int64_t *tgt = apply_target();
+      apply_thinned<<<grid, 256, 0, s>>>(g.n, g.vw, cand, d_prob, k, salt2 + rb * 7919, g.v0, pl,
+                                         part, tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
       HS_CHECK_LAUNCH();
+      rc = ar_applied();
+      if (rc) return rc;
     }
     return HS_OK;
   }
 
   // K6 on one level: fixed pass budget, convergence decided on the device.
-  int refine(const G &g, part_t *part, uint64_t salt2, bool finest = true) {
+  int refine(const Level &Lv, const Rep<part_t> &part, uint64_t salt2, bool finest = true) {
+    const G &g = Lv.g;
+    const part_t *pl = loc(part);
     int32_t *cand, *list, *conf;
-    uint32_t *st;
+    Rep<uint32_t> st;
     HS_CHECK_CUDA(dalloc(&cand, g.n, s));
-    HS_CHECK_CUDA(dalloc(&st, g.n, s));
+    const int64_t arena_mark = D.bump;  // st is released (stack order) when this level is done
+    int rc = alloc_rep(st, Lv.n_glob);
+    if (rc) return rc;
     HS_CHECK_CUDA(dalloc(&list, g.n, s));
     HS_CHECK_CUDA(dalloc(&conf, g.n, s));
-    int rc = weights(g, part);
+    rc = weights(g, pl);
     if (rc) return rc;
     // finest level with twins: ghost copies of the neighbours' parts inside
     // the adjacency stream (refinement reads 1 coalesced byte per entry)
     int32_t wconst = 0;
-    if (finest && g.twin) {
+    if (finest && g.twin && !D.on()) {
       HS_CHECK_CUDA(dalloc(&gp, g.nnz, s));
-      ghost_fill<<<hs::grid_for(g.nnz, 256), 256, 0, s>>>(g.nnz, g.adj, part, gp);
+      ghost_fill<<<hs::grid_for(g.nnz, 256), 256, 0, s>>>(g.nnz, g.adj, pl, gp);
       HS_CHECK_LAUNCH();
       HS_CHECK_CUDA(cudaMemsetAsync(ctl + 13, 0x7f, 2 * sizeof(int32_t), s));
       wrange_kernel<<<hs::grid_for(g.nnz, 256, hs::sm_count() * 8), 256, 0, s>>>(g.nnz, g.wgt,
@@ -985,7 +1192,7 @@ struct Kway {
     if (rc) return rc;
     const int T = team_for(g);
     const int tgrid = team_grid(g.n, T);
-    int max_passes = g.nnz > (4ll << 20) ? passes_big : passes_small;
+    int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big : passes_small;
     if (!finest && passes_coarse >= 0) max_passes = passes_coarse;
     // 16-bit packed connectivity counters are exact iff every vertex's
     // weighted degree stays below 2^16 on this level
@@ -994,6 +1201,8 @@ struct Kway {
       HS_CHECK_CUDA(cudaMemsetAsync(ctl + 12, 0, sizeof(int32_t), s));
       max_wdeg_kernel<<<hs::grid_for(g.n, 256, hs::sm_count() * 8), 256, 0, s>>>(g, ctl + 12);
       HS_CHECK_LAUNCH();
+      rc = ar({seg32(ctl + 12, 1, 1)});
+      if (rc) return rc;
       int32_t mx = 0;
       HS_CHECK_CUDA(cudaMemcpyAsync(&mx, ctl + 12, sizeof mx, cudaMemcpyDeviceToHost, s));
       HS_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -1007,23 +1216,30 @@ struct Kway {
       {
         hs::Prof P("refine_candidates", s, 28.0 * g.n + 12.0 * g.nnz);
         const int TR = k <= 16 ? refine_team_for(g) : team_for(g);
-        HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, part, k, d_pw, d_hi, d_lo, st,
+        HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, pl, k, d_pw, d_hi, d_lo, st,
                            list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst);
       }
       HS_CHECK_LAUNCH();
+      rc = barrier();  // every rank's candidate states are in place
+      if (rc) return rc;
       {
         hs::Prof P("refine_afterburner", s, 4.0 * g.n);  // lower bound: list-sized reads
-        HS_TEAM_DISPATCH(T, afterburner_t, tgrid, g, st, list, ctl + CTL_COUNT, k, conf, d_flows,
-                         ctl + CTL_NCONF, ctl + CTL_ACTIVE);
+        HS_TEAM_DISPATCH(T, afterburner_t, tgrid, g, loc(st), list, ctl + CTL_COUNT, k, conf,
+                         d_flows, ctl + CTL_NCONF, ctl + CTL_ACTIVE);
       }
       HS_CHECK_LAUNCH();
-      plan_kernel<<<1, kMaxParts, 0, s>>>(k, g.n, 0, d_flows, d_pw, d_hi, d_lo, d_target, d_prob,
-                                          ctl);
+      rc = ar_flows();
+      if (rc) return rc;
+      plan_kernel<<<1, kMaxParts, 0, s>>>(k, Lv.n_glob, 0, d_flows, d_pw, d_hi, d_lo, d_target,
+                                          d_prob, ctl);
       HS_CHECK_LAUNCH();
+      int64_t *tgt = apply_target();
       apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
-          list, ctl + CTL_COUNT, conf, g.vw, d_prob, k, salt2 + pass * 104729, part, d_pw,
-          ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
+          list, ctl + CTL_COUNT, conf, g.vw, d_prob, k, salt2 + pass * 104729, g.v0, pl, part,
+          tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
       HS_CHECK_LAUNCH();
+      rc = ar_applied();
+      if (rc) return rc;
     }
     rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8);
     if (gp) {
@@ -1031,7 +1247,8 @@ struct Kway {
       gp = nullptr;
     }
     cudaFreeAsync(cand, s);
-    cudaFreeAsync(st, s);
+    free_rep(st);
+    D.bump = arena_mark;
     cudaFreeAsync(list, s);
     cudaFreeAsync(conf, s);
     return rc;
@@ -1047,6 +1264,7 @@ struct Kway {
       HS_TEAM_DISPATCH(T, cut_t, team_grid(g.n, T), g, part, c2);
     }
     hs::count_launch();
+    if (ar({seg64((int64_t *)c2, 1)})) return -1;
     cudaMemcpyAsync(&h, c2, 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     cudaFreeAsync(c2, s);
@@ -1103,7 +1321,7 @@ struct Kway {
       HS_CHECK_CUDA(cudaMemcpyAsync(&cnt, ctl + 7, sizeof cnt, cudaMemcpyDeviceToHost, s));
       HS_CHECK_CUDA(cudaStreamSynchronize(s));  // host round trip 1
       if (prev_nnz_pending) {  // the previous level's live adjacency count has landed
-        levels.back().g.nnz = *h_nnz;
+        levels.back().g.nnz = levels.back().nnz_glob = *h_nnz;
         prev_nnz_pending = false;
       }
       if (timer.on)
@@ -1146,7 +1364,11 @@ struct Kway {
     int32_t nc = 0;
     HS_CHECK_CUDA(cudaMemcpyAsync(&nc, cid + n, sizeof nc, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));  // host round trip 2
-    if (nc > (int64_t)n * 92 / 100) {  // matching stalled: stop coarsening here
+    // sharded: coarse ids of rank r follow those of ranks < r
+    int64_t coff = 0, nc_glob = nc;
+    rc = exscan_host(nc, &coff, &nc_glob);
+    if (rc) return rc;
+    if (nc_glob > (int64_t)F.n_glob * 92 / 100) {  // matching stalled: stop coarsening here
       cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
       cudaFreeAsync(flag, s); cudaFreeAsync(cid, s);
       *stop = true;
@@ -1154,17 +1376,25 @@ struct Kway {
     }
     Level C;
     C.g.n = nc;
+    C.g.v0 = (int32_t)coff;
+    C.n_glob = (int32_t)nc_glob;
     int32_t *mem0, *mem1;
     int64_t *ub;
-    HS_CHECK_CUDA(dalloc(&F.cmap, n, s));
+    Rep<int32_t> cmap;
+    rc = alloc_rep(cmap, F.n_glob);
+    if (rc) return rc;
+    F.cmap = loc(cmap);
     HS_CHECK_CUDA(dalloc(&mem0, nc, s));
     HS_CHECK_CUDA(dalloc(&mem1, nc, s));
     HS_CHECK_CUDA(dalloc(&ub, nc + 1, s));
     HS_CHECK_CUDA(dalloc(&C.g.vw, nc, s));
     HS_CHECK_CUDA(dalloc(&C.g.deg, nc, s));
     HS_CHECK_CUDA(dalloc(&C.g.xbeg, nc + 1, s));
-    build_cmap<<<hs::grid_for(n, 256), 256, 0, s>>>(F.g, match, cid, F.cmap, mem0, mem1, C.g.vw, ub);
+    build_cmap<<<hs::grid_for(n, 256), 256, 0, s>>>(F.g, match, cid, (int32_t)coff, cmap, mem0,
+                                                    mem1, C.g.vw, ub);
     HS_CHECK_LAUNCH();
+    rc = barrier();  // every rank's part of the fine->coarse map is in place
+    if (rc) return rc;
     HS_CHECK_CUDA(cudaMemsetAsync(ub + nc, 0, sizeof(int64_t), s));
     rc = exclusive_scan<int64_t>(ub, C.g.xbeg, nc + 1, s);
     if (rc) return rc;
@@ -1177,7 +1407,7 @@ struct Kway {
     // Will this coarse level be the last one (merged average degree above
     // the stop threshold)? Estimate the merge ratio on a 1/64 sample.
     bool direct = false;
-    if (nc >= 65536) {
+    if (nc_glob >= 65536) {
       const int S = 64;
       contract_warp<<<warp_grid(nc / S + 1, kContractWarps), kContractWarps * 32, 0, s>>>(
           F.g, F.cmap, mem0, mem1, ub, nc, C.g, S);
@@ -1187,12 +1417,15 @@ struct Kway {
       HS_CHECK_CUDA(cudaMemsetAsync(sr, 0, 16, s));
       sample_ratio<<<hs::grid_for(nc / S + 1, 256), 256, 0, s>>>(ub, C.g.deg, nc, S, kWarpSlots, sr);
       HS_CHECK_LAUNCH();
+      rc = ar({seg64((int64_t *)sr, 2)});
+      if (rc) return rc;
       unsigned long long hr[2] = {0, 0};
       HS_CHECK_CUDA(cudaMemcpyAsync(hr, sr, 16, cudaMemcpyDeviceToHost, s));
       HS_CHECK_CUDA(cudaStreamSynchronize(s));
       cudaFreeAsync(sr, s);
       if (hr[1] > 0) {
-        const double merged_avg = (double)hr[0] / (double)hr[1] * (double)F.g.nnz / (double)nc;
+        const double merged_avg =
+            (double)hr[0] / (double)hr[1] * (double)F.nnz_glob / (double)nc_glob;
         direct = merged_avg > max_deg;
       }
     }
@@ -1235,11 +1468,14 @@ struct Kway {
     HS_CHECK_LAUNCH();
     {
       int32_t *gk = nullptr, *gv = nullptr;
-      int rc2 = global_tables(2 * capc, &gk, &gv);
+      int rc2 = D.on() ? (dalloc(&gk, 2 * capc, s) == cudaSuccess &&
+                                  dalloc(&gv, 2 * capc, s) == cudaSuccess ? HS_OK : HS_ECUDA)
+                       : global_tables(2 * capc, &gk, &gv);
       if (rc2) return rc2;
       hs::Prof P("contract_block_global", s, 0.0);
       contract_block<<<hs::sm_count() * 2, 1024, 0, s>>>(F.g, F.cmap, mem0, mem1, ub, list2,
                                                          ctl + 9, C.g, gk, gv, 0);
+      if (D.on()) { cudaFreeAsync(gk, s); cudaFreeAsync(gv, s); }
     }
     HS_CHECK_LAUNCH();
     cudaFreeAsync(list, s); cudaFreeAsync(list2, s); cudaFreeAsync(ncd, s);
@@ -1250,9 +1486,18 @@ struct Kway {
       hs::Scratch<char> tmp;
       HS_CHECK_CUDA(tmp.alloc(tb, s));
       HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, C.g.deg, d_nnz, nc, s));
-      HS_CHECK_CUDA(cudaMemcpyAsync(h_nnz, d_nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-      prev_nnz_pending = true;
       hs::count_launch(1);
+      if (D.on()) {  // local and global counts now (the stop rule needs the global one)
+        int64_t mine = 0, before = 0;
+        HS_CHECK_CUDA(cudaMemcpyAsync(&mine, d_nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        HS_CHECK_CUDA(cudaStreamSynchronize(s));
+        C.g.nnz = mine;
+        rc = exscan_host(mine, &before, &C.nnz_glob);
+        if (rc) return rc;
+      } else {
+        HS_CHECK_CUDA(cudaMemcpyAsync(h_nnz, d_nnz, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        prev_nnz_pending = true;
+      }
     }
     cudaFreeAsync(match, s); cudaFreeAsync(prop, s); cudaFreeAsync(fav, s);
     cudaFreeAsync(flag, s); cudaFreeAsync(cid, s); cudaFreeAsync(mem0, s);
@@ -1284,7 +1529,7 @@ struct Kway {
   int settle_nnz() {
     if (!prev_nnz_pending) return HS_OK;
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
-    levels.back().g.nnz = *h_nnz;
+    levels.back().g.nnz = levels.back().nnz_glob = *h_nnz;
     prev_nnz_pending = false;
     return HS_OK;
   }
@@ -1323,28 +1568,42 @@ struct Kway {
     return HS_OK;
   }
 
-  int initial(part_t **out_part) {
+  int initial(Rep<part_t> &best_rep) {
     Level &Cst = levels.back();
     G &g = Cst.g;
     const int nc = g.n;
-    part_t *best;
-    HS_CHECK_CUDA(dalloc(&best, nc, s));
-    // trial 0: id-range bands
+    int rc0 = alloc_rep(best_rep, Cst.n_glob);
+    if (rc0) return rc0;
+    part_t *best = loc(best_rep);
+    // trial 0: id-range bands (global prefix of the weights when sharded)
     {
       int64_t *vw64, *prefix;
       HS_CHECK_CUDA(dalloc(&vw64, nc + 1, s));
       HS_CHECK_CUDA(dalloc(&prefix, nc + 1, s));
       int rc = hs_widen32(g.vw, vw64, nc, s);
       if (rc) return rc;
-      rc = exclusive_scan<int64_t>(vw64, prefix, nc, s);
+      HS_CHECK_CUDA(cudaMemsetAsync(vw64 + nc, 0, sizeof(int64_t), s));
+      rc = exclusive_scan<int64_t>(vw64, prefix, nc + 1, s);
       if (rc) return rc;
-      range_parts<<<hs::grid_for(nc, 256), 256, 0, s>>>(nc, prefix, g.vw, d_cum, k, total_vw, best);
+      int64_t woff = 0;
+      if (D.on()) {
+        int64_t mine = 0, all = 0;
+        HS_CHECK_CUDA(cudaMemcpyAsync(&mine, prefix + nc, 8, cudaMemcpyDeviceToHost, s));
+        HS_CHECK_CUDA(cudaStreamSynchronize(s));
+        rc = exscan_host(mine, &woff, &all);
+        if (rc) return rc;
+      }
+      range_parts<<<hs::grid_for(nc, 256), 256, 0, s>>>(nc, prefix, woff, g.vw, d_cum, k,
+                                                        total_vw, g.v0, best_rep);
       HS_CHECK_LAUNCH();
       cudaFreeAsync(vw64, s);
       cudaFreeAsync(prefix, s);
+      rc = barrier();  // every rank's bands are in place
+      if (rc) return rc;
     }
     // warp trials (BFS-order LDG + greedy refinement) on small coarsest graphs
-    if (nc <= 32768) {
+    // (one GPU: the sharded path keeps the band start)
+    if (nc <= 32768 && !D.on()) {
       const int64_t best_cut = cut_of(g, best);
       std::vector<int64_t> pw;
       int rc = weights(g, best);
@@ -1383,43 +1642,57 @@ struct Kway {
       cudaFreeAsync(IA.parts, s); cudaFreeAsync(IA.order, s); cudaFreeAsync(IA.seen, s);
       cudaFreeAsync(IA.cut, s); cudaFreeAsync(IA.infeas, s); cudaFreeAsync(bt, s);
     }
-    *out_part = best;
     return HS_OK;
   }
 };
 
 }  // namespace
 
+extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
+                                   const int32_t *edge_w_i, const int32_t *edge_w_i_in,
+                                   const int32_t *node_w_i, int64_t *xadj, int32_t *adjncy,
+                                   int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,
+                                   int64_t *nnz_host, void *stream) {
+  HS_REQUIRE(g && edge_w_i && node_w_i && xadj && adjncy && adjwgt_i && vwgt_i, HS_EINVAL,
+             "hs_symmetrize: null argument");
+  const int nk = g->n - 1;
+  HS_REQUIRE(0 <= kv0 && kv0 <= kv1 && kv1 <= nk, HS_EINVAL, "kernel range [%d, %d) outside [0, %d)",
+             kv0, kv1, nk);
+  HS_REQUIRE(!twin || (kv0 == 0 && kv1 == nk), HS_EINVAL, "twin indices need the full range");
+  HS_REQUIRE(!twin || 2 * g->m < (1ll << 31), HS_ELIMIT, "twin indices need < 2^31 entries");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nl = kv1 - kv0;
+  hs::Scratch<int32_t> deg;
+  hs::Scratch<int64_t> deg64;
+  HS_CHECK_CUDA(deg.alloc(nl + 1, s));
+  HS_CHECK_CUDA(deg64.alloc(nl + 1, s));
+  // in/out pointers, in_src/out_dst, weights (in + out order), adj+wgt writes
+  const double frac = nk ? (double)nl / (double)nk : 0.0;
+  hs::Prof P("symmetrize", s, frac * (32.0 * g->n + 32.0 * g->m));
+  sym_degree<<<hs::grid_for(nl, 256), 256, 0, s>>>(*g, kv0, kv1, deg);
+  HS_CHECK_LAUNCH();
+  HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nl, 0, sizeof(int64_t), s));
+  int rc = hs_widen32(deg, deg64, nl, s);
+  if (rc) return rc;
+  rc = exclusive_scan<int64_t>(deg64, xadj, nl + 1, s);
+  if (rc) return rc;
+  sym_fill<<<std::max(1, std::min(hs::sm_count() * 32, (nl * 8 + 255) / 256)), 256, 0, s>>>(
+      *g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin);
+  HS_CHECK_LAUNCH();
+  if (nnz_host) {
+    HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  return HS_OK;
+}
+
 extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i,
                              const int32_t *edge_w_i_in, const int32_t *node_w_i, int64_t *xadj,
                              int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,
                              int64_t *nnz_host, void *stream) {
-  HS_REQUIRE(!twin || 2 * g->m < (1ll << 31), HS_ELIMIT, "twin indices need < 2^31 entries");
-  HS_REQUIRE(g && edge_w_i && node_w_i && xadj && adjncy && adjwgt_i && vwgt_i, HS_EINVAL,
-             "hs_symmetrize: null argument");
-  cudaStream_t s = (cudaStream_t)stream;
-  const int nk = g->n - 1;
-  hs::Scratch<int32_t> deg;
-  hs::Scratch<int64_t> deg64;
-  HS_CHECK_CUDA(deg.alloc(nk + 1, s));
-  HS_CHECK_CUDA(deg64.alloc(nk + 1, s));
-  // in/out pointers, in_src/out_dst, weights (in + out order), adj+wgt writes
-  hs::Prof P("symmetrize", s, 32.0 * g->n + 32.0 * g->m);
-  sym_degree<<<hs::grid_for(g->n, 256), 256, 0, s>>>(*g, deg);
-  HS_CHECK_LAUNCH();
-  HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nk, 0, sizeof(int64_t), s));
-  int rc = hs_widen32(deg, deg64, nk, s);
-  if (rc) return rc;
-  rc = exclusive_scan<int64_t>(deg64, xadj, nk + 1, s);
-  if (rc) return rc;
-  sym_fill<<<std::max(1, std::min(hs::sm_count() * 32, (g->n * 8 + 255) / 256)), 256, 0, s>>>(
-      *g, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin);
-  HS_CHECK_LAUNCH();
-  if (nnz_host) {
-    HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nk, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaStreamSynchronize(s));
-  }
-  return HS_OK;
+  HS_REQUIRE(g, HS_EINVAL, "hs_symmetrize: null argument");
+  return hs_symmetrize_range(g, 0, g->n - 1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy,
+                             adjwgt_i, vwgt_i, twin, nnz_host, stream);
 }
 
 namespace {
@@ -1437,14 +1710,12 @@ int hs_widen32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s) {
   return HS_OK;
 }
 
-extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double *tpwgts_host,
-                                 double tol, uint64_t seed, int32_t *part_out,
-                                 int64_t *stats_host, void *stream) {
-  HS_REQUIRE(ug && tpwgts_host && part_out, HS_EINVAL, "hs_partition_kway: null argument");
-  HS_REQUIRE(k >= 1 && k <= kMaxParts, HS_ELIMIT, "k must be in 1..%d", kMaxParts);
-  HS_REQUIRE(ug->n >= 1, HS_EINVAL, "empty graph");
-  HS_REQUIRE(ug->adjwgt_i && ug->vwgt_i, HS_EINVAL, "k-way path needs integer weights");
-  cudaStream_t s = (cudaStream_t)stream;
+namespace {
+// One GPU (dist == nullptr) or one rank of a sharded group: ug holds this
+// rank's rows [v0, v0 + ug->n) of an n_glob-vertex graph.
+int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_dist_t *dist,
+                   int32_t k, const double *tpwgts_host, double tol, uint64_t seed,
+                   int32_t *part_out, int64_t *stats_host, cudaStream_t s) {
   const int n0 = ug->n;
   const int64_t nnz0 = ug->nnz;
   Kway K(s);
@@ -1452,12 +1723,27 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   K.tol = tol;
   K.seed = seed;
   K.salt = seed * 0x9E3779B97F4A7C15ull + 0x1234567ull;
+  if (dist && dist->size > 1) {
+    K.D.rank = dist->rank;
+    K.D.P = dist->size;
+    for (int r = 0; r < dist->size; ++r) K.D.arena[r] = (char *)dist->arena[r];
+    K.D.arena_bytes = dist->arena_bytes;
+    K.D.threads = dist->mode == 1;
+    if (K.D.threads) K.hb = host_barrier_for(dist->arena[0]);
+    int rc0 = no_cross_stream_pool_waits();
+    if (rc0) return rc0;
+    rc0 = load_epoch(K.D, &K.D.epoch, s);
+    if (rc0) return rc0;
+    HS_CHECK_CUDA(cudaMemsetAsync(K.D.arena[K.D.rank] + 64, 0, 4, s));  // this rank's watchdog word
+    HS_CHECK_CUDA(dalloc(&K.d_dpw, k, s));
+    HS_CHECK_CUDA(dalloc(&K.d_arbuf, kArSlots, s));
+  }
   K.timer.mark("start");
 
   // ---- totals and the int32 weight guard ----
   int64_t *tot_dev;
-  HS_CHECK_CUDA(dalloc(&tot_dev, 2, s));
-  int64_t tot[2] = {0, 0};
+  HS_CHECK_CUDA(dalloc(&tot_dev, 3, s));
+  int64_t tot[3] = {0, 0, nnz0};
   {
     size_t tb = 0, tb2 = 0;
     HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, ug->adjwgt_i, tot_dev, nnz0, s));
@@ -1466,8 +1752,13 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
     HS_CHECK_CUDA(tmp.alloc(std::max(tb, tb2), s));
     HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, ug->adjwgt_i, tot_dev, nnz0, s));
     HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb2, ug->vwgt_i, tot_dev + 1, n0, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev + 2, &tot[2], 8, cudaMemcpyHostToDevice, s));
+    int rc = K.ar({Kway::seg64(tot_dev, 3)});  // sums over all ranks' rows
+    if (rc) return rc;
     HS_CHECK_CUDA(cudaMemcpyAsync(tot, tot_dev, sizeof tot, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    rc = K.check_peers();
+    if (rc) return rc;
     hs::count_launch(2);
   }
   cudaFreeAsync(tot_dev, s);
@@ -1479,8 +1770,11 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   L0.own_adj = false;
   L0.own_xbeg_vw = false;
   L0.g.n = n0;
+  L0.g.v0 = v0;
+  L0.n_glob = n_glob;
   L0.g.cap = nnz0;
   L0.g.nnz = nnz0;
+  L0.nnz_glob = tot[2];
   L0.g.xbeg = const_cast<int64_t *>(ug->xadj);
   L0.g.adj = const_cast<int32_t *>(ug->adjncy);
   L0.g.twin = ug->twin;
@@ -1540,16 +1834,16 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   // every further level costs a full pass over ~all edges.
   // Default: 1.5x the finest level's average degree (edges no longer shrink
   // with the vertices, so matching has no locality left to exploit).
-  const double deg0 = n0 ? (double)nnz0 / (double)n0 : 0.0;
+  const double deg0 = n_glob ? (double)L0.nnz_glob / (double)n_glob : 0.0;
   double max_deg = std::max(16.0, 1.5 * deg0);
   if (const char *e = getenv("HS_KWAY_MAXDEG")) max_deg = atof(e);
   K.max_deg = max_deg;
-  while (!stop && K.levels.back().g.n > coarse_target && (int)K.levels.size() < 40) {
+  while (!stop && K.levels.back().n_glob > coarse_target && (int)K.levels.size() < 40) {
     if (K.levels.size() > 1) {
       int rc0 = K.settle_nnz();
       if (rc0) return rc0;
-      const G &cg = K.levels.back().g;
-      if ((double)cg.nnz > max_deg * (double)cg.n) break;
+      const Level &cl = K.levels.back();
+      if ((double)cl.nnz_glob > max_deg * (double)cl.n_glob) break;
     }
     const bool ncu_win = K.levels.size() == 1 && getenv("HS_NCU_COARSEN0") != nullptr;
     if (ncu_win) cudaProfilerStart();
@@ -1564,45 +1858,50 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
     if (rc) return rc;
   }
   // ---- initial partition ----
-  part_t *cur = nullptr;
-  int rc = K.initial(&cur);
+  Rep<part_t> cur;
+  int rc = K.initial(cur);
   if (rc) return rc;
   K.timer.mark("initial partition");
-  const int coarsest_n = K.levels.back().g.n;
+  const int coarsest_n = K.levels.back().n_glob;
 
   // ---- uncoarsening + refinement ----
   for (int li = (int)K.levels.size() - 1; li >= 0; --li) {
     Level &Lv = K.levels[li];
     if (li != (int)K.levels.size() - 1) {
-      part_t *pf;
-      HS_CHECK_CUDA(dalloc(&pf, Lv.g.n, s));
-      project<<<hs::grid_for(Lv.g.n, 256), 256, 0, s>>>(Lv.g.n, Lv.cmap, cur, pf);
+      // every rank projects the whole (replicated) map into its own replica
+      Rep<part_t> pf;
+      rc = K.alloc_rep(pf, Lv.n_glob);
+      if (rc) return rc;
+      project<<<hs::grid_for(Lv.n_glob, 256), 256, 0, s>>>(Lv.n_glob, Lv.cmap, K.loc(cur),
+                                                           K.loc(pf));
       HS_CHECK_LAUNCH();
-      cudaFreeAsync(cur, s);
+      K.free_rep(cur);
       cur = pf;
     }
     // HS_NCU_LEVEL0=1: open the profiler window around the finest level only
     const bool ncu_win = li == 0 && getenv("HS_NCU_LEVEL0") != nullptr;
     if (ncu_win) cudaProfilerStart();
-    rc = K.refine(Lv.g, cur, K.salt ^ ((uint64_t)li << 40), li == 0);
+    rc = K.refine(Lv, cur, K.salt ^ ((uint64_t)li << 40), li == 0);
     if (ncu_win) cudaProfilerStop();
     if (rc) return rc;
     K.timer.mark("refine level");
   }
-  int8_to_int32<<<hs::grid_for(n0, 256), 256, 0, s>>>(cur, n0, part_out);
+  int8_to_int32<<<hs::grid_for(n_glob, 256), 256, 0, s>>>(K.loc(cur), n_glob, part_out);
   HS_CHECK_LAUNCH();
 
   // ---- statistics (cut with the caller's unscaled weights) ----
   G g0 = K.levels[0].g;  // the caller's arrays and unscaled weights
   g0.adj = const_cast<int32_t *>(ug->adjncy);
   g0.wgt = const_cast<int32_t *>(ug->adjwgt_i);
-  int64_t cut = K.cut_of(g0, cur);
+  int64_t cut = K.cut_of(g0, K.loc(cur));
   std::vector<int64_t> pw;
-  rc = K.weights(g0, cur);
+  rc = K.weights(g0, K.loc(cur));
   if (rc) return rc;
   rc = K.read_pw(pw);
   if (rc) return rc;
-  cudaFreeAsync(cur, s);
+  rc = K.check_peers();
+  if (rc) return rc;
+  K.free_rep(cur);
   K.timer.mark("stats");
   double maxdev = 0;
   for (int p = 0; p < k; ++p)
@@ -1623,7 +1922,7 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   }
   for (size_t i = 0; i < K.levels.size(); ++i) {
     Level &Lv = K.levels[i];
-    if (Lv.cmap) cudaFreeAsync(Lv.cmap, s);
+    if (Lv.cmap && !K.D.on()) cudaFreeAsync(Lv.cmap, s);  // sharded: lives in the arena
     cudaFreeAsync(Lv.g.deg, s);
     if (Lv.own_adj) cudaFreeAsync(Lv.g.adj, s);
     if (Lv.own_wgt) cudaFreeAsync(Lv.g.wgt, s);
@@ -1633,6 +1932,58 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   cudaFreeAsync(K.d_pw, s); cudaFreeAsync(K.d_flows, s); cudaFreeAsync(K.d_prob, s);
   cudaFreeAsync(K.d_cum, s); cudaFreeAsync(K.counter, s);
   cudaFreeAsync(K.ctl, s); cudaFreeAsync(K.d_nnz, s);
-
+  if (K.d_dpw) cudaFreeAsync(K.d_dpw, s);
+  if (K.d_arbuf) cudaFreeAsync(K.d_arbuf, s);
+  // no runtime error may leak to the caller's next CUDA call
+  const cudaError_t e = cudaGetLastError();
+  HS_REQUIRE(e == cudaSuccess, HS_ECUDA, "k-way: %s", cudaGetErrorString(e));
   return HS_OK;
+}
+}  // namespace
+
+extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double *tpwgts_host,
+                                 double tol, uint64_t seed, int32_t *part_out,
+                                 int64_t *stats_host, void *stream) {
+  HS_REQUIRE(ug && tpwgts_host && part_out, HS_EINVAL, "hs_partition_kway: null argument");
+  HS_REQUIRE(k >= 1 && k <= kMaxParts, HS_ELIMIT, "k must be in 1..%d", kMaxParts);
+  HS_REQUIRE(ug->n >= 1, HS_EINVAL, "empty graph");
+  HS_REQUIRE(ug->adjwgt_i && ug->vwgt_i, HS_EINVAL, "k-way path needs integer weights");
+  return partition_impl(ug, 0, ug->n, nullptr, k, tpwgts_host, tol, seed, part_out, stats_host,
+                        (cudaStream_t)stream);
+}
+
+extern "C" int64_t hs_kway_dist_arena_bytes(int32_t n_global) {
+  // parts of every level, one refinement state (4n), the fine->coarse maps
+  // of every level (levels shrink geometrically: sum <= 24n with slack),
+  // 256-byte rounding per array
+  return (int64_t)kArenaHeader + 24ll * (int64_t)n_global + (1ll << 20);
+}
+
+extern "C" int hs_partition_kway_dist(const hs_ugraph_t *ug, int32_t v0, int32_t n_global,
+                                      const hs_dist_t *dist, int32_t k,
+                                      const double *tpwgts_host, double tol, uint64_t seed,
+                                      int32_t *part_out, int64_t *stats_host, void *stream) {
+  HS_REQUIRE(ug && dist && tpwgts_host && part_out, HS_EINVAL,
+             "hs_partition_kway_dist: null argument");
+  HS_REQUIRE(k >= 1 && k <= kMaxParts, HS_ELIMIT, "k must be in 1..%d", kMaxParts);
+  HS_REQUIRE(dist->size >= 1 && dist->size <= kMaxRanks && dist->rank >= 0 &&
+                 dist->rank < dist->size, HS_EINVAL, "bad group (rank %d of %d, max %d ranks)",
+             dist->rank, dist->size, kMaxRanks);
+  HS_REQUIRE(ug->n >= 1 && v0 >= 0 && (int64_t)v0 + ug->n <= n_global, HS_EINVAL,
+             "rank range [%d, %lld) outside [0, %d) or empty", v0, (long long)v0 + ug->n,
+             n_global);
+  HS_REQUIRE(ug->adjwgt_i && ug->vwgt_i, HS_EINVAL, "k-way path needs integer weights");
+  HS_REQUIRE(!ug->twin, HS_EINVAL, "sharded partition takes no twin index");
+  if (dist->size == 1) {
+    HS_REQUIRE(v0 == 0 && ug->n == n_global, HS_EINVAL, "a 1-rank group owns the whole graph");
+    return partition_impl(ug, 0, n_global, nullptr, k, tpwgts_host, tol, seed, part_out,
+                          stats_host, (cudaStream_t)stream);
+  }
+  for (int r = 0; r < dist->size; ++r)
+    HS_REQUIRE(dist->arena[r], HS_EINVAL, "arena of rank %d missing", r);
+  HS_REQUIRE(dist->arena_bytes >= hs_kway_dist_arena_bytes(n_global), HS_ELIMIT,
+             "arena of %lld bytes < hs_kway_dist_arena_bytes(%d)", (long long)dist->arena_bytes,
+             n_global);
+  return partition_impl(ug, v0, n_global, dist, k, tpwgts_host, tol, seed, part_out, stats_host,
+                        (cudaStream_t)stream);
 }

@@ -101,8 +101,8 @@ __device__ __forceinline__ int st_gain(uint32_t s) { return (int)(s >> 14); }
 template <int T, int KR>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
-              const int64_t *lo, uint32_t *st, int32_t *list, int32_t *count, const int32_t *run,
-              const part_t *gp, int32_t wconst) {
+              const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
+              const int32_t *run, const part_t *gp, int32_t wconst) {
   if (run && !*run) return;
   __shared__ int32_t conn_s[KR != 0 ? 1 : kTeamBlock / T][kMaxParts];
   // KR < 0: per-lane private counters, [part][thread] so every lane hits its
@@ -132,7 +132,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
     int64_t b = 0;
     int d = 0;
     if (valid) {
-      own = part[v];
+      own = part[g.v0 + v];
       vwv = g.vw[v];
       b = g.xbeg[v];
       d = g.deg[v];
@@ -268,7 +268,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
     }
     const bool writer = valid && lane == 0;
     const int c = (bp >= 0 && bg > 0) ? bp : -1;
-    if (writer) st[v] = pack_state(own, c, bg);
+    if (writer) st.put(g.v0 + v, pack_state(own, c, bg));
     app.push(writer && c >= 0, v, list, count);
   }
   app.flush(list, count);
@@ -298,7 +298,7 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
     int delta = 0, v = 0, dest = -1, own = 0;
     if (valid) {
       v = list[i];
-      const uint32_t sv = st[v];
+      const uint32_t sv = st[g.v0 + v];
       dest = st_cand(sv);
       own = st_part(sv);
       const int gv = st_gain(sv);
@@ -322,7 +322,7 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
           const int cu = st_cand(su[q]);
           if (cu >= 0) {
             const int gu = st_gain(su[q]);
-            if (gu > gv || (gu == gv && u[q] < v)) pu = cu;
+            if (gu > gv || (gu == gv && u[q] < g.v0 + v)) pu = cu;
           }
           delta += (pu == dest ? w[q] : 0) - (pu == own ? w[q] : 0);
         }
@@ -351,9 +351,9 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
 // prob[own] * prob[k + dest] (hash of (salt, v): deterministic thinning).
 __global__ void apply_list(const int32_t *list, const int32_t *count, const int32_t *conf,
                            const int32_t *vw, const double *prob, int k, uint64_t salt,
-                           part_t *part, int64_t *pw, const int32_t *run,
-                           const int64_t *xbeg, const int32_t *deg, const int32_t *twin,
-                           part_t *gp) {
+                           int32_t v0, const part_t *part, Rep<part_t> prep, int64_t *pw,
+                           const int32_t *run, const int64_t *xbeg, const int32_t *deg,
+                           const int32_t *twin, part_t *gp) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -366,12 +366,12 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
     const int dest = conf[i];
     if (dest < 0) continue;
     const int v = list[i];
-    const int own = part[v];
+    const int own = part[v0 + v];
     const double pr = s_prob[own] * s_prob[k + dest];
-    if (pr < 1.0 &&
-        (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
+    const uint64_t gv = (uint64_t)(v0 + v);
+    if (pr < 1.0 && (double)mix32(salt ^ (gv * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
       continue;
-    part[v] = dest;
+    prep.put(v0 + v, (part_t)dest);
     if (gp)  // keep the ghost copies in the neighbours' lists current
       for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
     atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
@@ -406,20 +406,22 @@ propose_t(G g, const uint32_t *mw, int32_t *prop, int32_t *fav, uint64_t salt,
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
           const int j = j0 + q * T;
-          vq[q] = j < d ? __ldg(g.adj + b + j) : -1;
+          vq[q] = j < d ? __ldg(g.adj + b + j) - g.v0 : -1;  // local index
           wq[q] = j < d ? __ldg(g.wgt + b + j) : 0;
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) mq[q] = vq[q] >= 0 ? __ldg(mw + vq[q]) : 0x80000000u;
+        for (int q = 0; q < 2; ++q)
+          mq[q] = (unsigned)vq[q] < (unsigned)g.n ? __ldg(mw + vq[q]) : 0x80000000u;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
         const int v = vq[q];
-        if (v < 0 || v == u) continue;
+        // sharded: matching pairs vertices of one rank only (local contraction)
+        if ((unsigned)v >= (unsigned)g.n || v == u) continue;
         const uint32_t wv = mq[q];
         const int32_t vv = (int32_t)(wv & 0x7fffffffu);
         if (vu + vv > max_vw) continue;
         float r = rating(wq[q], vu, vv);
-        uint32_t h = edge_hash32(u, v, (uint32_t)salt);
+        uint32_t h = edge_hash32(g.v0 + u, g.v0 + v, (uint32_t)salt);
         if (fav && (r > fr || (r == fr && (h > fh || (h == fh && v < fv))))) {
           fr = r; fh = h; fv = v;
         }
@@ -458,7 +460,7 @@ cut_t(G g, const part_t *part, unsigned long long *cut2) {
   for (int64_t vb = (int64_t)warp_id_global() * (32 / T); vb < g.n; vb += step) {
     const int v = (int)(vb + (threadIdx.x & 31) / T);
     if (v >= g.n) continue;
-    const int pv = part[v];
+    const int pv = part[g.v0 + v];
     const int64_t b = g.xbeg[v];
     const int d = g.deg[v];
     for (int j = lane; j < d; j += T)

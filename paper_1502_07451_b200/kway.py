@@ -170,3 +170,188 @@ def levels(csr: DagCSR, mode: int = 0):
 def level_order(csr: DagCSR) -> torch.Tensor:
     lv, _, _, nl = _native.levels(csr, 0)
     return _native.level_order(csr, lv, nl)
+
+
+# ---------------------------------------------------------------------------
+# Sharded partition (config 4 at 2/4/8 GPUs): rank r owns a contiguous range
+# of kernel positions; see csrc/dist.cuh for the exchange protocol.
+# ---------------------------------------------------------------------------
+
+def undirected_degrees(csr: DagCSR) -> torch.Tensor:
+    """Degree of every kernel in the symmetrised graph (root edges dropped), int64."""
+    deg = (csr.in_ptr[1:] - csr.in_ptr[:-1]) + (csr.out_ptr[1:] - csr.out_ptr[:-1])
+    r = csr.root
+    fed = csr.out_dst[int(csr.out_ptr[r]):int(csr.out_ptr[r + 1])].long()
+    deg = deg.clone()
+    deg[fed] -= 1
+    return torch.cat([deg[:r], deg[r + 1:]])
+
+
+def split_bounds(deg_cumsum: np.ndarray, nranks: int) -> list:
+    """Rank boundaries over kernel positions balancing adjacency entries.
+
+    deg_cumsum[i] = entries of kernels 0..i (inclusive). Boundary b_r (r = 1..P-1)
+    is the first position whose inclusive sum exceeds r/P of the total; every
+    rank gets at least one kernel. Pure integer function: every rank derives
+    the same ranges.
+    """
+    n = int(len(deg_cumsum))
+    if nranks < 1 or nranks > n:
+        raise ValueError(f"need 1 <= ranks <= {n} kernels (got {nranks})")
+    total = int(deg_cumsum[-1]) if n else 0
+    b = [0]
+    for r in range(1, nranks):
+        t = (total * r) // nranks
+        x = int(np.searchsorted(deg_cumsum, t, side="right"))
+        x = max(x, b[-1] + 1)
+        x = min(x, n - (nranks - r))
+        b.append(x)
+    b.append(n)
+    return [(b[i], b[i + 1]) for i in range(nranks)]
+
+
+def shard_ranges(csr: DagCSR, nranks: int) -> list:
+    cs = torch.cumsum(undirected_degrees(csr), 0).cpu().numpy()
+    return split_bounds(cs, nranks)
+
+
+def symmetrize_range(csr: DagCSR, kv0: int, kv1: int, edge_w_i: Optional[torch.Tensor] = None,
+                     node_w_i: Optional[torch.Tensor] = None,
+                     edge_w_i_in: Optional[torch.Tensor] = None,
+                     cap: Optional[int] = None) -> UGraph:
+    """K1 for the rows of kernel positions [kv0, kv1) (global neighbour ids).
+
+    ``cap`` = the rows' adjacency entries when known (saves a host round trip).
+    """
+    dev = csr.device
+    if edge_w_i is None:
+        edge_w_i = integer_weights(csr.w_xfer)
+    if node_w_i is None:
+        node_w_i = integer_weights(csr.w_gpu)
+    nl = kv1 - kv0
+    if cap is None:
+        cap = int(undirected_degrees(csr)[kv0:kv1].sum().item()) if nl else 0
+    xadj = torch.empty(nl + 1, dtype=torch.int64, device=dev)
+    adjncy = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    adjwgt = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    vwgt = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+    nnz = _native.symmetrize_range(csr, kv0, kv1, edge_w_i.contiguous(), node_w_i.contiguous(),
+                                   xadj, adjncy, adjwgt, vwgt,
+                                   edge_w_i_in.contiguous() if edge_w_i_in is not None else None)
+    assert nnz == cap
+    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz], vwgt[:nl])
+
+
+class PartitionGroup:
+    """Exchange arenas of a sharded partition, one whole device allocation per rank.
+
+    mode "loopback": every rank's arena on this GPU (ranks run as host threads on
+    separate streams) — the exact cross-rank protocol on one device.
+    mode "ipc": this process is rank `rank` of a torch.distributed group with one
+    process per GPU; peers' arenas are CUDA-IPC mappings.
+    """
+
+    def __init__(self, n_global: int, nranks: int, mode: str = "loopback", rank: int = 0,
+                 group=None):
+        from .cholesky import _Buf, _ipc_handle, _ipc_open
+        if not 1 <= nranks <= 8:
+            raise ValueError("1..8 ranks")
+        self.n_global, self.nranks, self.mode = n_global, nranks, mode
+        self.bytes = _native.kway_dist_arena_bytes(n_global)
+        if mode == "loopback":
+            self.bufs = [_Buf(self.bytes) for _ in range(nranks)]
+            for b in self.bufs:
+                b.fill_bytes(0)
+            self.ptrs = [b.data_ptr() for b in self.bufs]
+        elif mode == "ipc":
+            import torch.distributed as dist
+            import ctypes
+            me = _Buf(self.bytes)
+            me.fill_bytes(0)
+            torch.cuda.synchronize()
+            self.bufs = [me]
+            h = ctypes.create_string_buffer(64)
+            _native.check(_ipc_handle(me.data_ptr(), h))
+            allh = [None] * nranks
+            dist.all_gather_object(allh, h.raw, group=group)
+            self.ptrs = []
+            for q in range(nranks):
+                if q == rank:
+                    self.ptrs.append(me.data_ptr())
+                    continue
+                p = ctypes.c_void_p()
+                _native.check(_ipc_open(allh[q], ctypes.byref(p)))
+                self.ptrs.append(p.value)
+            dist.barrier(group=group)  # every arena zeroed before any rank's first flag
+        else:
+            raise ValueError(mode)
+        torch.cuda.synchronize()
+
+    def dist(self, rank: int):
+        d = _native.HsDist()
+        d.rank, d.size, d.arena_bytes = rank, self.nranks, self.bytes
+        d.mode = 1 if self.mode == "loopback" else 0
+        for q, p in enumerate(self.ptrs):
+            d.arena[q] = p
+        return d
+
+
+def partition_kway_shard(ug_local: UGraph, v0: int, n_global: int, group: PartitionGroup,
+                         rank: int, k: int, tpwgts: Optional[Sequence[float]] = None,
+                         tol: float = 0.03, seed: int = 0,
+                         out: Optional[torch.Tensor] = None) -> KwayResult:
+    """One rank's share of a sharded partition; returns the WHOLE partition (every rank)."""
+    if tpwgts is None:
+        tpwgts = [1.0 / k] * k
+    if len(tpwgts) != k:
+        raise ValueError("need one target fraction per part")
+    part = out if out is not None else torch.empty(n_global, dtype=torch.int32,
+                                                   device=ug_local.xadj.device)
+    st = _native.partition_kway_dist(ug_local, v0, n_global, group.dist(rank), k, tpwgts, tol,
+                                     seed, part)
+    return KwayResult(part, st[0], st[1], st[2], st[3] / 1e9, bool(st[4]), st[5])
+
+
+def partition_kway_loopback(csr: DagCSR, nranks: int, k: int,
+                            tpwgts: Optional[Sequence[float]] = None, tol: float = 0.03,
+                            seed: int = 0, group: Optional[PartitionGroup] = None,
+                            shards: Optional[list] = None):
+    """All ranks of a sharded partition on this GPU (one host thread + stream per rank).
+
+    Returns the list of per-rank KwayResults (each holds the whole partition).
+    """
+    import threading
+    n_global = csr.n - 1
+    ranges = shard_ranges(csr, nranks)
+    if shards is None:
+        ew = integer_weights(csr.w_xfer)
+        shards = [symmetrize_range(csr, a, b, ew, integer_weights(csr.w_gpu), in_order(csr, ew))
+                  for a, b in ranges]
+    group = group or PartitionGroup(n_global, nranks)
+    dev = csr.device
+    cur = torch.cuda.current_stream()
+    streams = [torch.cuda.Stream(device=dev) for _ in range(nranks)]
+    for st in streams:
+        st.wait_stream(cur)
+    out, err = [None] * nranks, [None] * nranks
+
+    def run(r):
+        try:
+            torch.cuda.set_device(dev)
+            with torch.cuda.stream(streams[r]):
+                out[r] = partition_kway_shard(shards[r], ranges[r][0], n_global, group, r, k,
+                                              tpwgts, tol, seed)
+        except BaseException as e:  # noqa: BLE001 — re-raised on the caller's thread
+            err[r] = e
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(nranks)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for st in streams:
+        cur.wait_stream(st)
+    for e in err:
+        if e is not None:
+            raise e
+    return out

@@ -21,7 +21,8 @@ def declared_functions():
 def test_header_declares_entry_points():
     names = declared_functions()
     for must in ("hs_evaluate2", "hs_simulate_batch", "hs_levels", "hs_fm2", "hs_brute2",
-                 "hs_partition_kway", "hs_exact_totals", "hs_last_error"):
+                 "hs_partition_kway", "hs_exact_totals", "hs_last_error",
+                 "hs_partition_kway_dist", "hs_symmetrize_range", "hs_kway_dist_arena_bytes"):
         assert must in names
 
 
@@ -48,3 +49,16 @@ def test_status_plumbing_without_gpu():
     assert rc == -1
     lib.hs_last_error.restype = ctypes.c_char_p
     assert b"null" in lib.hs_last_error()
+
+
+def test_sharded_partition_validates_before_touching_the_device():
+    lib = ctypes.CDLL(LIB)
+    lib.hs_last_error.restype = ctypes.c_char_p
+    lib.hs_kway_dist_arena_bytes.restype = ctypes.c_int64
+    lib.hs_kway_dist_arena_bytes.argtypes = [ctypes.c_int32]
+    assert lib.hs_kway_dist_arena_bytes(10_000_000) >= 24 * 10_000_000
+    fn = lib.hs_partition_kway_dist
+    fn.restype = ctypes.c_int
+    rc = fn(None, 0, 10, None, 2, None, ctypes.c_double(0.03), ctypes.c_uint64(0), None, None,
+            None)
+    assert rc == -1 and b"null" in lib.hs_last_error()

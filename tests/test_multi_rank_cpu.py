@@ -86,3 +86,66 @@ def test_two_rank_owner_maps_agree_and_balance(T):
     assert max(res["loads"]) / (res["total"] / 2) < 1.2  # cyclic map balances work
     tasks, deps = cholesky_tasks(T)
     assert res["transfers"] == _transfers(deps, _owner_cyclic(tasks, 2)) > 0
+
+
+# ---- sharded partition: every rank must derive the same vertex ranges -----
+
+def _degrees(n, seed):
+    rng = np.random.default_rng(seed)
+    # layered-DAG-like skew: early kernels have many successors
+    return (10 + rng.poisson(20.0 * (1.0 - np.arange(n) / n))).astype(np.int64)
+
+
+def _range_worker(rank, world, port, n, q):
+    from paper_1502_07451_b200.kway import split_bounds
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    cs = np.cumsum(_degrees(n, seed=5))
+    b = split_bounds(cs, world)
+    mine = torch.tensor([x for ab in b for x in ab], dtype=torch.int64)
+    allb = [torch.zeros_like(mine) for _ in range(world)]
+    dist.all_gather(allb, mine)
+    # each rank's share of adjacency entries (what its kernels will scan)
+    a, e = b[rank]
+    share = torch.tensor([int(cs[e - 1] - (cs[a - 1] if a else 0))], dtype=torch.int64)
+    shares = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(shares, share)
+    if rank == 0:
+        q.put({"agree": all(torch.equal(allb[0], x) for x in allb), "bounds": b,
+               "shares": [int(s) for s in shares], "total": int(cs[-1])})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_shard_ranges_agree_and_balance():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_range_worker, args=(r, 2, port, 50_000, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    assert res["agree"]
+    b = res["bounds"]
+    assert b[0][0] == 0 and b[-1][1] == 50_000 and b[0][1] == b[1][0]
+    assert sum(res["shares"]) == res["total"]
+    assert max(res["shares"]) <= res["total"] / 2 * 1.01  # balanced by entries, not by count
+
+
+def test_split_bounds_edge_cases():
+    from paper_1502_07451_b200.kway import split_bounds
+    cs = np.cumsum(np.ones(10, dtype=np.int64))
+    assert split_bounds(cs, 1) == [(0, 10)]
+    assert split_bounds(cs, 10) == [(i, i + 1) for i in range(10)]
+    assert split_bounds(cs, 2) == [(0, 5), (5, 10)]
+    # one huge vertex: every rank still gets >= 1 vertex
+    cs = np.cumsum(np.array([1000, 1, 1, 1], dtype=np.int64))
+    b = split_bounds(cs, 4)
+    assert [e - a for a, e in b] == [1, 1, 1, 1]
+    with pytest.raises(ValueError):
+        split_bounds(cs, 5)
