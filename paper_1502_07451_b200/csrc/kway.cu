@@ -124,7 +124,8 @@ __global__ void sym_degree(hs_dag_t g, int kv0, int kv1, int32_t *deg) {
 // Team of 8 lanes per vertex: in-neighbours (root dropped) then
 // out-neighbours. ew_in (in-order weights) avoids a random gather through
 // in_eid when the caller has it; otherwise the weight is gathered.
-__global__ void sym_fill(hs_dag_t g, int kv0, int kv1, const int32_t *ew, const int32_t *ew_in,
+// 8 CTAs/SM (<= 32 registers): the gathers need the occupancy
+__global__ void __launch_bounds__(256, 8) sym_fill(hs_dag_t g, int kv0, int kv1, const int32_t *ew, const int32_t *ew_in,
                          const int32_t *nw, const int64_t *xadj, int32_t *adj, int32_t *wgt,
                          int32_t *vw, int32_t *twin) {
   constexpr int T = 8;

@@ -279,7 +279,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
 // neighbouring candidate moved. Confirmed moves land in conf[i] and in the
 // planned flows (flows[p] out of p, flows[k+q] into q); nconf counts them.
 template <int T>
-__global__ void __launch_bounds__(kTeamBlock)
+__global__ void __launch_bounds__(kTeamBlock, 6)  // <= 40 registers: occupancy for the gathers
 afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count, int k,
               int32_t *conf, int64_t *flows, int32_t *nconf, const int32_t *run) {
   if (run && !*run) return;
