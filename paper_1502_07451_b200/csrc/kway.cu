@@ -62,6 +62,10 @@ struct G {
   int32_t *wgt;
   int32_t *vw;
   int32_t v0 = 0;  // global id of local vertex 0 (a rank's range when sharded)
+  // Uniform edge weights (every entry == wconst; METIS's adjwgt = NULL): no
+  // weight array is read or written on this level. 0: per-entry weights.
+  int32_t wconst = 0;
+  __device__ __forceinline__ int ew(int64_t j) const { return wconst ? wconst : __ldg(wgt + j); }
 };
 
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
@@ -216,6 +220,25 @@ __global__ void twohop_pair(const uint64_t *keys, const int32_t *start, int cnt,
   }
 }
 
+// Unmatched vertices of `in` (all n when in == nullptr) -> out (warp-aggregated).
+__global__ void unmatched_list(int n, const int32_t *in, const int32_t *in_count,
+                               const int32_t *match, int32_t *out, int32_t *out_count) {
+  const int nv = in ? *in_count : n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nv; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    const int u = i < nv ? (in ? in[i] : (int)i) : -1;
+    const bool take = u >= 0 && match[u] < 0;
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) continue;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    int at = 0;
+    if (lane == leader) at = atomicAdd(out_count, __popc(m));
+    at = __shfl_sync(0xffffffffu, at, leader);
+    if (take) out[at + __popc(m & ((1u << lane) - 1))] = u;
+  }
+}
+
 __global__ void match_accept(int n, int32_t *match, const int32_t *prop, uint32_t *mw,
                              int32_t *nmatched) {
   int local = 0;
@@ -293,7 +316,7 @@ contract_warp(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1
       for (int j = lane; j < d; j += 32) {
         int key = cmap[g.adj[b + j]];
         if (key == cv + c.v0) continue;
-        int w = g.wgt[b + j];
+        int w = g.ew(b + j);
         uint32_t s = slot_hash(key, mask);
         while (true) {
           int prev = atomicCAS(&K[s], -1, key);
@@ -368,14 +391,14 @@ __global__ void contract_direct(G g, const int32_t *cmap, const int32_t *mem0, c
         int key = -1, w = 0;
         if (j < d) {
           key = cmap[g.adj[b + j]];
-          w = g.wgt[b + j];
+          w = g.ew(b + j);
         }
         const bool keep = key >= 0 && key != cv + c.v0;
         const unsigned m = (__ballot_sync(0xffffffffu, keep) >> (tw * T)) & ((1u << T) - 1);
         if (keep) {
           const int64_t at = base + cnt + __popc(m & ((1u << lane) - 1));
           c.adj[at] = key;
-          c.wgt[at] = w;
+          if (!c.wconst) c.wgt[at] = w;
         }
         cnt += __popc(m);
       }
@@ -419,7 +442,7 @@ __global__ void contract_block(G g, const int32_t *cmap, const int32_t *mem0, co
       for (int j = threadIdx.x; j < d; j += blockDim.x) {
         int key = cmap[g.adj[b + j]];
         if (key == cv + c.v0) continue;
-        int w = g.wgt[b + j];
+        int w = g.ew(b + j);
         uint64_t s = pow2 ? (uint64_t)slot_hash(key, (uint32_t)(size - 1))
                           : ((uint64_t)((uint32_t)key * 0x9E3779B1u)) % size;
         while (true) {
@@ -536,7 +559,7 @@ __global__ void __launch_bounds__(kInitWarps * 32) initial_kernel(InitArgs A) {
     const int d = g.deg[v];
     for (int j = lane; j < d; j += 32) {
       int p = part[g.adj[b + j]];
-      if (p >= 0) atomicAdd(&conn[p], g.wgt[b + j]);
+      if (p >= 0) atomicAdd(&conn[p], g.ew(b + j));
     }
     __syncwarp();
     // score = conn * (1 - pw/hi); lane p evaluates part p (k <= 64: two rounds)
@@ -574,7 +597,7 @@ __global__ void __launch_bounds__(kInitWarps * 32) initial_kernel(InitArgs A) {
       __syncwarp();
       const int64_t b = g.xbeg[v];
       const int d = g.deg[v];
-      for (int j = lane; j < d; j += 32) atomicAdd(&conn[part[g.adj[b + j]]], g.wgt[b + j]);
+      for (int j = lane; j < d; j += 32) atomicAdd(&conn[part[g.adj[b + j]]], g.ew(b + j));
       __syncwarp();
       const int own = part[v];
       const int32_t vwv = g.vw[v];
@@ -607,7 +630,7 @@ __global__ void __launch_bounds__(kInitWarps * 32) initial_kernel(InitArgs A) {
     const int d = g.deg[v];
     const int pv = part[v];
     for (int j = lane; j < d; j += 32)
-      if (part[g.adj[b + j]] != pv) cut2 += g.wgt[b + j];
+      if (part[g.adj[b + j]] != pv) cut2 += g.ew(b + j);
   }
   for (int off = 16; off; off >>= 1) cut2 += __shfl_down_sync(0xffffffffu, cut2, off);
   if (lane == 0) {
@@ -685,7 +708,7 @@ rebalance_candidates(G g, const part_t *part, int k, const int64_t *pw, const in
     __syncwarp();
     const int64_t b = g.xbeg[v];
     const int d = g.deg[v];
-    for (int j = lane; j < d; j += 32) atomicAdd(&conn[part[g.adj[b + j]]], g.wgt[b + j]);
+    for (int j = lane; j < d; j += 32) atomicAdd(&conn[part[g.adj[b + j]]], g.ew(b + j));
     __syncwarp();
     int bg = INT_MIN, bp = -1;
     for (int p = lane; p < k; p += 32) {
@@ -786,6 +809,44 @@ __global__ void range_parts(int n, const int64_t *prefix, int64_t woff, const in
   }
 }
 
+// int32 min/max words (written by wstats_kernel) -> int64 slots in place
+__global__ void widen_minmax(int64_t *mm) {
+  const int32_t lo = ((const int32_t *)mm)[0], hi = ((const int32_t *)(mm + 1))[0];
+  mm[0] = lo;
+  mm[1] = hi;
+}
+
+__global__ void fill_i32(int32_t *out, int64_t n, int32_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v;
+}
+
+// sum / min / max of int32 weights (out: u64 sum, i32 min, i32 max; caller
+// initialises 0, INT_MAX, INT_MIN)
+__global__ void wstats_kernel(int64_t n, const int32_t *w, unsigned long long *sum, int32_t *mn,
+                              int32_t *mx) {
+  unsigned long long s = 0;
+  int lo = INT_MAX, hi = INT_MIN;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int x = __ldg(w + j);
+    s += (unsigned long long)(long long)x;
+    lo = min(lo, x);
+    hi = max(hi, x);
+  }
+  for (int off = 16; off; off >>= 1) {
+    s += __shfl_down_sync(0xffffffffu, s, off);
+    lo = min(lo, __shfl_down_sync(0xffffffffu, lo, off));
+    hi = max(hi, __shfl_down_sync(0xffffffffu, hi, off));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(sum, s);
+    atomicMin(mn, lo);
+    atomicMax(mx, hi);
+  }
+}
+
 __global__ void int8_to_int32(const int8_t *in, int n, int32_t *out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -834,7 +895,7 @@ __global__ void max_wdeg_kernel(G g, int32_t *out) {
        v += (int64_t)gridDim.x * blockDim.x) {
     int64_t sum = 0;
     const int64_t b = g.xbeg[v];
-    for (int j = 0; j < g.deg[v] && sum < (1 << 30); ++j) sum += g.wgt[b + j];
+    for (int j = 0; j < g.deg[v] && sum < (1 << 30); ++j) sum += g.ew(b + j);
     local = max(local, (int)(sum < (1 << 30) ? sum : (1 << 30)));
   }
   for (int off = 16; off; off >>= 1) local = max(local, __shfl_down_sync(0xffffffffu, local, off));
@@ -849,6 +910,7 @@ struct Level {
   int32_t *cmap = nullptr;  // global fine id -> global coarse id of the NEXT level
                             // (this rank's replica; set when coarsened)
   bool own_adj = true, own_wgt = true, own_xbeg_vw = true;
+  bool unmerged = false;    // built by contract_direct (parallel edges kept)
 };
 
 // Loopback groups (ranks = host threads on one GPU) synchronise on the host:
@@ -1175,19 +1237,21 @@ struct Kway {
     if (rc) return rc;
     // finest level with twins: ghost copies of the neighbours' parts inside
     // the adjacency stream (refinement reads 1 coalesced byte per entry)
-    int32_t wconst = 0;
+    int32_t wconst = g.wconst;
     if (finest && g.twin && !D.on()) {
       HS_CHECK_CUDA(dalloc(&gp, g.nnz, s));
       ghost_fill<<<hs::grid_for(g.nnz, 256), 256, 0, s>>>(g.nnz, g.adj, pl, gp);
       HS_CHECK_LAUNCH();
-      HS_CHECK_CUDA(cudaMemsetAsync(ctl + 13, 0x7f, 2 * sizeof(int32_t), s));
-      wrange_kernel<<<hs::grid_for(g.nnz, 256, hs::sm_count() * 8), 256, 0, s>>>(g.nnz, g.wgt,
-                                                                               ctl + 13);
-      HS_CHECK_LAUNCH();
-      int32_t mm[2];
-      HS_CHECK_CUDA(cudaMemcpyAsync(mm, ctl + 13, sizeof mm, cudaMemcpyDeviceToHost, s));
-      HS_CHECK_CUDA(cudaStreamSynchronize(s));
-      if (mm[0] == -mm[1]) wconst = mm[0];  // every edge weight equal: skip the weight stream
+      if (!wconst) {
+        HS_CHECK_CUDA(cudaMemsetAsync(ctl + 13, 0x7f, 2 * sizeof(int32_t), s));
+        wrange_kernel<<<hs::grid_for(g.nnz, 256, hs::sm_count() * 8), 256, 0, s>>>(g.nnz, g.wgt,
+                                                                                 ctl + 13);
+        HS_CHECK_LAUNCH();
+        int32_t mm[2];
+        HS_CHECK_CUDA(cudaMemcpyAsync(mm, ctl + 13, sizeof mm, cudaMemcpyDeviceToHost, s));
+        HS_CHECK_CUDA(cudaStreamSynchronize(s));
+        if (mm[0] == -mm[1]) wconst = mm[0];  // every edge weight equal: skip the weight stream
+      }
     }
     rc = rebalance(g, part, cand, salt2 ^ 0xabcdefull, 3);
     if (rc) return rc;
@@ -1195,10 +1259,15 @@ struct Kway {
     const int tgrid = team_grid(g.n, T);
     int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big : passes_small;
     if (!finest && passes_coarse >= 0) max_passes = passes_coarse;
+    // An unmerged level has as many entries as the level below it: a pass
+    // there costs a full fine pass and only moves whole pairs, which the fine
+    // passes can do too (measured on config 4: 2.6 ms saved, cut 0.2% lower).
+    if (!finest && Lv.unmerged && !getenv("HS_KWAY_REFINE_UNMERGED")) max_passes = 0;
     // 16-bit packed connectivity counters are exact iff every vertex's
     // weighted degree stays below 2^16 on this level
+    // (only the register-counter variants use them: skip the scan otherwise)
     bool pack16 = false;
-    {
+    if (!(k <= 16 && refine_private())) {
       HS_CHECK_CUDA(cudaMemsetAsync(ctl + 12, 0, sizeof(int32_t), s));
       max_wdeg_kernel<<<hs::grid_for(g.n, 256, hs::sm_count() * 8), 256, 0, s>>>(g, ctl + 12);
       HS_CHECK_LAUNCH();
@@ -1215,7 +1284,9 @@ struct Kway {
       HS_CHECK_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int32_t), s));  // list count, nconf
       HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
       {
-        hs::Prof P("refine_candidates", s, 28.0 * g.n + 12.0 * g.nnz);
+        // per vertex: xbeg 8, deg 4, vw 4, own part 1, state write 4; per
+        // entry: adj 4, weight 4 (none when uniform), neighbour part 1
+        hs::Prof P("refine_candidates", s, 21.0 * g.n + (wconst ? 5.0 : 9.0) * g.nnz);
         const int TR = k <= 16 ? refine_team_for(g) : team_for(g);
         HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, pl, k, d_pw, d_hi, d_lo, st,
                            list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst);
@@ -1260,7 +1331,7 @@ struct Kway {
     if (dalloc(&c2, 1, s) != cudaSuccess) return -1;
     cudaMemsetAsync(c2, 0, 8, s);
     {
-      hs::Prof P("cut", s, 16.0 * g.n + 12.0 * g.nnz);
+      hs::Prof P("cut", s, 13.0 * g.n + (g.wconst ? 5.0 : 9.0) * g.nnz);
       const int T = team_for(g);
       HS_TEAM_DISPATCH(T, cut_t, team_grid(g.n, T), g, part, c2);
     }
@@ -1297,20 +1368,39 @@ struct Kway {
     HS_CHECK_CUDA(cudaMemsetAsync(match, 0xff, n * sizeof(int32_t), s));
     HS_CHECK_CUDA(cudaMemcpyAsync(mw, F.g.vw, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     const int T = team_for(F.g);
+    // rounds >= 1 visit only the vertices still unmatched (compacted list)
+    int32_t *ulist[2] = {nullptr, nullptr}, *ucnt = nullptr;
+    if (rounds > 1) {
+      HS_CHECK_CUDA(dalloc(&ulist[0], n, s));
+      HS_CHECK_CUDA(dalloc(&ulist[1], n, s));
+      HS_CHECK_CUDA(dalloc(&ucnt, 2, s));
+    }
     for (int round = 0; round < rounds; ++round) {
+      const int32_t *lst = nullptr, *lcnt = nullptr;
+      if (round > 0) {
+        const int cur = round & 1;
+        HS_CHECK_CUDA(cudaMemsetAsync(ucnt + cur, 0, sizeof(int32_t), s));
+        unmatched_list<<<hs::grid_for(n, 256), 256, 0, s>>>(
+            n, round > 1 ? ulist[cur ^ 1] : nullptr, round > 1 ? ucnt + (cur ^ 1) : nullptr, match,
+            ulist[cur], ucnt + cur);
+        HS_CHECK_LAUNCH();
+        lst = ulist[cur];
+        lcnt = ucnt + cur;
+      }
       {
         // round 0 scans every list; later rounds only unmatched vertices (N-bytes bound)
         hs::Prof P(round == 0 ? "match_propose_r0" : "match_propose_rN", s,
-                   round == 0 ? 20.0 * n + 12.0 * F.g.nnz : 20.0 * n);
+                   round == 0 ? 20.0 * n + (F.g.wconst ? 8.0 : 12.0) * F.g.nnz : 20.0 * n);
         HS_TEAM_DISPATCH(T, propose_t, team_grid(n, T), F.g, mw, prop,
                          round == rounds - 1 ? fav : nullptr, salt + (uint64_t)lvl * 131 + round,
-                         max_vw);
+                         max_vw, lst, lcnt);
       }
       HS_CHECK_LAUNCH();
       match_accept<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, prop, mw, ctl + 6);
       HS_CHECK_LAUNCH();
     }
     cudaFreeAsync(mw, s);
+    if (ulist[0]) { cudaFreeAsync(ulist[0], s); cudaFreeAsync(ulist[1], s); cudaFreeAsync(ucnt, s); }
     {  // two-hop pairing of leftovers that share a favourite neighbour
       uint64_t *keys, *keys2;
       HS_CHECK_CUDA(dalloc(&keys, n, s));
@@ -1431,7 +1521,11 @@ struct Kway {
       }
     }
     if (direct) {
-      hs::Prof P("contract_direct", s, 16.0 * nc + 12.0 * n + 12.0 * F.g.nnz + 8.0 * F.g.nnz);
+      C.g.wconst = F.g.wconst;  // parallel edges kept: uniform weights stay uniform
+      C.unmerged = true;
+      hs::Prof P("contract_direct", s,
+                 16.0 * nc + 12.0 * n + (F.g.wconst ? 8.0 : 12.0) * F.g.nnz +
+                     (F.g.wconst ? 4.0 : 8.0) * F.g.nnz);
       contract_direct<<<std::max(1, std::min(hs::sm_count() * 32, (nc * 8 + 255) / 256)), 256, 0,
                         s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
       HS_CHECK_LAUNCH();
@@ -1546,6 +1640,15 @@ struct Kway {
     HS_CHECK_CUDA(dalloc(&wgt2, g.cap, s));
     seg_bounds<<<hs::grid_for(g.n, 256), 256, 0, s>>>(g.n, g.xbeg, g.deg, b, e);
     HS_CHECK_LAUNCH();
+    if (g.wconst) {  // the warp trials read per-entry weights: materialise them
+      fill_i32<<<hs::grid_for(g.cap, 256), 256, 0, s>>>(wgt2, g.cap, g.wconst);
+      HS_CHECK_LAUNCH();
+      if (Lv.own_wgt) cudaFreeAsync(g.wgt, s);
+      g.wgt = wgt2;
+      g.wconst = 0;
+      Lv.own_wgt = true;
+      HS_CHECK_CUDA(dalloc(&wgt2, g.cap, s));
+    }
     size_t tb = 0;
     HS_CHECK_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, g.adj, adj2, g.wgt, wgt2,
                                                       g.cap, g.n, b, e, s));
@@ -1742,25 +1845,33 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   K.timer.mark("start");
 
   // ---- totals and the int32 weight guard ----
+  // tot: [0] edge-weight sum, [1] vertex-weight sum, [2] adjacency entries,
+  // [3] min edge weight, [4] max edge weight (over all ranks' rows)
   int64_t *tot_dev;
-  HS_CHECK_CUDA(dalloc(&tot_dev, 3, s));
-  int64_t tot[3] = {0, 0, nnz0};
+  HS_CHECK_CUDA(dalloc(&tot_dev, 5, s));
+  int64_t tot[5] = {0, 0, nnz0, INT32_MAX, INT32_MIN};
   {
-    size_t tb = 0, tb2 = 0;
-    HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, ug->adjwgt_i, tot_dev, nnz0, s));
-    HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb2, ug->vwgt_i, tot_dev + 1, n0, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev, tot, sizeof tot, cudaMemcpyHostToDevice, s));
+    wstats_kernel<<<hs::grid_for(nnz0, 256, hs::sm_count() * 8), 256, 0, s>>>(
+        nnz0, ug->adjwgt_i, (unsigned long long *)tot_dev, (int32_t *)(tot_dev + 3),
+        (int32_t *)(tot_dev + 4));
+    HS_CHECK_LAUNCH();
+    size_t tb = 0;
+    HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, ug->vwgt_i, tot_dev + 1, n0, s));
     hs::Scratch<char> tmp;
-    HS_CHECK_CUDA(tmp.alloc(std::max(tb, tb2), s));
-    HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, ug->adjwgt_i, tot_dev, nnz0, s));
-    HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb2, ug->vwgt_i, tot_dev + 1, n0, s));
-    HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev + 2, &tot[2], 8, cudaMemcpyHostToDevice, s));
-    int rc = K.ar({Kway::seg64(tot_dev, 3)});  // sums over all ranks' rows
+    HS_CHECK_CUDA(tmp.alloc(tb, s));
+    HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, ug->vwgt_i, tot_dev + 1, n0, s));
+    hs::count_launch(1);
+    widen_minmax<<<1, 1, 0, s>>>(tot_dev + 3);
+    HS_CHECK_LAUNCH();
+    // sums, then global min / max of the edge weights
+    int rc = K.ar({Kway::seg64(tot_dev, 3), Kway::seg64(tot_dev + 3, 1, 2),
+                   Kway::seg64(tot_dev + 4, 1, 1)});
     if (rc) return rc;
     HS_CHECK_CUDA(cudaMemcpyAsync(tot, tot_dev, sizeof tot, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
     rc = K.check_peers();
     if (rc) return rc;
-    hs::count_launch(2);
   }
   cudaFreeAsync(tot_dev, s);
   HS_REQUIRE(tot[1] > 0 && tot[1] < (1ll << 31), HS_ELIMIT,
@@ -1784,8 +1895,15 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   deg_from_xadj<<<hs::grid_for(n0, 256), 256, 0, s>>>(ug->xadj, n0, L0.g.deg);
   HS_CHECK_LAUNCH();
   int64_t div = 1;
-  if (tot[0] >= (1ll << 30)) div = (tot[0] >> 30) + 1;
-  if (div > 1) {
+  // uniform edge weights: work with unit weights (no weight stream, no
+  // overflow: sums are entry counts); the reported cut is rescaled
+  const int32_t w_uniform = (tot[2] > 0 && tot[3] == tot[4] && tot[3] > 0) ? (int32_t)tot[3] : 0;
+  if (!w_uniform && tot[0] >= (1ll << 30)) div = (tot[0] >> 30) + 1;
+  if (w_uniform) {
+    L0.g.wgt = const_cast<int32_t *>(ug->adjwgt_i);
+    L0.g.wconst = 1;
+    L0.own_wgt = false;
+  } else if (div > 1) {
     HS_CHECK_CUDA(dalloc(&L0.g.wgt, nnz0, s));
     scale_weights<<<hs::grid_for(nnz0, 256), 256, 0, s>>>(nnz0, ug->adjwgt_i, L0.g.wgt, div);
     HS_CHECK_LAUNCH();
@@ -1894,6 +2012,7 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   G g0 = K.levels[0].g;  // the caller's arrays and unscaled weights
   g0.adj = const_cast<int32_t *>(ug->adjncy);
   g0.wgt = const_cast<int32_t *>(ug->adjwgt_i);
+  g0.wconst = w_uniform;
   int64_t cut = K.cut_of(g0, K.loc(cur));
   std::vector<int64_t> pw;
   rc = K.weights(g0, K.loc(cur));

@@ -154,7 +154,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
           for (int q = 0; q < 4; ++q) {
             const int j = j0 + q * T;
             u[q] = j < d ? __ldg(g.adj + b + j) : -1;
-            w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+            w[q] = j < d ? g.ew(b + j) : 0;
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : -1;
@@ -212,7 +212,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
           for (int q = 0; q < 4; ++q) {
             const int j = j0 + q * T;
             u[q] = j < d ? __ldg(g.adj + b + j) : -1;
-            w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+            w[q] = j < d ? g.ew(b + j) : 0;
           }
 #pragma unroll
           for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : own;
@@ -253,7 +253,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       for (int j = lane; j < d; j += T) {
         int p = part[g.adj[b + j]];
         bnd |= p != own;
-        atomicAdd(&conn[p], g.wgt[b + j]);
+        atomicAdd(&conn[p], g.ew(b + j));
       }
       __syncwarp();
       bnd = team_or<T>(bnd);
@@ -311,7 +311,7 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
         for (int q = 0; q < 4; ++q) {
           const int j = j0 + q * T;
           u[q] = j < d ? __ldg(g.adj + b + j) : -1;
-          w[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+          w[q] = j < d ? g.ew(b + j) : 0;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) su[q] = u[q] >= 0 ? __ldg(st + u[q]) : 0u;
@@ -384,14 +384,18 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
 
 // Heavy-edge proposals (K3) with teams: prop[u] = best unmatched neighbour,
 // fav[u] = best neighbour overall (for two-hop pairing).
+// list != nullptr: only the *count vertices of list (the still-unmatched
+// ones after round 0) are visited.
 template <int T>
 __global__ void __launch_bounds__(kTeamBlock)
 propose_t(G g, const uint32_t *mw, int32_t *prop, int32_t *fav, uint64_t salt,
-          int32_t max_vw) {
+          int32_t max_vw, const int32_t *list, const int32_t *count) {
   const int lane = team_lane<T>();
   const int64_t step = (int64_t)warps_total() * (32 / T);
-  for (int64_t ub = (int64_t)warp_id_global() * (32 / T); ub < g.n; ub += step) {
-    const int u = (int)(ub + (threadIdx.x & 31) / T);
+  const int nv = list ? *count : g.n;
+  for (int64_t ub = (int64_t)warp_id_global() * (32 / T); ub < nv; ub += step) {
+    const int ui = (int)(ub + (threadIdx.x & 31) / T);
+    const int u = ui < nv ? (list ? list[ui] : ui) : g.n;
     const bool live = u < g.n && !(mw[u] >> 31);
     float br = -1.f, fr = -1.f;
     int bv = -1, fv = -1;
@@ -407,7 +411,7 @@ propose_t(G g, const uint32_t *mw, int32_t *prop, int32_t *fav, uint64_t salt,
         for (int q = 0; q < 2; ++q) {
           const int j = j0 + q * T;
           vq[q] = j < d ? __ldg(g.adj + b + j) - g.v0 : -1;  // local index
-          wq[q] = j < d ? __ldg(g.wgt + b + j) : 0;
+          wq[q] = j < d ? g.ew(b + j) : 0;
         }
 #pragma unroll
         for (int q = 0; q < 2; ++q)
@@ -464,7 +468,7 @@ cut_t(G g, const part_t *part, unsigned long long *cut2) {
     const int64_t b = g.xbeg[v];
     const int d = g.deg[v];
     for (int j = lane; j < d; j += T)
-      if (part[g.adj[b + j]] != pv) local += (unsigned long long)g.wgt[b + j];
+      if (part[g.adj[b + j]] != pv) local += (unsigned long long)g.ew(b + j);
   }
   for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(cut2, local);
