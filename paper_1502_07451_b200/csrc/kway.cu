@@ -129,10 +129,10 @@ __global__ void sym_degree(hs_dag_t g, int kv0, int kv1, int32_t *deg) {
 // out-neighbours. ew_in (in-order weights) avoids a random gather through
 // in_eid when the caller has it; otherwise the weight is gathered.
 // 8 CTAs/SM (<= 32 registers): the gathers need the occupancy
+template <int T>
 __global__ void __launch_bounds__(256, 8) sym_fill(hs_dag_t g, int kv0, int kv1, const int32_t *ew, const int32_t *ew_in,
                          const int32_t *nw, const int64_t *xadj, int32_t *adj, int32_t *wgt,
                          int32_t *vw, int32_t *twin) {
-  constexpr int T = 8;
   const int lane = (threadIdx.x & 31) % T;
   const int64_t step = (int64_t)warps_total() * (32 / T);
   for (int64_t vb = kv0 + (int64_t)warp_id_global() * (32 / T); vb < kv1; vb += step) {
@@ -369,9 +369,9 @@ __global__ void sample_ratio(const int64_t *ub, const int32_t *deg_c, int nc, in
 // mapped through cmap, self loops dropped, parallel edges kept. Refinement
 // gains, balance and cut are sums over entries, so they are identical on this
 // multigraph. Team of 8 lanes per coarse vertex, ballot-compacted stores.
+template <int T>
 __global__ void contract_direct(G g, const int32_t *cmap, const int32_t *mem0, const int32_t *mem1,
                                 int nc, G c) {
-  constexpr int T = 8;
   const int lane = (threadIdx.x & 31) % T, tw = (threadIdx.x & 31) / T;
   const int64_t step = (int64_t)warps_total() * (32 / T);
   for (int64_t vb = (int64_t)warp_id_global() * (32 / T); vb < nc; vb += step) {
@@ -1296,8 +1296,9 @@ struct Kway {
       if (rc) return rc;
       {
         hs::Prof P("refine_afterburner", s, 4.0 * g.n);  // lower bound: list-sized reads
-        HS_TEAM_DISPATCH(T, afterburner_t, tgrid, g, loc(st), list, ctl + CTL_COUNT, k, conf,
-                         d_flows, ctl + CTL_NCONF, ctl + CTL_ACTIVE);
+        const int TA = after_team_for(g);
+        HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), list,
+                         ctl + CTL_COUNT, k, conf, d_flows, ctl + CTL_NCONF, ctl + CTL_ACTIVE);
       }
       HS_CHECK_LAUNCH();
       rc = ar_flows();
@@ -1526,8 +1527,11 @@ struct Kway {
       hs::Prof P("contract_direct", s,
                  16.0 * nc + 12.0 * n + (F.g.wconst ? 8.0 : 12.0) * F.g.nnz +
                      (F.g.wconst ? 4.0 : 8.0) * F.g.nnz);
-      contract_direct<<<std::max(1, std::min(hs::sm_count() * 32, (nc * 8 + 255) / 256)), 256, 0,
-                        s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
+      static const int TC = getenv("HS_KWAY_TCONTRACT") ? atoi(getenv("HS_KWAY_TCONTRACT")) : 4;
+      const int cgrid = std::max(1, std::min(hs::sm_count() * 32, (nc * TC + 255) / 256));
+      if (TC == 2) contract_direct<2><<<cgrid, 256, 0, s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
+      else if (TC == 4) contract_direct<4><<<cgrid, 256, 0, s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
+      else contract_direct<8><<<cgrid, 256, 0, s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
       HS_CHECK_LAUNCH();
     } else {
     {
@@ -1780,8 +1784,13 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
   if (rc) return rc;
   rc = exclusive_scan<int64_t>(deg64, xadj, nl + 1, s);
   if (rc) return rc;
-  sym_fill<<<std::max(1, std::min(hs::sm_count() * 32, (nl * 8 + 255) / 256)), 256, 0, s>>>(
-      *g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin);
+  static const int TS = getenv("HS_KWAY_TSYM") ? atoi(getenv("HS_KWAY_TSYM")) : 4;  // measured: 4 lanes beat 8 and 2
+  const int sgrid = std::max(1, std::min(hs::sm_count() * 32, (nl * TS + 255) / 256));
+#define HS_SYM_ARGS *g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin
+  if (TS == 2) sym_fill<2><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
+  else if (TS == 4) sym_fill<4><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
+  else sym_fill<8><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
+#undef HS_SYM_ARGS
   HS_CHECK_LAUNCH();
   if (nnz_host) {
     HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));

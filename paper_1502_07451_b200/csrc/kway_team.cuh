@@ -98,7 +98,8 @@ __device__ __forceinline__ int st_gain(uint32_t s) { return (int)(s >> 14); }
 // summed across the team with xor shuffles — no shared-memory atomics (those
 // serialised whenever a vertex's neighbours share a part, the common case).
 // KR == 0: shared-memory accumulators for larger k.
-template <int T, int KR>
+// U: adjacency entries in flight per lane (private-counter path).
+template <int T, int KR, int U = 4>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
@@ -139,28 +140,28 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
     }
     if constexpr (KR < 0) {
       const int tcol = threadIdx.x, base_col = threadIdx.x - lane;
-      for (int j0 = lane; j0 < d; j0 += 4 * T) {
-        int w[4], p[4];
+      for (int j0 = lane; j0 < d; j0 += U * T) {
+        int w[U], p[U];
         if (gp) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < U; ++q) {
             const int j = j0 + q * T;
             p[q] = j < d ? (int)gp[b + j] : -1;
             w[q] = j < d ? (wconst ? wconst : __ldg(g.wgt + b + j)) : 0;
           }
         } else {
-          int u[4];
+          int u[U];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < U; ++q) {
             const int j = j0 + q * T;
             u[q] = j < d ? __ldg(g.adj + b + j) : -1;
             w[q] = j < d ? g.ew(b + j) : 0;
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : -1;
+          for (int q = 0; q < U; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : -1;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < U; ++q)
           if (p[q] >= 0) {
             bnd |= p[q] != own;
             priv_s[p[q]][tcol] += w[q];
@@ -484,9 +485,24 @@ inline bool refine_private() {
   return v == 1;
 }
 
+// entries in flight per lane of the 4-lane refinement scan (HS_KWAY_UNROLL)
+inline int refine_unroll() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("HS_KWAY_UNROLL");
+    v = e ? atoi(e) : 4;
+  }
+  return v;
+}
+
 inline int team_for(const G &g) {
   const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
-  return avg <= 24.0 ? 8 : (avg <= 64.0 ? 16 : 32);
+  static int sparse = -1;  // team on sparse levels (HS_KWAY_TSPARSE for sweeps)
+  if (sparse < 0) {
+    const char *e = getenv("HS_KWAY_TSPARSE");
+    sparse = e ? atoi(e) : 2;  // measured on config 4: 2 lanes beat 4 and 8 (degree ~20)
+  }
+  return avg <= 24.0 ? sparse : (avg <= 64.0 ? 16 : 32);
 }
 
 // team size of the refinement candidate scan (private-counter path supports
@@ -496,7 +512,21 @@ inline int refine_team_for(const G &g) {
   static int force = -2;
   if (force == -2) {
     const char *e = getenv("HS_KWAY_TREFINE");
-    force = e ? atoi(e) : 4;  // measured: 4 lanes per vertex beat 8 and 1 at degree ~20
+    // measured on config 4 (degree ~20): 2 lanes x 4 entries in flight beat
+    // 4x4 (-0.18 ms/pass), 1x8 and 8x4
+    force = e ? atoi(e) : 2;
+  }
+  if (avg <= 24.0 && force > 0) return force;
+  return team_for(g);
+}
+
+// team size of the afterburner on sparse levels (HS_KWAY_TAFTER overrides)
+inline int after_team_for(const G &g) {
+  const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
+  static int force = -2;
+  if (force == -2) {
+    const char *e = getenv("HS_KWAY_TAFTER");
+    force = e ? atoi(e) : 2;  // measured: 2 lanes beat 8 by 0.15 ms per pass (config 4)
   }
   if (avg <= 24.0 && force > 0) return force;
   return team_for(g);
@@ -506,7 +536,14 @@ inline int refine_team_for(const G &g) {
 #define HS_REFINE_DISPATCH(T_, K_, PACK16_, GRID, ...)                          \
   do {                                                                           \
     if ((K_) <= 16 && refine_private()) {                                        \
-      if ((T_) == 1) refine_cand_t<1, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);      \
+      const int U_ = refine_unroll();                                             \
+      if ((T_) == 1 && U_ == 16) refine_cand_t<1, -16, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 1 && U_ == 8) refine_cand_t<1, -16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 1) refine_cand_t<1, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 2 && U_ == 16) refine_cand_t<2, -16, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 2 && U_ == 4) refine_cand_t<2, -16, 4><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 2) refine_cand_t<2, -16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+      else if ((T_) == 4 && U_ == 8) refine_cand_t<4, -16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
       else if ((T_) == 4) refine_cand_t<4, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
       else if ((T_) == 8) refine_cand_t<8, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
       else if ((T_) == 16) refine_cand_t<16, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);\
@@ -528,7 +565,9 @@ inline int refine_team_for(const G &g) {
 
 #define HS_TEAM_DISPATCH(T_, KERNEL, GRID, ...)                                  \
   do {                                                                           \
-    if ((T_) == 8) KERNEL<8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);           \
+    if ((T_) == 2) KERNEL<2><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);           \
+    else if ((T_) == 4) KERNEL<4><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);      \
+    else if ((T_) == 8) KERNEL<8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);      \
     else if ((T_) == 16) KERNEL<16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);    \
     else KERNEL<32><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);                    \
   } while (0)

@@ -14,7 +14,14 @@ a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True
 a.record()
 for _ in range(3): r = kway.partition_kway(ug, 8, seed=0)
 b.record(); torch.cuda.synchronize()
-print(json.dumps({"ms": a.elapsed_time(b) / 3, "cut": r.cut, "frac": r.cut / (ug.nnz // 2 * 19), "levels": r.levels,
+for _ in range(2): kway.symmetrize(csr, ew, nw, kway.in_order(csr, ew))
+ew_in = kway.in_order(csr, ew)
+torch.cuda.synchronize()
+c, d = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+c.record()
+for _ in range(3): kway.symmetrize(csr, ew, nw, ew_in)
+d.record(); torch.cuda.synchronize()
+print(json.dumps({"ms": a.elapsed_time(b) / 3, "sym_ms": c.elapsed_time(d) / 3, "cut": r.cut, "frac": r.cut / (ug.nnz // 2 * 19), "levels": r.levels,
                   "coarsest": r.coarsest, "feasible": r.feasible, "passes": r.refine_passes}))
 ''' % here
 for spec in sys.argv[1:]:
