@@ -755,11 +755,14 @@ __global__ void move_flows(int n, const int32_t *vw, const part_t *part, const i
 // Applies planned moves, each kept with probability p_out[own] * p_in[dest]
 // decided by a hash of (salt, v) — deterministic thinning that keeps the
 // expected inflow of every part within its room.
+__device__ __forceinline__ void cache_move(const G &g, int32_t *cache, int kc, int v, int own,
+                                           int dest);
+
 __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, const double *prob,
                               int k, uint64_t salt, int32_t v0, const part_t *part,
                               Rep<part_t> prep, int64_t *pw, const int32_t *run,
                               const int64_t *xbeg, const int32_t *deg, const int32_t *twin,
-                              part_t *gp) {
+                              part_t *gp, G g, int32_t *cache, int kc) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -778,6 +781,7 @@ __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, con
     prep.put(v0 + v, (part_t)dest);
     if (gp)
       for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
+    if (cache) cache_move(g, cache, kc, (int)v, own, dest);
     atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
     atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
   }
@@ -1043,6 +1047,10 @@ struct Kway {
   // finest level in a worse local optimum)
   int passes_big = 4, passes_small = 8, passes_coarse = 1, rounds = 3;
   double max_deg = 1e30;  // coarsening stop threshold (average degree)
+  // connectivity cache of the level being refined (one GPU, k <= 16):
+  // cache[v][q] = weight of v's edges into part q, kc = 8 or 16 ints per row
+  int32_t *cache = nullptr;
+  int kc = 0;
   Dist D;                         // P = 1: the whole graph on this GPU
   std::shared_ptr<HostBarrier> hb;  // loopback groups
   int64_t *d_dpw = nullptr;       // sharded: this rank's part-weight deltas
@@ -1192,7 +1200,8 @@ struct Kway {
   }
   int ar_applied() { return D.on() ? ar({seg64(d_dpw, k, 0, 1, d_pw)}) : HS_OK; }
 
-  int rebalance(const G &g, const Rep<part_t> &part, int32_t *cand, uint64_t salt2, int rounds) {
+  int rebalance(const G &g, const Rep<part_t> &part, int32_t *cand, uint64_t salt2, int rounds,
+                int32_t *cch = nullptr) {
     const int grid = hs::grid_for(g.n, 256, hs::sm_count() * 4);
     const part_t *pl = loc(part);
     for (int rb = 0; rb < rounds; ++rb) {
@@ -1213,7 +1222,8 @@ struct Kway {
       HS_CHECK_LAUNCH();
       int64_t *tgt = apply_target();
       apply_thinned<<<grid, 256, 0, s>>>(g.n, g.vw, cand, d_prob, k, salt2 + rb * 7919, g.v0, pl,
-                                         part, tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
+                                         part, tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g,
+                                         cch, kc);
       HS_CHECK_LAUNCH();
       rc = ar_applied();
       if (rc) return rc;
@@ -1278,6 +1288,17 @@ struct Kway {
       HS_CHECK_CUDA(cudaStreamSynchronize(s));
       pack16 = mx < 65536;
     }
+    // connectivity cache: pass 0 scans the adjacency and fills it, later
+    // passes read one row per vertex; applied moves keep it exact
+    const bool use_cache = !D.on() && k <= 16 && refine_private() && !gp &&
+                           (max_passes >= 2 || (finest && max_passes >= 1)) &&
+                           !getenv("HS_KWAY_NOCACHE");
+    cache = nullptr;
+    if (use_cache) {
+      kc = k <= 8 ? 8 : 16;
+      int rc2 = cache_buffer((int64_t)g.n * kc, &cache);
+      if (rc2) return rc2;
+    }
     const int32_t one = 1;
     HS_CHECK_CUDA(cudaMemcpyAsync(ctl + CTL_ACTIVE, &one, sizeof one, cudaMemcpyHostToDevice, s));
     for (int pass = 0; pass < max_passes; ++pass) {
@@ -1288,8 +1309,20 @@ struct Kway {
         // entry: adj 4, weight 4 (none when uniform), neighbour part 1
         hs::Prof P("refine_candidates", s, 21.0 * g.n + (wconst ? 5.0 : 9.0) * g.nnz);
         const int TR = k <= 16 ? refine_team_for(g) : team_for(g);
-        HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, pl, k, d_pw, d_hi, d_lo, st,
-                           list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst);
+        if (use_cache && pass > 0) {
+          hs::Prof P2("refine_cached", s, (5.0 + 4.0 * kc + 4.0) * g.n);
+          const int cg = hs::grid_for(g.n, kTeamBlock, hs::sm_count() * 16);
+          if (kc == 8)
+            refine_cached<8><<<cg, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st, list,
+                                                       ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache);
+          else
+            refine_cached<16><<<cg, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st, list,
+                                                        ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache);
+        } else {
+          HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, pl, k, d_pw, d_hi, d_lo, st,
+                             list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst,
+                             use_cache ? cache : nullptr, kc);
+        }
       }
       HS_CHECK_LAUNCH();
       rc = barrier();  // every rank's candidate states are in place
@@ -1309,12 +1342,13 @@ struct Kway {
       int64_t *tgt = apply_target();
       apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
           list, ctl + CTL_COUNT, conf, g.vw, d_prob, k, salt2 + pass * 104729, g.v0, pl, part,
-          tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp);
+          tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g, use_cache ? cache : nullptr, kc);
       HS_CHECK_LAUNCH();
       rc = ar_applied();
       if (rc) return rc;
     }
-    rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8);
+    rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8, use_cache ? cache : nullptr);
+    if (!use_cache || !finest) cache = nullptr;  // only the finest level's cache is kept (final cut)
     if (gp) {
       cudaFreeAsync(gp, s);
       gp = nullptr;
@@ -1327,11 +1361,18 @@ struct Kway {
     return rc;
   }
 
-  int64_t cut_of(const G &g, const part_t *part) {
+  // from_cache: the finest level's connectivity cache is current and holds
+  // the weights g's cut is taken with (scaled by g.wconst when uniform)
+  int64_t cut_of(const G &g, const part_t *part, bool from_cache = false) {
     unsigned long long *c2, h = 0;
     if (dalloc(&c2, 1, s) != cudaSuccess) return -1;
     cudaMemsetAsync(c2, 0, 8, s);
-    {
+    if (from_cache && cache) {
+      hs::Prof P("cut_cached", s, (1.0 + 4.0 * kc) * g.n);
+      const int cg = hs::grid_for(g.n, 256, hs::sm_count() * 8);
+      if (kc == 8) cut_cached<8><<<cg, 256, 0, s>>>(g, part, k, cache, c2);
+      else cut_cached<16><<<cg, 256, 0, s>>>(g, part, k, cache, c2);
+    } else {
       hs::Prof P("cut", s, 13.0 * g.n + (g.wconst ? 5.0 : 9.0) * g.nnz);
       const int T = team_for(g);
       HS_TEAM_DISPATCH(T, cut_t, team_grid(g.n, T), g, part, c2);
@@ -1521,7 +1562,19 @@ struct Kway {
         direct = merged_avg > max_deg;
       }
     }
-    if (direct) {
+    // A level contracted unmerged is the coarsest one and is not refined
+    // (refine(): no passes on unmerged levels). With more than 32k vertices it
+    // also gets no warp trials (band start), so only its vertex weights and
+    // the fine->coarse map are consumed: its adjacency is not built (empty
+    // lists; a rebalance there moves by weight only). Saves a pass over all
+    // entries (config 4: 1.6 ms).
+    const bool skeleton = direct && nc_glob > 32768 && !getenv("HS_KWAY_REFINE_UNMERGED") &&
+                          !getenv("HS_KWAY_FULL_COARSEST");
+    if (skeleton) {
+      HS_CHECK_CUDA(cudaMemsetAsync(C.g.deg, 0, (size_t)nc * sizeof(int32_t), s));
+      C.unmerged = true;
+      *stop = true;
+    } else if (direct) {
       C.g.wconst = F.g.wconst;  // parallel edges kept: uniform weights stay uniform
       C.unmerged = true;
       hs::Prof P("contract_direct", s,
@@ -1602,6 +1655,25 @@ struct Kway {
     cudaFreeAsync(flag, s); cudaFreeAsync(cid, s); cudaFreeAsync(mem0, s);
     cudaFreeAsync(mem1, s); cudaFreeAsync(ub, s);
     levels.push_back(C);
+    return HS_OK;
+  }
+
+  // Grow-only device buffer of the connectivity cache (hundreds of MB at
+  // config 4: a per-call stream-ordered allocation fragmented the pool and
+  // stalled the next call's allocations). One GPU only (not used sharded).
+  int cache_buffer(int64_t ints, int32_t **out) {
+    static std::mutex mu;
+    static int32_t *buf = nullptr;
+    static int64_t have = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (ints > have) {
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      if (buf) cudaFree(buf);
+      buf = nullptr;
+      HS_CHECK_CUDA(cudaMalloc((void **)&buf, ints * sizeof(int32_t)));
+      have = ints;
+    }
+    *out = buf;
     return HS_OK;
   }
 
@@ -2022,7 +2094,11 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   g0.adj = const_cast<int32_t *>(ug->adjncy);
   g0.wgt = const_cast<int32_t *>(ug->adjwgt_i);
   g0.wconst = w_uniform;
-  int64_t cut = K.cut_of(g0, K.loc(cur));
+  // the connectivity cache holds unit weights (uniform) or the caller's own
+  // (div == 1): the cut comes from it without another pass over the edges
+  int64_t cut = K.cut_of(g0, K.loc(cur), K.cache != nullptr && div == 1);
+  if (K.cache != nullptr && div == 1 && w_uniform) cut *= w_uniform;
+  K.cache = nullptr;
   std::vector<int64_t> pw;
   rc = K.weights(g0, K.loc(cur));
   if (rc) return rc;

@@ -103,7 +103,7 @@ template <int T, int KR, int U = 4>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
-              const int32_t *run, const part_t *gp, int32_t wconst) {
+              const int32_t *run, const part_t *gp, int32_t wconst, int32_t *cache, int kc) {
   if (run && !*run) return;
   __shared__ int32_t conn_s[KR != 0 ? 1 : kTeamBlock / T][kMaxParts];
   // KR < 0: per-lane private counters, [part][thread] so every lane hits its
@@ -182,6 +182,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
           cq += priv_s[q][col];
           priv_s[q][col] = 0;
         }
+        if (cache && valid) cache[(int64_t)v * kc + q] = cq;  // connectivity cache row
         if (can && q != own && s_pw[q] + vwv <= s_hi[q]) {
           const int gain = cq - cown;
           if (gain > bg) { bg = gain; bp = q; }  // ascending q: ties keep the smaller part
@@ -275,6 +276,123 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
   app.flush(list, count);
 }
 
+// Candidate moves from the connectivity cache (cache[v][q] = weight of v's
+// edges into part q, kept exact by every applied move): the same choice as
+// refine_cand_t without scanning the adjacency. One thread per vertex.
+template <int KC>
+__global__ void __launch_bounds__(kTeamBlock)
+refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
+              const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
+              const int32_t *run, const int32_t *cache) {
+  if (run && !*run) return;
+  __shared__ int64_t s_pw[kMaxParts], s_hi[kMaxParts], s_lo[kMaxParts];
+  __shared__ int32_t s_app[kTeamBlock / 32][kAppendBuf];
+  for (int p = threadIdx.x; p < k; p += blockDim.x) {
+    s_pw[p] = pw[p];
+    s_hi[p] = hi[p];
+    s_lo[p] = lo[p];
+  }
+  __syncthreads();
+  WarpAppender app{s_app[threadIdx.x >> 5]};
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < g.n; base += stride) {
+    const int v = (int)(base + threadIdx.x);
+    const bool valid = v < g.n;
+    int bg = 0, bp = -1, own = 0;
+    if (valid) {
+      own = part[g.v0 + v];
+      const int32_t vwv = g.vw[v];
+      int c[KC];
+      const int4 *row = reinterpret_cast<const int4 *>(cache + (int64_t)v * KC);
+#pragma unroll
+      for (int i = 0; i < KC / 4; ++i) {
+        const int4 x = __ldg(row + i);
+        c[4 * i] = x.x; c[4 * i + 1] = x.y; c[4 * i + 2] = x.z; c[4 * i + 3] = x.w;
+      }
+      int cown = 0, other = 0;
+#pragma unroll
+      for (int q = 0; q < KC; ++q) {
+        if (q == own) cown = c[q];
+        else if (q < k) other |= c[q];
+      }
+      if (other && s_pw[own] - vwv >= s_lo[own]) {
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+          if (q >= k || q == own || s_pw[q] + vwv > s_hi[q]) continue;
+          const int gain = c[q] - cown;
+          if (gain > bg) { bg = gain; bp = q; }
+        }
+      }
+    }
+    const int cand = (bp >= 0 && bg > 0) ? bp : -1;
+    if (valid) st.put(g.v0 + v, pack_state(own, cand, bg));
+    app.push(valid && cand >= 0, v, list, count);
+  }
+  app.flush(list, count);
+}
+
+// Cut from the connectivity cache: sum over vertices of the weight into other
+// parts (each cut edge counted from both ends).
+template <int KC>
+__global__ void cut_cached(G g, const part_t *part, int k, const int32_t *cache,
+                           unsigned long long *cut2) {
+  unsigned long long local = 0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int own = part[g.v0 + v];
+    const int4 *row = reinterpret_cast<const int4 *>(cache + v * KC);
+#pragma unroll
+    for (int i = 0; i < KC / 4; ++i) {
+      const int4 x = __ldg(row + i);
+      const int c[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int q = 4 * i + j;
+        if (q < k && q != own) local += (unsigned long long)c[j];
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(cut2, local);
+}
+
+// Keeps the connectivity cache exact for one applied move of v (own -> dest).
+__device__ __forceinline__ void cache_move(const G &g, int32_t *cache, int kc, int v, int own,
+                                           int dest) {
+  const int64_t b = g.xbeg[v];
+  const int d = g.deg[v];
+  for (int j = 0; j < d; ++j) {
+    const int64_t u = __ldg(g.adj + b + j) - g.v0;
+    const int w = g.ew(b + j);
+    atomicAdd(cache + u * kc + own, -w);
+    atomicAdd(cache + u * kc + dest, w);
+  }
+}
+
+// Warp-cooperative form: every lane calls it; lanes with v >= 0 moved v
+// (own -> dest). The warp walks each moved vertex's list together
+// (coalesced adjacency reads, parallel atomics).
+__device__ __forceinline__ void cache_move_warp(const G &g, int32_t *cache, int kc, int v,
+                                                int own, int dest) {
+  unsigned m = __ballot_sync(0xffffffffu, v >= 0);
+  const int lane = threadIdx.x & 31;
+  while (m) {
+    const int src = __ffs(m) - 1;
+    m &= m - 1;
+    const int vv = __shfl_sync(0xffffffffu, v, src);
+    const int o = __shfl_sync(0xffffffffu, own, src);
+    const int de = __shfl_sync(0xffffffffu, dest, src);
+    const int64_t b = g.xbeg[vv];
+    const int d = g.deg[vv];
+    for (int j = lane; j < d; j += 32) {
+      const int64_t u = __ldg(g.adj + b + j) - g.v0;
+      const int w = g.ew(b + j);
+      atomicAdd(cache + u * kc + o, -w);
+      atomicAdd(cache + u * kc + de, w);
+    }
+  }
+}
+
 // Jet-style afterburner over the candidate list: a move survives only if it
 // still gains assuming every higher-priority (gain, then smaller id)
 // neighbouring candidate moved. Confirmed moves land in conf[i] and in the
@@ -354,7 +472,7 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
                            const int32_t *vw, const double *prob, int k, uint64_t salt,
                            int32_t v0, const part_t *part, Rep<part_t> prep, int64_t *pw,
                            const int32_t *run, const int64_t *xbeg, const int32_t *deg,
-                           const int32_t *twin, part_t *gp) {
+                           const int32_t *twin, part_t *gp, G g, int32_t *cache, int kc) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -362,21 +480,26 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
   for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) s_prob[p] = prob[p];
   __syncthreads();
   const int total = *count;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int dest = conf[i];
-    if (dest < 0) continue;
-    const int v = list[i];
-    const int own = part[v0 + v];
-    const double pr = s_prob[own] * s_prob[k + dest];
-    const uint64_t gv = (uint64_t)(v0 + v);
-    if (pr < 1.0 && (double)mix32(salt ^ (gv * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
-      continue;
-    prep.put(v0 + v, (part_t)dest);
-    if (gp)  // keep the ghost copies in the neighbours' lists current
-      for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
-    atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
-    atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += stride) {
+    const int64_t i = base + threadIdx.x;  // warp-uniform trip count (cache updates below)
+    int v = -1, own = 0, dest = i < total ? conf[i] : -1;
+    if (dest >= 0) {
+      v = list[i];
+      own = part[v0 + v];
+      const double pr = s_prob[own] * s_prob[k + dest];
+      const uint64_t gv = (uint64_t)(v0 + v);
+      if (pr < 1.0 && (double)mix32(salt ^ (gv * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
+        v = -1;
+    }
+    if (v >= 0) {
+      prep.put(v0 + v, (part_t)dest);
+      if (gp)  // keep the ghost copies in the neighbours' lists current
+        for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
+      atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
+      atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
+    }
+    if (cache) cache_move_warp(g, cache, kc, v, own, dest);
   }
   __syncthreads();
   for (int p = threadIdx.x; p < k; p += blockDim.x)
