@@ -181,6 +181,31 @@ __device__ __forceinline__ float rating(int w, int32_t a, int32_t b) {
   return (float)w * (float)w / ((float)a * (float)b);
 }
 
+// Block-aggregated append: every thread of the block calls it (block-uniform
+// loop trip); one global atomic per block and call (a counter hit by every
+// warp serialised in L2). Order of the appended items is unspecified.
+template <typename V>
+__device__ __forceinline__ void block_append(bool take, V value, V *out, int32_t *count) {
+  __shared__ int s_warp[32];
+  __shared__ int s_base;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, take);
+  if (lane == 0) s_warp[wid] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < nw; ++w) {
+      const int c = s_warp[w];
+      s_warp[w] = tot;
+      tot += c;
+    }
+    s_base = tot ? atomicAdd(count, tot) : 0;
+  }
+  __syncthreads();
+  if (take) out[s_base + s_warp[wid] + __popc(m & ((1u << lane) - 1))] = value;
+  __syncthreads();
+}
+
 // Two-hop ("leaf") matching: unmatched vertices that share a favourite
 // neighbour are paired in (favourite, id) order.
 __global__ void twohop_keys(int n, const int32_t *match, const int32_t *fav, uint64_t *keys,
@@ -190,14 +215,7 @@ __global__ void twohop_keys(int n, const int32_t *match, const int32_t *fav, uin
     const int64_t u = base + threadIdx.x;
     const bool take = u < n && match[u] < 0 && fav[u] >= 0;
     const uint64_t key = take ? ((uint64_t)(uint32_t)fav[u] << 32) | (uint64_t)u : 0;
-    // warp-aggregated append (one atomic per warp, not per vertex)
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (!m) continue;
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    int at = 0;
-    if (lane == leader) at = atomicAdd(count, __popc(m));
-    at = __shfl_sync(0xffffffffu, at, leader);
-    if (take) keys[at + __popc(m & ((1u << lane) - 1))] = key;
+    block_append<uint64_t>(take, key, keys, count);
   }
 }
 
@@ -228,14 +246,7 @@ __global__ void unmatched_list(int n, const int32_t *in, const int32_t *in_count
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < nv; base += stride) {
     const int64_t i = base + threadIdx.x;
     const int u = i < nv ? (in ? in[i] : (int)i) : -1;
-    const bool take = u >= 0 && match[u] < 0;
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (!m) continue;
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    int at = 0;
-    if (lane == leader) at = atomicAdd(out_count, __popc(m));
-    at = __shfl_sync(0xffffffffu, at, leader);
-    if (take) out[at + __popc(m & ((1u << lane) - 1))] = u;
+    block_append<int32_t>(u >= 0 && match[u] < 0, u, out, out_count);
   }
 }
 
@@ -670,10 +681,10 @@ __global__ void part_weights(int n, const int32_t *vw, const part_t *part, int k
     const int64_t i = base + threadIdx.x;
     const int p = i < n ? part[i] : -1;
     const unsigned w = i < n ? (unsigned)vw[i] : 0u;  // 32 x vw < 2^31
-    for (int q = 0; q < k; ++q) {
-      const unsigned sum = __reduce_add_sync(0xffffffffu, p == q ? w : 0u);
-      if (lane == 0 && sum) atomicAdd(&s[q], (unsigned long long)sum);
-    }
+    // one reduction per distinct part present in the warp
+    const unsigned peers = __match_any_sync(0xffffffffu, p);
+    const unsigned sum = __reduce_add_sync(peers, w);
+    if (p >= 0 && lane == __ffs(peers) - 1 && sum) atomicAdd(&s[p], (unsigned long long)sum);
   }
   __syncthreads();
   for (int p = threadIdx.x; p < k; p += blockDim.x)
@@ -1207,6 +1218,13 @@ struct Kway {
     for (int rb = 0; rb < rounds; ++rb) {
       balance_check<<<1, 32, 0, s>>>(k, d_pw, d_hi, ctl);
       HS_CHECK_LAUNCH();
+      // balanced (the usual case): stop here instead of launching the
+      // remaining device-gated rounds (five launches each); every rank reads
+      // the same all-reduced part weights, so sharded ranks agree
+      int32_t over = 1;
+      HS_CHECK_CUDA(cudaMemcpyAsync(&over, ctl + CTL_OVER, 4, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      if (!over) break;
       rebalance_candidates<<<warp_grid(g.n, kRefWarps), kRefWarps * 32, 0, s>>>(
           g, pl, k, d_pw, d_hi, d_target, cand, ctl + CTL_OVER);
       HS_CHECK_LAUNCH();
