@@ -4,10 +4,11 @@
 Headline (BASELINE.json metric "DAG partition ms @10M tasks; ..."): one step =
 one multilevel k=8 partition (K1 symmetrize + K3-K6) of the config-4 layered
 task DAG, 10,000,000 tasks / 100,000,000 edges, device-resident, generated on
-the device (synthetic, seed = rank). ``value`` = device ms per step (max over
-ranks; with --gpus N every rank partitions its own 10M DAG: replicas, weak
-scaling). The DAG (~2.4 GB of CSR) is far larger than L2 (126 MB), so no L2
-flush is needed between steps.
+the device (synthetic, seed 0). ``value`` = device ms per step (max over
+ranks). With --gpus N the ONE 10M DAG is partitioned by all N ranks together
+(sharded by vertex range, exchanges over CUDA-IPC-mapped peer arenas:
+strong scaling). The DAG (~2.4 GB of CSR) is far larger than L2 (126 MB), so
+no L2 flush is needed between steps.
 
 Also reported: ``cholesky`` — the metric's second half, config 3 (tiled
 Cholesky n=32768, b=512, 45,760 tasks) executed on this GPU, GFLOP/s against
@@ -72,9 +73,48 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.proc = None
+        self.thread = None
+        self.samples = []  # (sm_mhz, sm_max_mhz, reason names)
         self.path = os.path.join("/tmp", f"hs_clocks_{os.getpid()}.csv")
 
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+        pynvml.nvmlInit()
+        try:
+            p = torch.cuda.get_device_properties(self.idx)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:  # noqa: BLE001 — fall back to the CUDA index
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+
+    def _poll(self, nv, h):
+        # NVML every 5 ms: a 10 ms step still gets samples inside the timed region
+        import threading
+        bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                "sw_power_cap": 0x4}
+        smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            try:
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            except Exception:  # noqa: BLE001 — older binding name
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            self.samples.append((float(sm), float(smax), {k for k, b in bits.items() if r & b}))
+            self.ready.set()
+            self.stop.wait(0.005)
+
     def __enter__(self):
+        import threading
+        try:
+            nv, h = self._nvml_handle()
+            self.stop, self.ready = threading.Event(), threading.Event()
+            self.thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
+            self.thread.start()
+            self.ready.wait(2.0)
+            return self
+        except Exception:  # noqa: BLE001 — no NVML binding: nvidia-smi every 50 ms
+            self.thread = None
         try:
             self.out = open(self.path, "w")
             self.proc = subprocess.Popen(
@@ -86,6 +126,9 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -95,6 +138,11 @@ class ClockSampler:
             self.out.close()
 
     def summary(self):
+        if self.samples:
+            sm = [x[0] for x in self.samples]
+            reasons = set().union(*[x[2] for x in self.samples])
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+                    "samples": len(sm), "source": "nvml 5 ms", "reasons": sorted(reasons)}
         if self.proc is None or not os.path.exists(self.path):
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm, smax, reasons = [], [], set()

@@ -1346,7 +1346,19 @@ struct Kway {
       rc = barrier();  // every rank's candidate states are in place
       if (rc) return rc;
       {
-        hs::Prof P("refine_afterburner", s, 4.0 * g.n);  // lower bound: list-sized reads
+        // algorithmic bytes need the candidate count: read it (sync) only in
+        // instrumented (profiling) steps. Per candidate: list 4, own state 4,
+        // xbeg 8, deg 4, vw 4, decision 4; per entry (average degree): adj 4,
+        // weight 4 (none when uniform), neighbour state 4.
+        double ab_bytes = 0.0;
+        if (hs::prof_enabled()) {
+          int32_t cnt = 0;
+          cudaMemcpyAsync(&cnt, ctl + CTL_COUNT, 4, cudaMemcpyDeviceToHost, s);
+          cudaStreamSynchronize(s);
+          const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
+          ab_bytes = (double)cnt * (28.0 + avg * (g.wconst ? 8.0 : 12.0));
+        }
+        hs::Prof P("refine_afterburner", s, ab_bytes);
         const int TA = after_team_for(g);
         HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), list,
                          ctl + CTL_COUNT, k, conf, d_flows, ctl + CTL_NCONF, ctl + CTL_ACTIVE);

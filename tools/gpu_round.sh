@@ -32,21 +32,22 @@ for w in $WHAT; do
         --profile-from-start off -o $O/kway_c0_$TAG -f python tools/ncu_kway.py \
         > $O/ncu_kwayc_$TAG.log 2>&1
       echo "ncu coarsen0 rc=$?"
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sym_fill|cut_t" \
+      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sym_fill|cut_" \
         -c 2 -o $O/kway_sc_$TAG -f python tools/ncu_kway.py > $O/ncu_kways_$TAG.log 2>&1
       echo "ncu sym/cut rc=$?"
       python tools/ncu_summary.py $O/ncu_summary_$TAG.json \
-        refine_candidates=$O/kway_l0_$TAG.ncu-rep:refine_cand \
+        refine_candidates=$O/kway_l0_$TAG.ncu-rep:refine_cand_t \
+        refine_cached=$O/kway_l0_$TAG.ncu-rep:refine_cached \
         refine_afterburner=$O/kway_l0_$TAG.ncu-rep:afterburner \
         apply_list=$O/kway_l0_$TAG.ncu-rep:apply_list \
         match_propose_r0=$O/kway_c0_$TAG.ncu-rep:propose_t \
-        contract_direct=$O/kway_c0_$TAG.ncu-rep:contract_direct \
-        contract_warp=$O/kway_c0_$TAG.ncu-rep:contract_warp \
+        match_accept=$O/kway_c0_$TAG.ncu-rep:match_accept \
+        build_cmap=$O/kway_c0_$TAG.ncu-rep:build_cmap \
         symmetrize=$O/kway_sc_$TAG.ncu-rep:sym_fill \
-        cut=$O/kway_sc_$TAG.ncu-rep:cut_t \
+        cut=$O/kway_sc_$TAG.ncu-rep:cut_ \
         --launches $O/launches_$TAG.csv > /dev/null 2>&1
       echo "summary rc=$?"; gzip -f $O/launches_$TAG.csv
-      ncu -i $O/kway_l0_$TAG.ncu-rep --page source --csv -k regex:refine_cand > $O/src_refine_$TAG.csv 2>/dev/null
+      ncu -i $O/kway_l0_$TAG.ncu-rep --page source --csv -k regex:afterburner > $O/src_refine_$TAG.csv 2>/dev/null
       ncu -i $O/kway_l0_$TAG.ncu-rep --page details --csv > $O/details_l0_$TAG.csv 2>/dev/null
       ncu -i $O/kway_c0_$TAG.ncu-rep --page details --csv > $O/details_c0_$TAG.csv 2>/dev/null
       gzip -f $O/src_refine_$TAG.csv $O/details_*_$TAG.csv
