@@ -163,6 +163,21 @@ int hs_evaluate_kway(const hs_dag_t *g, const int32_t *part, int32_t batch, int3
 int hs_levels(const hs_dag_t *g, int mode, int32_t *level, double *finish,
               double *cp_host, int32_t *n_levels_host, void *stream);
 
+/* Device validation (validate, graph.py:113-150) of the checks a CSR can
+ * violate. counts_host[7] = offenders per check, first_host[7] = smallest
+ * offending index (-1 if none): 0 node with a negative weight, 1 root with
+ * non-zero weights, 2 self-loop edge, 3 edge with negative transfer weight,
+ * 4 edge with negative byte count, 5 node never released by Kahn's algorithm
+ * with self-loops ignored (first = the reference's CycleError member,
+ * graph.py:153-172), 6 non-root node without predecessors. node_bad [n] /
+ * edge_bad [m] (optional, device int8) receive per-item bit masks (node:
+ * 1 negative, 2 root weight, 4 no predecessor, 8 on/after a cycle; edge:
+ * 1 self-loop, 2 negative transfer, 4 negative bytes). Synchronous. The
+ * object-model checks (duplicate ids/edges, unknown endpoints, root kind)
+ * stay on the host. */
+int hs_validate_dag(const hs_dag_t *g, int64_t *counts_host, int32_t *first_host,
+                    int8_t *node_bad, int8_t *edge_bad, void *stream);
+
 /* Level order: nodes sorted by (level, index) — order[n]. */
 int hs_level_order(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
                    int32_t *order, void *stream);

@@ -283,6 +283,20 @@ def symmetrize_range(csr, kv0: int, kv1: int, edge_w_i, node_w_i, xadj, adjncy, 
     return nnz.value
 
 
+_validate_dag = _opt("hs_validate_dag", _P, _P, _P, _P, _P, _P)
+
+
+def validate_dag(csr, node_bad: Optional[torch.Tensor] = None,
+                 edge_bad: Optional[torch.Tensor] = None):
+    """(counts[7], first[7]) of the device validation checks (hs_validate_dag)."""
+    fn = _need(_validate_dag, "hs_validate_dag")
+    counts = (ctypes.c_int64 * 7)()
+    first = (ctypes.c_int32 * 7)()
+    check(fn(ctypes.byref(csr.struct()), counts, first, ptr(node_bad), ptr(edge_bad),
+             stream_ptr()))
+    return list(counts), list(first)
+
+
 def kway_dist_arena_bytes(n_global: int) -> int:
     return int(_lib.hs_kway_dist_arena_bytes(n_global))
 

@@ -107,6 +107,46 @@ class DagCSR:
             raise ValueError(f"root node {graph.root} missing")
         return cls.from_host(h)
 
+    def validate(self) -> List[str]:
+        """``validate`` (graph.py:113-150) on the device, in the reference's message order.
+
+        Covers the checks a CSR can violate (weights, self-loops, cycles,
+        kernels without predecessors); the object-model checks (duplicate
+        ids/edges, unknown endpoints, root kind) only exist on ``TaskGraph``.
+        """
+        node_bad = torch.zeros(self.n, dtype=torch.int8, device=self.device)
+        edge_bad = torch.zeros(max(self.m, 1), dtype=torch.int8, device=self.device)
+        counts, first = _native.validate_dag(self, node_bad, edge_bad)
+        ids = self.ids if self.ids is not None else np.arange(self.n, dtype=np.int64)
+        out: List[str] = []
+        if counts[0] or counts[1]:  # node loop (graph.py:125-129), node order
+            nb = node_bad.cpu().numpy()
+            for v in np.nonzero(nb & 3)[0]:
+                if nb[v] & 1:
+                    out.append(f"node {int(ids[v])} has negative weight")
+                if nb[v] & 2:
+                    out.append(f"SOURCE node {int(ids[v])} must have zero weights")
+        if counts[2] or counts[3] or counts[4]:  # edge loop (graph.py:130-140), sorted edges
+            eb = edge_bad[:self.m].cpu().numpy()
+            bad = np.nonzero(eb)[0]
+            src = np.searchsorted(self.out_ptr.cpu().numpy(), bad, side="right") - 1
+            dst = self.out_dst.cpu().numpy()[bad]
+            for e, u, v in zip(bad, src, dst):
+                uu, vv = int(ids[u]), int(ids[v])
+                if eb[e] & 1:
+                    out.append(f"self-loop on node {uu}")
+                if eb[e] & 2:
+                    out.append(f"edge ({uu}, {vv}) has negative transfer weight")
+                if eb[e] & 4:
+                    out.append(f"edge ({uu}, {vv}) has negative byte count")
+        if counts[5]:  # topological_order's CycleError (graph.py:171)
+            out.append(f"cycle through node {int(ids[first[5]])}")
+        if counts[6]:  # graph.py:145-148, node order
+            nb = node_bad.cpu().numpy()
+            out += [f"initial kernel {int(ids[v])} has no edge from root"
+                    for v in np.nonzero(nb & 4)[0]]
+        return out
+
     def struct(self) -> _native.HsDag:
         if self._struct is None:
             p = _native.ptr
