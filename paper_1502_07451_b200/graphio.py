@@ -1,0 +1,154 @@
+"""METIS wire boundary on the device.
+
+Same names, arguments and errors as the reference's graphio
+(pkg/src/hetsched/graphio.py:272-339):
+
+* ``emit_metis(graph, node_weight_source, scale) -> str``: the undirected
+  METIS graph of the kernels (graphio.py:277-304). Integerisation
+  ``max(1, floor(w*scale + 0.5))`` (graphio.py:272-274) on the device, K1
+  symmetrisation, then ``hs_emit_metis`` formats every line in HBM (row byte
+  lengths, a scan, one warp per row writing digits).
+* ``parse_partition_file(text, graph, targets, node_weight_source, tolerance)
+  -> Partition`` (graphio.py:307-330): ``hs_parse_partition`` splits lines
+  like ``str.splitlines``, strips ASCII whitespace and decides every line that
+  is a plain signed decimal. The few lines it cannot decide (non-ASCII
+  whitespace, ``1_0``-style digit separators, more than 18 digits) come back
+  with their line numbers and are finished with Python's own ``int()`` so that
+  values and error messages match the reference exactly.
+* ``emit_partition_file(partition, graph) -> str`` (graphio.py:333-339).
+
+``emit_metis_csr`` / ``parse_partition_bytes`` are the CSR-native forms for
+graphs beyond the object model (config 4: 10M vertices, ~2.6 GB of text).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Tuple
+
+import numpy as np
+import torch
+
+from . import _native
+from .costs import PartitionTargets
+from .csr import DagCSR
+from .graph import CPU, GPU, TaskGraph
+from .partition import Partition, PartitionError, _finish
+
+_P = ctypes.c_void_p
+_emit = _native._opt("hs_emit_metis", _P, _P, ctypes.c_int64, _P, _P)
+_parse = _native._opt("hs_parse_partition", _P, ctypes.c_int64, ctypes.c_int32, _P, _P, _P,
+                      ctypes.c_int32, _P, _P)
+
+
+def _scaled(w: torch.Tensor, scale: int) -> torch.Tensor:
+    """graphio.py:272-274 elementwise: max(1, floor(w*scale + 0.5)) as int32."""
+    return torch.clamp(torch.floor(w * scale + 0.5), min=1).to(torch.int32)
+
+
+def emit_metis_csr(csr: DagCSR, node_weight_source: str = GPU, scale: int = 100) -> torch.Tensor:
+    """METIS text of a device DAG (header included) as a uint8 device tensor."""
+    from .kway import in_order, symmetrize
+    fn = _native._need(_emit, "hs_emit_metis")
+    w_node = csr.w_gpu if node_weight_source == GPU else csr.w_cpu
+    r = csr.root
+    inter = torch.ones(csr.m, dtype=torch.bool, device=csr.device)
+    inter[int(csr.out_ptr[r]):int(csr.out_ptr[r + 1])] = False  # root edges
+    kern = torch.ones(csr.n, dtype=torch.bool, device=csr.device)
+    kern[r] = False
+    if bool((w_node[kern] == 0).all()) and bool((csr.w_xfer[inter] == 0).all()):
+        raise PartitionError("all weights are zero; cannot integerize for export")
+    ew = _scaled(csr.w_xfer, scale)
+    ug = symmetrize(csr, ew, _scaled(w_node, scale), in_order(csr, ew))
+    n_inter = int(inter.sum().item())
+    header = f"{ug.n} {n_inter} 011\n".encode()
+    size = ctypes.c_int64(0)
+    _native.check(fn(ctypes.byref(ug.struct()), None, 0, ctypes.byref(size),
+                     _native.stream_ptr()))
+    out = torch.empty(len(header) + size.value, dtype=torch.uint8, device=csr.device)
+    out[:len(header)] = torch.frombuffer(bytearray(header), dtype=torch.uint8).to(csr.device)
+    _native.check(fn(ctypes.byref(ug.struct()), out.data_ptr() + len(header), size.value,
+                     ctypes.byref(size), _native.stream_ptr()))
+    return out
+
+
+def emit_metis(graph: TaskGraph, node_weight_source: str = GPU, scale: int = 100) -> str:
+    """graphio.py:277-304 — the kernels as an undirected METIS graph, on the device."""
+    text = emit_metis_csr(graph.csr(), node_weight_source, scale)
+    return bytes(text.cpu().numpy()).decode("ascii")
+
+
+def parse_partition_bytes(data, n_expected: int,
+                          device=None) -> Tuple[Optional[torch.Tensor], Optional[str]]:
+    """Device parse of a METIS partition file: (int8 [n_expected] groups, None) or
+    (None, the reference's error message)."""
+    fn = _native._need(_parse, "hs_parse_partition")
+    dev = device or _native.device()
+    raw = data.encode("utf-8") if isinstance(data, str) else bytes(data)
+    buf = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev) if raw else \
+        torch.empty(1, dtype=torch.uint8, device=dev)
+    part = torch.zeros(max(n_expected, 1), dtype=torch.int8, device=dev)
+    cap = 64
+    while True:
+        odd = (ctypes.c_int64 * (3 * cap))()
+        vals = (ctypes.c_int64 * cap)()
+        info = (ctypes.c_int64 * 4)()
+        _native.check(fn(buf.data_ptr(), len(raw), int(n_expected), part.data_ptr(), odd, vals,
+                         cap, info, _native.stream_ptr()))
+        if info[1] <= cap:
+            break
+        cap = int(info[1])
+    n_lines = info[0]
+    fixes = []
+    text = None
+    for i in range(info[1]):
+        line_idx, cls, slot = odd[3 * i], odd[3 * i + 1], odd[3 * i + 2]
+        lineno = line_idx + 1
+        if cls == 3:  # a plain integer other than 0/1 (graphio.py:323-324)
+            return None, f"line {lineno}: group must be 0 or 1, got {vals[i]}"
+        # undecided on the device: Python's own int() on that one line
+        if text is None:
+            text = raw.decode("utf-8").splitlines()
+        line = text[line_idx].strip()
+        try:
+            v = int(line)
+        except ValueError:
+            return None, f"line {lineno}: not an integer: {line!r}"
+        if v not in (0, 1):
+            return None, f"line {lineno}: group must be 0 or 1, got {v}"
+        fixes.append((slot, v))
+    if n_lines != n_expected:
+        return None, f"partition file has {n_lines} lines for {n_expected} kernels"
+    if fixes:
+        idx = torch.tensor([s for s, _ in fixes], dtype=torch.int64, device=dev)
+        part[idx] = torch.tensor([v for _, v in fixes], dtype=torch.int8, device=dev)
+    return part[:n_expected], None
+
+
+def parse_partition_file(text: str, graph: TaskGraph, targets: Optional[PartitionTargets] = None,
+                         node_weight_source: str = GPU, tolerance: float = 0.03) -> Partition:
+    """graphio.py:307-330 — read a METIS partition file (one 0/1 line per kernel)."""
+    ids = graph.kernel_ids()
+    part, err = parse_partition_bytes(text, len(ids))
+    if err is not None:
+        raise PartitionError(err)
+    groups = part.cpu().numpy()
+    assignment = {nid: (CPU if g == 0 else GPU) for nid, g in zip(ids, groups.tolist())}
+    if targets is None:
+        from .costs import workload_ratio
+        targets = workload_ratio(graph)
+    return _finish(graph, assignment, targets, node_weight_source, tolerance)
+
+
+def emit_partition_file(partition: Partition, graph: TaskGraph) -> str:
+    """graphio.py:333-339 — inverse of parse_partition_file (0 = CPU, 1 = GPU)."""
+    return "".join("0\n" if partition.assignment[nid] == CPU else "1\n"
+                   for nid in graph.kernel_ids())
+
+
+def emit_partition_bytes(part: torch.Tensor) -> torch.Tensor:
+    """Device form of emit_partition_file for a 0/1 part array: '0\\n'/'1\\n' per kernel."""
+    p = part.to(torch.uint8)
+    out = torch.empty(2 * p.numel(), dtype=torch.uint8, device=p.device)
+    out[0::2] = p + ord("0")
+    out[1::2] = ord("\n")
+    return out
