@@ -115,3 +115,28 @@ def test_known_answers():
     assert r["makespan"] == 7.0 and r["transfer_count"] == 2
     g = mk({1: (2.0, 5.0), 2: (2.0, 5.0)}, [(1, 2, 1.0)])
     assert O.critical_path(g) == 4.0
+
+
+def test_oracle_metis_io_matches_reference_golden():
+    """The oracle's METIS restatement against the reference's own outputs."""
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "metis_io.json")) as f:
+        gold = json.load(f)
+    for rec in gold["graphs"]:
+        og = O.OGraph(rec["spec"])
+        assert O.emit_metis(og, "GPU") == rec["metis_GPU"]
+        assert O.emit_metis(og, "CPU") == rec["metis_CPU"]
+        assert O.emit_metis(og, "GPU", scale=7) == rec["metis_scale7"]
+    og = O.OGraph(gold["partition_graph"])
+    n = len(og.kernel_ids())
+    for rec in gold["partition_files"]:
+        if "error" in rec:
+            try:
+                O.parse_partition_groups(rec["text"], n)
+                raise AssertionError(rec["name"])
+            except ValueError as exc:
+                assert str(exc) == rec["error"]
+        else:
+            got = O.parse_partition_groups(rec["text"], n)
+            assert ["CPU" if v == 0 else "GPU" for v in got] == rec["assignment"]
