@@ -68,6 +68,66 @@ struct G {
   __device__ __forceinline__ int ew(int64_t j) const { return wconst ? wconst : __ldg(wgt + j); }
 };
 
+// Connectivity (gain) cache: row v holds kc counters of cw bytes (1, 2 or 4;
+// the host picks the narrowest width that cannot overflow: every counter is at
+// most v's weighted degree). Narrow rows keep the cache L2-resident.
+struct Conn {
+  uint8_t *p = nullptr;
+  int kc = 0, cw = 4;
+  __device__ __forceinline__ void set(int64_t v, int q, int val) const {
+    uint8_t *a = p + (v * kc + q) * cw;
+    if (cw == 1) *a = (uint8_t)val;
+    else if (cw == 2) *reinterpret_cast<uint16_t *>(a) = (uint16_t)val;
+    else *reinterpret_cast<int32_t *>(a) = val;
+  }
+  // exact update for one edge of weight w whose far end moved own -> dest:
+  // word-granular atomics (no carry/borrow can cross a counter: counters stay
+  // in [0, weighted degree]); one atomic when both counters share a word
+  __device__ __forceinline__ void move(int64_t u, int own, int dest, int w) const {
+    const int64_t row = u * kc * cw;
+    if (cw == 4) {
+      atomicAdd(reinterpret_cast<int32_t *>(p + row) + own, -w);
+      atomicAdd(reinterpret_cast<int32_t *>(p + row) + dest, w);
+      return;
+    }
+    const int64_t bo = row + own * cw, bd = row + dest * cw;
+    const unsigned so = (unsigned)(bo & 3) * 8u, sd = (unsigned)(bd & 3) * 8u;
+    unsigned *wo = reinterpret_cast<unsigned *>(p + (bo & ~3ll));
+    unsigned *wd = reinterpret_cast<unsigned *>(p + (bd & ~3ll));
+    const unsigned dn = 0u - ((unsigned)w << so), up = (unsigned)w << sd;
+    if (wo == wd) {
+      atomicAdd(wo, dn + up);
+    } else {
+      atomicAdd(wo, dn);
+      atomicAdd(wd, up);
+    }
+  }
+};
+
+// KC counters of CW bytes of row v (KC * CW is 8, 16, 32 or 64 bytes)
+template <int KC, int CW>
+__device__ __forceinline__ void conn_row(const uint8_t *p, int64_t v, int (&c)[KC]) {
+  constexpr int WORDS = KC * CW / 4;
+  uint32_t w[WORDS];
+  const uint8_t *row = p + v * KC * CW;
+  if constexpr (WORDS == 2) {
+    const uint2 x = __ldg(reinterpret_cast<const uint2 *>(row));
+    w[0] = x.x; w[1] = x.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < WORDS / 4; ++i) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4 *>(row) + i);
+      w[4 * i] = x.x; w[4 * i + 1] = x.y; w[4 * i + 2] = x.z; w[4 * i + 3] = x.w;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < KC; ++q) {
+    if constexpr (CW == 4) c[q] = (int)w[q];
+    else if constexpr (CW == 2) c[q] = (int)((w[q >> 1] >> ((q & 1) * 16)) & 0xffffu);
+    else c[q] = (int)((w[q >> 2] >> ((q & 3) * 8)) & 0xffu);
+  }
+}
+
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
   x ^= x >> 33;
   x *= 0xff51afd7ed558ccdull;
@@ -169,10 +229,16 @@ __global__ void __launch_bounds__(256, 8) sym_fill(hs_dag_t g, int kv0, int kv1,
 }
 
 // ------------------------------------------------------------------ K3 ---
-__global__ void deg_from_xadj(const int64_t *xadj, int n, int32_t *deg) {
+__global__ void deg_from_xadj(const int64_t *xadj, int n, int32_t *deg, int32_t *max_deg) {
+  int mx = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    deg[i] = (int32_t)(xadj[i + 1] - xadj[i]);
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int d = (int32_t)(xadj[i + 1] - xadj[i]);
+    deg[i] = d;
+    mx = max(mx, d);
+  }
+  for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, off));
+  if (max_deg && (threadIdx.x & 31) == 0) atomicMax(max_deg, mx);
 }
 
 // Edge rating w^2 / (c(u) c(v)) ("expansion*2"): prefers heavy edges between
@@ -766,14 +832,14 @@ __global__ void move_flows(int n, const int32_t *vw, const part_t *part, const i
 // Applies planned moves, each kept with probability p_out[own] * p_in[dest]
 // decided by a hash of (salt, v) — deterministic thinning that keeps the
 // expected inflow of every part within its room.
-__device__ __forceinline__ void cache_move(const G &g, int32_t *cache, int kc, int v, int own,
+__device__ __forceinline__ void cache_move(const G &g, const Conn &cache, int v, int own,
                                            int dest);
 
 __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, const double *prob,
                               int k, uint64_t salt, int32_t v0, const part_t *part,
                               Rep<part_t> prep, int64_t *pw, const int32_t *run,
                               const int64_t *xbeg, const int32_t *deg, const int32_t *twin,
-                              part_t *gp, G g, int32_t *cache, int kc) {
+                              part_t *gp, G g, Conn cache) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -792,7 +858,7 @@ __global__ void apply_thinned(int n, const int32_t *vw, const int32_t *cand, con
     prep.put(v0 + v, (part_t)dest);
     if (gp)
       for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
-    if (cache) cache_move(g, cache, kc, (int)v, own, dest);
+    if (cache.p) cache_move(g, cache, (int)v, own, dest);
     atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
     atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
   }
@@ -1060,8 +1126,8 @@ struct Kway {
   double max_deg = 1e30;  // coarsening stop threshold (average degree)
   // connectivity cache of the level being refined (one GPU, k <= 16):
   // cache[v][q] = weight of v's edges into part q, kc = 8 or 16 ints per row
-  int32_t *cache = nullptr;
-  int kc = 0;
+  Conn cache;                 // cache.p == nullptr: none
+  int64_t max_deg0 = 0;       // largest degree of the finest level (cache width)
   Dist D;                         // P = 1: the whole graph on this GPU
   std::shared_ptr<HostBarrier> hb;  // loopback groups
   int64_t *d_dpw = nullptr;       // sharded: this rank's part-weight deltas
@@ -1212,7 +1278,7 @@ struct Kway {
   int ar_applied() { return D.on() ? ar({seg64(d_dpw, k, 0, 1, d_pw)}) : HS_OK; }
 
   int rebalance(const G &g, const Rep<part_t> &part, int32_t *cand, uint64_t salt2, int rounds,
-                int32_t *cch = nullptr) {
+                Conn cch = Conn()) {
     const int grid = hs::grid_for(g.n, 256, hs::sm_count() * 4);
     const part_t *pl = loc(part);
     for (int rb = 0; rb < rounds; ++rb) {
@@ -1241,7 +1307,7 @@ struct Kway {
       int64_t *tgt = apply_target();
       apply_thinned<<<grid, 256, 0, s>>>(g.n, g.vw, cand, d_prob, k, salt2 + rb * 7919, g.v0, pl,
                                          part, tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g,
-                                         cch, kc);
+                                         cch);
       HS_CHECK_LAUNCH();
       rc = ar_applied();
       if (rc) return rc;
@@ -1311,10 +1377,15 @@ struct Kway {
     const bool use_cache = !D.on() && k <= 16 && refine_private() && !gp &&
                            (max_passes >= 2 || (finest && max_passes >= 1)) &&
                            !getenv("HS_KWAY_NOCACHE");
-    cache = nullptr;
+    cache = Conn();
     if (use_cache) {
-      kc = k <= 8 ? 8 : 16;
-      int rc2 = cache_buffer((int64_t)g.n * kc, &cache);
+      cache.kc = k <= 8 ? 8 : 16;
+      // counters never exceed a vertex's weighted degree: with unit weights on
+      // the finest level that is its degree (known), else 32-bit counters
+      const int64_t bound = (finest && g.wconst == 1) ? max_deg0 : (1ll << 31);
+      cache.cw = bound < 256 ? 1 : (bound < 65536 ? 2 : 4);
+      if (getenv("HS_KWAY_CACHE32")) cache.cw = 4;
+      int rc2 = cache_buffer((int64_t)g.n * cache.kc * cache.cw, &cache.p);
       if (rc2) return rc2;
     }
     const int32_t one = 1;
@@ -1328,18 +1399,21 @@ struct Kway {
         hs::Prof P("refine_candidates", s, 21.0 * g.n + (wconst ? 5.0 : 9.0) * g.nnz);
         const int TR = k <= 16 ? refine_team_for(g) : team_for(g);
         if (use_cache && pass > 0) {
-          hs::Prof P2("refine_cached", s, (5.0 + 4.0 * kc + 4.0) * g.n);
+          hs::Prof P2("refine_cached", s, (5.0 + cache.cw * cache.kc + 4.0) * g.n);
           const int cg = hs::grid_for(g.n, kTeamBlock, hs::sm_count() * 16);
-          if (kc == 8)
-            refine_cached<8><<<cg, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st, list,
-                                                       ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache);
-          else
-            refine_cached<16><<<cg, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st, list,
-                                                        ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache);
+#define HS_RC(KC, CW)                                                                      \
+  refine_cached<KC, CW><<<cg, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st, list,     \
+                                                  ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache.p)
+          if (cache.kc == 8) {
+            if (cache.cw == 1) HS_RC(8, 1); else if (cache.cw == 2) HS_RC(8, 2); else HS_RC(8, 4);
+          } else {
+            if (cache.cw == 1) HS_RC(16, 1); else if (cache.cw == 2) HS_RC(16, 2); else HS_RC(16, 4);
+          }
+#undef HS_RC
         } else {
           HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, pl, k, d_pw, d_hi, d_lo, st,
                              list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst,
-                             use_cache ? cache : nullptr, kc);
+                             use_cache ? cache : Conn());
         }
       }
       HS_CHECK_LAUNCH();
@@ -1372,13 +1446,13 @@ struct Kway {
       int64_t *tgt = apply_target();
       apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
           list, ctl + CTL_COUNT, conf, g.vw, d_prob, k, salt2 + pass * 104729, g.v0, pl, part,
-          tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g, use_cache ? cache : nullptr, kc);
+          tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g, use_cache ? cache : Conn());
       HS_CHECK_LAUNCH();
       rc = ar_applied();
       if (rc) return rc;
     }
-    rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8, use_cache ? cache : nullptr);
-    if (!use_cache || !finest) cache = nullptr;  // only the finest level's cache is kept (final cut)
+    rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8, use_cache ? cache : Conn());
+    if (!use_cache || !finest) cache = Conn();  // only the finest level's cache is kept (final cut)
     if (gp) {
       cudaFreeAsync(gp, s);
       gp = nullptr;
@@ -1397,11 +1471,16 @@ struct Kway {
     unsigned long long *c2, h = 0;
     if (dalloc(&c2, 1, s) != cudaSuccess) return -1;
     cudaMemsetAsync(c2, 0, 8, s);
-    if (from_cache && cache) {
-      hs::Prof P("cut_cached", s, (1.0 + 4.0 * kc) * g.n);
+    if (from_cache && cache.p) {
+      hs::Prof P("cut_cached", s, (1.0 + cache.cw * cache.kc) * g.n);
       const int cg = hs::grid_for(g.n, 256, hs::sm_count() * 8);
-      if (kc == 8) cut_cached<8><<<cg, 256, 0, s>>>(g, part, k, cache, c2);
-      else cut_cached<16><<<cg, 256, 0, s>>>(g, part, k, cache, c2);
+#define HS_CC(KC, CW) cut_cached<KC, CW><<<cg, 256, 0, s>>>(g, part, k, cache.p, c2)
+      if (cache.kc == 8) {
+        if (cache.cw == 1) HS_CC(8, 1); else if (cache.cw == 2) HS_CC(8, 2); else HS_CC(8, 4);
+      } else {
+        if (cache.cw == 1) HS_CC(16, 1); else if (cache.cw == 2) HS_CC(16, 2); else HS_CC(16, 4);
+      }
+#undef HS_CC
     } else {
       hs::Prof P("cut", s, 13.0 * g.n + (g.wconst ? 5.0 : 9.0) * g.nnz);
       const int T = team_for(g);
@@ -1691,17 +1770,17 @@ struct Kway {
   // Grow-only device buffer of the connectivity cache (hundreds of MB at
   // config 4: a per-call stream-ordered allocation fragmented the pool and
   // stalled the next call's allocations). One GPU only (not used sharded).
-  int cache_buffer(int64_t ints, int32_t **out) {
+  int cache_buffer(int64_t bytes, uint8_t **out) {
     static std::mutex mu;
-    static int32_t *buf = nullptr;
+    static uint8_t *buf = nullptr;
     static int64_t have = 0;
     std::lock_guard<std::mutex> lk(mu);
-    if (ints > have) {
+    if (bytes > have) {
       HS_CHECK_CUDA(cudaStreamSynchronize(s));
       if (buf) cudaFree(buf);
       buf = nullptr;
-      HS_CHECK_CUDA(cudaMalloc((void **)&buf, ints * sizeof(int32_t)));
-      have = ints;
+      HS_CHECK_CUDA(cudaMalloc((void **)&buf, bytes));
+      have = bytes;
     }
     *out = buf;
     return HS_OK;
@@ -1957,12 +2036,17 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
 
   // ---- totals and the int32 weight guard ----
   // tot: [0] edge-weight sum, [1] vertex-weight sum, [2] adjacency entries,
-  // [3] min edge weight, [4] max edge weight (over all ranks' rows)
+  // [3] min edge weight, [4] max edge weight, [5] max degree (all ranks' rows)
   int64_t *tot_dev;
-  HS_CHECK_CUDA(dalloc(&tot_dev, 5, s));
-  int64_t tot[5] = {0, 0, nnz0, INT32_MAX, INT32_MIN};
+  HS_CHECK_CUDA(dalloc(&tot_dev, 6, s));
+  int64_t tot[6] = {0, 0, nnz0, INT32_MAX, INT32_MIN, 0};
+  int32_t *deg_l0;
+  HS_CHECK_CUDA(dalloc(&deg_l0, n0, s));
   {
     HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev, tot, sizeof tot, cudaMemcpyHostToDevice, s));
+    deg_from_xadj<<<hs::grid_for(n0, 256), 256, 0, s>>>(ug->xadj, n0, deg_l0,
+                                                        (int32_t *)(tot_dev + 5));
+    HS_CHECK_LAUNCH();
     wstats_kernel<<<hs::grid_for(nnz0, 256, hs::sm_count() * 8), 256, 0, s>>>(
         nnz0, ug->adjwgt_i, (unsigned long long *)tot_dev, (int32_t *)(tot_dev + 3),
         (int32_t *)(tot_dev + 4));
@@ -1977,7 +2061,7 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
     HS_CHECK_LAUNCH();
     // sums, then global min / max of the edge weights
     int rc = K.ar({Kway::seg64(tot_dev, 3), Kway::seg64(tot_dev + 3, 1, 2),
-                   Kway::seg64(tot_dev + 4, 1, 1)});
+                   Kway::seg64(tot_dev + 4, 2, 1)});
     if (rc) return rc;
     HS_CHECK_CUDA(cudaMemcpyAsync(tot, tot_dev, sizeof tot, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -2002,9 +2086,8 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   L0.g.adj = const_cast<int32_t *>(ug->adjncy);
   L0.g.twin = ug->twin;
   L0.g.vw = const_cast<int32_t *>(ug->vwgt_i);
-  HS_CHECK_CUDA(dalloc(&L0.g.deg, n0, s));
-  deg_from_xadj<<<hs::grid_for(n0, 256), 256, 0, s>>>(ug->xadj, n0, L0.g.deg);
-  HS_CHECK_LAUNCH();
+  L0.g.deg = deg_l0;
+  K.max_deg0 = tot[5];
   int64_t div = 1;
   // uniform edge weights: work with unit weights (no weight stream, no
   // overflow: sums are entry counts); the reported cut is rescaled
@@ -2126,9 +2209,10 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   g0.wconst = w_uniform;
   // the connectivity cache holds unit weights (uniform) or the caller's own
   // (div == 1): the cut comes from it without another pass over the edges
-  int64_t cut = K.cut_of(g0, K.loc(cur), K.cache != nullptr && div == 1);
-  if (K.cache != nullptr && div == 1 && w_uniform) cut *= w_uniform;
-  K.cache = nullptr;
+  const bool cached_cut = K.cache.p != nullptr && div == 1;
+  int64_t cut = K.cut_of(g0, K.loc(cur), cached_cut);
+  if (cached_cut && w_uniform) cut *= w_uniform;
+  K.cache = Conn();
   std::vector<int64_t> pw;
   rc = K.weights(g0, K.loc(cur));
   if (rc) return rc;

@@ -103,7 +103,7 @@ template <int T, int KR, int U = 4>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
-              const int32_t *run, const part_t *gp, int32_t wconst, int32_t *cache, int kc) {
+              const int32_t *run, const part_t *gp, int32_t wconst, Conn cache) {
   if (run && !*run) return;
   __shared__ int32_t conn_s[KR != 0 ? 1 : kTeamBlock / T][kMaxParts];
   // KR < 0: per-lane private counters, [part][thread] so every lane hits its
@@ -182,7 +182,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
           cq += priv_s[q][col];
           priv_s[q][col] = 0;
         }
-        if (cache && valid) cache[(int64_t)v * kc + q] = cq;  // connectivity cache row
+        if (cache.p && valid) cache.set(v, q, cq);  // connectivity cache row
         if (can && q != own && s_pw[q] + vwv <= s_hi[q]) {
           const int gain = cq - cown;
           if (gain > bg) { bg = gain; bp = q; }  // ascending q: ties keep the smaller part
@@ -279,11 +279,11 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
 // Candidate moves from the connectivity cache (cache[v][q] = weight of v's
 // edges into part q, kept exact by every applied move): the same choice as
 // refine_cand_t without scanning the adjacency. One thread per vertex.
-template <int KC>
+template <int KC, int CW>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
-              const int32_t *run, const int32_t *cache) {
+              const int32_t *run, const uint8_t *cache) {
   if (run && !*run) return;
   __shared__ int64_t s_pw[kMaxParts], s_hi[kMaxParts], s_lo[kMaxParts];
   __shared__ int32_t s_app[kTeamBlock / 32][kAppendBuf];
@@ -303,12 +303,7 @@ refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       own = part[g.v0 + v];
       const int32_t vwv = g.vw[v];
       int c[KC];
-      const int4 *row = reinterpret_cast<const int4 *>(cache + (int64_t)v * KC);
-#pragma unroll
-      for (int i = 0; i < KC / 4; ++i) {
-        const int4 x = __ldg(row + i);
-        c[4 * i] = x.x; c[4 * i + 1] = x.y; c[4 * i + 2] = x.z; c[4 * i + 3] = x.w;
-      }
+      conn_row<KC, CW>(cache, v, c);
       int cown = 0, other = 0;
 #pragma unroll
       for (int q = 0; q < KC; ++q) {
@@ -333,47 +328,37 @@ refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
 
 // Cut from the connectivity cache: sum over vertices of the weight into other
 // parts (each cut edge counted from both ends).
-template <int KC>
-__global__ void cut_cached(G g, const part_t *part, int k, const int32_t *cache,
+template <int KC, int CW>
+__global__ void cut_cached(G g, const part_t *part, int k, const uint8_t *cache,
                            unsigned long long *cut2) {
   unsigned long long local = 0;
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < g.n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int own = part[g.v0 + v];
-    const int4 *row = reinterpret_cast<const int4 *>(cache + v * KC);
+    int c[KC];
+    conn_row<KC, CW>(cache, v, c);
 #pragma unroll
-    for (int i = 0; i < KC / 4; ++i) {
-      const int4 x = __ldg(row + i);
-      const int c[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int q = 4 * i + j;
-        if (q < k && q != own) local += (unsigned long long)c[j];
-      }
-    }
+    for (int q = 0; q < KC; ++q)
+      if (q < k && q != own) local += (unsigned long long)c[q];
   }
   for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(cut2, local);
 }
 
 // Keeps the connectivity cache exact for one applied move of v (own -> dest).
-__device__ __forceinline__ void cache_move(const G &g, int32_t *cache, int kc, int v, int own,
+__device__ __forceinline__ void cache_move(const G &g, const Conn &cache, int v, int own,
                                            int dest) {
   const int64_t b = g.xbeg[v];
   const int d = g.deg[v];
-  for (int j = 0; j < d; ++j) {
-    const int64_t u = __ldg(g.adj + b + j) - g.v0;
-    const int w = g.ew(b + j);
-    atomicAdd(cache + u * kc + own, -w);
-    atomicAdd(cache + u * kc + dest, w);
-  }
+  for (int j = 0; j < d; ++j)
+    cache.move(__ldg(g.adj + b + j) - g.v0, own, dest, g.ew(b + j));
 }
 
 // Warp-cooperative form: every lane calls it; lanes with v >= 0 moved v
 // (own -> dest). The warp walks each moved vertex's list together
 // (coalesced adjacency reads, parallel atomics).
-__device__ __forceinline__ void cache_move_warp(const G &g, int32_t *cache, int kc, int v,
-                                                int own, int dest) {
+__device__ __forceinline__ void cache_move_warp(const G &g, const Conn &cache, int v, int own,
+                                                int dest) {
   unsigned m = __ballot_sync(0xffffffffu, v >= 0);
   const int lane = threadIdx.x & 31;
   while (m) {
@@ -384,12 +369,7 @@ __device__ __forceinline__ void cache_move_warp(const G &g, int32_t *cache, int 
     const int de = __shfl_sync(0xffffffffu, dest, src);
     const int64_t b = g.xbeg[vv];
     const int d = g.deg[vv];
-    for (int j = lane; j < d; j += 32) {
-      const int64_t u = __ldg(g.adj + b + j) - g.v0;
-      const int w = g.ew(b + j);
-      atomicAdd(cache + u * kc + o, -w);
-      atomicAdd(cache + u * kc + de, w);
-    }
+    for (int j = lane; j < d; j += 32) cache.move(__ldg(g.adj + b + j) - g.v0, o, de, g.ew(b + j));
   }
 }
 
@@ -472,7 +452,7 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
                            const int32_t *vw, const double *prob, int k, uint64_t salt,
                            int32_t v0, const part_t *part, Rep<part_t> prep, int64_t *pw,
                            const int32_t *run, const int64_t *xbeg, const int32_t *deg,
-                           const int32_t *twin, part_t *gp, G g, int32_t *cache, int kc) {
+                           const int32_t *twin, part_t *gp, G g, Conn cache) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -499,7 +479,7 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
       atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
       atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
     }
-    if (cache) cache_move_warp(g, cache, kc, v, own, dest);
+    if (cache.p) cache_move_warp(g, cache, v, own, dest);
   }
   __syncthreads();
   for (int p = threadIdx.x; p < k; p += blockDim.x)
