@@ -55,7 +55,7 @@ struct ArArgs {
   int nseg = 0;
   uint64_t timeout_ns = 30ull * 1000000000ull;
   int phase = 0;  // 0: post + wait + reduce; 1: post only; 2: reduce only (host-synchronised)
-  ArSeg seg[4];
+  ArSeg seg[6];
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
@@ -81,7 +81,7 @@ __device__ __forceinline__ int64_t *ar_slots(char *a, int parity, int rank) {
 // One CTA. Barrier + reduction of up to kArSlots values (0 values = barrier).
 __global__ void __launch_bounds__(256) ar_kernel(ArArgs A) {
   const int par = A.epoch & 1;
-  int off[5];
+  int off[7];
   off[0] = 0;
   for (int s = 0; s < A.nseg; ++s) off[s + 1] = off[s] + A.seg[s].n;
   const int tot = off[A.nseg];

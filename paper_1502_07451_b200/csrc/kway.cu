@@ -992,6 +992,7 @@ struct Level {
                             // (this rank's replica; set when coarsened)
   bool own_adj = true, own_wgt = true, own_xbeg_vw = true;
   bool unmerged = false;    // built by contract_direct (parallel edges kept)
+  int32_t vconst = 0;       // every vertex weighs vconst (0: not uniform / unknown)
 };
 
 // Loopback groups (ranks = host threads on one GPU) synchronise on the host:
@@ -1148,7 +1149,7 @@ struct Kway {
     A.epoch = ++D.epoch;
     int tot = 0;
     for (const ArSeg &g : segs) {
-      HS_REQUIRE(A.nseg < 4, HS_EINVAL, "all-reduce: too many segments");
+      HS_REQUIRE(A.nseg < 6, HS_EINVAL, "all-reduce: too many segments");
       A.seg[A.nseg++] = g;
       tot += g.n;
     }
@@ -1544,7 +1545,8 @@ struct Kway {
                    round == 0 ? 20.0 * n + (F.g.wconst ? 8.0 : 12.0) * F.g.nnz : 20.0 * n);
         HS_TEAM_DISPATCH(T, propose_t, team_grid(n, T), F.g, mw, prop,
                          round == rounds - 1 ? fav : nullptr, salt + (uint64_t)lvl * 131 + round,
-                         max_vw, lst, lcnt);
+                         max_vw, lst, lcnt, round == 0 ? F.vconst : 0,
+                         F.vconst != 0 && F.g.wconst != 0);
       }
       HS_CHECK_LAUNCH();
       match_accept<<<hs::grid_for(n, 256), 256, 0, s>>>(n, match, prop, mw, ctl + 6);
@@ -2036,10 +2038,11 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
 
   // ---- totals and the int32 weight guard ----
   // tot: [0] edge-weight sum, [1] vertex-weight sum, [2] adjacency entries,
-  // [3] min edge weight, [4] max edge weight, [5] max degree (all ranks' rows)
+  // [3] min edge weight, [4] max edge weight, [5] max degree, [6] min vertex
+  // weight, [7] max vertex weight (all ranks' rows)
   int64_t *tot_dev;
-  HS_CHECK_CUDA(dalloc(&tot_dev, 6, s));
-  int64_t tot[6] = {0, 0, nnz0, INT32_MAX, INT32_MIN, 0};
+  HS_CHECK_CUDA(dalloc(&tot_dev, 8, s));
+  int64_t tot[8] = {0, 0, nnz0, INT32_MAX, INT32_MIN, 0, INT32_MAX, INT32_MIN};
   int32_t *deg_l0;
   HS_CHECK_CUDA(dalloc(&deg_l0, n0, s));
   {
@@ -2051,17 +2054,18 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
         nnz0, ug->adjwgt_i, (unsigned long long *)tot_dev, (int32_t *)(tot_dev + 3),
         (int32_t *)(tot_dev + 4));
     HS_CHECK_LAUNCH();
-    size_t tb = 0;
-    HS_CHECK_CUDA(cub::DeviceReduce::Sum(nullptr, tb, ug->vwgt_i, tot_dev + 1, n0, s));
-    hs::Scratch<char> tmp;
-    HS_CHECK_CUDA(tmp.alloc(tb, s));
-    HS_CHECK_CUDA(cub::DeviceReduce::Sum(tmp.p, tb, ug->vwgt_i, tot_dev + 1, n0, s));
-    hs::count_launch(1);
+    wstats_kernel<<<hs::grid_for(n0, 256, hs::sm_count() * 8), 256, 0, s>>>(
+        n0, ug->vwgt_i, (unsigned long long *)(tot_dev + 1), (int32_t *)(tot_dev + 6),
+        (int32_t *)(tot_dev + 7));
+    HS_CHECK_LAUNCH();
     widen_minmax<<<1, 1, 0, s>>>(tot_dev + 3);
     HS_CHECK_LAUNCH();
-    // sums, then global min / max of the edge weights
+    widen_minmax<<<1, 1, 0, s>>>(tot_dev + 6);
+    HS_CHECK_LAUNCH();
+    // sums, then global minima / maxima
     int rc = K.ar({Kway::seg64(tot_dev, 3), Kway::seg64(tot_dev + 3, 1, 2),
-                   Kway::seg64(tot_dev + 4, 2, 1)});
+                   Kway::seg64(tot_dev + 4, 2, 1), Kway::seg64(tot_dev + 6, 1, 2),
+                   Kway::seg64(tot_dev + 7, 1, 1)});
     if (rc) return rc;
     HS_CHECK_CUDA(cudaMemcpyAsync(tot, tot_dev, sizeof tot, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -2088,6 +2092,7 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   L0.g.vw = const_cast<int32_t *>(ug->vwgt_i);
   L0.g.deg = deg_l0;
   K.max_deg0 = tot[5];
+  L0.vconst = (tot[6] == tot[7] && n_glob > 0 && !getenv("HS_KWAY_NOVCONST")) ? (int32_t)tot[6] : 0;
   int64_t div = 1;
   // uniform edge weights: work with unit weights (no weight stream, no
   // overflow: sums are entry counts); the reported cut is rescaled

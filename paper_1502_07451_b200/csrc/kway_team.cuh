@@ -493,7 +493,8 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
 template <int T>
 __global__ void __launch_bounds__(kTeamBlock)
 propose_t(G g, const uint32_t *mw, int32_t *prop, int32_t *fav, uint64_t salt,
-          int32_t max_vw, const int32_t *list, const int32_t *count) {
+          int32_t max_vw, const int32_t *list, const int32_t *count, int32_t vconst,
+          bool uniform) {
   const int lane = team_lane<T>();
   const int64_t step = (int64_t)warps_total() * (32 / T);
   const int nv = list ? *count : g.n;
@@ -518,9 +519,12 @@ propose_t(G g, const uint32_t *mw, int32_t *prop, int32_t *fav, uint64_t salt,
           vq[q] = j < d ? __ldg(g.adj + b + j) - g.v0 : -1;  // local index
           wq[q] = j < d ? g.ew(b + j) : 0;
         }
+        // vconst != 0: first round with uniform vertex weights — every vertex
+        // is unmatched and weighs vconst, so no per-neighbour gather
 #pragma unroll
         for (int q = 0; q < PU; ++q)
-          mq[q] = (unsigned)vq[q] < (unsigned)g.n ? __ldg(mw + vq[q]) : 0x80000000u;
+          mq[q] = (unsigned)vq[q] < (unsigned)g.n ? (vconst ? (uint32_t)vconst : __ldg(mw + vq[q]))
+                                                  : 0x80000000u;
 #pragma unroll
         for (int q = 0; q < PU; ++q) {
         const int v = vq[q];
@@ -529,7 +533,8 @@ propose_t(G g, const uint32_t *mw, int32_t *prop, int32_t *fav, uint64_t salt,
         const uint32_t wv = mq[q];
         const int32_t vv = (int32_t)(wv & 0x7fffffffu);
         if (vu + vv > max_vw) continue;
-        float r = rating(wq[q], vu, vv);
+        // uniform edge and vertex weights: every rating is equal (hash decides)
+        float r = uniform ? 1.f : rating(wq[q], vu, vv);
         uint32_t h = edge_hash32(g.v0 + u, g.v0 + v, (uint32_t)salt);
         if (fav && (r > fr || (r == fr && (h > fh || (h == fh && v < fv))))) {
           fr = r; fh = h; fv = v;
