@@ -38,6 +38,8 @@
 #include <vector>
 #include <algorithm>
 #include <cuda_profiler_api.h>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 #include <mutex>
 #include <condition_variable>
 #include <chrono>
@@ -1268,6 +1270,45 @@ struct Kway {
 
   // Up to `rounds` rebalancing rounds, each gated on the device by "some part
   // is above its bound" — no host round trip.
+  // Cluster launch of afterburner_dsm: kAbCluster CTAs of kAbThreads per
+  // cluster, each holding 1/kAbCluster of the candidate bitmap.
+  int launch_afterburner_dsm(const G &g, const uint32_t *stl, const int32_t *list, int32_t *conf,
+                             const uint32_t *bm, int64_t bm_words) {
+    const int64_t slice = (bm_words + kAbCluster - 1) / kAbCluster;
+    const size_t smem = (size_t)slice * 4;
+    const int clusters = std::max(1, hs::sm_count() / kAbCluster);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(clusters * kAbCluster);
+    cfg.blockDim = dim3(kAbThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kAbCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+#define HS_AB(KC, CW)                                                                         \
+  do {                                                                                        \
+    auto fn = afterburner_dsm<2, KC, CW>;                                                     \
+    HS_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                       (int)smem));                                           \
+    HS_CHECK_CUDA(cudaLaunchKernelEx(&cfg, fn, g, stl, list, (const int32_t *)(ctl + CTL_COUNT), \
+                                     k, conf, d_flows, ctl + CTL_NCONF,                        \
+                                     (const int32_t *)(ctl + CTL_ACTIVE), bm, bm_words, slice, \
+                                     (const uint8_t *)cache.p));                               \
+  } while (0)
+    if (cache.kc == 8) {
+      if (cache.cw == 1) HS_AB(8, 1); else if (cache.cw == 2) HS_AB(8, 2); else HS_AB(8, 4);
+    } else {
+      if (cache.cw == 1) HS_AB(16, 1); else if (cache.cw == 2) HS_AB(16, 2); else HS_AB(16, 4);
+    }
+#undef HS_AB
+    hs::count_launch();
+    return HS_OK;
+  }
+
   // Planned flows and move counts of all ranks (a no-op on one GPU).
   int ar_flows() { return ar({seg64(d_flows, 2 * k), seg32(ctl + CTL_NCONF, 1)}); }
   // Part-weight deltas of this rank's applied moves -> every rank's d_pw.
@@ -1389,6 +1430,16 @@ struct Kway {
       int rc2 = cache_buffer((int64_t)g.n * cache.kc * cache.cw, &cache.p);
       if (rc2) return rc2;
     }
+    // afterburner over a cluster-distributed candidate bitmap (needs the cache
+    // for the gains and a bitmap that fits kAbCluster CTAs' shared memory).
+    // Opt-in (HS_KWAY_DSM=1): measured 4x slower than the L2 gathers on
+    // config 4 (random 4-byte DSMEM loads across an 8-CTA cluster, ~2 ms vs
+    // 0.5 ms per pass), kept for the record.
+    const int64_t bm_words = ((int64_t)g.n + 31) / 32;
+    const bool use_dsm = use_cache && bm_words <= (int64_t)kAbCluster * kAbSliceMax &&
+                         getenv("HS_KWAY_DSM") != nullptr;
+    uint32_t *d_bm = nullptr;
+    if (use_dsm) HS_CHECK_CUDA(dalloc(&d_bm, bm_words, s));
     const int32_t one = 1;
     HS_CHECK_CUDA(cudaMemcpyAsync(ctl + CTL_ACTIVE, &one, sizeof one, cudaMemcpyHostToDevice, s));
     for (int pass = 0; pass < max_passes; ++pass) {
@@ -1433,10 +1484,21 @@ struct Kway {
           const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
           ab_bytes = (double)cnt * (28.0 + avg * (g.wconst ? 8.0 : 12.0));
         }
+        if (use_dsm) {
+          HS_CHECK_CUDA(cudaMemsetAsync(d_bm, 0, bm_words * 4, s));
+          list_bitmap<<<hs::grid_for(g.n, 256, hs::sm_count() * 8), 256, 0, s>>>(
+              list, ctl + CTL_COUNT, d_bm);
+          HS_CHECK_LAUNCH();
+        }
         hs::Prof P("refine_afterburner", s, ab_bytes);
-        const int TA = after_team_for(g);
-        HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), list,
-                         ctl + CTL_COUNT, k, conf, d_flows, ctl + CTL_NCONF, ctl + CTL_ACTIVE);
+        if (use_dsm) {
+          rc = launch_afterburner_dsm(g, loc(st), list, conf, d_bm, bm_words);
+          if (rc) return rc;
+        } else {
+          const int TA = after_team_for(g);
+          HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), list,
+                           ctl + CTL_COUNT, k, conf, d_flows, ctl + CTL_NCONF, ctl + CTL_ACTIVE);
+        }
       }
       HS_CHECK_LAUNCH();
       rc = ar_flows();
@@ -1459,6 +1521,7 @@ struct Kway {
       gp = nullptr;
     }
     cudaFreeAsync(cand, s);
+    if (d_bm) cudaFreeAsync(d_bm, s);
     free_rep(st);
     D.bump = arena_mark;
     cudaFreeAsync(list, s);

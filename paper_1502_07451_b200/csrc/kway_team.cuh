@@ -446,6 +446,119 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
   if (threadIdx.x == 0 && s_n) atomicAdd(nconf, s_n);
 }
 
+// ---- afterburner over a cluster-distributed candidate bitmap ----------------
+// With the connectivity cache, a candidate's afterburner delta is its cached
+// gain plus corrections from the neighbours that are themselves candidates of
+// higher priority; non-candidate neighbours need no lookup at all. Which
+// neighbours are candidates is one bit per vertex: the bitmap (1.25 MB at
+// 10M vertices) is split across the distributed shared memory of a thread-
+// block cluster (kAbCluster CTAs, one per SM), so the per-neighbour test is a
+// DSMEM load instead of an L2 request; only candidate neighbours gather their
+// packed state from global memory.
+constexpr int kAbCluster = 8;
+constexpr int kAbThreads = 1024;
+constexpr int64_t kAbSliceMax = (216 << 10) / 4;  // bitmap words per CTA (216 KB of smem)
+
+__global__ void list_bitmap(const int32_t *list, const int32_t *count, uint32_t *bm) {
+  const int total = *count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = list[i];
+    atomicOr(bm + (v >> 5), 1u << (v & 31));
+  }
+}
+
+template <int T, int KC, int CW>
+__global__ void __launch_bounds__(kAbThreads, 1)
+afterburner_dsm(G g, const uint32_t *st, const int32_t *list, const int32_t *count, int k,
+                int32_t *conf, int64_t *flows, int32_t *nconf, const int32_t *run,
+                const uint32_t *bm, int64_t bm_words, int64_t slice_words, const uint8_t *cache) {
+  extern __shared__ uint32_t s_bm[];  // this CTA's slice of the candidate bitmap
+  __shared__ unsigned long long sf[2 * kMaxParts];
+  __shared__ int s_n;
+  cg::cluster_group cluster = cg::this_cluster();
+  const bool active = !(run && !*run);
+  const unsigned rank = cluster.block_rank();
+  if (active) {
+    // interleaved: bitmap word w lives in rank (w % kAbCluster), slot w / kAbCluster
+    for (int64_t i = threadIdx.x; i < slice_words; i += blockDim.x) {
+      const int64_t gw = i * kAbCluster + rank;
+      s_bm[i] = gw < bm_words ? __ldg(bm + gw) : 0u;
+    }
+  }
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) sf[p] = 0;
+  if (threadIdx.x == 0) s_n = 0;
+  cluster.sync();  // every slice loaded before any remote read
+  int local = 0;
+  if (active) {
+    const int lane = team_lane<T>();
+    const int total = *count;
+    const int64_t step = (int64_t)warps_total() * (32 / T);
+    for (int64_t ib = (int64_t)warp_id_global() * (32 / T); ib < total; ib += step) {
+      const int64_t i = ib + (threadIdx.x & 31) / T;
+      const bool valid = i < total;
+      int delta = 0, v = 0, dest = -1, own = 0;
+      if (valid) {
+        v = list[i];
+        const uint32_t sv = st[g.v0 + v];
+        dest = st_cand(sv);
+        own = st_part(sv);
+        const int gv = st_gain(sv);
+        const int64_t b = g.xbeg[v];
+        const int d = g.deg[v];
+        constexpr int U = 8;  // entries in flight per lane
+        for (int j0 = lane; j0 < d; j0 += U * T) {
+          int u[U];
+          uint32_t bit[U];
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const int j = j0 + q * T;
+            u[q] = j < d ? __ldg(g.adj + b + j) : -1;
+          }
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            bit[q] = 0;
+            if (u[q] >= 0) {
+              const unsigned wd = (unsigned)u[q] >> 5;
+              const uint32_t *rb = cluster.map_shared_rank(s_bm, wd % kAbCluster);
+              bit[q] = (rb[wd / kAbCluster] >> (u[q] & 31)) & 1u;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            if (!bit[q]) continue;  // not a candidate: the cached gain covers it
+            const uint32_t su = __ldg(st + u[q]);
+            const int gu = st_gain(su);
+            if (!(gu > gv || (gu == gv && u[q] < g.v0 + v))) continue;  // lower priority
+            const int pu = st_part(su), cu = st_cand(su), w = g.ew(b + j0 + q * T);
+            delta += ((cu == dest) - (cu == own) - (pu == dest) + (pu == own)) * w;
+          }
+        }
+      }
+      delta = team_sum<T>(delta);
+      if (valid && lane == 0) {
+        int c[KC];
+        conn_row<KC, CW>(cache, v, c);
+        delta += c[dest] - c[own];  // the cached gain of v's move
+        const bool ok = delta > 0;
+        conf[i] = ok ? dest : -1;
+        if (ok) {
+          const unsigned long long w = (unsigned long long)g.vw[v];
+          atomicAdd(&sf[own], w);
+          atomicAdd(&sf[k + dest], w);
+          ++local;
+        }
+      }
+    }
+  }
+  if (local) atomicAdd(&s_n, local);
+  __syncthreads();
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x)
+    if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
+  if (threadIdx.x == 0 && s_n) atomicAdd(nconf, s_n);
+  cluster.sync();  // no CTA leaves while a peer may still read its slice
+}
+
 // Applies confirmed moves of the list, each kept with probability
 // prob[own] * prob[k + dest] (hash of (salt, v): deterministic thinning).
 __global__ void apply_list(const int32_t *list, const int32_t *count, const int32_t *conf,
