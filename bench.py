@@ -676,6 +676,11 @@ def secondary(csr10m, args):
     out["cfg2_evaluate_64_assignments_ms"] = ms
     out["cfg2_transfer_count"] = int(e["xfer_count"][0])
     out["cfg2_transfer_bytes"] = int(e["xfer_bytes"][0])
+    # level-synchronous makespan of the k=8 assignment (K7 mode 3)
+    node_part = parts[0].contiguous()
+    ms, (mk, _) = timed(lambda: kway.assigned_makespan(c2, node_part, k=8))
+    out["cfg2_assigned_makespan_ms"] = ms
+    out["cfg2_assigned_makespan"] = mk
     out["cfg5_policy_sweep"] = policy_sweep(4096)
     return out
 

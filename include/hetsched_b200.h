@@ -178,6 +178,17 @@ int hs_levels(const hs_dag_t *g, int mode, int32_t *level, double *finish,
 int hs_validate_dag(const hs_dag_t *g, int64_t *counts_host, int32_t *first_host,
                     int8_t *node_bad, int8_t *edge_bad, void *stream);
 
+/* Level-synchronous makespan of a given assignment:
+ * finish[v] = max over in-edges (finish[u] + w_xfer(u,v) if the edge crosses)
+ * + (dev[part[v]] ? w_gpu[v] : w_cpu[v]); an edge crosses when part[u] !=
+ * part[v], or, from the root (data in host memory), when v's part is a GPU
+ * part. part: [n] int32 in [0, k) (root entry ignored); dev: [k] int8 (0 CPU,
+ * 1 GPU). makespan_host = max finish — the infinite-workers lower bound of
+ * the schedule the assignment induces (sim.py:239-247 with transfers).
+ * fp64 max/add once per node: order-independent, bit-exact. */
+int hs_assigned_makespan(const hs_dag_t *g, const int32_t *part, const int8_t *dev, int32_t k,
+                         int32_t *level, double *finish, double *makespan_host, void *stream);
+
 /* Level order: nodes sorted by (level, index) — order[n]. */
 int hs_level_order(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
                    int32_t *order, void *stream);

@@ -195,6 +195,20 @@ def levels(csr, mode: int = 0, sync: bool = True):
     return level, finish, cp.value, nl.value
 
 
+_assigned_makespan = _opt("hs_assigned_makespan", _P, _P, _P, _i32, _P, _P, _P, _P)
+
+
+def assigned_makespan(csr, part: torch.Tensor, dev: torch.Tensor):
+    """(makespan, finish f64 [n]) of a node-space assignment (hs_assigned_makespan)."""
+    fn = _need(_assigned_makespan, "hs_assigned_makespan")
+    level = torch.empty(csr.n, dtype=torch.int32, device=csr.device)
+    finish = torch.empty(csr.n, dtype=torch.float64, device=csr.device)
+    ms = ctypes.c_double(0.0)
+    check(fn(ctypes.byref(csr.struct()), ptr(part), ptr(dev), int(dev.numel()), ptr(level),
+             ptr(finish), ctypes.byref(ms), stream_ptr()))
+    return ms.value, finish
+
+
 def level_order(csr, level: torch.Tensor, n_levels: int) -> torch.Tensor:
     order = torch.empty(csr.n, dtype=torch.int32, device=csr.device)
     check(_level_order(ctypes.byref(csr.struct()), ptr(level), n_levels, ptr(order),

@@ -46,6 +46,10 @@ struct LevelArgs {
   int32_t *max_level; // [1]
   unsigned long long *cp_bits;  // [1] max finish as ordered bits (finish >= 0)
   int32_t *processed; // [1]
+  // mode 3 (a given assignment): part[v] of every node, dev[p] = 1 when part
+  // p runs GPU kernels (w_gpu), 0 for CPU (w_cpu)
+  const int32_t *part;
+  const int8_t *dev;
 };
 
 constexpr int kStage = 2048;  // frontier entries staged per block and level
@@ -80,16 +84,24 @@ __global__ void levels_kernel(LevelArgs A) {
       double reach = 0.0;
       int lv = 0;
       bool first = true;
+      const int pv = (A.mode == 3 && v != g.root) ? A.part[v] : 0;
       for (int64_t j = g.in_ptr[v]; j < g.in_ptr[v + 1]; ++j) {
         int p = g.in_src[j];
         double f = __ldcg(&A.finish[p]);
+        if (A.mode == 3) {
+          // an input crosses when it comes from another part; the root's
+          // data starts in host memory, so it crosses into GPU parts only
+          const bool cross = p == g.root ? A.dev[pv] != 0 : A.part[p] != pv;
+          if (cross) f = f + g.w_xfer[g.in_eid[j]];
+        }
         reach = first ? f : pmax(reach, f);
         first = false;
         int lp = __ldcg(&A.level[p]) + 1;
         lv = lp > lv ? lp : lv;
       }
       double dur = A.mode == 0 ? pmin(g.w_cpu[v], g.w_gpu[v])
-                               : (A.mode == 1 ? g.w_gpu[v] : g.w_cpu[v]);
+                   : (A.mode == 1 ? g.w_gpu[v]
+                                  : (A.mode == 2 ? g.w_cpu[v] : (A.dev[pv] ? g.w_gpu[v] : g.w_cpu[v])));
       double f = reach + dur;
       __stcg(&A.finish[v], f);
       __stcg(&A.level[v], lv);
@@ -126,11 +138,34 @@ __global__ void levels_kernel(LevelArgs A) {
 
 }  // namespace
 
+namespace {
+int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *dev,
+                int32_t *level, double *finish, double *cp_host, int32_t *n_levels_host,
+                cudaStream_t s);
+}
+
 extern "C" int hs_levels(const hs_dag_t *g, int mode, int32_t *level, double *finish,
                          double *cp_host, int32_t *n_levels_host, void *stream) {
   HS_REQUIRE(g && level && finish, HS_EINVAL, "hs_levels: null argument");
   HS_REQUIRE(mode >= 0 && mode <= 2, HS_EINVAL, "hs_levels: mode must be 0..2");
-  cudaStream_t s = (cudaStream_t)stream;
+  return levels_impl(g, mode, nullptr, nullptr, level, finish, cp_host, n_levels_host,
+                     (cudaStream_t)stream);
+}
+
+extern "C" int hs_assigned_makespan(const hs_dag_t *g, const int32_t *part, const int8_t *dev,
+                                    int32_t k, int32_t *level, double *finish,
+                                    double *makespan_host, void *stream) {
+  HS_REQUIRE(g && part && dev && level && finish && makespan_host, HS_EINVAL,
+             "hs_assigned_makespan: null argument");
+  HS_REQUIRE(k >= 1, HS_EINVAL, "hs_assigned_makespan: k must be >= 1");
+  int32_t nl = 0;
+  return levels_impl(g, 3, part, dev, level, finish, makespan_host, &nl, (cudaStream_t)stream);
+}
+
+namespace {
+int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *dev,
+                int32_t *level, double *finish, double *cp_host, int32_t *n_levels_host,
+                cudaStream_t s) {
   const int64_t n = g->n;
   hs::Scratch<int32_t> indeg, fronts, small;
   hs::Scratch<unsigned long long> cp;
@@ -153,6 +188,8 @@ extern "C" int hs_levels(const hs_dag_t *g, int mode, int32_t *level, double *fi
   A.cp_bits = cp;
   A.level = level;
   A.finish = finish;
+  A.part = part;
+  A.dev = dev;
   const int block = 256;
   int per_sm = 0;
   HS_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, levels_kernel, block, 0));
@@ -185,6 +222,7 @@ extern "C" int hs_levels(const hs_dag_t *g, int mode, int32_t *level, double *fi
   }
   return HS_OK;
 }
+}  // namespace
 
 extern "C" int hs_level_order(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
                               int32_t *order, void *stream) {

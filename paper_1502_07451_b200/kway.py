@@ -167,6 +167,23 @@ def levels(csr: DagCSR, mode: int = 0):
     return _native.levels(csr, mode)
 
 
+def assigned_makespan(csr: DagCSR, part: torch.Tensor, gpu_parts: Optional[Sequence[int]] = None,
+                      k: Optional[int] = None):
+    """Level-synchronous makespan of a k-way assignment (node index space, K7 mode 3).
+
+    Parts listed in ``gpu_parts`` run at GPU speed (w_gpu), the others at CPU
+    speed; default: every part is a GPU. Cross-part edges add their transfer
+    time; the root's outputs start in host memory. Returns (makespan, finish).
+    """
+    k = int(k if k is not None else int(part.max().item()) + 1)
+    dev = torch.zeros(k, dtype=torch.int8, device=csr.device)
+    if gpu_parts is None:
+        dev.fill_(1)
+    else:
+        dev[list(gpu_parts)] = 1
+    return _native.assigned_makespan(csr, part.to(torch.int32).contiguous(), dev)
+
+
 def level_order(csr: DagCSR) -> torch.Tensor:
     lv, _, _, nl = _native.levels(csr, 0)
     return _native.level_order(csr, lv, nl)

@@ -96,3 +96,43 @@ def test_levels_and_critical_path_match_oracle():
     assert all(got[i] == want[i] for i in range(csr.n))
     order = kway.level_order(csr).cpu().numpy().tolist()
     assert order == O.level_order(g)
+
+
+def test_assigned_makespan_matches_oracle(small_cases):
+    """K7 mode 3 (level-synchronous makespan of a given assignment) vs the oracle, bit-exact."""
+    import random
+    from oracle import hetsched_oracle as O
+    from paper_1502_07451_b200.csr import DagCSR
+    from _util import graph_from_spec
+    rng = random.Random(5)
+    for case in small_cases[:25]:
+        g = graph_from_spec(case["spec"])
+        og = O.OGraph(case["spec"])
+        csr = DagCSR.from_taskgraph(g)
+        ids = [int(i) for i in csr.ids]
+        for k, gpu_parts in ((2, {1}), (4, {1, 2, 3}), (3, {0})):
+            part = {nid: rng.randrange(k) for nid in ids}
+            dev_part = torch.tensor([part[i] for i in ids], dtype=torch.int32, device="cuda")
+            ms, _ = kway.assigned_makespan(csr, dev_part, sorted(gpu_parts), k=k)
+            assert ms == O.assigned_makespan(og, part, gpu_parts)
+
+
+def test_assigned_makespan_layered_partition():
+    """20k/200k layered DAG partitioned k=8: device makespan == oracle restatement."""
+    from oracle import hetsched_oracle as O
+    csr = kway.layered_dag(20_000, 200_000, seed=9)
+    r = kway.partition_kway(csr, 8, seed=0)
+    node_part = kway.kernel_to_node_parts(csr, r.part)
+    ms, fin = kway.assigned_makespan(csr, node_part, k=8)
+    out_ptr = csr.out_ptr.cpu().numpy()
+    dst = csr.out_dst.cpu().numpy()
+    wx = csr.w_xfer.cpu().numpy()
+    wc, wg = csr.w_cpu.cpu().numpy(), csr.w_gpu.cpu().numpy()
+    spec = {"root": 0, "nodes": [[i, "MA", 512, float(wc[i]), float(wg[i])] for i in range(csr.n)],
+            "edges": [[u, int(dst[e]), 0, float(wx[e])] for u in range(csr.n)
+                      for e in range(out_ptr[u], out_ptr[u + 1])]}
+    spec["nodes"][0][1] = "SOURCE"
+    p = node_part.cpu().numpy()
+    want = O.assigned_makespan(O.OGraph(spec), {i: int(p[i]) for i in range(csr.n)},
+                               set(range(8)))
+    assert ms == want and ms > 0
