@@ -403,19 +403,20 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
       const int gv = st_gain(sv);
       const int64_t b = g.xbeg[v];
       const int d = g.deg[v];
-      for (int j0 = lane; j0 < d; j0 += 4 * T) {
-        int u[4], w[4];
-        uint32_t su[4];
+      constexpr int AU = 4;  // entries in flight per lane (8 spills under the 40-register cap)
+      for (int j0 = lane; j0 < d; j0 += AU * T) {
+        int u[AU], w[AU];
+        uint32_t su[AU];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < AU; ++q) {
           const int j = j0 + q * T;
           u[q] = j < d ? __ldg(g.adj + b + j) : -1;
           w[q] = j < d ? g.ew(b + j) : 0;
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) su[q] = u[q] >= 0 ? __ldg(st + u[q]) : 0u;
+        for (int q = 0; q < AU; ++q) su[q] = u[q] >= 0 ? __ldg(st + u[q]) : 0u;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < AU; ++q) {
           if (u[q] < 0) continue;
           int pu = st_part(su[q]);
           const int cu = st_cand(su[q]);
