@@ -94,7 +94,8 @@ typedef struct hs_ugraph {
     const int64_t *xadj;     /* [n+1] */
     const int32_t *adjncy;   /* [nnz] */
     const double *adjwgt;    /* [nnz] fp64 edge weights (exact 2-way path) */
-    const int32_t *adjwgt_i; /* [nnz] integer edge weights (k-way path) */
+    const int32_t *adjwgt_i; /* [nnz] integer edge weights (k-way path);
+                                NULL = every edge weighs 1 (METIS adjwgt = NULL) */
     const double *vwgt;      /* [n]  fp64 vertex weights (exact 2-way path) */
     const int32_t *vwgt_i;   /* [n]  integer vertex weights (k-way path);
                                 total must be < 2^31 */
@@ -291,7 +292,11 @@ int hs_METIS_PartGraphKway(const int32_t *nvtxs, const int32_t *ncon, const int3
  * edge_w_i_in (optional) holds the same weights in in-order (the DAG's CSC
  * copy of the edge attribute); without it they are gathered via in_eid.
  * twin (optional, [2m] int32) receives each entry's reverse-entry position. 
- * xadj/adjncy/adjwgt_i/vwgt_i are caller buffers sized (n-1)+1 / 2m. */
+ * xadj/adjncy/adjwgt_i/vwgt_i are caller buffers sized (n-1)+1 / 2m.
+ * adjwgt_i == NULL writes no edge weights (the caller found them uniform with
+ * hs_int32_stats and partitions with adjwgt_i = NULL, i.e. unit weights as in
+ * METIS's adjwgt = NULL, scaling the cut by the common weight); edge_w_i may
+ * then be NULL too. */
 int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i, const int32_t *edge_w_i_in,
                   const int32_t *node_w_i, int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i,
                   int32_t *vwgt_i, int32_t *twin, int64_t *nnz_host, void *stream);
@@ -303,6 +308,10 @@ int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1, const int32
                         const int32_t *edge_w_i_in, const int32_t *node_w_i, int64_t *xadj,
                         int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,
                         int64_t *nnz_host, void *stream);
+
+/* Sum, minimum and maximum of n int32 values on the device (one pass; the
+ * uniform-weight test before K1). Synchronous on stream. */
+int hs_int32_stats(const int32_t *w, int64_t n, int64_t *sum_min_max_host, void *stream);
 
 /* ---- sharded k-way partition (config 4 at 2/4/8 GPUs) ---------------------
  * One call per rank, all ranks concurrently (one process per GPU, or one host

@@ -103,6 +103,7 @@ _partition_kway = _opt("hs_partition_kway", _P, _i32, _P, _f64, ctypes.c_uint64,
 _symmetrize = _opt("hs_symmetrize", _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P)
 _symmetrize_range = _opt("hs_symmetrize_range", _P, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _P,
                          _P, _P)
+_int32_stats = _opt("hs_int32_stats", _P, _i64, _P, _P)
 _partition_kway_dist = _opt("hs_partition_kway_dist", _P, _i32, _i32, _P, _i32, _P, _f64,
                             ctypes.c_uint64, _P, _P, _P)
 if hasattr(_lib, "hs_kway_dist_arena_bytes"):
@@ -276,6 +277,14 @@ def partition_kway(ug, k: int, tpwgts, tol: float, seed: int, part: torch.Tensor
     check(fn(ctypes.byref(ug.struct()), k, tp, float(tol), ctypes.c_uint64(seed & (2**64 - 1)),
              ptr(part), stats, stream_ptr()))
     return list(stats)
+
+
+def int32_stats(t: torch.Tensor) -> Tuple[int, int, int]:
+    """(sum, min, max) of an int32 device tensor (hs_int32_stats)."""
+    fn = _need(_int32_stats, "hs_int32_stats")
+    out = (ctypes.c_int64 * 3)()
+    check(fn(ptr(t), t.numel(), out, stream_ptr()))
+    return out[0], out[1], out[2]
 
 
 def symmetrize(csr, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, edge_w_i_in=None,

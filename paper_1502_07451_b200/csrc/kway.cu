@@ -167,6 +167,7 @@ __device__ __forceinline__ int warps_total() { return (int)(((int64_t)gridDim.x 
 // one root edge per node).
 __device__ __forceinline__ int64_t root_slot(const hs_dag_t &g, int v) {
   int64_t lo = g.in_ptr[v], hi = g.in_ptr[v + 1];
+  if (g.root == 0) return (lo < hi && g.in_src[lo] == 0) ? lo : -1;  // the root sorts first
   while (lo < hi) {  // lower_bound(root)
     int64_t mid = (lo + hi) >> 1;
     if (g.in_src[mid] < g.root) lo = mid + 1; else hi = mid;
@@ -212,7 +213,7 @@ __global__ void __launch_bounds__(256, 8) sym_fill(hs_dag_t g, int kv0, int kv1,
       const int64_t at = pos + (j - i0) - (rs >= 0 && j > rs ? 1 : 0);
       const int ku = u < g.root ? u : u - 1;
       adj[at] = ku;
-      wgt[at] = ew_in ? ew_in[j] : ew[g.in_eid[j]];
+      if (wgt) wgt[at] = ew_in ? ew_in[j] : ew[g.in_eid[j]];
       if (twin) {  // the reverse entry is v in u's out-part: xadj[ku+1] - outdeg(u) + rank
         const int64_t e = g.in_eid[j];
         const int64_t tw = xadj[ku + 1] - g.out_ptr[u + 1] + e;
@@ -225,8 +226,80 @@ __global__ void __launch_bounds__(256, 8) sym_fill(hs_dag_t g, int kv0, int kv1,
     for (int64_t j = o0 + lane; j < o1; j += T) {
       const int u = g.out_dst[j];
       adj[opos + (j - o0)] = u < g.root ? u : u - 1;
-      wgt[opos + (j - o0)] = ew[j];
+      if (wgt) wgt[opos + (j - o0)] = ew[j];
     }
+  }
+}
+
+// Chunked K1 (no twin index): one warp per 32 consecutive kernel positions.
+// Consecutive nodes own consecutive ranges of in_src and out_dst, so the warp
+// streams the chunk's in-entries and then its out-entries with coalesced
+// loads and near-contiguous stores; each entry finds its vertex by a 5-step
+// search over the chunk's list prefix in shared memory. Same output as
+// sym_fill (the per-vertex order is in-list then out-list).
+constexpr int kSymWarps = 8;
+__global__ void __launch_bounds__(kSymWarps * 32) sym_fill_chunk(
+    hs_dag_t g, int kv0, int kv1, const int32_t *ew, const int32_t *ew_in, const int32_t *nw,
+    const int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw) {
+  __shared__ int s_ipre[kSymWarps][32], s_opre[kSymWarps][32], s_rs[kSymWarps][32],
+      s_ilen[kSymWarps][32];
+  __shared__ int64_t s_ib[kSymWarps][32], s_ob[kSymWarps][32], s_pos[kSymWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nl = kv1 - kv0;
+  const int64_t nchunks = (nl + 31) / 32;
+  for (int64_t c = warp_id_global(); c < nchunks; c += warps_total()) {
+    const int li = (int)(c * 32) + lane;
+    const int cnt = min(32, nl - (int)(c * 32));
+    int ilen = 0, olen = 0, rsr = INT32_MAX;
+    if (li < nl) {
+      const int v = node_of(g, kv0 + li);
+      const int64_t ib = g.in_ptr[v], ie = g.in_ptr[v + 1];
+      const int64_t ob = g.out_ptr[v], oe = g.out_ptr[v + 1];
+      const int64_t rs = root_slot(g, v);
+      ilen = (int)(ie - ib);
+      olen = (int)(oe - ob);
+      if (rs >= 0) rsr = (int)(rs - ib);
+      s_ib[w][lane] = ib;
+      s_ob[w][lane] = ob;
+      s_pos[w][lane] = xadj[li];
+      s_rs[w][lane] = rsr;
+      s_ilen[w][lane] = ilen - (rs >= 0 ? 1 : 0);
+      vw[li] = nw[v];
+    }
+    int ip = ilen, op = olen;  // inclusive scans
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, ip, o), b = __shfl_up_sync(0xffffffffu, op, o);
+      if (lane >= o) { ip += a; op += b; }
+    }
+    s_ipre[w][lane] = ip - ilen;
+    s_opre[w][lane] = op - olen;
+    const int tin = __shfl_sync(0xffffffffu, ip, 31), tout = __shfl_sync(0xffffffffu, op, 31);
+    __syncwarp();
+    for (int f = lane; f < tin; f += 32) {
+      int t = 0;
+      for (int st = 16; st; st >>= 1)
+        if (t + st < cnt && s_ipre[w][t + st] <= f) t += st;
+      const int r = f - s_ipre[w][t];
+      const int rs = s_rs[w][t];
+      if (r == rs) continue;
+      const int64_t j = s_ib[w][t] + r;
+      const int64_t at = s_pos[w][t] + r - (r > rs ? 1 : 0);
+      const int u = g.in_src[j];
+      adj[at] = u < g.root ? u : u - 1;
+      if (wgt) wgt[at] = ew_in ? ew_in[j] : ew[g.in_eid[j]];
+    }
+    for (int f = lane; f < tout; f += 32) {
+      int t = 0;
+      for (int st = 16; st; st >>= 1)
+        if (t + st < cnt && s_opre[w][t + st] <= f) t += st;
+      const int r = f - s_opre[w][t];
+      const int64_t j = s_ob[w][t] + r;
+      const int64_t at = s_pos[w][t] + s_ilen[w][t] + r;
+      const int u = g.out_dst[j];
+      adj[at] = u < g.root ? u : u - 1;
+      if (wgt) wgt[at] = ew[j];
+    }
+    __syncwarp();
   }
 }
 
@@ -2007,8 +2080,9 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
                                    const int32_t *node_w_i, int64_t *xadj, int32_t *adjncy,
                                    int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,
                                    int64_t *nnz_host, void *stream) {
-  HS_REQUIRE(g && edge_w_i && node_w_i && xadj && adjncy && adjwgt_i && vwgt_i, HS_EINVAL,
-             "hs_symmetrize: null argument");
+  HS_REQUIRE(g && node_w_i && xadj && adjncy && vwgt_i, HS_EINVAL, "hs_symmetrize: null argument");
+  HS_REQUIRE(!adjwgt_i || edge_w_i, HS_EINVAL, "hs_symmetrize: adjwgt_i needs edge_w_i");
+  HS_REQUIRE(adjwgt_i || !twin, HS_EINVAL, "hs_symmetrize: unit weights take no twin index");
   const int nk = g->n - 1;
   HS_REQUIRE(0 <= kv0 && kv0 <= kv1 && kv1 <= nk, HS_EINVAL, "kernel range [%d, %d) outside [0, %d)",
              kv0, kv1, nk);
@@ -2022,7 +2096,10 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
   HS_CHECK_CUDA(deg64.alloc(nl + 1, s));
   // in/out pointers, in_src/out_dst, weights (in + out order), adj+wgt writes
   const double frac = nk ? (double)nl / (double)nk : 0.0;
-  hs::Prof P("symmetrize", s, frac * (32.0 * g->n + 32.0 * g->m));
+  // per node: in/out pointers, xadj, node weight read + write; per edge:
+  // in_src + out_dst read, two adjacency writes, and with weights the out-
+  // and in-order weight reads and two weight writes
+  hs::Prof P("symmetrize", s, frac * (32.0 * g->n + (adjwgt_i ? 32.0 : 16.0) * g->m));
   sym_degree<<<hs::grid_for(nl, 256), 256, 0, s>>>(*g, kv0, kv1, deg);
   HS_CHECK_LAUNCH();
   HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nl, 0, sizeof(int64_t), s));
@@ -2032,8 +2109,15 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
   if (rc) return rc;
   static const int TS = getenv("HS_KWAY_TSYM") ? atoi(getenv("HS_KWAY_TSYM")) : 4;  // measured: 4 lanes beat 8 and 2
   const int sgrid = std::max(1, std::min(hs::sm_count() * 32, (nl * TS + 255) / 256));
+  static const bool chunked = !getenv("HS_KWAY_SYM_TEAM");
 #define HS_SYM_ARGS *g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin
-  if (TS == 2) sym_fill<2><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
+  if (chunked && !twin) {
+    const int64_t chunks = ((int64_t)nl + 31) / 32;
+    const int cgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)hs::sm_count() * 8, (chunks + kSymWarps - 1) / kSymWarps));
+    sym_fill_chunk<<<cgrid, kSymWarps * 32, 0, s>>>(*g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i,
+                                                    xadj, adjncy, adjwgt_i, vwgt_i);
+  } else if (TS == 2) sym_fill<2><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
   else if (TS == 4) sym_fill<4><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
   else sym_fill<8><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
 #undef HS_SYM_ARGS
@@ -2042,6 +2126,28 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
     HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
   }
+  return HS_OK;
+}
+
+extern "C" int hs_int32_stats(const int32_t *w, int64_t n, int64_t *sum_min_max_host,
+                              void *stream) {
+  HS_REQUIRE(sum_min_max_host && (w || n == 0) && n >= 0, HS_EINVAL,
+             "hs_int32_stats: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t h[3] = {0, INT32_MAX, INT32_MIN};
+  if (n > 0) {
+    hs::Scratch<int64_t> d;
+    HS_CHECK_CUDA(d.alloc(3, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(d.p, h, sizeof h, cudaMemcpyHostToDevice, s));
+    wstats_kernel<<<hs::grid_for(n, 256, hs::sm_count() * 8), 256, 0, s>>>(
+        n, w, (unsigned long long *)d.p, (int32_t *)(d.p + 1), (int32_t *)(d.p + 2));
+    HS_CHECK_LAUNCH();
+    widen_minmax<<<1, 1, 0, s>>>(d.p + 1);
+    HS_CHECK_LAUNCH();
+    HS_CHECK_CUDA(cudaMemcpyAsync(h, d.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  }
+  for (int i = 0; i < 3; ++i) sum_min_max_host[i] = h[i];
   return HS_OK;
 }
 
@@ -2113,10 +2219,18 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
     deg_from_xadj<<<hs::grid_for(n0, 256), 256, 0, s>>>(ug->xadj, n0, deg_l0,
                                                         (int32_t *)(tot_dev + 5));
     HS_CHECK_LAUNCH();
-    wstats_kernel<<<hs::grid_for(nnz0, 256, hs::sm_count() * 8), 256, 0, s>>>(
-        nnz0, ug->adjwgt_i, (unsigned long long *)tot_dev, (int32_t *)(tot_dev + 3),
-        (int32_t *)(tot_dev + 4));
-    HS_CHECK_LAUNCH();
+    if (ug->adjwgt_i) {
+      wstats_kernel<<<hs::grid_for(nnz0, 256, hs::sm_count() * 8), 256, 0, s>>>(
+          nnz0, ug->adjwgt_i, (unsigned long long *)tot_dev, (int32_t *)(tot_dev + 3),
+          (int32_t *)(tot_dev + 4));
+      HS_CHECK_LAUNCH();
+    } else {  // METIS's adjwgt = NULL: every edge weighs 1 (sum = entries)
+      const int64_t unit[3] = {nnz0, 1, 1};
+      HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev, unit, 8, cudaMemcpyHostToDevice, s));
+      const int32_t one1[2] = {1, 1};
+      HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev + 3, one1, 4, cudaMemcpyHostToDevice, s));
+      HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev + 4, one1, 4, cudaMemcpyHostToDevice, s));
+    }
     wstats_kernel<<<hs::grid_for(n0, 256, hs::sm_count() * 8), 256, 0, s>>>(
         n0, ug->vwgt_i, (unsigned long long *)(tot_dev + 1), (int32_t *)(tot_dev + 6),
         (int32_t *)(tot_dev + 7));
@@ -2334,7 +2448,7 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   HS_REQUIRE(ug && tpwgts_host && part_out, HS_EINVAL, "hs_partition_kway: null argument");
   HS_REQUIRE(k >= 1 && k <= kMaxParts, HS_ELIMIT, "k must be in 1..%d", kMaxParts);
   HS_REQUIRE(ug->n >= 1, HS_EINVAL, "empty graph");
-  HS_REQUIRE(ug->adjwgt_i && ug->vwgt_i, HS_EINVAL, "k-way path needs integer weights");
+  HS_REQUIRE(ug->vwgt_i, HS_EINVAL, "k-way path needs integer vertex weights");
   return partition_impl(ug, 0, ug->n, nullptr, k, tpwgts_host, tol, seed, part_out, stats_host,
                         (cudaStream_t)stream);
 }
@@ -2359,7 +2473,7 @@ extern "C" int hs_partition_kway_dist(const hs_ugraph_t *ug, int32_t v0, int32_t
   HS_REQUIRE(ug->n >= 1 && v0 >= 0 && (int64_t)v0 + ug->n <= n_global, HS_EINVAL,
              "rank range [%d, %lld) outside [0, %d) or empty", v0, (long long)v0 + ug->n,
              n_global);
-  HS_REQUIRE(ug->adjwgt_i && ug->vwgt_i, HS_EINVAL, "k-way path needs integer weights");
+  HS_REQUIRE(ug->vwgt_i, HS_EINVAL, "k-way path needs integer vertex weights");
   HS_REQUIRE(!ug->twin, HS_EINVAL, "sharded partition takes no twin index");
   if (dist->size == 1) {
     HS_REQUIRE(v0 == 0 && ug->n == n_global, HS_EINVAL, "a 1-rank group owns the whole graph");

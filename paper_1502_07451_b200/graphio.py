@@ -58,7 +58,7 @@ def emit_metis_csr(csr: DagCSR, node_weight_source: str = GPU, scale: int = 100)
     if bool((w_node[kern] == 0).all()) and bool((csr.w_xfer[inter] == 0).all()):
         raise PartitionError("all weights are zero; cannot integerize for export")
     ew = _scaled(csr.w_xfer, scale)
-    ug = symmetrize(csr, ew, _scaled(w_node, scale), in_order(csr, ew))
+    ug = symmetrize(csr, ew, _scaled(w_node, scale), in_order(csr, ew), unit_ok=False)
     n_inter = int(inter.sum().item())
     header = f"{ug.n} {n_inter} 011\n".encode()
     size = ctypes.c_int64(0)

@@ -29,20 +29,44 @@ from .csr import DagCSR
 class UGraph:
     """Undirected integer-weighted kernel graph on the device (hs_ugraph_t)."""
 
-    def __init__(self, xadj, adjncy, adjwgt, vwgt, twin=None):
-        self.xadj, self.adjncy, self.adjwgt, self.vwgt = xadj, adjncy, adjwgt, vwgt
+    def __init__(self, xadj, adjncy, adjwgt, vwgt, twin=None, unit_weight: int = 1):
+        """``adjwgt=None``: every edge weighs ``unit_weight`` (no weight array on
+        the device; the partitioner sees unit weights, METIS's adjwgt = NULL)."""
+        self.xadj, self.adjncy, self._adjwgt, self.vwgt = xadj, adjncy, adjwgt, vwgt
         self.twin = twin
+        self.unit_weight = int(unit_weight)
         self.n = int(vwgt.numel())
         self.nnz = int(adjncy.numel())
         self._struct = None
+
+    @property
+    def adjwgt(self) -> torch.Tensor:
+        """Per-entry int32 edge weights (materialised when uniform)."""
+        if self._adjwgt is None:
+            return torch.full((self.nnz,), self.unit_weight, dtype=torch.int32,
+                              device=self.adjncy.device)
+        return self._adjwgt
+
+    @property
+    def weight_scale(self) -> int:
+        """Factor between the partitioner's cut and the caller's weights."""
+        return self.unit_weight if self._adjwgt is None else 1
 
     def struct(self):
         if self._struct is None:
             p = _native.ptr
             self._struct = _native.HsUGraph(self.n, self.nnz, p(self.xadj), p(self.adjncy), None,
-                                            p(self.adjwgt), None, p(self.vwgt),
+                                            p(self._adjwgt), None, p(self.vwgt),
                                             p(self.twin) if self.twin is not None else None)
         return self._struct
+
+
+def _uniform_weight(edge_w_i: torch.Tensor) -> int:
+    """The common value of the edge weights if they are all equal and positive, else 0."""
+    if edge_w_i.numel() == 0 or os.environ.get("HS_KWAY_WEIGHTS") == "1":
+        return 0
+    _, lo, hi = _native.int32_stats(edge_w_i)
+    return lo if lo == hi and lo > 0 else 0
 
 
 def layered_dag(n_kernels: int, m_inter: int, seed: int = 0, kind: str = "MA", size: int = 512,
@@ -90,11 +114,13 @@ def integer_weights(w: torch.Tensor, scale: int = 100) -> torch.Tensor:
 
 def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,
                node_w_i: Optional[torch.Tensor] = None,
-               edge_w_i_in: Optional[torch.Tensor] = None) -> UGraph:
+               edge_w_i_in: Optional[torch.Tensor] = None, unit_ok: bool = True) -> UGraph:
     """K1 on the device; default weights are the integerised w_xfer / w_gpu.
 
     ``edge_w_i_in`` is the same edge weight in in-order (CSC copy,
     ``edge_w_i[csr.in_eid]``); passing it saves a random gather.
+    ``unit_ok``: uniform edge weights produce no weight array (the partitioner
+    runs on unit weights and rescales the cut); False always writes them.
     """
     dev = csr.device
     if edge_w_i is None:
@@ -105,17 +131,20 @@ def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,
     xadj = torch.empty(nk + 1, dtype=torch.int64, device=dev)
     nnz_cap = 2 * csr.m
     adjncy = torch.empty(nnz_cap, dtype=torch.int32, device=dev)
-    adjwgt = torch.empty(nnz_cap, dtype=torch.int32, device=dev)
     vwgt = torch.empty(nk, dtype=torch.int32, device=dev)
     # reverse-entry index for ghost-part refinement: opt-in (its random scatter
     # costs more in K1 than the ghost reads save in K6 on issue-bound passes)
     want_twin = os.environ.get("HS_KWAY_GHOST") == "1" and nnz_cap < 2 ** 31
     twin = torch.empty(nnz_cap, dtype=torch.int32, device=dev) if want_twin else None
-    nnz = _native.symmetrize(csr, edge_w_i.contiguous(), node_w_i.contiguous(), xadj, adjncy,
-                             adjwgt, vwgt,
-                             edge_w_i_in.contiguous() if edge_w_i_in is not None else None, twin)
-    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz], vwgt,
-                  twin[:nnz] if twin is not None else None)
+    # uniform edge weights (one matrix per transfer): no weight stream at all
+    w0 = 0 if want_twin or not unit_ok else _uniform_weight(edge_w_i)
+    adjwgt = None if w0 else torch.empty(nnz_cap, dtype=torch.int32, device=dev)
+    nnz = _native.symmetrize(csr, None if w0 else edge_w_i.contiguous(), node_w_i.contiguous(),
+                             xadj, adjncy, adjwgt, vwgt,
+                             edge_w_i_in.contiguous() if edge_w_i_in is not None and not w0
+                             else None, twin)
+    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz] if adjwgt is not None else None, vwgt,
+                  twin[:nnz] if twin is not None else None, unit_weight=w0 or 1)
 
 
 @dataclass
@@ -143,7 +172,8 @@ def partition_kway(graph, k: int, tpwgts: Optional[Sequence[float]] = None, tol:
         raise ValueError("need one target fraction per part")
     part = out if out is not None else torch.empty(ug.n, dtype=torch.int32, device=ug.xadj.device)
     st = _native.partition_kway(ug, k, tpwgts, tol, seed, part)
-    return KwayResult(part, st[0], st[1], st[2], st[3] / 1e9, bool(st[4]), st[5])
+    return KwayResult(part, st[0] * ug.weight_scale, st[1], st[2], st[3] / 1e9, bool(st[4]),
+                      st[5])
 
 
 def evaluate_batch(csr: DagCSR, parts: torch.Tensor, k: int,
@@ -250,13 +280,17 @@ def symmetrize_range(csr: DagCSR, kv0: int, kv1: int, edge_w_i: Optional[torch.T
         cap = int(undirected_degrees(csr)[kv0:kv1].sum().item()) if nl else 0
     xadj = torch.empty(nl + 1, dtype=torch.int64, device=dev)
     adjncy = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-    adjwgt = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    # the uniformity test reads the whole weight array: every rank decides alike
+    w0 = _uniform_weight(edge_w_i)
+    adjwgt = None if w0 else torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
     vwgt = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
-    nnz = _native.symmetrize_range(csr, kv0, kv1, edge_w_i.contiguous(), node_w_i.contiguous(),
-                                   xadj, adjncy, adjwgt, vwgt,
-                                   edge_w_i_in.contiguous() if edge_w_i_in is not None else None)
+    nnz = _native.symmetrize_range(csr, kv0, kv1, None if w0 else edge_w_i.contiguous(),
+                                   node_w_i.contiguous(), xadj, adjncy, adjwgt, vwgt,
+                                   edge_w_i_in.contiguous() if edge_w_i_in is not None and not w0
+                                   else None)
     assert nnz == cap
-    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz], vwgt[:nl])
+    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz] if adjwgt is not None else None, vwgt[:nl],
+                  unit_weight=w0 or 1)
 
 
 class PartitionGroup:
@@ -326,7 +360,8 @@ def partition_kway_shard(ug_local: UGraph, v0: int, n_global: int, group: Partit
                                                    device=ug_local.xadj.device)
     st = _native.partition_kway_dist(ug_local, v0, n_global, group.dist(rank), k, tpwgts, tol,
                                      seed, part)
-    return KwayResult(part, st[0], st[1], st[2], st[3] / 1e9, bool(st[4]), st[5])
+    return KwayResult(part, st[0] * ug_local.weight_scale, st[1], st[2], st[3] / 1e9,
+                      bool(st[4]), st[5])
 
 
 def partition_kway_loopback(csr: DagCSR, nranks: int, k: int,

@@ -50,6 +50,60 @@ def test_symmetrize_adjacency_sets():
         assert sorted(adj[xadj[v]:xadj[v + 1]].tolist()) == sorted(want.get(v, []))
 
 
+def _expected_rows(csr, ew):
+    """K1's exact entry sequence: per kernel, in-list (root dropped) then out-list."""
+    op, od = csr.out_ptr.cpu().numpy(), csr.out_dst.cpu().numpy()
+    ip, isrc = csr.in_ptr.cpu().numpy(), csr.in_src.cpu().numpy()
+    ieid = csr.in_eid.cpu().numpy()
+    root = csr.root
+    adj, wgt, xadj = [], [], [0]
+    for v in range(csr.n):
+        if v == root:
+            continue
+        ins = [(u, ew[e]) for u, e in zip(isrc[ip[v]:ip[v + 1]], ieid[ip[v]:ip[v + 1]])
+               if u != root]
+        outs = list(zip(od[op[v]:op[v + 1]], ew[op[v]:op[v + 1]]))
+        for u, w in ins + outs:
+            adj.append(u if u < root else u - 1)
+            wgt.append(w)
+        xadj.append(len(adj))
+    return np.array(xadj), np.array(adj), np.array(wgt)
+
+
+@pytest.mark.parametrize("n,m", [(50, 300), (3000, 30000), (20011, 150007)])
+def test_symmetrize_exact_sequence(n, m):
+    """Chunked K1 writes the same entries in the same order as the per-vertex
+    definition, with non-uniform weights (in-order copy or in_eid gather)."""
+    csr = kway.layered_dag(n, m, 2)
+    ew = torch.randint(1, 1000, (csr.m,), dtype=torch.int32, device=csr.device)
+    xadj_e, adj_e, wgt_e = _expected_rows(csr, ew.cpu().numpy())
+    for w_in in (None, kway.in_order(csr, ew)):
+        ug = kway.symmetrize(csr, ew, None, w_in)
+        assert ug.weight_scale == 1
+        assert (ug.xadj.cpu().numpy() == xadj_e).all()
+        assert (ug.adjncy.cpu().numpy() == adj_e).all()
+        assert (ug.adjwgt.cpu().numpy() == wgt_e).all()
+
+
+def test_uniform_weights_unit_path_identical(monkeypatch):
+    """Uniform edge weights: K1 writes no weight stream (adjwgt NULL = unit
+    weights) and the partition and cut equal the explicit-weight run's."""
+    csr = kway.layered_dag(20000, 200000, 4)
+    ew = torch.full((csr.m,), 37, dtype=torch.int32, device=csr.device)
+    ug = kway.symmetrize(csr, ew)
+    assert ug._adjwgt is None and ug.weight_scale == 37
+    monkeypatch.setenv("HS_KWAY_WEIGHTS", "1")
+    ugw = kway.symmetrize(csr, ew)
+    assert ugw._adjwgt is not None
+    assert (ugw.adjncy == ug.adjncy).all() and (ugw.adjwgt == ug.adjwgt).all()
+    r = kway.partition_kway(ug, 8, tol=0.03, seed=3)
+    rw = kway.partition_kway(ugw, 8, tol=0.03, seed=3)
+    assert (r.part == rw.part).all() and r.cut == rw.cut
+    p = r.part.long()
+    src = torch.repeat_interleave(torch.arange(ug.n, device=p.device), ug.xadj.diff())
+    assert r.cut == int(((p[src] != p[ug.adjncy.long()]).sum().item() // 2) * 37)
+
+
 @pytest.mark.parametrize("n,m,k", [(5000, 50000, 2), (20000, 200000, 8), (100000, 1000000, 8)])
 def test_kway_valid_balanced_deterministic(n, m, k):
     csr = kway.layered_dag(n, m, 0)
