@@ -353,37 +353,54 @@ def run_ours(args):
             json.dump(kernels, f, indent=1)
 
     # ---- e2e: public API from pinned host buffers, result read back ----
-    # the arrays the step reads: DAG structure (out/in CSR) and the integer
-    # weights; fp64 node/edge weights and byte counts are not inputs of K1/K3-K6
-    host = {name: getattr(csr, name).cpu().pin_memory()
-            for name in ("out_ptr", "out_dst", "in_ptr", "in_src")}
+    # the caller's DAG as a sorted edge list (out-CSR) plus the integer edge
+    # and node weights; the in-CSR is derived on the device (hs_dag_transpose)
+    # rather than shipped; fp64 weights and byte counts are not inputs of K1-K6
+    host = {name: getattr(csr, name).cpu().pin_memory() for name in ("out_ptr", "out_dst")}
     host_ew, host_nw = ew.cpu().pin_memory(), nw.cpu().pin_memory()
-    host_ew_in = ew_in.cpu().pin_memory()
     h2d = sum(t.numel() * t.element_size() for t in host.values())
-    h2d += host_ew.numel() * 4 + host_nw.numel() * 4 + host_ew_in.numel() * 4
+    h2d += host_ew.numel() * 4 + host_nw.numel() * 4
     d2h = (csr.n - 1) * 4
     from paper_1502_07451_b200.csr import DagCSR
 
+    side = torch.cuda.Stream(device=dev)
+    part_host = torch.empty(n_glob, dtype=torch.int32).pin_memory()
+
     def e2e_step():
+        # the edge list first; the weights' copy (side stream, queued behind
+        # it on the copy engine) overlaps the device transpose
+        main = torch.cuda.current_stream()
         d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
-        g = DagCSR(csr.n, csr.m, 0, d["out_ptr"], d["out_dst"], d["in_ptr"], d["in_src"],
-                   None, None, None, None, None)
-        r = partition(g, host_ew.to(dev, non_blocking=True), host_nw.to(dev, non_blocking=True),
-                      host_ew_in.to(dev, non_blocking=True))
-        return r.part.to("cpu")
+        copied = torch.cuda.Event()
+        copied.record(main)
+        side.wait_event(copied)
+        with torch.cuda.stream(side):
+            ew_d = host_ew.to(dev, non_blocking=True)
+            nw_d = host_nw.to(dev, non_blocking=True)
+        g = DagCSR.from_out_csr(csr.root, d["out_ptr"], d["out_dst"])
+        main.wait_stream(side)
+        ew_d.record_stream(main)
+        nw_d.record_stream(main)
+        r = partition(g, ew_d, nw_d, None)
+        part_host.copy_(r.part, non_blocking=True)  # into the caller's pinned buffer
+        return part_host
 
     e2e_steps = max(1, min(args.steps, 3))
-    e2e_step()
+    for _ in range(2):
+        e2e_step()
     torch.cuda.synchronize()
     barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
+    marks = [torch.cuda.Event(enable_timing=True) for _ in range(e2e_steps + 1)]
+    marks[0].record(stream)
+    for i in range(e2e_steps):
         e2e_step()
-    e1.record(stream)
+        marks[i + 1].record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
+    e2e_each = [marks[i].elapsed_time(marks[i + 1]) for i in range(e2e_steps)]
+    e2e_ms = marks[0].elapsed_time(marks[-1]) / e2e_steps
+    if os.environ.get("HS_BENCH_DEBUG"):
+        print("e2e steps ms", e2e_each, "reserved GB", torch.cuda.memory_reserved() / 1e9,
+              file=sys.stderr, flush=True)
     if world > 1:
         e2e_ms = allmax(e2e_ms, dev)
     del host

@@ -309,6 +309,14 @@ int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1, const int32
                         int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,
                         int64_t *nnz_host, void *stream);
 
+/* In-CSR of a DAG from its out-CSR, on the device: in_ptr [n+1], in_src /
+ * in_eid [m] in the reference's in_edges order (per destination, ascending
+ * source, graph.py:89-90; in_eid = the edge's out-order index). Replaces the
+ * host-side construction of the second half of hs_dag_t, so a caller ships
+ * only out_ptr/out_dst. Deterministic. m < 2^31. */
+int hs_dag_transpose(int32_t n, int64_t m, const int64_t *out_ptr, const int32_t *out_dst,
+                     int64_t *in_ptr, int32_t *in_src, int32_t *in_eid, void *stream);
+
 /* Sum, minimum and maximum of n int32 values on the device (one pass; the
  * uniform-weight test before K1). Synchronous on stream. */
 int hs_int32_stats(const int32_t *w, int64_t n, int64_t *sum_min_max_host, void *stream);

@@ -103,6 +103,7 @@ _partition_kway = _opt("hs_partition_kway", _P, _i32, _P, _f64, ctypes.c_uint64,
 _symmetrize = _opt("hs_symmetrize", _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P)
 _symmetrize_range = _opt("hs_symmetrize_range", _P, _i32, _i32, _P, _P, _P, _P, _P, _P, _P, _P,
                          _P, _P)
+_dag_transpose = _opt("hs_dag_transpose", _i32, _i64, _P, _P, _P, _P, _P, _P)
 _int32_stats = _opt("hs_int32_stats", _P, _i64, _P, _P)
 _partition_kway_dist = _opt("hs_partition_kway_dist", _P, _i32, _i32, _P, _i32, _P, _f64,
                             ctypes.c_uint64, _P, _P, _P)
@@ -277,6 +278,12 @@ def partition_kway(ug, k: int, tpwgts, tol: float, seed: int, part: torch.Tensor
     check(fn(ctypes.byref(ug.struct()), k, tp, float(tol), ctypes.c_uint64(seed & (2**64 - 1)),
              ptr(part), stats, stream_ptr()))
     return list(stats)
+
+
+def dag_transpose(n: int, m: int, out_ptr, out_dst, in_ptr, in_src, in_eid) -> None:
+    fn = _need(_dag_transpose, "hs_dag_transpose")
+    check(fn(n, m, ptr(out_ptr), ptr(out_dst), ptr(in_ptr), ptr(in_src), ptr(in_eid),
+             stream_ptr()))
 
 
 def int32_stats(t: torch.Tensor) -> Tuple[int, int, int]:

@@ -101,6 +101,20 @@ class DagCSR:
                    t(h.bytes), ids=h.ids, host=h)
 
     @classmethod
+    def from_out_csr(cls, root: int, out_ptr: torch.Tensor, out_dst: torch.Tensor,
+                     w_cpu=None, w_gpu=None, w_xfer=None, nbytes=None) -> "DagCSR":
+        """DAG from its device out-CSR alone (edges sorted by (src, dst)); the
+        in-CSR is built on the device (``hs_dag_transpose``)."""
+        n, m = int(out_ptr.numel()) - 1, int(out_dst.numel())
+        dev = out_ptr.device
+        in_ptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+        in_src = torch.empty(m, dtype=torch.int32, device=dev)
+        in_eid = torch.empty(m, dtype=torch.int32, device=dev)
+        _native.dag_transpose(n, m, out_ptr, out_dst, in_ptr, in_src, in_eid)
+        return cls(n, m, root, out_ptr, out_dst, in_ptr, in_src, in_eid, w_cpu, w_gpu, w_xfer,
+                   nbytes)
+
+    @classmethod
     def from_taskgraph(cls, graph) -> "DagCSR":
         h = HostDag.from_taskgraph(graph)
         if h.root < 0:

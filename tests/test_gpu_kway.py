@@ -29,6 +29,83 @@ def test_generator_matches_oracle(n, m, seed):
     assert all(lay[v] == layer[v] for v in range(1, n + 1))
 
 
+def test_dag_transpose_empty():
+    from paper_1502_07451_b200.csr import DagCSR
+    dev = torch.device("cuda")
+    t = DagCSR.from_out_csr(0, torch.zeros(2, dtype=torch.int64, device=dev),
+                            torch.zeros(0, dtype=torch.int32, device=dev))
+    assert t.in_ptr.tolist() == [0, 0] and t.in_src.numel() == 0
+
+
+@pytest.mark.parametrize("n,m,seed", [(2, 1, 0), (50, 300, 0), (3000, 30000, 5),
+                                      (100000, 1000000, 9)])
+def test_dag_transpose_matches_generator(n, m, seed):
+    """hs_dag_transpose rebuilds the in-CSR (ascending sources, out-order ids) exactly."""
+    from paper_1502_07451_b200.csr import DagCSR
+    csr = kway.layered_dag(n, m, seed)
+    t = DagCSR.from_out_csr(csr.root, csr.out_ptr, csr.out_dst)
+    assert torch.equal(t.in_ptr, csr.in_ptr)
+    assert torch.equal(t.in_src, csr.in_src)
+    assert torch.equal(t.in_eid, csr.in_eid)
+
+
+def _middle_root_dag(seed, n=400, m=3000):
+    """HostDag whose root sits in the middle of the index order (kernel edges u < v)."""
+    from paper_1502_07451_b200.csr import HostDag
+    rng = np.random.default_rng(seed)
+    root = n // 2
+    kern = np.array([v for v in range(n) if v != root])
+    pairs = set()
+    while len(pairs) < m:
+        a, b = sorted(rng.choice(kern, 2, replace=False).tolist())
+        pairs.add((a, b))
+    has_in = {b for _, b in pairs}
+    pairs |= {(root, v) for v in kern.tolist() if v not in has_in}
+    e = np.array(sorted(pairs), dtype=np.int32)
+    ids = np.arange(n, dtype=np.int64)
+    return HostDag(ids, root, e[:, 0].copy(), e[:, 1].copy(), rng.random(n), rng.random(n),
+                   rng.random(len(e)), np.full(len(e), 4096, dtype=np.int64))
+
+
+def test_dag_transpose_long_segments():
+    """Fan-ins past the short (32) and CTA (4096) segment-sort limits."""
+    from paper_1502_07451_b200.csr import DagCSR, HostDag
+    n = 7000
+    edges = {(0, v) for v in range(1, 5001)}
+    edges |= {(u, 6001) for u in range(1, 5001)} | {(u, 6002) for u in range(4000, 4100)}
+    edges |= {(u, 6003) for u in range(1, 40)} | {(6001, 6500), (6002, 6500)}
+    edges |= {(0, v) for v in range(5001, n) if v not in (6001, 6002, 6003, 6500)}
+    e = np.array(sorted(edges), dtype=np.int32)
+    h = HostDag(np.arange(n, dtype=np.int64), 0, e[:, 0].copy(), e[:, 1].copy(), np.ones(n),
+                np.ones(n), np.ones(len(e)), np.full(len(e), 8, dtype=np.int64))
+    csr = DagCSR.from_host(h)
+    t = DagCSR.from_out_csr(csr.root, csr.out_ptr, csr.out_dst)
+    assert torch.equal(t.in_ptr, csr.in_ptr)
+    assert torch.equal(t.in_src, csr.in_src)
+    assert torch.equal(t.in_eid, csr.in_eid)
+
+
+def test_dag_transpose_object_model_and_middle_root():
+    """Object-model DAGs and a root in the middle of the id order, against the
+    host lowering; K1 on the device-built CSC equals K1 on the host-built one."""
+    from _util import random_weighted_graph
+    from paper_1502_07451_b200.csr import DagCSR
+    csrs = [DagCSR.from_taskgraph(random_weighted_graph(s, max_kernels=40)) for s in range(8)]
+    csrs += [DagCSR.from_host(_middle_root_dag(s)) for s in range(3)]
+    for csr in csrs:
+        t = DagCSR.from_out_csr(csr.root, csr.out_ptr, csr.out_dst)
+        assert torch.equal(t.in_ptr, csr.in_ptr)
+        assert torch.equal(t.in_src, csr.in_src)
+        assert torch.equal(t.in_eid, csr.in_eid)
+        ew = kway.integer_weights(csr.w_xfer)
+        nw = kway.integer_weights(csr.w_gpu)
+        a, b = kway.symmetrize(csr, ew, nw), kway.symmetrize(t, ew, nw)
+        assert torch.equal(a.xadj, b.xadj) and torch.equal(a.adjncy, b.adjncy)
+        assert torch.equal(a.adjwgt, b.adjwgt) and torch.equal(a.vwgt, b.vwgt)
+        xadj_e, adj_e, wgt_e = _expected_rows(csr, ew.cpu().numpy())
+        assert (a.adjncy.cpu().numpy() == adj_e).all() and (a.adjwgt.cpu().numpy() == wgt_e).all()
+
+
 def _host_graph(csr):
     src = np.repeat(np.arange(csr.n), np.diff(csr.out_ptr.cpu().numpy()))
     return src, csr.out_dst.cpu().numpy(), csr.bytes.cpu().numpy()
