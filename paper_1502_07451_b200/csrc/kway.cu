@@ -2376,19 +2376,22 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   if (const char *e = getenv("HS_KWAY_MAXDEG")) max_deg = atof(e);
   K.max_deg = max_deg;
   // Skip coarsening when its only product would be the band start on a
-  // skeleton level: one GPU, a triangle-free-looking finest graph (matching
+  // skeleton level: a triangle-free-looking finest graph (matching
   // merges nothing but the matched edges, so the first coarse level's average
   // degree is ~2*deg0 - 2 > max_deg and coarsening stops there) that is still
   // too large for warp trials (> 32k coarse vertices). The bands are then cut
   // on the finest ids directly: config 4 measured 9.0 -> 6.3 ms, cut +0.2%.
-  if (!K.D.on() && n_glob / 2 > 32768 && 2.0 * deg0 - 2.0 > max_deg &&
-      !getenv("HS_KWAY_COARSEN")) {
+  // Sharded: every rank probes its own rows (neighbours in other shards are
+  // skipped) and the counts are all-reduced, so all ranks decide alike.
+  if (n_glob / 2 > 32768 && 2.0 * deg0 - 2.0 > max_deg && !getenv("HS_KWAY_COARSEN")) {
     unsigned long long *pr, h[2] = {0, 0};
     HS_CHECK_CUDA(dalloc(&pr, 2, s));
     HS_CHECK_CUDA(cudaMemsetAsync(pr, 0, 16, s));
     const int stride = std::max(1, n_glob / 16384);
     locality_probe<<<hs::sm_count() * 4, 256, 0, s>>>(L0.g, stride, pr);
     HS_CHECK_LAUNCH();
+    int rcp = K.ar({Kway::seg64((int64_t *)pr, 2)});
+    if (rcp) return rcp;
     HS_CHECK_CUDA(cudaMemcpyAsync(h, pr, 16, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
     cudaFreeAsync(pr, s);
