@@ -1563,7 +1563,6 @@ struct Kway {
       {
         // per vertex: xbeg 8, deg 4, vw 4, own part 1, state write 4; per
         // entry: adj 4, weight 4 (none when uniform), neighbour part 1
-        hs::Prof P("refine_candidates", s, 21.0 * g.n + (wconst ? 5.0 : 9.0) * g.nnz);
         const int TR = k <= 16 ? refine_team_for(g) : team_for(g);
         if (use_cache && pass > 0) {
           hs::Prof P2("refine_cached", s, (5.0 + cache.cw * cache.kc + 4.0) * g.n);
@@ -1578,6 +1577,8 @@ struct Kway {
           }
 #undef HS_RC
         } else {
+          hs::Prof P("refine_candidates", s, 21.0 * g.n + (wconst ? 5.0 : 9.0) * g.nnz +
+                                                 (use_cache ? (double)cache.cw * cache.kc * g.n : 0.0));
           HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, pl, k, d_pw, d_hi, d_lo, st,
                              list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst,
                              use_cache ? cache : Conn());

@@ -28,28 +28,24 @@ for w in $WHAT; do
         --profile-from-start off -o $O/kway_l0_$TAG -f python tools/ncu_kway.py \
         > $O/ncu_kway_$TAG.log 2>&1
       echo "ncu level0 rc=$?"
-      HS_NCU_COARSEN0=1 timeout 900 ncu --set full --clock-control none --import-source on \
-        --profile-from-start off -o $O/kway_c0_$TAG -f python tools/ncu_kway.py \
-        > $O/ncu_kwayc_$TAG.log 2>&1
-      echo "ncu coarsen0 rc=$?"
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sym_fill|cut_" \
-        -c 2 -o $O/kway_sc_$TAG -f python tools/ncu_kway.py > $O/ncu_kways_$TAG.log 2>&1
-      echo "ncu sym/cut rc=$?"
+      timeout 900 ncu --set full --clock-control none --import-source on \
+        -k regex:"sym_fill|cut_|edge_pairs|split_pairs|ptr_from_keys|locality" \
+        -c 8 -o $O/kway_sc_$TAG -f python tools/ncu_kway.py > $O/ncu_kways_$TAG.log 2>&1
+      echo "ncu sym/cut/transpose rc=$?"
       python tools/ncu_summary.py $O/ncu_summary_$TAG.json \
         refine_candidates=$O/kway_l0_$TAG.ncu-rep:refine_cand_t \
         refine_cached=$O/kway_l0_$TAG.ncu-rep:refine_cached \
         refine_afterburner=$O/kway_l0_$TAG.ncu-rep:afterburner \
         apply_list=$O/kway_l0_$TAG.ncu-rep:apply_list \
-        match_propose_r0=$O/kway_c0_$TAG.ncu-rep:propose_t \
-        match_accept=$O/kway_c0_$TAG.ncu-rep:match_accept \
-        build_cmap=$O/kway_c0_$TAG.ncu-rep:build_cmap \
         symmetrize=$O/kway_sc_$TAG.ncu-rep:sym_fill \
         cut=$O/kway_sc_$TAG.ncu-rep:cut_ \
+        transpose_pairs=$O/kway_sc_$TAG.ncu-rep:edge_pairs \
+        locality_probe=$O/kway_sc_$TAG.ncu-rep:locality \
         --launches $O/launches_$TAG.csv > /dev/null 2>&1
       echo "summary rc=$?"; gzip -f $O/launches_$TAG.csv
       ncu -i $O/kway_l0_$TAG.ncu-rep --page source --csv -k regex:afterburner > $O/src_refine_$TAG.csv 2>/dev/null
       ncu -i $O/kway_l0_$TAG.ncu-rep --page details --csv > $O/details_l0_$TAG.csv 2>/dev/null
-      ncu -i $O/kway_c0_$TAG.ncu-rep --page details --csv > $O/details_c0_$TAG.csv 2>/dev/null
+      ncu -i $O/kway_sc_$TAG.ncu-rep --page details --csv > $O/details_sc_$TAG.csv 2>/dev/null
       gzip -f $O/src_refine_$TAG.csv $O/details_*_$TAG.csv
       ls -la $O
       rm -f $O/kway_*_$TAG.ncu-rep ;;
