@@ -1241,6 +1241,7 @@ struct Kway {
   // beat 4 + 4 on both time and cut (over-refined coarse levels trap the
   // finest level in a worse local optimum)
   int passes_big = 4, passes_small = 8, passes_coarse = 1, rounds = 3;
+  bool passes_env = false;
   double max_deg = 1e30;  // coarsening stop threshold (average degree)
   // connectivity cache of the level being refined (one GPU, k <= 16):
   // cache[v][q] = weight of v's edges into part q, kc = 8 or 16 ints per row
@@ -1355,7 +1356,7 @@ struct Kway {
     r.p[0] = nullptr;
   }
   Kway(cudaStream_t st) : s(st), timer(st) {
-    if (const char *e = getenv("HS_KWAY_PASSES")) passes_big = std::max(1, atoi(e));
+    if (const char *e = getenv("HS_KWAY_PASSES")) passes_big = std::max(1, atoi(e)), passes_env = true;
     if (const char *e = getenv("HS_KWAY_PASSES_COARSE")) passes_coarse = std::max(0, atoi(e));
     if (const char *e = getenv("HS_KWAY_ROUNDS")) rounds = std::max(1, atoi(e));
   }
@@ -1508,7 +1509,15 @@ struct Kway {
     if (rc) return rc;
     const int T = team_for(g);
     const int tgrid = team_grid(g.n, T);
-    int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big : passes_small;
+    // one GPU, list-based afterburner: thin candidates before evaluating them
+    // (the sharded path keeps thinning after; its st is replicated). A pass
+    // then costs ~0.6 ms instead of ~1.1 ms on config 4, so the finest level
+    // gets one pass more (5: cut within 0.2% of 4 unthinned passes, 6.2 vs
+    // 6.4 ms; 6 passes: 0.5% lower cut at 6.8 ms).
+    static const int prethin_env = getenv("HS_KWAY_PRETHIN") ? atoi(getenv("HS_KWAY_PRETHIN")) : 1;
+    const bool prethin = prethin_env && !D.on() && !getenv("HS_KWAY_DSM");
+    int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big + (prethin && !passes_env ? 1 : 0)
+                                               : passes_small;
     if (!finest && passes_coarse >= 0) max_passes = passes_coarse;
     // An unmerged level has as many entries as the level below it: a pass
     // there costs a full fine pass and only moves whole pairs, which the fine
@@ -1557,6 +1566,8 @@ struct Kway {
     if (use_dsm) HS_CHECK_CUDA(dalloc(&d_bm, bm_words, s));
     const int32_t one = 1;
     HS_CHECK_CUDA(cudaMemcpyAsync(ctl + CTL_ACTIVE, &one, sizeof one, cudaMemcpyHostToDevice, s));
+    int32_t *kept = nullptr;
+    if (prethin) HS_CHECK_CUDA(dalloc(&kept, g.n, s));
     for (int pass = 0; pass < max_passes; ++pass) {
       HS_CHECK_CUDA(cudaMemsetAsync(ctl, 0, 2 * sizeof(int32_t), s));  // list count, nconf
       HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
@@ -1606,14 +1617,38 @@ struct Kway {
               list, ctl + CTL_COUNT, d_bm);
           HS_CHECK_LAUNCH();
         }
+        if (prethin) {  // pre-plan: thin the candidates to the balance room first
+          HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
+          const int fg = hs::grid_for(g.n, 256, hs::sm_count() * 4);
+          if (k <= 8)
+            cand_flows_reg<8><<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
+                                                 ctl + CTL_ACTIVE);
+          else if (k <= 16)
+            cand_flows_reg<16><<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
+                                                  ctl + CTL_ACTIVE);
+          else
+            cand_flows<<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
+                                          ctl + CTL_ACTIVE);
+          HS_CHECK_LAUNCH();
+          plan_kernel<<<1, kMaxParts, 0, s>>>(k, Lv.n_glob, 2, d_flows, d_pw, d_hi, d_lo,
+                                              d_target, d_prob, ctl);
+          HS_CHECK_LAUNCH();
+          HS_CHECK_CUDA(cudaMemsetAsync(ctl + CTL_KEPT, 0, sizeof(int32_t), s));
+          thin_cands<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
+              loc(st), list, ctl + CTL_COUNT, d_prob, k, salt2 ^ (0xA5A5ull + pass * 7877),
+              ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT);
+          HS_CHECK_LAUNCH();
+          HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
+        }
         hs::Prof P("refine_afterburner", s, ab_bytes);
         if (use_dsm) {
           rc = launch_afterburner_dsm(g, loc(st), list, conf, d_bm, bm_words);
           if (rc) return rc;
         } else {
           const int TA = after_team_for(g);
-          HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), list,
-                           ctl + CTL_COUNT, k, conf, d_flows, ctl + CTL_NCONF, ctl + CTL_ACTIVE);
+          HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), prethin ? kept : list,
+                           ctl + (prethin ? CTL_KEPT : CTL_COUNT), k, conf, d_flows,
+                           ctl + CTL_NCONF, ctl + CTL_ACTIVE);
         }
       }
       HS_CHECK_LAUNCH();
@@ -1624,11 +1659,23 @@ struct Kway {
       HS_CHECK_LAUNCH();
       int64_t *tgt = apply_target();
       apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
-          list, ctl + CTL_COUNT, conf, g.vw, d_prob, k, salt2 + pass * 104729, g.v0, pl, part,
+          prethin ? kept : list, ctl + (prethin ? CTL_KEPT : CTL_COUNT), conf, g.vw, d_prob, k,
+          salt2 + pass * 104729, g.v0, pl, part,
           tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g, use_cache ? cache : Conn());
       HS_CHECK_LAUNCH();
       rc = ar_applied();
       if (rc) return rc;
+      if (timer.on && finest) {  // HS_KWAY_TRACE: candidates / confirmed / thinning per pass
+        int32_t c2[11];
+        double pr[2 * kMaxParts];
+        cudaMemcpyAsync(c2, ctl, sizeof c2, cudaMemcpyDeviceToHost, s);
+        cudaMemcpyAsync(pr, d_prob, 2 * k * sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        double pmin = 1.0;
+        for (int q = 0; q < 2 * k; ++q) pmin = std::min(pmin, pr[q]);
+        fprintf(stderr, "[kway] pass %d: candidates %d kept %d confirmed %d min keep-prob %.3f\n",
+                pass, c2[0], prethin ? c2[CTL_KEPT] : c2[0], c2[1], pmin);
+      }
     }
     rc = rebalance(g, part, cand, salt2 ^ 0x5555ull, 8, use_cache ? cache : Conn());
     if (!use_cache || !finest) cache = Conn();  // only the finest level's cache is kept (final cut)
@@ -1642,6 +1689,7 @@ struct Kway {
     D.bump = arena_mark;
     cudaFreeAsync(list, s);
     cudaFreeAsync(conf, s);
+    if (kept) cudaFreeAsync(kept, s);
     return rc;
   }
 

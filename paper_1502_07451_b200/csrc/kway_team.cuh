@@ -395,8 +395,9 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
     const int64_t i = ib + (threadIdx.x & 31) / T;
     const bool valid = i < total;
     int delta = 0, v = 0, dest = -1, own = 0;
-    if (valid) {
-      v = list[i];
+    if (valid) v = list[i];
+    const bool live = valid && v >= 0;  // v < 0: dropped by the pre-plan thinning
+    if (live) {
       const uint32_t sv = st[g.v0 + v];
       dest = st_cand(sv);
       own = st_part(sv);
@@ -430,7 +431,7 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
     }
     delta = team_sum<T>(delta);
     if (valid && lane == 0) {
-      const bool ok = delta > 0;
+      const bool ok = live && delta > 0;
       conf[i] = ok ? dest : -1;
       if (ok) {
         const unsigned long long w = (unsigned long long)g.vw[v];
@@ -445,6 +446,106 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
   for (int p = threadIdx.x; p < 2 * k; p += blockDim.x)
     if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
   if (threadIdx.x == 0 && s_n) atomicAdd(nconf, s_n);
+}
+
+// Pre-plan of a refinement pass (one GPU): the part flows every candidate
+// would cause, before the afterburner... k <= KC: per-thread register
+// counters (selects, no indexing), warp-reduced, one shared atomic per warp
+// and counter (shared atomics on k addresses serialised: 0.25 ms a pass).
+template <int KC>
+__global__ void __launch_bounds__(256) cand_flows_reg(const uint32_t *st, const int32_t *list,
+                                                      const int32_t *count, const int32_t *vw,
+                                                      int k, int64_t *flows, const int32_t *run) {
+  if (run && !*run) return;
+  __shared__ unsigned long long sf[2 * KC];
+  for (int p = threadIdx.x; p < 2 * KC; p += blockDim.x) sf[p] = 0;
+  __syncthreads();
+  unsigned long long out[KC], in[KC];
+#pragma unroll
+  for (int q = 0; q < KC; ++q) out[q] = in[q] = 0;
+  const int total = *count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = list[i];
+    const uint32_t sv = st[v];
+    const unsigned long long w = (unsigned long long)vw[v];
+    const int own = st_part(sv), dest = st_cand(sv);
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      out[q] += own == q ? w : 0ull;
+      in[q] += dest == q ? w : 0ull;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < KC; ++q) {
+    for (int off = 16; off; off >>= 1) {
+      out[q] += __shfl_down_sync(0xffffffffu, out[q], off);
+      in[q] += __shfl_down_sync(0xffffffffu, in[q], off);
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      if (out[q]) atomicAdd(&sf[q], out[q]);
+      if (in[q]) atomicAdd(&sf[KC + q], in[q]);
+    }
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < k; p += blockDim.x) {
+    if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
+    if (sf[KC + p]) atomicAdd((unsigned long long *)&flows[k + p], sf[KC + p]);
+  }
+}
+
+__global__ void cand_flows(const uint32_t *st, const int32_t *list, const int32_t *count,
+                           const int32_t *vw, int k, int64_t *flows, const int32_t *run) {
+  if (run && !*run) return;
+  __shared__ unsigned long long sf[2 * kMaxParts];
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) sf[p] = 0;
+  __syncthreads();
+  const int total = *count;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int v = list[i];
+    const uint32_t sv = st[v];
+    const unsigned long long w = (unsigned long long)vw[v];
+    atomicAdd(&sf[st_part(sv)], w);
+    atomicAdd(&sf[k + st_cand(sv)], w);
+  }
+  __syncthreads();
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x)
+    if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
+}
+
+// ...and the thinning it implies, applied to the candidates themselves: a
+// candidate is kept with probability prob[own] * prob[k + dest] (hash coin of
+// (salt, v)); a dropped one loses its candidate mark (neighbours see it stay),
+// kept ones are compacted into kept[] (order irrelevant: the afterburner and
+// apply work per entry), so the afterburner neither evaluates dropped moves
+// nor assumes they happen.
+__global__ void thin_cands(uint32_t *st, const int32_t *list, const int32_t *count,
+                           const double *prob, int k, uint64_t salt, const int32_t *run,
+                           int32_t *kept, int32_t *kept_count) {
+  if (run && !*run) return;
+  __shared__ double s_prob[2 * kMaxParts];
+  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) s_prob[p] = prob[p];
+  __syncthreads();
+  const int total = *count;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += stride) {
+    const int64_t i = base + threadIdx.x;  // block-uniform trip count (block_append)
+    int v = -1;
+    bool keep = false;
+    if (i < total) {
+      v = list[i];
+      const uint32_t sv = st[v];
+      const double pr = s_prob[st_part(sv)] * s_prob[k + st_cand(sv)];
+      keep = pr >= 1.0 ||
+             (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) < pr * 4294967296.0;
+      if (!keep) st[v] = sv & 127u;  // own part, no candidate
+    }
+    block_append(keep, v, kept, kept_count);
+  }
 }
 
 // ---- afterburner over a cluster-distributed candidate bitmap ----------------
@@ -799,7 +900,8 @@ inline int after_team_for(const G &g) {
 // ctl layout (int32): [0] list count, [1] confirmed/planned moves,
 // [2] ACTIVE (refinement continues), [3] APPLY (this pass applies moves),
 // [4] passes done, [5] OVER (some part above its bound), [6] unused.
-enum { CTL_COUNT = 0, CTL_NCONF = 1, CTL_ACTIVE = 2, CTL_APPLY = 3, CTL_PASSES = 4, CTL_OVER = 5 };
+enum { CTL_COUNT = 0, CTL_NCONF = 1, CTL_ACTIVE = 2, CTL_APPLY = 3, CTL_PASSES = 4, CTL_OVER = 5,
+       CTL_KEPT = 10 };
 
 // mode 0 (refine): thinning keeps the expected post-move weight of every
 // part inside [lo, hi]; refinement stops once < 0.5% of vertices improve.
@@ -809,11 +911,11 @@ __global__ void plan_kernel(int k, int n, int mode, const int64_t *flows, const 
                             const int64_t *hi, const int64_t *lo, const int64_t *target,
                             double *prob, int32_t *ctl) {
   const int p = threadIdx.x;
-  const bool gate = mode == 0 ? ctl[CTL_ACTIVE] != 0 : ctl[CTL_OVER] != 0;
+  const bool gate = mode != 1 ? ctl[CTL_ACTIVE] != 0 : ctl[CTL_OVER] != 0;
   const int nconf = ctl[CTL_NCONF];
   __syncthreads();
   if (!gate) {
-    if (p == 0) ctl[CTL_APPLY] = 0;
+    if (p == 0 && mode != 2) ctl[CTL_APPLY] = 0;
     return;
   }
   if (p < k) {
@@ -830,7 +932,7 @@ __global__ void plan_kernel(int k, int n, int mode, const int64_t *flows, const 
     prob[p] = fmax(0.0, po);
     prob[k + p] = fmax(0.0, pi);
   }
-  if (p == 0) {
+  if (p == 0 && mode != 2) {  // mode 2: pre-plan, probabilities only
     ctl[CTL_APPLY] = nconf > 0;
     if (mode == 0) {
       if (nconf > 0) ctl[CTL_PASSES] += 1;
