@@ -1511,12 +1511,13 @@ struct Kway {
     const int tgrid = team_grid(g.n, T);
     // one GPU, list-based afterburner: thin candidates before evaluating them
     // (the sharded path keeps thinning after; its st is replicated). A pass
-    // then costs ~0.6 ms instead of ~1.1 ms on config 4, so the finest level
-    // gets one pass more (5: cut within 0.2% of 4 unthinned passes, 6.2 vs
-    // 6.4 ms; 6 passes: 0.5% lower cut at 6.8 ms).
+    // then costs ~0.4 ms instead of ~1.1 ms on config 4, so the finest level
+    // gets two passes more. Measured (ms, cut): 4 (4.67, 1,339.9M),
+    // 5 (5.07, 1,328.5M), 6 (5.48, 1,320.1M), 7 (5.80, 1,314.1M),
+    // 8 (6.10, 1,309.7M); 4 unthinned passes were (6.38, 1,326.6M).
     static const int prethin_env = getenv("HS_KWAY_PRETHIN") ? atoi(getenv("HS_KWAY_PRETHIN")) : 1;
     const bool prethin = prethin_env && !D.on() && !getenv("HS_KWAY_DSM");
-    int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big + (prethin && !passes_env ? 1 : 0)
+    int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big + (prethin && !passes_env ? 2 : 0)
                                                : passes_small;
     if (!finest && passes_coarse >= 0) max_passes = passes_coarse;
     // An unmerged level has as many entries as the level below it: a pass
