@@ -373,6 +373,61 @@ __device__ __forceinline__ void cache_move_warp(const G &g, const Conn &cache, i
   }
 }
 
+// The same, flattened: the warp's moved vertices' neighbour lists are one
+// sequence (prefix of degrees in shared memory), so every lane works on every
+// step and the adjacency loads of different vertices overlap instead of
+// running vertex by vertex.
+struct MoveScratch {
+  int64_t b[8][32];
+  int pre[8][32];
+  int od[8][32];
+};
+__device__ __forceinline__ void cache_move_flat(const G &g, const Conn &cache, int v, int own,
+                                                int dest, MoveScratch &ms) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int d = 0;
+  int64_t b = 0;
+  if (v >= 0) {
+    b = g.xbeg[v];
+    d = g.deg[v];
+  }
+  int inc = d;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int x = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += x;
+  }
+  const int tot = __shfl_sync(0xffffffffu, inc, 31);
+  if (tot == 0) return;
+  ms.b[w][lane] = b;
+  ms.pre[w][lane] = inc - d;
+  ms.od[w][lane] = (own << 16) | (dest & 0xffff);
+  __syncwarp();
+  for (int f = lane; f < tot; f += 32) {
+    int t = 0;
+    for (int st = 16; st; st >>= 1)
+      if (ms.pre[w][t + st] <= f) t += st;
+    const int64_t j = ms.b[w][t] + (f - ms.pre[w][t]);
+    const int od = ms.od[w][t];
+    cache.move(__ldg(g.adj + j) - g.v0, od >> 16, od & 0xffff, g.ew(j));
+  }
+  __syncwarp();
+}
+
+// Warp-aggregated s[key] += val over the lanes with key >= 0 (one shared
+// atomic per distinct key instead of one per lane; |partial sums| < 2^31
+// because the total vertex weight is).
+__device__ __forceinline__ void warp_add_by_key(long long *s, int key, int val) {
+  unsigned rem = __ballot_sync(0xffffffffu, key >= 0);
+  while (rem) {
+    const int src = __ffs(rem) - 1;
+    const int kk = __shfl_sync(0xffffffffu, key, src);
+    const unsigned grp = __ballot_sync(0xffffffffu, key == kk);
+    const int sum = __reduce_add_sync(0xffffffffu, key == kk ? val : 0);
+    if ((threadIdx.x & 31) == src) atomicAdd((unsigned long long *)&s[kk], (unsigned long long)(long long)sum);
+    rem &= ~grp;
+  }
+}
+
 // Jet-style afterburner over the candidate list: a move survives only if it
 // still gains assuming every higher-priority (gain, then smaller id)
 // neighbouring candidate moved. Confirmed moves land in conf[i] and in the
@@ -671,6 +726,7 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
+  __shared__ MoveScratch ms;  // 256 threads = 8 warps
   for (int p = threadIdx.x; p < k; p += blockDim.x) s[p] = 0;
   for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) s_prob[p] = prob[p];
   __syncthreads();
@@ -687,14 +743,16 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
       if (pr < 1.0 && (double)mix32(salt ^ (gv * 0x9E3779B97F4A7C15ull)) >= pr * 4294967296.0)
         v = -1;
     }
+    int wv = 0;
     if (v >= 0) {
       prep.put(v0 + v, (part_t)dest);
       if (gp)  // keep the ghost copies in the neighbours' lists current
         for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
-      atomicAdd((unsigned long long *)&s[dest], (unsigned long long)(long long)vw[v]);
-      atomicAdd((unsigned long long *)&s[own], (unsigned long long)(-(long long)vw[v]));
+      wv = vw[v];
     }
-    if (cache.p) cache_move_warp(g, cache, v, own, dest);
+    warp_add_by_key(s, v >= 0 ? dest : -1, wv);
+    warp_add_by_key(s, v >= 0 ? own : -1, -wv);
+    if (cache.p) cache_move_flat(g, cache, v, own, dest, ms);
   }
   __syncthreads();
   for (int p = threadIdx.x; p < k; p += blockDim.x)
