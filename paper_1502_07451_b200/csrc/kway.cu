@@ -1591,9 +1591,19 @@ struct Kway {
         } else {
           hs::Prof P("refine_candidates", s, 21.0 * g.n + (wconst ? 5.0 : 9.0) * g.nnz +
                                                  (use_cache ? (double)cache.cw * cache.kc * g.n : 0.0));
+          // pass 0 on a band start (no coarsening, no trials): neighbour parts
+          // from the band bounds, no gathers (the device flag rejects other starts)
+          int32_t *bands = nullptr;
+          if (pass == 0 && finest && !D.on() && !gp && levels.size() == 1) {
+            HS_CHECK_CUDA(dalloc(&bands, k + 2, s));
+            HS_CHECK_CUDA(cudaMemsetAsync(bands + k + 1, 1, sizeof(int32_t), s));
+            band_starts<<<hs::grid_for(g.n, 256), 256, 0, s>>>(g.n, pl, k, bands);
+            HS_CHECK_LAUNCH();
+          }
           HS_REFINE_DISPATCH(TR, k, pack16, team_grid(g.n, TR), g, pl, k, d_pw, d_hi, d_lo, st,
                              list, ctl + CTL_COUNT, ctl + CTL_ACTIVE, gp, wconst,
-                             use_cache ? cache : Conn());
+                             use_cache ? cache : Conn(), bands);
+          if (bands) cudaFreeAsync(bands, s);
         }
       }
       HS_CHECK_LAUNCH();

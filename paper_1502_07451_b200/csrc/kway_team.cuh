@@ -103,8 +103,36 @@ template <int T, int KR, int U = 4>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
-              const int32_t *run, const part_t *gp, int32_t wconst, Conn cache) {
+              const int32_t *run, const part_t *gp, int32_t wconst, Conn cache,
+              const int32_t *bands) {
   if (run && !*run) return;
+  // bands (optional): the partition is still id-range bands (bands[q] = first
+  // global id of part q, bands[k+1] != 0 when that holds): a neighbour's part
+  // is then a 6-step search in shared memory instead of a gather
+  __shared__ int32_t s_band[kMaxParts + 1];
+  __shared__ int s_use_bands;
+  if (threadIdx.x == 0) s_use_bands = bands != nullptr && bands[k + 1] != 0;
+  if (bands)
+    for (int p = threadIdx.x; p <= k; p += blockDim.x) s_band[p] = bands[p];
+  __syncthreads();
+  const bool use_bands = s_use_bands != 0;
+  // k <= 8: the bounds live in registers and a part is a sum of 7 compares
+  int kb[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) kb[q] = (use_bands && q < k && k <= 8) ? s_band[q] : INT_MAX;
+  auto part_of = [&](int u) -> int {
+    if (!use_bands) return (int)__ldg(part + u);
+    if (k <= 8) {
+      int q = 0;
+#pragma unroll
+      for (int i = 1; i < 8; ++i) q += u >= kb[i];
+      return q;
+    }
+    int q = 0;
+    for (int st2 = 32; st2; st2 >>= 1)
+      if (q + st2 < k && s_band[q + st2] <= u) q += st2;
+    return q;
+  };
   __shared__ int32_t conn_s[KR != 0 ? 1 : kTeamBlock / T][kMaxParts];
   // KR < 0: per-lane private counters, [part][thread] so every lane hits its
   // own bank; zeroed here and re-zeroed by the lanes that reduce them
@@ -158,7 +186,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
             w[q] = j < d ? g.ew(b + j) : 0;
           }
 #pragma unroll
-          for (int q = 0; q < U; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : -1;
+          for (int q = 0; q < U; ++q) p[q] = u[q] >= 0 ? part_of(u[q]) : -1;
         }
 #pragma unroll
         for (int q = 0; q < U; ++q)
@@ -175,6 +203,11 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       __syncwarp();
       // lane handles parts lane, lane + T, ...: team total, then re-zero
       const bool can = valid && bnd && s_pw[own] - vwv >= s_lo[own];
+      // 8-byte rows (8 one-byte counters, config 4): the team assembles the
+      // row in registers and one lane stores it (one 8-byte store instead of
+      // eight byte stores per vertex)
+      const bool row8 = cache.p && cache.kc * cache.cw == 8 && cache.cw == 1;
+      unsigned long long row = 0;
       for (int q = lane; q < k; q += T) {
         int cq = 0;
         for (int c = 0; c < T; ++c) {
@@ -182,11 +215,16 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
           cq += priv_s[q][col];
           priv_s[q][col] = 0;
         }
-        if (cache.p && valid) cache.set(v, q, cq);  // connectivity cache row
+        if (row8) row |= (unsigned long long)(cq & 0xff) << (8 * q);
+        else if (cache.p && valid) cache.set(v, q, cq);  // connectivity cache row
         if (can && q != own && s_pw[q] + vwv <= s_hi[q]) {
           const int gain = cq - cown;
           if (gain > bg) { bg = gain; bp = q; }  // ascending q: ties keep the smaller part
         }
+      }
+      if (row8) {
+        for (int off = T / 2; off; off >>= 1) row |= __shfl_xor_sync(0xffffffffu, row, off, T);
+        if (valid && lane == 0) reinterpret_cast<unsigned long long *>(cache.p)[v] = row;
       }
       __syncwarp();
       team_argmax<T>(bg, bp);
@@ -217,7 +255,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
             w[q] = j < d ? g.ew(b + j) : 0;
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? (int)__ldg(part + u[q]) : own;
+          for (int q = 0; q < 4; ++q) p[q] = u[q] >= 0 ? part_of(u[q]) : own;
         }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -253,7 +291,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       for (int p = lane; p < k; p += T) conn[p] = 0;
       __syncwarp();
       for (int j = lane; j < d; j += T) {
-        int p = part[g.adj[b + j]];
+        int p = part_of(g.adj[b + j]);
         bnd |= p != own;
         atomicAdd(&conn[p], g.ew(b + j));
       }
@@ -501,6 +539,20 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
   for (int p = threadIdx.x; p < 2 * k; p += blockDim.x)
     if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
   if (threadIdx.x == 0 && s_n) atomicAdd(nconf, s_n);
+}
+
+// First id of every part when the parts are non-decreasing in the vertex id
+// (the band start of `range_parts`): bands[q] for q < k, bands[k] = n, and
+// bands[k+1] cleared if some part[v] < part[v-1]. Caller sets bands[k+1] != 0.
+__global__ void band_starts(int n, const part_t *part, int k, int32_t *bands) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int a = v == 0 ? -1 : (int)part[v - 1], b = part[v];
+    if (b < a) bands[k + 1] = 0;
+    for (int q = a + 1; q <= b; ++q) bands[q] = (int32_t)v;
+    if (v == n - 1)
+      for (int q = b + 1; q <= k; ++q) bands[q] = n;
+  }
 }
 
 // Pre-plan of a refinement pass (one GPU): the part flows every candidate
