@@ -1581,7 +1581,8 @@ struct Kway {
           const int cg = hs::grid_for(g.n, kTeamBlock, hs::sm_count() * 16);
 #define HS_RC(KC, CW)                                                                      \
   refine_cached<KC, CW><<<cg, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st, list,     \
-                                                  ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache.p)
+                                                  ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache.p, \
+                                                  prethin ? d_flows : nullptr)
           if (cache.kc == 8) {
             if (cache.cw == 1) HS_RC(8, 1); else if (cache.cw == 2) HS_RC(8, 2); else HS_RC(8, 4);
           } else {
@@ -1629,9 +1630,11 @@ struct Kway {
           HS_CHECK_LAUNCH();
         }
         if (prethin) {  // pre-plan: thin the candidates to the balance room first
-          HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
+          // passes > 0 (cache): refine_cached already summed the flows
+          const bool fused = use_cache && pass > 0;
           const int fg = hs::grid_for(g.n, 256, hs::sm_count() * 4);
-          if (k <= 8)
+          if (fused) {
+          } else if (k <= 8)
             cand_flows_reg<8><<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
                                                  ctl + CTL_ACTIVE);
           else if (k <= 16)
@@ -1640,12 +1643,12 @@ struct Kway {
           else
             cand_flows<<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
                                           ctl + CTL_ACTIVE);
-          HS_CHECK_LAUNCH();
+          if (!fused) HS_CHECK_LAUNCH();
           plan_kernel<<<1, kMaxParts, 0, s>>>(k, Lv.n_glob, 2, d_flows, d_pw, d_hi, d_lo,
                                               d_target, d_prob, ctl);
           HS_CHECK_LAUNCH();
           HS_CHECK_CUDA(cudaMemsetAsync(ctl + CTL_KEPT, 0, sizeof(int32_t), s));
-          thin_cands<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
+          thin_cands<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
               loc(st), list, ctl + CTL_COUNT, d_prob, k, salt2 ^ (0xA5A5ull + pass * 7877),
               ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT);
           HS_CHECK_LAUNCH();
@@ -1669,7 +1672,7 @@ struct Kway {
                                           d_prob, ctl);
       HS_CHECK_LAUNCH();
       int64_t *tgt = apply_target();
-      apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(
+      apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
           prethin ? kept : list, ctl + (prethin ? CTL_KEPT : CTL_COUNT), conf, g.vw, d_prob, k,
           salt2 + pass * 104729, g.v0, pl, part,
           tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g, use_cache ? cache : Conn());

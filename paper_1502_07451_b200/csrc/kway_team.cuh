@@ -321,16 +321,27 @@ template <int KC, int CW>
 __global__ void __launch_bounds__(kTeamBlock)
 refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
-              const int32_t *run, const uint8_t *cache) {
+              const int32_t *run, const uint8_t *cache, int64_t *flows) {
   if (run && !*run) return;
-  __shared__ int64_t s_pw[kMaxParts], s_hi[kMaxParts], s_lo[kMaxParts];
+  // room of every part in 32 bits (total vertex weight < 2^31): a move of
+  // weight w may enter q iff w <= s_in[q] and leave p iff w <= s_out[p]
+  __shared__ int32_t s_in[KC], s_out[KC];
+  __shared__ unsigned long long sf[2 * KC];
   __shared__ int32_t s_app[kTeamBlock / 32][kAppendBuf];
-  for (int p = threadIdx.x; p < k; p += blockDim.x) {
-    s_pw[p] = pw[p];
-    s_hi[p] = hi[p];
-    s_lo[p] = lo[p];
+  auto room = [](int64_t r) -> int32_t {
+    return r < 0 ? -1 : (r > (int64_t)INT32_MAX ? INT32_MAX : (int32_t)r);
+  };
+  for (int p = threadIdx.x; p < KC; p += blockDim.x) {
+    s_in[p] = p < k ? room(hi[p] - pw[p]) : -1;
+    s_out[p] = p < k ? room(pw[p] - lo[p]) : -1;
   }
+  for (int p = threadIdx.x; p < 2 * KC; p += blockDim.x) sf[p] = 0;
   __syncthreads();
+  // flows != nullptr: the pre-plan's candidate flows, fused (register
+  // counters per thread; a thread's partial sums stay below the total weight)
+  uint32_t fo[KC], fi[KC];
+#pragma unroll
+  for (int q = 0; q < KC; ++q) fo[q] = fi[q] = 0;
   WarpAppender app{s_app[threadIdx.x >> 5]};
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < g.n; base += stride) {
@@ -348,12 +359,19 @@ refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
         if (q == own) cown = c[q];
         else if (q < k) other |= c[q];
       }
-      if (other && s_pw[own] - vwv >= s_lo[own]) {
+      if (other && vwv <= s_out[own]) {
 #pragma unroll
         for (int q = 0; q < KC; ++q) {
-          if (q >= k || q == own || s_pw[q] + vwv > s_hi[q]) continue;
+          if (q == own || vwv > s_in[q]) continue;  // s_in = -1 past k
           const int gain = c[q] - cown;
           if (gain > bg) { bg = gain; bp = q; }
+        }
+      }
+      if (flows && bp >= 0 && bg > 0) {
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+          fo[q] += own == q ? (uint32_t)vwv : 0u;
+          fi[q] += bp == q ? (uint32_t)vwv : 0u;
         }
       }
     }
@@ -362,6 +380,25 @@ refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
     app.push(valid && cand >= 0, v, list, count);
   }
   app.flush(list, count);
+  if (flows) {
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      unsigned long long a = fo[q], b = fi[q];
+      for (int off = 16; off; off >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, off);
+        b += __shfl_down_sync(0xffffffffu, b, off);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        if (a) atomicAdd(&sf[q], a);
+        if (b) atomicAdd(&sf[KC + q], b);
+      }
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < k; p += blockDim.x) {
+      if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
+      if (sf[KC + p]) atomicAdd((unsigned long long *)&flows[k + p], sf[KC + p]);
+    }
+  }
 }
 
 // Cut from the connectivity cache: sum over vertices of the weight into other
@@ -635,12 +672,14 @@ __global__ void thin_cands(uint32_t *st, const int32_t *list, const int32_t *cou
                            int32_t *kept, int32_t *kept_count) {
   if (run && !*run) return;
   __shared__ double s_prob[2 * kMaxParts];
+  __shared__ int32_t s_app[8][kAppendBuf];  // 256 threads
   for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) s_prob[p] = prob[p];
   __syncthreads();
+  WarpAppender app{s_app[threadIdx.x >> 5]};
   const int total = *count;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < total; base += stride) {
-    const int64_t i = base + threadIdx.x;  // block-uniform trip count (block_append)
+    const int64_t i = base + threadIdx.x;  // warp-uniform trip count (appender)
     int v = -1;
     bool keep = false;
     if (i < total) {
@@ -651,8 +690,9 @@ __global__ void thin_cands(uint32_t *st, const int32_t *list, const int32_t *cou
              (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) < pr * 4294967296.0;
       if (!keep) st[v] = sv & 127u;  // own part, no candidate
     }
-    block_append(keep, v, kept, kept_count);
+    app.push(keep, v, kept, kept_count);
   }
+  app.flush(kept, kept_count);
 }
 
 // ---- afterburner over a cluster-distributed candidate bitmap ----------------
