@@ -238,38 +238,97 @@ __global__ void __launch_bounds__(256, 8) sym_fill(hs_dag_t g, int kv0, int kv1,
 // search over the chunk's list prefix in shared memory. Same output as
 // sym_fill (the per-vertex order is in-list then out-list).
 constexpr int kSymWarps = 8;
-__global__ void __launch_bounds__(kSymWarps * 32) sym_fill_chunk(
+// Row start of kernel position kv in the undirected graph, without a degree
+// pass or scan: both CSRs are prefix sums already, minus the root's own
+// lists, minus `roots_before` = root edges into nodes < node_of(kv).
+// Assumes no edge into the root (validate()).
+__device__ __forceinline__ int64_t sym_row_start(const hs_dag_t &g, int kv, int64_t roots_before) {
+  const int v = node_of(g, kv);
+  const int r = g.root;
+  int64_t x = (g.in_ptr[v] - g.in_ptr[0]) + (g.out_ptr[v] - g.out_ptr[0]);
+  if (v > r) x -= (g.in_ptr[r + 1] - g.in_ptr[r]) + (g.out_ptr[r + 1] - g.out_ptr[r]);
+  return x - roots_before;
+}
+// Root edges into nodes < v: a lower_bound over the root's sorted out-list,
+// short-cut when v lies past its last target or before its first.
+__device__ __forceinline__ int64_t roots_below(const hs_dag_t &g, int v) {
+  const int64_t rb = g.out_ptr[g.root], re = g.out_ptr[g.root + 1];
+  if (re == rb || g.out_dst[re - 1] < v) return re - rb;
+  if (g.out_dst[rb] >= v) return 0;
+  int64_t lo = rb, hi = re;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (g.out_dst[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo - rb;
+}
+__device__ __forceinline__ int64_t sym_row_start(const hs_dag_t &g, int kv) {
+  return sym_row_start(g, kv, roots_below(g, node_of(g, kv)));
+}
+
+__global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
     hs_dag_t g, int kv0, int kv1, const int32_t *ew, const int32_t *ew_in, const int32_t *nw,
-    const int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw) {
+    int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw) {
   __shared__ int s_ipre[kSymWarps][32], s_opre[kSymWarps][32], s_rs[kSymWarps][32],
       s_ilen[kSymWarps][32];
   __shared__ int64_t s_ib[kSymWarps][32], s_ob[kSymWarps][32], s_pos[kSymWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nl = kv1 - kv0;
   const int64_t nchunks = (nl + 31) / 32;
+  // kv = n-1 (one past the last kernel) maps to node n: the totals
+  int64_t x0 = 0;
+  if (lane == 0) x0 = sym_row_start(g, kv0);
+  x0 = __shfl_sync(0xffffffffu, x0, 0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) xadj[nl] = sym_row_start(g, kv1) - x0;
   for (int64_t c = warp_id_global(); c < nchunks; c += warps_total()) {
     const int li = (int)(c * 32) + lane;
     const int cnt = min(32, nl - (int)(c * 32));
-    int ilen = 0, olen = 0, rsr = INT32_MAX;
+    int ilen = 0, olen = 0, rsr = INT32_MAX, hasr = 0;
+    int64_t ib = 0, ob = 0, rs = -1;
     if (li < nl) {
       const int v = node_of(g, kv0 + li);
-      const int64_t ib = g.in_ptr[v], ie = g.in_ptr[v + 1];
-      const int64_t ob = g.out_ptr[v], oe = g.out_ptr[v + 1];
-      const int64_t rs = root_slot(g, v);
+      ib = g.in_ptr[v];
+      const int64_t ie = g.in_ptr[v + 1];
+      ob = g.out_ptr[v];
+      const int64_t oe = g.out_ptr[v + 1];
+      rs = root_slot(g, v);
       ilen = (int)(ie - ib);
       olen = (int)(oe - ob);
+      hasr = rs >= 0;
       if (rs >= 0) rsr = (int)(rs - ib);
       s_ib[w][lane] = ib;
       s_ob[w][lane] = ob;
-      s_pos[w][lane] = xadj[li];
       s_rs[w][lane] = rsr;
-      s_ilen[w][lane] = ilen - (rs >= 0 ? 1 : 0);
+      s_ilen[w][lane] = ilen - hasr;
       vw[li] = nw[v];
     }
-    int ip = ilen, op = olen;  // inclusive scans
+    // the chunk's first row start: root edges below its first node from the
+    // first lane that has one (its in_eid is its rank among the root's
+    // targets), else one search by lane 0
+    const unsigned rmask = __ballot_sync(0xffffffffu, hasr);
+    int64_t rb = 0;
+    if (rmask) {
+      const int fl = __ffs(rmask) - 1;
+      if (lane == fl) rb = g.in_eid ? (int64_t)g.in_eid[rs] - g.out_ptr[g.root]
+                                    : roots_below(g, node_of(g, kv0 + li));
+      rb = __shfl_sync(0xffffffffu, rb, fl);
+    } else if (lane == 0) {
+      rb = roots_below(g, node_of(g, kv0 + li));
+    }
+    if (!rmask) rb = __shfl_sync(0xffffffffu, rb, 0);
+    int64_t xc = 0;
+    if (lane == 0) xc = sym_row_start(g, kv0 + li, rb) - x0;
+    xc = __shfl_sync(0xffffffffu, xc, 0);
+    int ip = ilen, op = olen, rp = hasr;  // inclusive scans
     for (int o = 1; o < 32; o <<= 1) {
       const int a = __shfl_up_sync(0xffffffffu, ip, o), b = __shfl_up_sync(0xffffffffu, op, o);
-      if (lane >= o) { ip += a; op += b; }
+      const int r2 = __shfl_up_sync(0xffffffffu, rp, o);
+      if (lane >= o) { ip += a; op += b; rp += r2; }
+    }
+    if (li < nl) {
+      const int64_t pos = xc + (ip - ilen) + (op - olen) - (rp - hasr);
+      xadj[li] = pos;
+      s_pos[w][lane] = pos;
     }
     s_ipre[w][lane] = ip - ilen;
     s_opre[w][lane] = op - olen;
@@ -1615,14 +1674,6 @@ struct Kway {
         // instrumented (profiling) steps. Per candidate: list 4, own state 4,
         // xbeg 8, deg 4, vw 4, decision 4; per entry (average degree): adj 4,
         // weight 4 (none when uniform), neighbour state 4.
-        double ab_bytes = 0.0;
-        if (hs::prof_enabled()) {
-          int32_t cnt = 0;
-          cudaMemcpyAsync(&cnt, ctl + CTL_COUNT, 4, cudaMemcpyDeviceToHost, s);
-          cudaStreamSynchronize(s);
-          const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
-          ab_bytes = (double)cnt * (28.0 + avg * (g.wconst ? 8.0 : 12.0));
-        }
         if (use_dsm) {
           HS_CHECK_CUDA(cudaMemsetAsync(d_bm, 0, bm_words * 4, s));
           list_bitmap<<<hs::grid_for(g.n, 256, hs::sm_count() * 8), 256, 0, s>>>(
@@ -1653,6 +1704,14 @@ struct Kway {
               ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT);
           HS_CHECK_LAUNCH();
           HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
+        }
+        double ab_bytes = 0.0;
+        if (hs::prof_enabled()) {
+          int32_t cnt = 0;
+          cudaMemcpyAsync(&cnt, ctl + (prethin ? CTL_KEPT : CTL_COUNT), 4, cudaMemcpyDeviceToHost, s);
+          cudaStreamSynchronize(s);
+          const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
+          ab_bytes = (double)cnt * (28.0 + avg * (g.wconst ? 8.0 : 12.0));
         }
         hs::Prof P("refine_afterburner", s, ab_bytes);
         if (use_dsm) {
@@ -2195,16 +2254,31 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
   HS_REQUIRE(!twin || 2 * g->m < (1ll << 31), HS_ELIMIT, "twin indices need < 2^31 entries");
   cudaStream_t s = (cudaStream_t)stream;
   const int nl = kv1 - kv0;
-  hs::Scratch<int32_t> deg;
-  hs::Scratch<int64_t> deg64;
-  HS_CHECK_CUDA(deg.alloc(nl + 1, s));
-  HS_CHECK_CUDA(deg64.alloc(nl + 1, s));
   // in/out pointers, in_src/out_dst, weights (in + out order), adj+wgt writes
   const double frac = nk ? (double)nl / (double)nk : 0.0;
   // per node: in/out pointers, xadj, node weight read + write; per edge:
   // in_src + out_dst read, two adjacency writes, and with weights the out-
   // and in-order weight reads and two weight writes
   hs::Prof P("symmetrize", s, frac * (32.0 * g->n + (adjwgt_i ? 32.0 : 16.0) * g->m));
+  static const bool chunked = !getenv("HS_KWAY_SYM_TEAM");
+  if (chunked && !twin) {
+    // row starts come from the CSR prefixes (sym_row_start): no degree pass
+    const int64_t chunks = ((int64_t)nl + 31) / 32;
+    const int cgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((int64_t)hs::sm_count() * 8, (chunks + kSymWarps - 1) / kSymWarps));
+    sym_fill_chunk<<<cgrid, kSymWarps * 32, 0, s>>>(*g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i,
+                                                    xadj, adjncy, adjwgt_i, vwgt_i);
+    HS_CHECK_LAUNCH();
+    if (nnz_host) {
+      HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    }
+    return HS_OK;
+  }
+  hs::Scratch<int32_t> deg;
+  hs::Scratch<int64_t> deg64;
+  HS_CHECK_CUDA(deg.alloc(nl + 1, s));
+  HS_CHECK_CUDA(deg64.alloc(nl + 1, s));
   sym_degree<<<hs::grid_for(nl, 256), 256, 0, s>>>(*g, kv0, kv1, deg);
   HS_CHECK_LAUNCH();
   HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nl, 0, sizeof(int64_t), s));
@@ -2214,15 +2288,8 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
   if (rc) return rc;
   static const int TS = getenv("HS_KWAY_TSYM") ? atoi(getenv("HS_KWAY_TSYM")) : 4;  // measured: 4 lanes beat 8 and 2
   const int sgrid = std::max(1, std::min(hs::sm_count() * 32, (nl * TS + 255) / 256));
-  static const bool chunked = !getenv("HS_KWAY_SYM_TEAM");
 #define HS_SYM_ARGS *g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin
-  if (chunked && !twin) {
-    const int64_t chunks = ((int64_t)nl + 31) / 32;
-    const int cgrid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((int64_t)hs::sm_count() * 8, (chunks + kSymWarps - 1) / kSymWarps));
-    sym_fill_chunk<<<cgrid, kSymWarps * 32, 0, s>>>(*g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i,
-                                                    xadj, adjncy, adjwgt_i, vwgt_i);
-  } else if (TS == 2) sym_fill<2><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
+  if (TS == 2) sym_fill<2><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
   else if (TS == 4) sym_fill<4><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
   else sym_fill<8><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
 #undef HS_SYM_ARGS
