@@ -238,6 +238,7 @@ __global__ void __launch_bounds__(256, 8) sym_fill(hs_dag_t g, int kv0, int kv1,
 // search over the chunk's list prefix in shared memory. Same output as
 // sym_fill (the per-vertex order is in-list then out-list).
 constexpr int kSymWarps = 8;
+constexpr int kSymOwnCap = 768;   // per warp and list kind: entries of a 32-vertex chunk
 // Row start of kernel position kv in the undirected graph, without a degree
 // pass or scan: both CSRs are prefix sums already, minus the root's own
 // lists, minus `roots_before` = root edges into nodes < node_of(kv).
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
   __shared__ int s_ipre[kSymWarps][32], s_opre[kSymWarps][32], s_rs[kSymWarps][32],
       s_ilen[kSymWarps][32];
   __shared__ int64_t s_ib[kSymWarps][32], s_ob[kSymWarps][32], s_pos[kSymWarps][32];
+  __shared__ uint8_t s_own[kSymWarps][2][kSymOwnCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nl = kv1 - kv0;
   const int64_t nchunks = (nl + 31) / 32;
@@ -333,11 +335,23 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
     s_ipre[w][lane] = ip - ilen;
     s_opre[w][lane] = op - olen;
     const int tin = __shfl_sync(0xffffffffu, ip, 31), tout = __shfl_sync(0xffffffffu, op, 31);
+    // owner map (entry -> lane) when the chunk's lists fit: each lane marks
+    // its own ranges once instead of every entry searching the prefix
+    const bool own_map = tin <= kSymOwnCap && tout <= kSymOwnCap;
+    if (own_map && li < nl) {
+      const int a = ip - ilen, b = op - olen;
+      for (int r = 0; r < ilen; ++r) s_own[w][0][a + r] = (uint8_t)lane;
+      for (int r = 0; r < olen; ++r) s_own[w][1][b + r] = (uint8_t)lane;
+    }
     __syncwarp();
     for (int f = lane; f < tin; f += 32) {
       int t = 0;
-      for (int st = 16; st; st >>= 1)
-        if (t + st < cnt && s_ipre[w][t + st] <= f) t += st;
+      if (own_map) {
+        t = s_own[w][0][f];
+      } else {
+        for (int st = 16; st; st >>= 1)
+          if (t + st < cnt && s_ipre[w][t + st] <= f) t += st;
+      }
       const int r = f - s_ipre[w][t];
       const int rs = s_rs[w][t];
       if (r == rs) continue;
@@ -349,8 +363,12 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
     }
     for (int f = lane; f < tout; f += 32) {
       int t = 0;
-      for (int st = 16; st; st >>= 1)
-        if (t + st < cnt && s_opre[w][t + st] <= f) t += st;
+      if (own_map) {
+        t = s_own[w][1][f];
+      } else {
+        for (int st = 16; st; st >>= 1)
+          if (t + st < cnt && s_opre[w][t + st] <= f) t += st;
+      }
       const int r = f - s_opre[w][t];
       const int64_t j = s_ob[w][t] + r;
       const int64_t at = s_pos[w][t] + s_ilen[w][t] + r;
