@@ -270,9 +270,9 @@ __device__ __forceinline__ int64_t sym_row_start(const hs_dag_t &g, int kv) {
 __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
     hs_dag_t g, int kv0, int kv1, const int32_t *ew, const int32_t *ew_in, const int32_t *nw,
     int64_t *xadj, int32_t *adj, int32_t *wgt, int32_t *vw) {
-  __shared__ int s_ipre[kSymWarps][32], s_opre[kSymWarps][32], s_rs[kSymWarps][32],
-      s_ilen[kSymWarps][32];
-  __shared__ int64_t s_ib[kSymWarps][32], s_ob[kSymWarps][32], s_pos[kSymWarps][32];
+  __shared__ int s_ipre[kSymWarps][32], s_opre[kSymWarps][32], s_rs[kSymWarps][32];
+  __shared__ int64_t s_ib[kSymWarps][32], s_ob[kSymWarps][32], s_pos[kSymWarps][32],
+      s_oat[kSymWarps][32];
   __shared__ uint8_t s_own[kSymWarps][2][kSymOwnCap];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int nl = kv1 - kv0;
@@ -298,10 +298,6 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
       olen = (int)(oe - ob);
       hasr = rs >= 0;
       if (rs >= 0) rsr = (int)(rs - ib);
-      s_ib[w][lane] = ib;
-      s_ob[w][lane] = ob;
-      s_rs[w][lane] = rsr;
-      s_ilen[w][lane] = ilen - hasr;
       vw[li] = nw[v];
     }
     // the chunk's first row start: root edges below its first node from the
@@ -330,8 +326,13 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
     if (li < nl) {
       const int64_t pos = xc + (ip - ilen) + (op - olen) - (rp - hasr);
       xadj[li] = pos;
-      s_pos[w][lane] = pos;
+      // offsets relative to the chunk entry index f of each list kind
+      s_pos[w][lane] = pos - (ip - ilen);                 // in: at = s_pos + f (- 1 past the root slot)
+      s_rs[w][lane] = hasr ? (ip - ilen) + rsr : INT32_MAX;  // f of the root slot
+      s_oat[w][lane] = pos + (ilen - hasr) - (op - olen);  // out: at = s_oat + f
+      s_ob[w][lane] = ob - (op - olen);                  // out: j = s_ob + f
     }
+    if (lane == 0) s_ib[w][0] = ib;  // first in-list start of the chunk
     s_ipre[w][lane] = ip - ilen;
     s_opre[w][lane] = op - olen;
     const int tin = __shfl_sync(0xffffffffu, ip, 31), tout = __shfl_sync(0xffffffffu, op, 31);
@@ -352,11 +353,12 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
         for (int st = 16; st; st >>= 1)
           if (t + st < cnt && s_ipre[w][t + st] <= f) t += st;
       }
-      const int r = f - s_ipre[w][t];
-      const int rs = s_rs[w][t];
-      if (r == rs) continue;
-      const int64_t j = s_ib[w][t] + r;
-      const int64_t at = s_pos[w][t] + r - (r > rs ? 1 : 0);
+      // in-lists of consecutive nodes are one contiguous run (the root has
+      // none): j follows from f; f at the root slot is skipped
+      const int rsf = s_rs[w][t];
+      if (f == rsf) continue;
+      const int64_t j = s_ib[w][0] + f;
+      const int64_t at = s_pos[w][t] + f - (f > rsf ? 1 : 0);
       const int u = g.in_src[j];
       adj[at] = u < g.root ? u : u - 1;
       if (wgt) wgt[at] = ew_in ? ew_in[j] : ew[g.in_eid[j]];
@@ -369,9 +371,8 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
         for (int st = 16; st; st >>= 1)
           if (t + st < cnt && s_opre[w][t + st] <= f) t += st;
       }
-      const int r = f - s_opre[w][t];
-      const int64_t j = s_ob[w][t] + r;
-      const int64_t at = s_pos[w][t] + s_ilen[w][t] + r;
+      const int64_t j = s_ob[w][t] + f;  // out-lists: the root's may sit between
+      const int64_t at = s_oat[w][t] + f;
       const int u = g.out_dst[j];
       adj[at] = u < g.root ? u : u - 1;
       if (wgt) wgt[at] = ew[j];
