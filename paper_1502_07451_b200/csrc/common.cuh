@@ -87,9 +87,16 @@ struct Prof {
       cudaEventRecord(a, s);
     }
   }
+  // stop(): record the end now (e.g. before a host read that determines
+  // `bytes`); the booking happens at destruction
+  bool stopped = false;
+  void stop() {
+    if (a && !stopped) cudaEventRecord(b, s);
+    stopped = true;
+  }
   ~Prof() {
     if (a) {
-      cudaEventRecord(b, s);
+      if (!stopped) cudaEventRecord(b, s);
       prof_record(name, a, b, bytes);
     }
   }

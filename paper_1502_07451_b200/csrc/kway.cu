@@ -1718,10 +1718,20 @@ struct Kway {
                                               d_target, d_prob, ctl);
           HS_CHECK_LAUNCH();
           HS_CHECK_CUDA(cudaMemsetAsync(ctl + CTL_KEPT, 0, sizeof(int32_t), s));
-          thin_cands<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
-              loc(st), list, ctl + CTL_COUNT, d_prob, k, salt2 ^ (0xA5A5ull + pass * 7877),
-              ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT);
-          HS_CHECK_LAUNCH();
+          {
+            hs::Prof P("refine_thin", s, 0.0);
+            thin_cands<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
+                loc(st), list, ctl + CTL_COUNT, d_prob, k, salt2 ^ (0xA5A5ull + pass * 7877),
+                ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT);
+            HS_CHECK_LAUNCH();
+            if (hs::prof_enabled()) {  // per candidate: list + state read, kept or state write
+              P.stop();
+              int32_t c = 0;
+              cudaMemcpyAsync(&c, ctl + CTL_COUNT, 4, cudaMemcpyDeviceToHost, s);
+              cudaStreamSynchronize(s);
+              P.bytes = 12.0 * c;
+            }
+          }
           HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
         }
         double ab_bytes = 0.0;
@@ -1750,11 +1760,28 @@ struct Kway {
                                           d_prob, ctl);
       HS_CHECK_LAUNCH();
       int64_t *tgt = apply_target();
-      apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
-          prethin ? kept : list, ctl + (prethin ? CTL_KEPT : CTL_COUNT), conf, g.vw, d_prob, k,
-          salt2 + pass * 104729, g.v0, pl, part,
-          tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g, use_cache ? cache : Conn());
-      HS_CHECK_LAUNCH();
+      {
+        const bool prof = hs::prof_enabled();
+        if (prof) HS_CHECK_CUDA(cudaMemsetAsync(ctl + CTL_MOVED, 0, sizeof(int32_t), s));
+        hs::Prof P("refine_apply", s, 0.0);
+        apply_list<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
+            prethin ? kept : list, ctl + (prethin ? CTL_KEPT : CTL_COUNT), conf, g.vw, d_prob, k,
+            salt2 + pass * 104729, g.v0, pl, part,
+            tgt, ctl + CTL_APPLY, g.xbeg, g.deg, g.twin, gp, g, use_cache ? cache : Conn(),
+            prof ? ctl + CTL_MOVED : nullptr);
+        HS_CHECK_LAUNCH();
+        if (prof) {  // per entry: list, conf, part read; per move: vw, part write,
+                     // xbeg, deg, then per neighbour: adj entry + a 4-byte
+                     // read-modify-write of its cache row (with the cache)
+          P.stop();
+          int32_t c2[2] = {0, 0};
+          cudaMemcpyAsync(&c2[0], ctl + (prethin ? CTL_KEPT : CTL_COUNT), 4, cudaMemcpyDeviceToHost, s);
+          cudaMemcpyAsync(&c2[1], ctl + CTL_MOVED, 4, cudaMemcpyDeviceToHost, s);
+          cudaStreamSynchronize(s);
+          const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
+          P.bytes = 9.0 * c2[0] + (double)c2[1] * (17.0 + (use_cache ? 12.0 * avg : 0.0));
+        }
+      }
       rc = ar_applied();
       if (rc) return rc;
       if (timer.on && finest) {  // HS_KWAY_TRACE: candidates / confirmed / thinning per pass

@@ -814,7 +814,8 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
                            const int32_t *vw, const double *prob, int k, uint64_t salt,
                            int32_t v0, const part_t *part, Rep<part_t> prep, int64_t *pw,
                            const int32_t *run, const int64_t *xbeg, const int32_t *deg,
-                           const int32_t *twin, part_t *gp, G g, Conn cache) {
+                           const int32_t *twin, part_t *gp, G g, Conn cache,
+                           int32_t *moved) {
   if (run && !*run) return;
   __shared__ long long s[kMaxParts];
   __shared__ double s_prob[2 * kMaxParts];
@@ -841,6 +842,10 @@ __global__ void apply_list(const int32_t *list, const int32_t *count, const int3
       if (gp)  // keep the ghost copies in the neighbours' lists current
         for (int64_t j = xbeg[v], e = xbeg[v] + deg[v]; j < e; ++j) gp[twin[j]] = (part_t)dest;
       wv = vw[v];
+    }
+    if (moved) {  // profiling: applied moves (warp-aggregated)
+      const unsigned mm = __ballot_sync(0xffffffffu, v >= 0);
+      if ((threadIdx.x & 31) == 0 && mm) atomicAdd(moved, __popc(mm));
     }
     warp_add_by_key(s, v >= 0 ? dest : -1, wv);
     warp_add_by_key(s, v >= 0 ? own : -1, -wv);
@@ -1051,7 +1056,7 @@ inline int after_team_for(const G &g) {
 // [2] ACTIVE (refinement continues), [3] APPLY (this pass applies moves),
 // [4] passes done, [5] OVER (some part above its bound), [6] unused.
 enum { CTL_COUNT = 0, CTL_NCONF = 1, CTL_ACTIVE = 2, CTL_APPLY = 3, CTL_PASSES = 4, CTL_OVER = 5,
-       CTL_KEPT = 10 };
+       CTL_KEPT = 10, CTL_MOVED = 11 };
 
 // mode 0 (refine): thinning keeps the expected post-move weight of every
 // part inside [lo, hi]; refinement stops once < 0.5% of vertices improve.
