@@ -106,3 +106,17 @@ def test_unknown_policy_message():
     from paper_1502_07451_b200.policies import build_policy
     with pytest.raises(ValueError, match="unknown policy"):
         build_policy("fifo", make_graph({1: (1.0, 1.0)}, []))
+
+
+def test_unit_weight_ugraph_host_side():
+    """adjwgt=None (uniform edge weights, hs_ugraph_t.adjwgt_i = NULL): the
+    materialised weights and the cut scale the partitioner's result uses."""
+    import torch
+    from paper_1502_07451_b200.kway import UGraph
+    xadj = torch.tensor([0, 2, 3, 4], dtype=torch.int64)
+    adj = torch.tensor([1, 2, 0, 0], dtype=torch.int32)
+    vw = torch.ones(3, dtype=torch.int32)
+    ug = UGraph(xadj, adj, None, vw, unit_weight=37)
+    assert ug.weight_scale == 37 and ug.adjwgt.tolist() == [37] * 4
+    ugw = UGraph(xadj, adj, torch.full((4,), 37, dtype=torch.int32), vw)
+    assert ugw.weight_scale == 1 and torch.equal(ugw.adjwgt, ug.adjwgt)
