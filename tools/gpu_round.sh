@@ -36,7 +36,8 @@ for w in $WHAT; do
         refine_candidates=$O/kway_l0_$TAG.ncu-rep:refine_cand_t \
         refine_cached=$O/kway_l0_$TAG.ncu-rep:refine_cached \
         refine_afterburner=$O/kway_l0_$TAG.ncu-rep:afterburner \
-        apply_list=$O/kway_l0_$TAG.ncu-rep:apply_list \
+        refine_apply=$O/kway_l0_$TAG.ncu-rep:apply_list \
+        refine_thin=$O/kway_l0_$TAG.ncu-rep:thin_cands \
         symmetrize=$O/kway_sc_$TAG.ncu-rep:sym_fill \
         cut=$O/kway_sc_$TAG.ncu-rep:cut_ \
         transpose_pairs=$O/kway_sc_$TAG.ncu-rep:edge_pairs \
