@@ -1587,14 +1587,14 @@ struct Kway {
     if (rc) return rc;
     const int T = team_for(g);
     const int tgrid = team_grid(g.n, T);
-    // one GPU, list-based afterburner: thin candidates before evaluating them
-    // (the sharded path keeps thinning after; its st is replicated). A pass
+    // list-based afterburner: thin candidates before evaluating them (sharded:
+    // flows all-reduced, dropped states stored into every replica). A pass
     // then costs ~0.4 ms instead of ~1.1 ms on config 4, so the finest level
     // gets two passes more. Measured (ms, cut): 4 (4.67, 1,339.9M),
     // 5 (5.07, 1,328.5M), 6 (5.48, 1,320.1M), 7 (5.80, 1,314.1M),
     // 8 (6.10, 1,309.7M); 4 unthinned passes were (6.38, 1,326.6M).
     static const int prethin_env = getenv("HS_KWAY_PRETHIN") ? atoi(getenv("HS_KWAY_PRETHIN")) : 1;
-    const bool prethin = prethin_env && !D.on() && !getenv("HS_KWAY_DSM");
+    const bool prethin = prethin_env && !getenv("HS_KWAY_DSM");
     int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big + (prethin && !passes_env ? 2 : 0)
                                                : passes_small;
     if (!finest && passes_coarse >= 0) max_passes = passes_coarse;
@@ -1706,14 +1706,16 @@ struct Kway {
           if (fused) {
           } else if (k <= 8)
             cand_flows_reg<8><<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
-                                                 ctl + CTL_ACTIVE);
+                                                 ctl + CTL_ACTIVE, g.v0);
           else if (k <= 16)
             cand_flows_reg<16><<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
-                                                  ctl + CTL_ACTIVE);
+                                                  ctl + CTL_ACTIVE, g.v0);
           else
             cand_flows<<<fg, 256, 0, s>>>(loc(st), list, ctl + CTL_COUNT, g.vw, k, d_flows,
-                                          ctl + CTL_ACTIVE);
+                                          ctl + CTL_ACTIVE, g.v0);
           if (!fused) HS_CHECK_LAUNCH();
+          rc = ar_flows();  // sharded: every rank plans with the global flows
+          if (rc) return rc;
           plan_kernel<<<1, kMaxParts, 0, s>>>(k, Lv.n_glob, 2, d_flows, d_pw, d_hi, d_lo,
                                               d_target, d_prob, ctl);
           HS_CHECK_LAUNCH();
@@ -1721,7 +1723,7 @@ struct Kway {
           {
             hs::Prof P("refine_thin", s, 0.0);
             thin_cands<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
-                loc(st), list, ctl + CTL_COUNT, d_prob, k, salt2 ^ (0xA5A5ull + pass * 7877),
+                st, g.v0, list, ctl + CTL_COUNT, d_prob, k, salt2 ^ (0xA5A5ull + pass * 7877),
                 ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT);
             HS_CHECK_LAUNCH();
             if (hs::prof_enabled()) {  // per candidate: list + state read, kept or state write
@@ -1733,6 +1735,8 @@ struct Kway {
             }
           }
           HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
+          rc = barrier();  // dropped candidates' states are in every replica
+          if (rc) return rc;
         }
         double ab_bytes = 0.0;
         if (hs::prof_enabled()) {

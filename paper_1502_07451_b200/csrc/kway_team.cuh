@@ -592,14 +592,15 @@ __global__ void band_starts(int n, const part_t *part, int k, int32_t *bands) {
   }
 }
 
-// Pre-plan of a refinement pass (one GPU): the part flows every candidate
+// Pre-plan of a refinement pass: the part flows every candidate
 // would cause, before the afterburner... k <= KC: per-thread register
 // counters (selects, no indexing), warp-reduced, one shared atomic per warp
 // and counter (shared atomics on k addresses serialised: 0.25 ms a pass).
 template <int KC>
 __global__ void __launch_bounds__(256) cand_flows_reg(const uint32_t *st, const int32_t *list,
                                                       const int32_t *count, const int32_t *vw,
-                                                      int k, int64_t *flows, const int32_t *run) {
+                                                      int k, int64_t *flows, const int32_t *run,
+                                                      int32_t v0) {
   if (run && !*run) return;
   __shared__ unsigned long long sf[2 * KC];
   for (int p = threadIdx.x; p < 2 * KC; p += blockDim.x) sf[p] = 0;
@@ -611,7 +612,7 @@ __global__ void __launch_bounds__(256) cand_flows_reg(const uint32_t *st, const 
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int v = list[i];
-    const uint32_t sv = st[v];
+    const uint32_t sv = st[v0 + v];
     const unsigned long long w = (unsigned long long)vw[v];
     const int own = st_part(sv), dest = st_cand(sv);
 #pragma unroll
@@ -642,7 +643,8 @@ __global__ void __launch_bounds__(256) cand_flows_reg(const uint32_t *st, const 
 }
 
 __global__ void cand_flows(const uint32_t *st, const int32_t *list, const int32_t *count,
-                           const int32_t *vw, int k, int64_t *flows, const int32_t *run) {
+                           const int32_t *vw, int k, int64_t *flows, const int32_t *run,
+                           int32_t v0) {
   if (run && !*run) return;
   __shared__ unsigned long long sf[2 * kMaxParts];
   for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) sf[p] = 0;
@@ -651,7 +653,7 @@ __global__ void cand_flows(const uint32_t *st, const int32_t *list, const int32_
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int v = list[i];
-    const uint32_t sv = st[v];
+    const uint32_t sv = st[v0 + v];
     const unsigned long long w = (unsigned long long)vw[v];
     atomicAdd(&sf[st_part(sv)], w);
     atomicAdd(&sf[k + st_cand(sv)], w);
@@ -667,7 +669,7 @@ __global__ void cand_flows(const uint32_t *st, const int32_t *list, const int32_
 // kept ones are compacted into kept[] (order irrelevant: the afterburner and
 // apply work per entry), so the afterburner neither evaluates dropped moves
 // nor assumes they happen.
-__global__ void thin_cands(uint32_t *st, const int32_t *list, const int32_t *count,
+__global__ void thin_cands(Rep<uint32_t> st, int32_t v0, const int32_t *list, const int32_t *count,
                            const double *prob, int k, uint64_t salt, const int32_t *run,
                            int32_t *kept, int32_t *kept_count) {
   if (run && !*run) return;
@@ -684,11 +686,12 @@ __global__ void thin_cands(uint32_t *st, const int32_t *list, const int32_t *cou
     bool keep = false;
     if (i < total) {
       v = list[i];
-      const uint32_t sv = st[v];
+      const uint32_t sv = st.p[0][v0 + v];
       const double pr = s_prob[st_part(sv)] * s_prob[k + st_cand(sv)];
+      const uint64_t gv = (uint64_t)(v0 + v);
       keep = pr >= 1.0 ||
-             (double)mix32(salt ^ ((uint64_t)v * 0x9E3779B97F4A7C15ull)) < pr * 4294967296.0;
-      if (!keep) st[v] = sv & 127u;  // own part, no candidate
+             (double)mix32(salt ^ (gv * 0x9E3779B97F4A7C15ull)) < pr * 4294967296.0;
+      if (!keep) st.put(gv, sv & 127u);  // own part, no candidate (every replica)
     }
     app.push(keep, v, kept, kept_count);
   }
