@@ -318,7 +318,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
 // edges into part q, kept exact by every applied move): the same choice as
 // refine_cand_t without scanning the adjacency. One thread per vertex.
 template <int KC, int CW>
-__global__ void __launch_bounds__(kTeamBlock)
+__global__ void __launch_bounds__(kTeamBlock, 6)  // <= 40 registers: the loop is latency-bound
 refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
               const int64_t *lo, Rep<uint32_t> st, int32_t *list, int32_t *count,
               const int32_t *run, const uint8_t *cache, int64_t *flows) {
