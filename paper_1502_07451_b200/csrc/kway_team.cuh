@@ -116,6 +116,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
     for (int p = threadIdx.x; p <= k; p += blockDim.x) s_band[p] = bands[p];
   __syncthreads();
   const bool use_bands = s_use_bands != 0;
+  const bool bands_unit = use_bands && k <= 8 && wconst == 1 && gp == nullptr;
   // k <= 8: the bounds live in registers and a part is a sum of 7 compares
   int kb[8];
 #pragma unroll
@@ -168,6 +169,35 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
     }
     if constexpr (KR < 0) {
       const int tcol = threadIdx.x, base_col = threadIdx.x - lane;
+      if (bands_unit) {
+        // band start, unit weights, k <= 8: per-lane suffix counters in
+        // registers (ge[i] = neighbours with id >= band i's start), no
+        // per-entry shared-memory read-modify-write; the part counts go to
+        // the private columns once, so the team reduction below is unchanged
+        int ge[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ge[i] = 0;
+        for (int j0 = lane; j0 < d; j0 += U * T) {
+          int u[U];
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            const int j = j0 + q * T;
+            u[q] = j < d ? __ldg(g.adj + b + j) : -1;
+          }
+#pragma unroll
+          for (int q = 0; q < U; ++q) {
+            ge[0] += u[q] >= 0;
+#pragma unroll
+            for (int i = 1; i < 8; ++i) ge[i] += u[q] >= kb[i];
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int c = ge[q] - (q < 7 ? ge[q + 1] : 0);
+          if (q < k) priv_s[q][tcol] = c;
+          bnd |= (q != own) && c > 0;
+        }
+      } else
       for (int j0 = lane; j0 < d; j0 += U * T) {
         int w[U], p[U];
         if (gp) {
