@@ -1719,12 +1719,11 @@ struct Kway {
           plan_kernel<<<1, kMaxParts, 0, s>>>(k, Lv.n_glob, 2, d_flows, d_pw, d_hi, d_lo,
                                               d_target, d_prob, ctl);
           HS_CHECK_LAUNCH();
-          HS_CHECK_CUDA(cudaMemsetAsync(ctl + CTL_KEPT, 0, sizeof(int32_t), s));
-          {
+          {  // (the pre-plan zeroed the kept count)
             hs::Prof P("refine_thin", s, 0.0);
             thin_cands<<<hs::grid_for(g.n, 256, hs::sm_count() * 16), 256, 0, s>>>(
                 st, g.v0, list, ctl + CTL_COUNT, d_prob, k, salt2 ^ (0xA5A5ull + pass * 7877),
-                ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT);
+                ctl + CTL_ACTIVE, kept, ctl + CTL_KEPT, d_flows);
             HS_CHECK_LAUNCH();
             if (hs::prof_enabled()) {  // per candidate: list + state read, kept or state write
               P.stop();
@@ -1734,7 +1733,6 @@ struct Kway {
               P.bytes = 12.0 * c;
             }
           }
-          HS_CHECK_CUDA(cudaMemsetAsync(d_flows, 0, 2 * k * sizeof(int64_t), s));
           rc = barrier();  // dropped candidates' states are in every replica
           if (rc) return rc;
         }

@@ -701,7 +701,11 @@ __global__ void cand_flows(const uint32_t *st, const int32_t *list, const int32_
 // nor assumes they happen.
 __global__ void thin_cands(Rep<uint32_t> st, int32_t v0, const int32_t *list, const int32_t *count,
                            const double *prob, int k, uint64_t salt, const int32_t *run,
-                           int32_t *kept, int32_t *kept_count) {
+                           int32_t *kept, int32_t *kept_count, int64_t *flows) {
+  // flows (read by the pre-plan, which has finished) are zeroed here for the
+  // afterburner's confirmed-move sums
+  if (blockIdx.x == 0)
+    for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) flows[p] = 0;
   if (run && !*run) return;
   __shared__ double s_prob[2 * kMaxParts];
   __shared__ int32_t s_app[8][kAppendBuf];  // 256 threads
@@ -1120,6 +1124,7 @@ __global__ void plan_kernel(int k, int n, int mode, const int64_t *flows, const 
     prob[p] = fmax(0.0, po);
     prob[k + p] = fmax(0.0, pi);
   }
+  if (p == 0 && mode == 2) ctl[CTL_KEPT] = 0;  // the thinning's list count
   if (p == 0 && mode != 2) {  // mode 2: pre-plan, probabilities only
     ctl[CTL_APPLY] = nconf > 0;
     if (mode == 0) {
