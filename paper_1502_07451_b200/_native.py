@@ -295,11 +295,13 @@ def int32_stats(t: torch.Tensor) -> Tuple[int, int, int]:
 
 
 def symmetrize(csr, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, edge_w_i_in=None,
-               twin=None) -> int:
+               twin=None, read_nnz: bool = True) -> int:
+    """read_nnz=False: no host read of the entry count (returns -1; the caller knows it)."""
     fn = _need(_symmetrize, "hs_symmetrize")
-    nnz = ctypes.c_int64(0)
+    nnz = ctypes.c_int64(-1)
     check(fn(ctypes.byref(csr.struct()), ptr(edge_w_i), ptr(edge_w_i_in), ptr(node_w_i), ptr(xadj),
-             ptr(adjncy), ptr(adjwgt_i), ptr(vwgt_i), ptr(twin), ctypes.byref(nnz), stream_ptr()))
+             ptr(adjncy), ptr(adjwgt_i), ptr(vwgt_i), ptr(twin),
+             ctypes.byref(nnz) if read_nnz else None, stream_ptr()))
     return nnz.value
 
 

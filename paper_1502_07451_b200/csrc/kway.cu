@@ -2434,6 +2434,11 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   int64_t tot[8] = {0, 0, nnz0, INT32_MAX, INT32_MIN, 0, INT32_MAX, INT32_MIN};
   int32_t *deg_l0;
   HS_CHECK_CUDA(dalloc(&deg_l0, n0, s));
+  // locality probe buffers (launched with the totals, read with them)
+  const bool probe_wanted = n_glob / 2 > 32768 && !getenv("HS_KWAY_COARSEN");
+  unsigned long long *probe_dev = nullptr, probe_h[2] = {0, 0};
+  HS_CHECK_CUDA(dalloc(&probe_dev, 2, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(probe_dev, 0, 16, s));
   {
     HS_CHECK_CUDA(cudaMemcpyAsync(tot_dev, tot, sizeof tot, cudaMemcpyHostToDevice, s));
     deg_from_xadj<<<hs::grid_for(n0, 256), 256, 0, s>>>(ug->xadj, n0, deg_l0,
@@ -2459,12 +2464,26 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
     HS_CHECK_LAUNCH();
     widen_minmax<<<1, 1, 0, s>>>(tot_dev + 6);
     HS_CHECK_LAUNCH();
+    // the locality probe (see below) rides on the same host read
+    if (probe_wanted) {
+      HS_CHECK_CUDA(cudaMemsetAsync(probe_dev, 0, 16, s));
+      G pg;
+      pg.n = n0;
+      pg.v0 = v0;
+      pg.xbeg = const_cast<int64_t *>(ug->xadj);
+      pg.deg = deg_l0;
+      pg.adj = const_cast<int32_t *>(ug->adjncy);
+      const int stride = std::max(1, n_glob / 16384);
+      locality_probe<<<hs::sm_count() * 4, 256, 0, s>>>(pg, stride, probe_dev);
+      HS_CHECK_LAUNCH();
+    }
     // sums, then global minima / maxima
     int rc = K.ar({Kway::seg64(tot_dev, 3), Kway::seg64(tot_dev + 3, 1, 2),
                    Kway::seg64(tot_dev + 4, 2, 1), Kway::seg64(tot_dev + 6, 1, 2),
-                   Kway::seg64(tot_dev + 7, 1, 1)});
+                   Kway::seg64(tot_dev + 7, 1, 1), Kway::seg64((int64_t *)probe_dev, 2)});
     if (rc) return rc;
     HS_CHECK_CUDA(cudaMemcpyAsync(tot, tot_dev, sizeof tot, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(probe_h, probe_dev, sizeof probe_h, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
     rc = K.check_peers();
     if (rc) return rc;
@@ -2561,23 +2580,14 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   // on the finest ids directly: config 4 measured 9.0 -> 6.3 ms, cut +0.2%.
   // Sharded: every rank probes its own rows (neighbours in other shards are
   // skipped) and the counts are all-reduced, so all ranks decide alike.
-  if (n_glob / 2 > 32768 && 2.0 * deg0 - 2.0 > max_deg && !getenv("HS_KWAY_COARSEN")) {
-    unsigned long long *pr, h[2] = {0, 0};
-    HS_CHECK_CUDA(dalloc(&pr, 2, s));
-    HS_CHECK_CUDA(cudaMemsetAsync(pr, 0, 16, s));
-    const int stride = std::max(1, n_glob / 16384);
-    locality_probe<<<hs::sm_count() * 4, 256, 0, s>>>(L0.g, stride, pr);
-    HS_CHECK_LAUNCH();
-    int rcp = K.ar({Kway::seg64((int64_t *)pr, 2)});
-    if (rcp) return rcp;
-    HS_CHECK_CUDA(cudaMemcpyAsync(h, pr, 16, cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaStreamSynchronize(s));
-    cudaFreeAsync(pr, s);
+  if (probe_wanted && 2.0 * deg0 - 2.0 > max_deg) {
+    const unsigned long long *h = probe_h;
     if (h[0] > 0 && (double)h[1] < 0.02 * (double)h[0]) stop = true;
     if (K.timer.on)
       fprintf(stderr, "[kway] locality probe: %llu/%llu pairs share a neighbour%s\n", h[1], h[0],
                       stop ? " -> no coarsening" : "");
   }
+  cudaFreeAsync(probe_dev, s);
   if (getenv("HS_KWAY_NOCOARSEN")) stop = true;
   while (!stop && K.levels.back().n_glob > coarse_target && (int)K.levels.size() < 40) {
     if (K.levels.size() > 1) {

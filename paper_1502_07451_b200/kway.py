@@ -61,6 +61,15 @@ class UGraph:
         return self._struct
 
 
+def _root_out_degree(csr: DagCSR) -> int:
+    """Edges leaving the root (one host read per DAG object, then cached)."""
+    d = getattr(csr, "_root_outdeg", None)
+    if d is None:
+        d = int((csr.out_ptr[csr.root + 1] - csr.out_ptr[csr.root]).item())
+        csr._root_outdeg = d
+    return d
+
+
 def _uniform_weight(edge_w_i: torch.Tensor) -> int:
     """The common value of the edge weights if they are all equal and positive, else 0."""
     if edge_w_i.numel() == 0 or os.environ.get("HS_KWAY_WEIGHTS") == "1":
@@ -139,10 +148,14 @@ def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,
     # uniform edge weights (one matrix per transfer): no weight stream at all
     w0 = 0 if want_twin or not unit_ok else _uniform_weight(edge_w_i)
     adjwgt = None if w0 else torch.empty(nnz_cap, dtype=torch.int32, device=dev)
-    nnz = _native.symmetrize(csr, None if w0 else edge_w_i.contiguous(), node_w_i.contiguous(),
+    # entry count = 2 x (edges not leaving the root), cached per DAG: no host
+    # read of it after K1
+    nnz = 2 * (csr.m - _root_out_degree(csr))
+    got = _native.symmetrize(csr, None if w0 else edge_w_i.contiguous(), node_w_i.contiguous(),
                              xadj, adjncy, adjwgt, vwgt,
                              edge_w_i_in.contiguous() if edge_w_i_in is not None and not w0
-                             else None, twin)
+                             else None, twin, read_nnz=False)
+    assert got == -1
     return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz] if adjwgt is not None else None, vwgt,
                   twin[:nnz] if twin is not None else None, unit_weight=w0 or 1)
 
