@@ -1816,7 +1816,10 @@ struct Kway {
 
   // from_cache: the finest level's connectivity cache is current and holds
   // the weights g's cut is taken with (scaled by g.wconst when uniform)
-  int64_t cut_of(const G &g, const part_t *part, bool from_cache = false) {
+  // defer != nullptr: leave the (all-reduced) doubled cut on the device in
+  // *defer for the caller to read with other results (returns 0)
+  int64_t cut_of(const G &g, const part_t *part, bool from_cache = false,
+                 unsigned long long **defer = nullptr) {
     unsigned long long *c2, h = 0;
     if (dalloc(&c2, 1, s) != cudaSuccess) return -1;
     cudaMemsetAsync(c2, 0, 8, s);
@@ -1837,6 +1840,10 @@ struct Kway {
     }
     hs::count_launch();
     if (ar({seg64((int64_t *)c2, 1)})) return -1;
+    if (defer) {
+      *defer = c2;
+      return 0;
+    }
     cudaMemcpyAsync(&h, c2, 8, cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     cudaFreeAsync(c2, s);
@@ -2648,14 +2655,23 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   // the connectivity cache holds unit weights (uniform) or the caller's own
   // (div == 1): the cut comes from it without another pass over the edges
   const bool cached_cut = K.cache.p != nullptr && div == 1;
-  int64_t cut = K.cut_of(g0, K.loc(cur), cached_cut);
-  if (cached_cut && w_uniform) cut *= w_uniform;
+  unsigned long long *cut_dev = nullptr;
+  if (K.cut_of(g0, K.loc(cur), cached_cut, &cut_dev) < 0 || !cut_dev)
+    HS_REQUIRE(false, HS_ECUDA, "k-way: cut failed");
   K.cache = Conn();
-  std::vector<int64_t> pw;
   rc = K.weights(g0, K.loc(cur));
   if (rc) return rc;
-  rc = K.read_pw(pw);
-  if (rc) return rc;
+  // one host read for the cut and the part weights
+  std::vector<int64_t> pw(k);
+  unsigned long long cut2 = 0;
+  HS_CHECK_CUDA(cudaMemcpyAsync(&cut2, cut_dev, 8, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaMemcpyAsync(pw.data(), K.d_pw, k * 8, cudaMemcpyDeviceToHost, s));
+  int32_t ctl_h[16];
+  HS_CHECK_CUDA(cudaMemcpyAsync(ctl_h, K.ctl, sizeof ctl_h, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(cut_dev, s);
+  int64_t cut = (int64_t)(cut2 / 2);
+  if (cached_cut && w_uniform) cut *= w_uniform;
   rc = K.check_peers();
   if (rc) return rc;
   K.free_rep(cur);
@@ -2663,9 +2679,6 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   double maxdev = 0;
   for (int p = 0; p < k; ++p)
     maxdev = std::max(maxdev, fabs((double)pw[p] / (double)K.total_vw - tpwgts_host[p]));
-  int32_t ctl_h[16];
-  HS_CHECK_CUDA(cudaMemcpyAsync(ctl_h, K.ctl, sizeof ctl_h, cudaMemcpyDeviceToHost, s));
-  HS_CHECK_CUDA(cudaStreamSynchronize(s));
   const int64_t passes = ctl_h[CTL_PASSES];
   if (stats_host) {
     stats_host[0] = cut;
