@@ -92,6 +92,13 @@ struct Conn {
       atomicAdd(reinterpret_cast<int32_t *>(p + row) + dest, w);
       return;
     }
+    if (kc * cw == 8) {  // 8-byte rows: one 64-bit atomic for both counters (no
+                         // borrow/carry can cross a counter, as below)
+      const unsigned long long delta = ((unsigned long long)(unsigned)w << (8 * cw * dest)) -
+                                       ((unsigned long long)(unsigned)w << (8 * cw * own));
+      atomicAdd(reinterpret_cast<unsigned long long *>(p + row), delta);
+      return;
+    }
     const int64_t bo = row + own * cw, bd = row + dest * cw;
     const unsigned so = (unsigned)(bo & 3) * 8u, sd = (unsigned)(bd & 3) * 8u;
     unsigned *wo = reinterpret_cast<unsigned *>(p + (bo & ~3ll));
