@@ -684,6 +684,18 @@ def secondary(csr10m, args):
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps, r
 
+    # the full multilevel path on the 10M DAG (matching, contraction, band
+    # start on the coarse ids) with the locality probe's shortcut disabled
+    ew4, nw4 = kway.integer_weights(csr10m.w_xfer), kway.integer_weights(csr10m.w_gpu)
+    os.environ["HS_KWAY_COARSEN"] = "1"
+    try:
+        ms, r = timed(lambda: kway.partition_kway(kway.symmetrize(csr10m, ew4, nw4), 8, tol=TOL))
+    finally:
+        del os.environ["HS_KWAY_COARSEN"]
+    out["cfg4_forced_coarsening_ms"] = ms
+    out["cfg4_forced_coarsening_cut"] = r.cut
+    out["cfg4_forced_coarsening_levels"] = r.levels
+    del ew4, nw4
     # K7 levels + critical path on the 10M DAG
     ms, (lv, fin, cp, nl) = timed(lambda: kway.levels(csr10m))
     out["cfg4_levels_critical_path_ms"] = ms

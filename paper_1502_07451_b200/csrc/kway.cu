@@ -1596,10 +1596,10 @@ struct Kway {
     const int tgrid = team_grid(g.n, T);
     // list-based afterburner: thin candidates before evaluating them (sharded:
     // flows all-reduced, dropped states stored into every replica). A pass
-    // then costs ~0.4 ms instead of ~1.1 ms on config 4, so the finest level
-    // gets two passes more. Measured (ms, cut): 4 (4.67, 1,339.9M),
-    // 5 (5.07, 1,328.5M), 6 (5.48, 1,320.1M), 7 (5.80, 1,314.1M),
-    // 8 (6.10, 1,309.7M); 4 unthinned passes were (6.38, 1,326.6M).
+    // then costs ~0.2-0.4 ms instead of ~1.1 ms on config 4, so the finest
+    // level gets two passes more. Measured step (ms, cut) by passes:
+    // 6 (4.25, 1,320.1M), 8 (4.75, 1,309.7M), 10 (5.20, 1,304.2M),
+    // 12 (5.47, 1,302.4M, converged); 4 unthinned passes were (6.38, 1,326.6M).
     static const int prethin_env = getenv("HS_KWAY_PRETHIN") ? atoi(getenv("HS_KWAY_PRETHIN")) : 1;
     const bool prethin = prethin_env && !getenv("HS_KWAY_DSM");
     int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big + (prethin && !passes_env ? 2 : 0)
