@@ -181,7 +181,9 @@ def test_uniform_weights_unit_path_identical(monkeypatch):
     assert r.cut == int(((p[src] != p[ug.adjncy.long()]).sum().item() // 2) * 37)
 
 
-@pytest.mark.parametrize("n,m,k", [(5000, 50000, 2), (20000, 200000, 8), (100000, 1000000, 8)])
+@pytest.mark.parametrize("n,m,k", [(5000, 50000, 2), (20000, 200000, 8), (100000, 1000000, 8),
+                                   (100000, 1000000, 3), (100000, 1000000, 16),
+                                   (200000, 2000000, 32)])
 def test_kway_valid_balanced_deterministic(n, m, k):
     csr = kway.layered_dag(n, m, 0)
     ug = kway.symmetrize(csr)
