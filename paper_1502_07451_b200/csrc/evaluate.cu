@@ -3,6 +3,8 @@
 // Reference: partition.evaluate / _finish (pkg/src/hetsched/partition.py:60-84),
 // graph.total_weights (graph.py:327-332), costs.workload_ratio
 // (costs.py:239-253).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "numeric.cuh"
 
@@ -193,6 +195,67 @@ __global__ void evalk_kernel(hs_dag_t g, const int32_t *part, int k, const int64
                              s_load[i]);
 }
 
+// Thread per source vertex (one assignment per blockIdx.y): the out-list is
+// walked in ascending destination order, so the first edge into each foreign
+// part pays the transfer, as in the warp version; every lane is busy on task
+// DAGs with ~10 successors (the warp version idled 2/3 of its lanes).
+__global__ void __launch_bounds__(256) evalk_thread(hs_dag_t g, const int32_t *part, int k,
+                                                    const int64_t *vwgt, int64_t *cut_bytes,
+                                                    int64_t *cut_edges, int64_t *loads,
+                                                    int64_t *xcount, int64_t *xbytes) {
+  __shared__ unsigned long long s_load[kMaxK];
+  __shared__ unsigned long long s_sum[4];
+  const int b = blockIdx.y;
+  const int32_t *p = part + (int64_t)b * g.n;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) s_load[i] = 0;
+  if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
+  __syncthreads();
+  long long cb = 0, ce = 0, xc = 0, xb = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < g.n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    if (u == g.root) continue;
+    const int pu = p[u];
+    atomicAdd(&s_load[pu], (unsigned long long)vwgt[u]);
+    const int64_t e1 = g.out_ptr[u + 1];
+    uint64_t seen = 0;  // parts already charged a transfer for u's item
+    for (int64_t e = g.out_ptr[u]; e < e1; ++e) {
+      const int v = __ldg(g.out_dst + e);
+      if (v == g.root) continue;
+      const int pv = __ldg(p + v);
+      if (pv == pu) continue;
+      const int64_t by = __ldg(g.bytes + e);
+      cb += by;
+      ce += 1;
+      if (!((seen >> pv) & 1ull)) {
+        seen |= 1ull << pv;
+        xc += 1;
+        xb += by;
+      }
+    }
+  }
+  for (int off = 16; off; off >>= 1) {
+    cb += __shfl_down_sync(0xffffffffu, cb, off);
+    ce += __shfl_down_sync(0xffffffffu, ce, off);
+    xc += __shfl_down_sync(0xffffffffu, xc, off);
+    xb += __shfl_down_sync(0xffffffffu, xb, off);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&s_sum[0], (unsigned long long)cb);
+    atomicAdd(&s_sum[1], (unsigned long long)ce);
+    atomicAdd(&s_sum[2], (unsigned long long)xc);
+    atomicAdd(&s_sum[3], (unsigned long long)xb);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    atomicAdd((unsigned long long *)&cut_bytes[b], s_sum[0]);
+    atomicAdd((unsigned long long *)&cut_edges[b], s_sum[1]);
+    atomicAdd((unsigned long long *)&xcount[b], s_sum[2]);
+    atomicAdd((unsigned long long *)&xbytes[b], s_sum[3]);
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    if (s_load[i]) atomicAdd((unsigned long long *)&loads[(int64_t)b * k + i], s_load[i]);
+}
+
 }  // namespace
 
 extern "C" int hs_exact_totals(const hs_dag_t *g, int include_root, double *out_host,
@@ -258,8 +321,15 @@ extern "C" int hs_evaluate_kway(const hs_dag_t *g, const int32_t *part, int32_t 
     // per assignment: out_ptr, out_dst, bytes, part[dst] gather, part[src], vwgt
     hs::Prof P("evaluate_kway", s, (double)batch * (8.0 * (g->n + 1) + 4.0 * g->m + 8.0 * g->m +
                                                     4.0 * g->m + 4.0 * g->n + 8.0 * g->n));
-    evalk_kernel<<<grid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
-                                       xfer_count, xfer_bytes);
+    static const bool warp_ver = getenv("HS_EVALK_WARP") != nullptr;
+    if (warp_ver) {
+      evalk_kernel<<<grid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
+                                         xfer_count, xfer_bytes);
+    } else {
+      dim3 tgrid(hs::grid_for((int64_t)g->n, 256, hs::sm_count() * 8), batch);
+      evalk_thread<<<tgrid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
+                                         xfer_count, xfer_bytes);
+    }
   }
   HS_CHECK_LAUNCH();
   return HS_OK;
