@@ -276,9 +276,19 @@ int hs_partition_kway(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host
 
 /* METIS_PartGraphKway-compatible front end (idx_t = int32, real_t = float,
  * HOST arrays, ncon = 1): the paper's partitioning tool boundary
- * (graphio.py:277-304). Balance: ubvec[0] (default 1.03)
+ * (graphio.py:277-304). Exported twice: under METIS's own
+ * name (a METIS caller relinks against this library unchanged) and with the
+ * hs_ prefix. Returns METIS's codes: METIS_OK = 1, METIS_ERROR_INPUT = -2,
+ * METIS_ERROR_MEMORY = -3, METIS_ERROR = -4 (message in hs_last_error()).
+ * Balance: ubvec[0] (default 1.03, or 1 + options[METIS_OPTION_UFACTOR]/1000)
  * becomes tol = (ubvec - 1) * min_p tpwgts[p] in the |w_p/W - t_p| <= tol
- * sense. objval = edge cut. Synchronous, default stream. */
+ * sense. Honoured options: SEED (8), UFACTOR (16), NUMBERING (17; 1 =
+ * 1-based xadj/adjncy/part). objval = edge cut. Synchronous, default stream. */
+int METIS_PartGraphKway(const int32_t *nvtxs, const int32_t *ncon, const int32_t *xadj,
+                        const int32_t *adjncy, const int32_t *vwgt, const int32_t *vsize,
+                        const int32_t *adjwgt, const int32_t *nparts, const float *tpwgts,
+                        const float *ubvec, const int32_t *options, int32_t *objval,
+                        int32_t *part);
 int hs_METIS_PartGraphKway(const int32_t *nvtxs, const int32_t *ncon, const int32_t *xadj,
                            const int32_t *adjncy, const int32_t *vwgt, const int32_t *vsize,
                            const int32_t *adjwgt, const int32_t *nparts, const float *tpwgts,

@@ -116,10 +116,10 @@ class DagCSR:
 
     @classmethod
     def from_taskgraph(cls, graph) -> "DagCSR":
-        h = HostDag.from_taskgraph(graph)
-        if h.root < 0:
-            raise ValueError(f"root node {graph.root} missing")
-        return cls.from_host(h)
+        """A graph without its root node lowers with root = -1 (no node is the
+        root): totals, workload ratio and critical path are defined on it as in
+        the reference (graph.py:327-332, costs.py:239-253, sim.py:239-247)."""
+        return cls.from_host(HostDag.from_taskgraph(graph))
 
     def validate(self) -> List[str]:
         """``validate`` (graph.py:113-150) on the device, in the reference's message order.
@@ -172,9 +172,11 @@ class DagCSR:
 
     @property
     def n_kernels(self) -> int:
-        return self.n - 1
+        return self.n - 1 if self.root >= 0 else self.n
 
     def kernel_pos(self, idx: np.ndarray) -> np.ndarray:
+        if self.root < 0:
+            return idx
         return np.where(idx < self.root, idx, idx - 1)
 
     def twoway(self) -> "TwoWayGraph":
@@ -201,9 +203,10 @@ class TwoWayGraph:
 
     @classmethod
     def from_host(cls, h: HostDag, dev) -> "TwoWayGraph":
-        n = h.n - 1
+        n = h.n - 1 if h.root >= 0 else h.n
         keep = (h.src != h.root) & (h.dst != h.root)
-        kp = lambda a: np.where(a < h.root, a, a - 1).astype(np.int32)  # noqa: E731
+        kp = lambda a: (np.where(a < h.root, a, a - 1) if h.root >= 0  # noqa: E731
+                        else a).astype(np.int32)
         eu, ev, ew = kp(h.src[keep]), kp(h.dst[keep]), h.w_xfer[keep]
         ne = len(eu)
         node = np.concatenate([eu, ev])

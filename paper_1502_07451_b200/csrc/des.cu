@@ -18,7 +18,6 @@
 
 namespace {
 
-constexpr int kMaxWorkers = 64;
 constexpr double kAbsent = -1.0;  // arrival sentinel: item not on that memory node
 
 __device__ __forceinline__ double pmax(double a, double b) { return b > a ? b : a; }
@@ -40,6 +39,10 @@ struct SimArgs {
   int32_t *qnext;    // [N]
   int32_t *ready;    // [N]
   double *arr;       // [2*(N+M)]
+  // per-worker state, [batch][W] (any worker count, MachineModel has no cap)
+  double *w_free, *w_end, *w_est;
+  int32_t *w_kid, *w_qh, *w_qt;
+  int8_t *w_busy;
 };
 
 struct Sim {
@@ -55,12 +58,10 @@ struct Sim {
   int64_t root_e0;  // first out-edge of the root
   // machine
   int C, W, policy;
-  double free_time[kMaxWorkers];
-  double run_end[kMaxWorkers];
-  int32_t run_kid[kMaxWorkers];
-  bool busyw[kMaxWorkers];
-  double est_free[kMaxWorkers];
-  int32_t qhead[kMaxWorkers], qtail[kMaxWorkers];
+  // per-worker state (this simulation's rows of the [batch][W] scratch)
+  double *free_time, *run_end, *est_free;
+  int32_t *run_kid, *qhead, *qtail;
+  int8_t *busyw;
   double bus_free, est_bus;
   // outputs
   int64_t tcount, tbytes, kpd[2], finished;
@@ -228,6 +229,11 @@ __global__ void des_kernel(SimArgs A) {
   S.ev = A.ev ? A.ev + A.ev_off[b] : nullptr;
   S.ev_cap = A.ev ? A.ev_off[b + 1] - A.ev_off[b] : 0;
   S.ev_n = 0;
+  {
+    const int64_t o = (int64_t)b * S.W;
+    S.free_time = A.w_free + o; S.run_end = A.w_end + o; S.est_free = A.w_est + o;
+    S.run_kid = A.w_kid + o; S.qhead = A.w_qh + o; S.qtail = A.w_qt + o; S.busyw = A.w_busy + o;
+  }
   for (int w = 0; w < S.W; ++w) {
     S.free_time[w] = 0.0; S.busyw[w] = false; S.est_free[w] = 0.0;
     S.qhead[w] = -1; S.qtail[w] = -1; S.run_end[w] = 0.0; S.run_kid[w] = -1;
@@ -291,8 +297,8 @@ extern "C" int hs_simulate_batch(const hs_dag_batch_t *g, int policy, const int8
   HS_REQUIRE(policy >= 0 && policy <= 2, HS_EPOLICY, "unknown policy id %d", policy);
   HS_REQUIRE(policy != 2 || pin, HS_EINVAL, "gp policy needs a pin map");
   HS_REQUIRE(cpu_workers >= 0 && gpu_workers >= 0 && cpu_workers + gpu_workers > 0 &&
-                 cpu_workers + gpu_workers <= kMaxWorkers,
-             HS_ELIMIT, "worker counts must be >= 0, total in 1..%d", kMaxWorkers);
+                 (int64_t)cpu_workers + gpu_workers <= (1 << 24),
+             HS_ELIMIT, "worker counts must be >= 0, total in 1..2^24");
   HS_REQUIRE(!ev || ev_off, HS_EINVAL, "events need ev_off");
   if (g->batch == 0) return HS_OK;
   cudaStream_t s = (cudaStream_t)stream;
@@ -304,14 +310,27 @@ extern "C" int hs_simulate_batch(const hs_dag_batch_t *g, int policy, const int8
   HS_CHECK_CUDA(qnext.alloc(N, s));
   HS_CHECK_CUDA(ready.alloc(N, s));
   HS_CHECK_CUDA(arr.alloc(2 * (N + M), s));
+  const int64_t BW = (int64_t)g->batch * (cpu_workers + gpu_workers);
+  hs::Scratch<double> wd;
+  hs::Scratch<int32_t> wi;
+  hs::Scratch<int8_t> wb;
+  HS_CHECK_CUDA(wd.alloc(3 * BW, s));
+  HS_CHECK_CUDA(wi.alloc(3 * BW, s));
+  HS_CHECK_CUDA(wb.alloc(BW, s));
   SimArgs A;
+  A.w_free = wd.p; A.w_end = wd.p + BW; A.w_est = wd.p + 2 * BW;
+  A.w_kid = wi.p; A.w_qh = wi.p + BW; A.w_qt = wi.p + 2 * BW;
+  A.w_busy = wb.p;
   A.g = *g;
   A.policy = policy; A.pin = pin; A.C = cpu_workers; A.G = gpu_workers;
   A.makespan = makespan; A.tcount = transfer_count; A.tbytes = transfer_bytes;
   A.busy = busy; A.kpd = kpd; A.status = status;
   A.ev = ev; A.ev_off = ev_off; A.ev_count = ev_count;
   A.pending = pending; A.qnext = qnext; A.ready = ready; A.arr = arr;
-  const int block = 64;
+  // one simulation per thread: small blocks spread the batch over every SM
+  // (4096 simulations -> 128 blocks of 32 instead of 64 blocks of 64)
+  int block = 32;
+  while (block < 128 && (int64_t)g->batch >= (int64_t)block * 2 * 2 * hs::sm_count()) block *= 2;
   {
     // every graph's CSR + weights read once, scratch state initialised once
     hs::Prof P("des", s, 40.0 * N + 36.0 * M);

@@ -12,7 +12,7 @@ namespace {
 
 using hs::kAccLimbs;
 
-__device__ __forceinline__ int kpos(int v, int root) { return v < root ? v : v - 1; }
+__device__ __forceinline__ int kpos(int v, int root) { return (root < 0 || v < root) ? v : v - 1; }
 
 // ---------------------------------------------------------------- K0 -----
 // acc layout: [3][kAccLimbs] int64 (w_cpu, w_gpu, w_xfer).
@@ -120,89 +120,19 @@ __global__ void eval2_exact_round(const unsigned long long *acc, int batch, doub
   total[b] = hs::superacc_round(a + 2 * kAccLimbs);
 }
 
-// k-way: one warp per producer u; lanes stride its out-edges. Integer sums
-// are order-independent, so block partials + atomics stay deterministic.
+// k-way evaluation. Integer sums are order-independent, so block partials +
+// atomics stay deterministic.
 constexpr int kMaxK = 64;
-__global__ void evalk_kernel(hs_dag_t g, const int32_t *part, int k, const int64_t *vwgt,
-                             int64_t *cut_bytes, int64_t *cut_edges, int64_t *loads,
-                             int64_t *xcount, int64_t *xbytes) {
-  __shared__ unsigned long long s_load[kMaxK];
-  __shared__ unsigned long long s_sum[4];
-  const int b = blockIdx.y;
-  const int32_t *p = part + (int64_t)b * g.n;
-  for (int i = threadIdx.x; i < k; i += blockDim.x) s_load[i] = 0;
-  if (threadIdx.x < 4) s_sum[threadIdx.x] = 0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  long long cb = 0, ce = 0, xc = 0, xb = 0;
-  for (int64_t u = warp; u < g.n; u += nwarps) {
-    if (u == g.root) continue;
-    const int pu = p[u];
-    if (lane == 0) atomicAdd(&s_load[pu], (unsigned long long)vwgt[u]);
-    const int64_t e0 = g.out_ptr[u], e1 = g.out_ptr[u + 1];
-    uint64_t seen = 0;  // parts already charged a transfer for u's item
-    for (int64_t base = e0; base < e1; base += 32) {
-      int64_t e = base + lane;
-      int pv = -1;
-      int64_t by = 0;
-      if (e < e1) {
-        int v = g.out_dst[e];
-        if (v != g.root) {
-          pv = p[v];
-          by = g.bytes[e];
-        }
-      }
-      bool cutting = pv >= 0 && pv != pu;
-      if (cutting) { cb += by; ce += 1; }
-      // first edge (lowest dst) of u into each foreign part pays one transfer
-      unsigned cut_mask = __ballot_sync(0xffffffffu, cutting);
-      while (cut_mask) {
-        int src = __ffs(cut_mask) - 1;
-        int q = __shfl_sync(0xffffffffu, pv, src);
-        int64_t qb = __shfl_sync(0xffffffffu, by, src);
-        unsigned same = __ballot_sync(0xffffffffu, cutting && pv == q);
-        if (!((seen >> q) & 1ull)) {
-          seen |= 1ull << q;
-          if (lane == 0) { xc += 1; xb += qb; }
-        }
-        cut_mask &= ~same;
-      }
-    }
-  }
-  for (int off = 16; off; off >>= 1) {
-    cb += __shfl_down_sync(0xffffffffu, cb, off);
-    ce += __shfl_down_sync(0xffffffffu, ce, off);
-    xc += __shfl_down_sync(0xffffffffu, xc, off);
-    xb += __shfl_down_sync(0xffffffffu, xb, off);
-  }
-  if (lane == 0) {
-    atomicAdd(&s_sum[0], (unsigned long long)cb);
-    atomicAdd(&s_sum[1], (unsigned long long)ce);
-    atomicAdd(&s_sum[2], (unsigned long long)xc);
-    atomicAdd(&s_sum[3], (unsigned long long)xb);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    atomicAdd((unsigned long long *)&cut_bytes[b], s_sum[0]);
-    atomicAdd((unsigned long long *)&cut_edges[b], s_sum[1]);
-    atomicAdd((unsigned long long *)&xcount[b], s_sum[2]);
-    atomicAdd((unsigned long long *)&xbytes[b], s_sum[3]);
-  }
-  for (int i = threadIdx.x; i < k; i += blockDim.x)
-    if (s_load[i]) atomicAdd((unsigned long long *)&loads[(int64_t)b * k + i],
-                             s_load[i]);
-}
 
 // Thread per source vertex (one assignment per blockIdx.y): the out-list is
 // walked in ascending destination order, so the first edge into each foreign
-// part pays the transfer, as in the warp version; every lane is busy on task
-// DAGs with ~10 successors (the warp version idled 2/3 of its lanes).
+// part pays the transfer; every lane is busy on task DAGs with ~10
+// successors (a warp per vertex idled 2/3 of its lanes: 1.44 vs 0.72 ms).
 __global__ void __launch_bounds__(256) evalk_thread(hs_dag_t g, const int32_t *part, int k,
                                                     const int64_t *vwgt, int64_t *cut_bytes,
                                                     int64_t *cut_edges, int64_t *loads,
-                                                    int64_t *xcount, int64_t *xbytes) {
+                                                    int64_t *xcount, int64_t *xbytes,
+                                                    int32_t *bad) {
   __shared__ unsigned long long s_load[kMaxK];
   __shared__ unsigned long long s_sum[4];
   const int b = blockIdx.y;
@@ -215,6 +145,10 @@ __global__ void __launch_bounds__(256) evalk_thread(hs_dag_t g, const int32_t *p
        u += (int64_t)gridDim.x * blockDim.x) {
     if (u == g.root) continue;
     const int pu = p[u];
+    if ((unsigned)pu >= (unsigned)k) {  // no out-of-range shared/shift access
+      atomicExch((int *)&bad[b], 1);
+      continue;
+    }
     atomicAdd(&s_load[pu], (unsigned long long)vwgt[u]);
     const int64_t e1 = g.out_ptr[u + 1];
     uint64_t seen = 0;  // parts already charged a transfer for u's item
@@ -223,6 +157,10 @@ __global__ void __launch_bounds__(256) evalk_thread(hs_dag_t g, const int32_t *p
       if (v == g.root) continue;
       const int pv = __ldg(p + v);
       if (pv == pu) continue;
+      if ((unsigned)pv >= (unsigned)k) {
+        atomicExch((int *)&bad[b], 1);
+        continue;
+      }
       const int64_t by = __ldg(g.bytes + e);
       cb += by;
       ce += 1;
@@ -254,6 +192,16 @@ __global__ void __launch_bounds__(256) evalk_thread(hs_dag_t g, const int32_t *p
   }
   for (int i = threadIdx.x; i < k; i += blockDim.x)
     if (s_load[i]) atomicAdd((unsigned long long *)&loads[(int64_t)b * k + i], s_load[i]);
+}
+
+// An assignment holding a part id outside [0, k) on a non-root node reports
+// cut_edges = xfer_count = -1 (its other outputs are meaningless).
+__global__ void evalk_flag(const int32_t *bad, int batch, int64_t *cut_edges, int64_t *xcount) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < batch && bad[b]) {
+    cut_edges[b] = -1;
+    xcount[b] = -1;
+  }
 }
 
 }  // namespace
@@ -316,21 +264,19 @@ extern "C" int hs_evaluate_kway(const hs_dag_t *g, const int32_t *part, int32_t 
   HS_CHECK_CUDA(cudaMemsetAsync(xfer_count, 0, batch * sizeof(int64_t), s));
   HS_CHECK_CUDA(cudaMemsetAsync(xfer_bytes, 0, batch * sizeof(int64_t), s));
   HS_CHECK_CUDA(cudaMemsetAsync(loads, 0, (size_t)batch * k * sizeof(int64_t), s));
-  dim3 grid(hs::grid_for((int64_t)g->n * 32, 256, hs::sm_count() * 8), batch);
+  hs::Scratch<int32_t> bad;
+  HS_CHECK_CUDA(bad.alloc(batch, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(bad, 0, batch * sizeof(int32_t), s));
   {
     // per assignment: out_ptr, out_dst, bytes, part[dst] gather, part[src], vwgt
     hs::Prof P("evaluate_kway", s, (double)batch * (8.0 * (g->n + 1) + 4.0 * g->m + 8.0 * g->m +
                                                     4.0 * g->m + 4.0 * g->n + 8.0 * g->n));
-    static const bool warp_ver = getenv("HS_EVALK_WARP") != nullptr;
-    if (warp_ver) {
-      evalk_kernel<<<grid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
-                                         xfer_count, xfer_bytes);
-    } else {
-      dim3 tgrid(hs::grid_for((int64_t)g->n, 256, hs::sm_count() * 8), batch);
-      evalk_thread<<<tgrid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
-                                         xfer_count, xfer_bytes);
-    }
+    dim3 tgrid(hs::grid_for((int64_t)g->n, 256, hs::sm_count() * 8), batch);
+    evalk_thread<<<tgrid, 256, 0, s>>>(*g, part, k, vwgt_i, cut_bytes, cut_edges, loads,
+                                       xfer_count, xfer_bytes, bad);
   }
+  HS_CHECK_LAUNCH();
+  evalk_flag<<<(batch + 255) / 256, 256, 0, s>>>(bad, batch, cut_edges, xfer_count);
   HS_CHECK_LAUNCH();
   return HS_OK;
 }

@@ -51,6 +51,12 @@ def emit_metis_csr(csr: DagCSR, node_weight_source: str = GPU, scale: int = 100)
     fn = _native._need(_emit, "hs_emit_metis")
     w_node = csr.w_gpu if node_weight_source == GPU else csr.w_cpu
     r = csr.root
+    if r < 0:
+        raise PartitionError("graph has no root node; cannot export kernels")
+    # K1 lowers kernels by dropping the root's out-list; an edge INTO the root
+    # (a cyclic, never-validated graph) has no place in that layout
+    if int(csr.in_ptr[r + 1] - csr.in_ptr[r]) != 0:
+        raise PartitionError("graph has edges into the root; validate() it before export")
     inter = torch.ones(csr.m, dtype=torch.bool, device=csr.device)
     inter[int(csr.out_ptr[r]):int(csr.out_ptr[r + 1])] = False  # root edges
     kern = torch.ones(csr.n, dtype=torch.bool, device=csr.device)

@@ -65,7 +65,14 @@ def _root_out_degree(csr: DagCSR) -> int:
     """Edges leaving the root (one host read per DAG object, then cached)."""
     d = getattr(csr, "_root_outdeg", None)
     if d is None:
-        d = int((csr.out_ptr[csr.root + 1] - csr.out_ptr[csr.root]).item())
+        if csr.root < 0:
+            raise ValueError("DAG has no root node")
+        r = csr.root
+        both = torch.stack([csr.out_ptr[r + 1] - csr.out_ptr[r],
+                            csr.in_ptr[r + 1] - csr.in_ptr[r]]).tolist()
+        if both[1] != 0:  # K1's row layout drops the root's out-list only
+            raise ValueError("DAG has edges into the root (validate() it first)")
+        d = int(both[0])
         csr._root_outdeg = d
     return d
 
@@ -190,13 +197,25 @@ def partition_kway(graph, k: int, tpwgts: Optional[Sequence[float]] = None, tol:
 
 
 def evaluate_batch(csr: DagCSR, parts: torch.Tensor, k: int,
-                   node_w_i: Optional[torch.Tensor] = None) -> Dict[str, torch.Tensor]:
-    """K2 for B k-way assignments (int32 [B, n], node index space incl. root)."""
+                   node_w_i: Optional[torch.Tensor] = None,
+                   check: bool = True) -> Dict[str, torch.Tensor]:
+    """K2 for B k-way assignments (int32 [B, n], node index space incl. root).
+
+    A part id outside [0, k) on a non-root node is never used as an index: the
+    kernel flags that assignment (cut_edges = xfer_count = -1). ``check``
+    (default) turns a flagged assignment into ValueError (one host read);
+    ``check=False`` leaves the flag to the caller and keeps the call async.
+    """
     if node_w_i is None:
         node_w_i = integer_weights(csr.w_gpu).to(torch.int64)
     if parts.dim() == 1:
         parts = parts.unsqueeze(0)
-    return _native.evaluate_kway(csr, parts.contiguous(), k, node_w_i.contiguous())
+    out = _native.evaluate_kway(csr, parts.contiguous(), k, node_w_i.contiguous())
+    if check:
+        bad = torch.nonzero(out["cut_edges"] < 0).flatten().tolist()
+        if bad:
+            raise ValueError(f"assignment {bad[0]} has a part id outside [0, {k})")
+    return out
 
 
 def kernel_to_node_parts(csr: DagCSR, kpart: torch.Tensor) -> torch.Tensor:

@@ -89,11 +89,18 @@ def _check_graph(graph: TaskGraph) -> None:
 
 
 def _pin_array(graphs: Sequence[TaskGraph], policies) -> Optional[torch.Tensor]:
+    """Per-node pin bytes (1 = GPU). Every non-root kernel must be pinned: the
+    reference's on_ready looks the kernel up in the pin map and raises
+    KeyError for a missing one (policies.py:92-93); the root is never queued."""
     pins = []
     for g, p in zip(graphs, policies):
         ids = g.csr().host.ids
         pm = p.pin_map
-        pins.append(np.fromiter((1 if pm.get(int(i), CPU) == GPU else 0 for i in ids),
+        root = g.root
+        missing = [int(i) for i in ids if int(i) != root and int(i) not in pm]
+        if missing:
+            raise KeyError(missing[0])
+        pins.append(np.fromiter((1 if int(i) != root and pm[int(i)] == GPU else 0 for i in ids),
                                 dtype=np.int8, count=len(ids)))
     return torch.from_numpy(np.concatenate(pins)).to(_native.device())
 

@@ -13,7 +13,7 @@ def declared_functions():
     for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
         text = open(h).read()
         text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
-        for m in re.finditer(r"\b(hs_[a-z0-9_]+)\s*\(", text):
+        for m in re.finditer(r"\b(hs_[a-z0-9_]+|METIS_[A-Za-z]+)\s*\(", text):
             names.add(m.group(1))
     return sorted(names)
 
@@ -22,7 +22,8 @@ def test_header_declares_entry_points():
     names = declared_functions()
     for must in ("hs_evaluate2", "hs_simulate_batch", "hs_levels", "hs_fm2", "hs_brute2",
                  "hs_partition_kway", "hs_exact_totals", "hs_last_error",
-                 "hs_partition_kway_dist", "hs_symmetrize_range", "hs_kway_dist_arena_bytes"):
+                 "hs_partition_kway_dist", "hs_symmetrize_range", "hs_kway_dist_arena_bytes",
+                 "METIS_PartGraphKway"):
         assert must in names
 
 
