@@ -274,6 +274,16 @@ int hs_partition_kway(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host
                       double tol, uint64_t seed, int32_t *part, int64_t *stats_host,
                       void *stream);
 
+/* hs_partition_kway plus caller-supplied start partitions of the finest
+ * graph (device int32 [n_starts][n], values in 0..k-1; n <= 4096): each start
+ * is FM-refined with the partitioner's own candidates and competes under the
+ * same (balance violation, cut) ranking, so the result is never worse than
+ * the best start refined. The Python layer passes the reference heuristic's
+ * recursive 2-way partition here (partition.py:258-295). */
+int hs_partition_kway_starts(const hs_ugraph_t *g, int32_t k, const double *tpwgts_host,
+                             double tol, uint64_t seed, const int32_t *starts, int32_t n_starts,
+                             int32_t *part, int64_t *stats_host, void *stream);
+
 /* METIS_PartGraphKway-compatible front end (idx_t = int32, real_t = float,
  * HOST arrays, ncon = 1): the paper's partitioning tool boundary
  * (graphio.py:277-304). Exported twice: under METIS's own

@@ -271,12 +271,24 @@ def brute2(n, weights, r_cpu, tol, edge_a, edge_b, edge_w):
     return mask.value, bool(feas.value)
 
 
-def partition_kway(ug, k: int, tpwgts, tol: float, seed: int, part: torch.Tensor):
-    fn = _need(_partition_kway, "hs_partition_kway")
+_partition_kway_starts = _opt("hs_partition_kway_starts", _P, _i32, _P, ctypes.c_double,
+                              ctypes.c_uint64, _P, _i32, _P, _P, _P)
+
+
+def partition_kway(ug, k: int, tpwgts, tol: float, seed: int, part: torch.Tensor,
+                   starts: Optional[torch.Tensor] = None):
+    """hs_partition_kway, or hs_partition_kway_starts with int32 [S, n] device starts."""
     tp = (ctypes.c_double * k)(*[float(x) for x in tpwgts])
     stats = (ctypes.c_int64 * 8)()
-    check(fn(ctypes.byref(ug.struct()), k, tp, float(tol), ctypes.c_uint64(seed & (2**64 - 1)),
-             ptr(part), stats, stream_ptr()))
+    sd = ctypes.c_uint64(seed & (2**64 - 1))
+    if starts is not None and starts.shape[0] > 0:
+        fn = _need(_partition_kway_starts, "hs_partition_kway_starts")
+        check(fn(ctypes.byref(ug.struct()), k, tp, float(tol), sd, ptr(starts),
+                 int(starts.shape[0]), ptr(part), stats, stream_ptr()))
+    else:
+        fn = _need(_partition_kway, "hs_partition_kway")
+        check(fn(ctypes.byref(ug.struct()), k, tp, float(tol), sd, ptr(part), stats,
+                 stream_ptr()))
     return list(stats)
 
 

@@ -765,169 +765,19 @@ __global__ void classify_long(const int64_t *ub, const int32_t *ncp, int64_t lo,
 }
 
 // ------------------------------------------------------------------ K5 ---
-// One warp per trial on the coarsest graph: BFS order from a hashed start,
-// streaming LDG assignment, then greedy single-vertex refinement passes.
-struct InitArgs {
-  G g;
-  int k;
-  const int64_t *hi;  // [k] max part weight
-  const int64_t *lo;  // [k] min part weight
-  uint64_t seed;
-  int trials;
-  int8_t *parts;      // [trials][n]
-  int32_t *order;     // [trials][n] scratch
-  int8_t *seen;       // [trials][n] scratch
-  int64_t *cut;       // [trials]
-  int32_t *infeas;    // [trials]
-};
+// Initial partitions and small-level refinement: CTA-resident FM.
+#include "kway_fm.cuh"
 
-constexpr int kInitWarps = 4;
+// levels up to this many vertices are refined by FM candidates (one GPU)
+constexpr int kFmMaxLevel = 4096;
+constexpr int kFmInitPasses = 8, kFmRefinePasses = 6, kFmCopies = 16;
+// coarsening stops on density only past this many adjacency entries
+constexpr int64_t kDenseStopNnz = 4ll << 20;
 
-__global__ void __launch_bounds__(kInitWarps * 32) initial_kernel(InitArgs A) {
-  __shared__ int32_t conn_s[kInitWarps][kMaxParts];
-  __shared__ int64_t pw_s[kInitWarps][kMaxParts];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int trial = blockIdx.x * kInitWarps + wl;
-  if (trial >= A.trials) return;
-  const G &g = A.g;
-  const int n = g.n, k = A.k;
-  int8_t *part = A.parts + (int64_t)trial * n;
-  int32_t *ord = A.order + (int64_t)trial * n;
-  int8_t *seen = A.seen + (int64_t)trial * n;
-  int32_t *conn = conn_s[wl];
-  int64_t *pw = pw_s[wl];
-  for (int i = lane; i < n; i += 32) { seen[i] = 0; part[i] = -1; }
-  for (int p = lane; p < k; p += 32) pw[p] = 0;
-  __syncwarp();
-  // BFS order; restarts at hashed unvisited vertices (scan from a hashed offset)
-  int head = 0, tail = 0;
-  int scan_pos = (int)(mix32(A.seed * 7919 + trial) % (uint32_t)n);
-  int scanned = 0;
-  while (tail < n) {
-    if (head == tail) {  // new component root
-      while (seen[scan_pos]) { scan_pos = scan_pos + 1 == n ? 0 : scan_pos + 1; ++scanned; }
-      if (lane == 0) { seen[scan_pos] = 1; ord[tail] = scan_pos; }
-      __syncwarp();
-      ++tail;
-    }
-    int v = ord[head++];
-    const int64_t b = g.xbeg[v];
-    const int d = g.deg[v];
-    for (int j0 = 0; j0 < d; j0 += 32) {
-      int j = j0 + lane;
-      int u = j < d ? g.adj[b + j] : -1;
-      bool fresh = u >= 0 && !seen[u];
-      // de-duplicate within the batch: only the first lane holding u claims it
-      unsigned same = __match_any_sync(0xffffffffu, u);
-      bool first = fresh && (__ffs(same) - 1 == lane);
-      unsigned m = __ballot_sync(0xffffffffu, first);
-      if (first) {
-        seen[u] = 1;
-        ord[tail + __popc(m & ((1u << lane) - 1))] = u;
-      }
-      tail += __popc(m);
-      __syncwarp();
-    }
-  }
-  // streaming LDG assignment in BFS order
-  for (int idx = 0; idx < n; ++idx) {
-    const int v = ord[idx];
-    for (int p = lane; p < k; p += 32) conn[p] = 0;
-    __syncwarp();
-    const int64_t b = g.xbeg[v];
-    const int d = g.deg[v];
-    for (int j = lane; j < d; j += 32) {
-      int p = part[g.adj[b + j]];
-      if (p >= 0) atomicAdd(&conn[p], g.ew(b + j));
-    }
-    __syncwarp();
-    // score = conn * (1 - pw/hi); lane p evaluates part p (k <= 64: two rounds)
-    double best = -1.0;
-    int bp = -1;
-    for (int p = lane; p < k; p += 32) {
-      int64_t after = pw[p] + g.vw[v];
-      if (after > A.hi[p]) continue;
-      double fill = (double)pw[p] / (double)A.hi[p];
-      double s = (double)conn[p] * (1.0 - fill) + (1.0 - fill) * 1e-9;
-      if (s > best || (s == best && p < bp)) { best = s; bp = p; }
-    }
-    for (int off = 16; off; off >>= 1) {
-      double ob = __shfl_down_sync(0xffffffffu, best, off);
-      int op = __shfl_down_sync(0xffffffffu, bp, off);
-      if (op >= 0 && (bp < 0 || ob > best || (ob == best && op < bp))) { best = ob; bp = op; }
-    }
-    bp = __shfl_sync(0xffffffffu, bp, 0);
-    if (bp < 0) {  // nothing fits: least relatively loaded part
-      double lf = 1e300;
-      for (int p = 0; p < k; ++p) {
-        double f = (double)pw[p] / (double)A.hi[p];
-        if (f < lf) { lf = f; bp = p; }
-      }
-    }
-    if (lane == 0) { part[v] = (int8_t)bp; pw[bp] += g.vw[v]; }
-    __syncwarp();
-  }
-  // greedy refinement passes (sequential per vertex, warp-parallel adjacency)
-  for (int pass = 0; pass < 4; ++pass) {
-    int moved = 0;
-    for (int idx = 0; idx < n; ++idx) {
-      const int v = ord[idx];
-      for (int p = lane; p < k; p += 32) conn[p] = 0;
-      __syncwarp();
-      const int64_t b = g.xbeg[v];
-      const int d = g.deg[v];
-      for (int j = lane; j < d; j += 32) atomicAdd(&conn[part[g.adj[b + j]]], g.ew(b + j));
-      __syncwarp();
-      const int own = part[v];
-      const int32_t vwv = g.vw[v];
-      int bg = 0, bp = -1;
-      for (int p = lane; p < k; p += 32) {
-        if (p == own) continue;
-        if (pw[p] + vwv > A.hi[p] || pw[own] - vwv < A.lo[own]) continue;
-        int gain = conn[p] - conn[own];
-        if (gain > bg || (gain == bg && bp >= 0 && p < bp)) { bg = gain; bp = p; }
-      }
-      for (int off = 16; off; off >>= 1) {
-        int og = __shfl_down_sync(0xffffffffu, bg, off);
-        int op = __shfl_down_sync(0xffffffffu, bp, off);
-        if (op >= 0 && (bp < 0 || og > bg || (og == bg && op < bp))) { bg = og; bp = op; }
-      }
-      bp = __shfl_sync(0xffffffffu, bp, 0);
-      bg = __shfl_sync(0xffffffffu, bg, 0);
-      if (bp >= 0 && bg > 0) {
-        if (lane == 0) { part[v] = (int8_t)bp; pw[bp] += vwv; pw[own] -= vwv; }
-        ++moved;
-      }
-      __syncwarp();
-    }
-    if (!moved) break;
-  }
-  // cut (each undirected edge counted twice) and feasibility
-  int64_t cut2 = 0;
-  for (int v = 0; v < n; ++v) {
-    const int64_t b = g.xbeg[v];
-    const int d = g.deg[v];
-    const int pv = part[v];
-    for (int j = lane; j < d; j += 32)
-      if (part[g.adj[b + j]] != pv) cut2 += g.ew(b + j);
-  }
-  for (int off = 16; off; off >>= 1) cut2 += __shfl_down_sync(0xffffffffu, cut2, off);
-  if (lane == 0) {
-    int bad = 0;
-    for (int p = 0; p < k; ++p) bad += (pw[p] > A.hi[p] || pw[p] < A.lo[p]);
-    A.cut[trial] = cut2 / 2;
-    A.infeas[trial] = bad;
-  }
-}
-
-__global__ void pick_best(const int64_t *cut, const int32_t *infeas, int trials, int32_t *best) {
-  if (threadIdx.x || blockIdx.x) return;
-  int b = 0;
-  for (int t = 1; t < trials; ++t) {
-    bool better = (infeas[t] != 0) != (infeas[b] != 0) ? infeas[t] == 0 : cut[t] < cut[b];
-    if (better) b = t;
-  }
-  *best = b;
+int dev_id() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
 }
 
 // ------------------------------------------------------------------ K6 ---
@@ -1331,6 +1181,10 @@ struct Kway {
   // connectivity cache of the level being refined (one GPU, k <= 16):
   // cache[v][q] = weight of v's edges into part q, kc = 8 or 16 ints per row
   Conn cache;                 // cache.p == nullptr: none
+  // caller's start partitions of the finest level (int32 [n_starts][n]),
+  // refined and ranked with the FM candidates
+  const int32_t *starts = nullptr;
+  int n_starts = 0;
   int64_t max_deg0 = 0;       // largest degree of the finest level (cache width)
   Dist D;                         // P = 1: the whole graph on this GPU
   std::shared_ptr<HostBarrier> hb;  // loopback groups
@@ -2221,6 +2075,86 @@ struct Kway {
     return HS_OK;
   }
 
+  // FM candidates on a small level (one GPU): n_init recursive-bisection
+  // starts, `copies` copies of `cur` (each searches with its own hash salt)
+  // and the caller's starts at the finest level; the best by (violation,
+  // cut) replaces cur. No host round trip.
+  int fm_level(const Level &Lv, part_t *cur, int n_init, int copies, bool with_starts,
+               int passes, uint64_t salt2) {
+    const G &g = Lv.g;
+    const int n = g.n;
+    const int n_ext = with_starts ? n_starts : 0;
+    const int64_t rows = (int64_t)n * k * 4;
+    const int64_t flags = 2 * (int64_t)((n + 15) & ~15);
+    int smem_max = 0;
+    HS_CHECK_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                         dev_id()));
+    const int64_t static_smem = 8 * 1024;  // fm_kernel's own __shared__ arrays
+    const bool sm = flags + rows + static_smem <= smem_max;
+    if (!sm) {  // global rows: keep the scratch within 512 MB
+      const int64_t cap = std::max<int64_t>(1, (512ll << 20) / std::max<int64_t>(rows, 1));
+      while ((int64_t)n_init + copies + n_ext > cap && n_init > 0) --n_init;
+      while ((int64_t)n_init + copies + n_ext > cap && copies > 1) --copies;
+    }
+    const int C = n_init + copies + n_ext;
+    part_t *parts;
+    int32_t *trail, *conn = nullptr;
+    int64_t *cut, *viol;
+    HS_CHECK_CUDA(dalloc(&parts, (int64_t)C * n, s));
+    HS_CHECK_CUDA(dalloc(&trail, (int64_t)C * n, s));
+    HS_CHECK_CUDA(dalloc(&cut, C, s));
+    HS_CHECK_CUDA(dalloc(&viol, C, s));
+    if (!sm) HS_CHECK_CUDA(dalloc(&conn, (int64_t)C * n * k, s));
+    if (copies) {
+      fm_fill_copies<<<hs::grid_for((int64_t)copies * n, 256), 256, 0, s>>>(cur, n, parts, n_init,
+                                                                            copies);
+      HS_CHECK_LAUNCH();
+    }
+    if (n_ext) {
+      fm_fill_starts<<<hs::grid_for((int64_t)n_ext * n, 256), 256, 0, s>>>(
+          starts, (int64_t)n_ext * n, parts + (int64_t)(n_init + copies) * n);
+      HS_CHECK_LAUNCH();
+    }
+    FmArgs A;
+    A.g = g;
+    A.k = k;
+    A.hi = d_hi;
+    A.lo = d_lo;
+    A.cum = d_cum;
+    A.tol_split = tol;
+    A.parts = parts;
+    A.conn_g = conn;
+    A.trail = trail;
+    A.cut = cut;
+    A.viol = viol;
+    A.n_init = n_init;
+    A.salt = salt2;
+    A.passes = passes;
+    A.stall = std::max(32, std::min(400, n / 8));
+    const int64_t dyn = flags + (sm ? rows : 0);
+    {
+      hs::Prof P("fm_level", s, 0.0);
+      if (sm) {
+        HS_CHECK_CUDA(cudaFuncSetAttribute(fm_kernel<true>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        fm_kernel<true><<<C, kFmThreads, dyn, s>>>(A);
+      } else {
+        HS_CHECK_CUDA(cudaFuncSetAttribute(fm_kernel<false>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        fm_kernel<false><<<C, kFmThreads, dyn, s>>>(A);
+      }
+    }
+    HS_CHECK_LAUNCH();
+    fm_pick<<<hs::grid_for(n, 256, 64), 256, 0, s>>>(viol, cut, C, parts, n, cur, nullptr);
+    HS_CHECK_LAUNCH();
+    cudaFreeAsync(parts, s);
+    cudaFreeAsync(trail, s);
+    cudaFreeAsync(cut, s);
+    cudaFreeAsync(viol, s);
+    if (conn) cudaFreeAsync(conn, s);
+    return HS_OK;
+  }
+
   int initial(Rep<part_t> &best_rep) {
     Level &Cst = levels.back();
     G &g = Cst.g;
@@ -2254,46 +2188,13 @@ struct Kway {
       rc = barrier();  // every rank's bands are in place
       if (rc) return rc;
     }
-    // warp trials (BFS-order LDG + greedy refinement) on small coarsest graphs
-    // (one GPU: the sharded path keeps the band start)
-    if (nc <= 32768 && !D.on()) {
-      const int64_t best_cut = cut_of(g, best);
-      std::vector<int64_t> pw;
-      int rc = weights(g, best);
-      if (rc) return rc;
-      rc = read_pw(pw);
-      if (rc) return rc;
-      const bool best_feas = feasible(pw);
-      rc = sort_lists(Cst);  // trials depend on list order: make it canonical
-      if (rc) return rc;
-      const int trials = nc <= 8192 ? 256 : 64;
-      InitArgs IA;
-      IA.g = g; IA.k = k; IA.hi = d_hi; IA.lo = d_lo; IA.seed = seed; IA.trials = trials;
-      int32_t *bt;
-      HS_CHECK_CUDA(dalloc(&IA.parts, (int64_t)trials * nc, s));
-      HS_CHECK_CUDA(dalloc(&IA.order, (int64_t)trials * nc, s));
-      HS_CHECK_CUDA(dalloc(&IA.seen, (int64_t)trials * nc, s));
-      HS_CHECK_CUDA(dalloc(&IA.cut, trials, s));
-      HS_CHECK_CUDA(dalloc(&IA.infeas, trials, s));
-      HS_CHECK_CUDA(dalloc(&bt, 1, s));
-      initial_kernel<<<(trials + kInitWarps - 1) / kInitWarps, kInitWarps * 32, 0, s>>>(IA);
-      HS_CHECK_LAUNCH();
-      pick_best<<<1, 1, 0, s>>>(IA.cut, IA.infeas, trials, bt);
-      HS_CHECK_LAUNCH();
-      int32_t bti = 0, binf = 0;
-      int64_t bcut = 0;
-      HS_CHECK_CUDA(cudaMemcpyAsync(&bti, bt, 4, cudaMemcpyDeviceToHost, s));
-      HS_CHECK_CUDA(cudaStreamSynchronize(s));
-      HS_CHECK_CUDA(cudaMemcpyAsync(&bcut, IA.cut + bti, 8, cudaMemcpyDeviceToHost, s));
-      HS_CHECK_CUDA(cudaMemcpyAsync(&binf, IA.infeas + bti, 4, cudaMemcpyDeviceToHost, s));
-      HS_CHECK_CUDA(cudaStreamSynchronize(s));
-      bool tf = binf == 0;
-      if ((tf && !best_feas) || (tf == best_feas && bcut < best_cut)) {
-        HS_CHECK_CUDA(cudaMemcpyAsync(best, IA.parts + (int64_t)bti * nc, nc,
-                                      cudaMemcpyDeviceToDevice, s));
-      }
-      cudaFreeAsync(IA.parts, s); cudaFreeAsync(IA.order, s); cudaFreeAsync(IA.seen, s);
-      cudaFreeAsync(IA.cut, s); cudaFreeAsync(IA.infeas, s); cudaFreeAsync(bt, s);
+    // small coarsest graph (one GPU): recursive-bisection FM candidates, the
+    // refined band start and (when this is the finest level) the caller's
+    // starts; the band start alone otherwise
+    if (nc <= kFmMaxLevel && !D.on() && k > 1) {
+      const int n_init = nc <= 1024 ? 2 * hs::sm_count() : hs::sm_count();
+      return fm_level(Cst, best, n_init, 1, levels.size() == 1, kFmInitPasses,
+                      salt ^ 0xC0A25E57ull);
     }
     return HS_OK;
   }
@@ -2414,10 +2315,13 @@ namespace {
 // rank's rows [v0, v0 + ug->n) of an n_glob-vertex graph.
 int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_dist_t *dist,
                    int32_t k, const double *tpwgts_host, double tol, uint64_t seed,
-                   int32_t *part_out, int64_t *stats_host, cudaStream_t s) {
+                   int32_t *part_out, int64_t *stats_host, cudaStream_t s,
+                   const int32_t *starts = nullptr, int32_t n_starts = 0) {
   const int n0 = ug->n;
   const int64_t nnz0 = ug->nnz;
   Kway K(s);
+  K.starts = starts;
+  K.n_starts = n_starts;
   K.k = k;
   K.tol = tol;
   K.seed = seed;
@@ -2544,12 +2448,23 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
 
   // ---- balance bounds ----
   K.hi.resize(k); K.lo.resize(k); K.target.resize(k); K.cum.assign(k + 1, 0.0);
+  // |w/W - t| <= tol evaluated in doubles exactly as the reported deviation
+  // (and the reference's err, partition.py:72,83): hi / lo are the extreme
+  // integers that pass, so "in bounds" and "feasible" never disagree
+  const double W = (double)K.total_vw;
+  auto ok = [&](int64_t x, double t) { return fabs((double)x / W - t) <= tol; };
   for (int p = 0; p < k; ++p) {
     double t = tpwgts_host[p];
-    K.hi[p] = (int64_t)floor((t + tol) * (double)K.total_vw);
-    double l = (t - tol) * (double)K.total_vw;
-    K.lo[p] = l <= 0 ? 0 : (int64_t)ceil(l);
-    K.target[p] = (int64_t)llround(t * (double)K.total_vw);
+    int64_t h = (int64_t)floor((t + tol) * W);
+    while (ok(h + 1, t)) ++h;
+    while (h > 0 && !ok(h, t) && (double)h / W > t) --h;
+    double l = (t - tol) * W;
+    int64_t lo = l <= 0 ? 0 : (int64_t)ceil(l);
+    while (lo > 0 && ok(lo - 1, t)) --lo;
+    while (!ok(lo, t) && (double)lo / W < t && lo < h) ++lo;
+    K.hi[p] = h;
+    K.lo[p] = lo;
+    K.target[p] = (int64_t)llround(t * W);
     K.cum[p + 1] = K.cum[p] + t;
   }
   HS_CHECK_CUDA(dalloc(&K.d_hi, k, s));
@@ -2575,7 +2490,12 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   K.timer.mark("setup");
 
   // ---- coarsening ----
-  const int coarse_target = std::max(64 * k, 1024);
+  // coarsest level: ~30 vertices per part and at least n / (20 log2 k) (the
+  // recursive-bisection FM candidates work there), never above the FM range
+  int lg = 1;
+  while ((1 << lg) < k) ++lg;
+  const int coarse_target =
+      std::min(kFmMaxLevel / 2, std::max(30 * k, (int)(n_glob / (20ll * lg))));
   bool stop = false;
   // Coarsening also stops once the coarse graph turns dense (average degree
   // above max_deg): on random-like DAGs the edge count stops shrinking while
@@ -2608,7 +2528,9 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
       int rc0 = K.settle_nnz();
       if (rc0) return rc0;
       const Level &cl = K.levels.back();
-      if ((double)cl.nnz_glob > max_deg * (double)cl.n_glob) break;
+      // a dense level stops coarsening only when another level would cost
+      // real passes over many entries; small levels coarsen to the target
+      if ((double)cl.nnz_glob > max_deg * (double)cl.n_glob && cl.nnz_glob > kDenseStopNnz) break;
     }
     const bool ncu_win = K.levels.size() == 1 && getenv("HS_NCU_COARSEN0") != nullptr;
     if (ncu_win) cudaProfilerStart();
@@ -2642,6 +2564,17 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
       HS_CHECK_LAUNCH();
       K.free_rep(cur);
       cur = pf;
+    }
+    if (!K.D.on() && Lv.g.n <= kFmMaxLevel && k > 1) {
+      // small level: FM candidates from the projected partition (the
+      // coarsest one was refined by its initial candidates already)
+      if (li != (int)K.levels.size() - 1) {
+        rc = K.fm_level(Lv, K.loc(cur), 0, kFmCopies, li == 0, kFmRefinePasses,
+                        K.salt ^ ((uint64_t)li << 40) ^ 0xF00Dull);
+        if (rc) return rc;
+      }
+      K.timer.mark("refine level (fm)");
+      continue;
     }
     // HS_NCU_LEVEL0=1: open the profiler window around the finest level only
     const bool ncu_win = li == 0 && getenv("HS_NCU_LEVEL0") != nullptr;
@@ -2727,6 +2660,21 @@ extern "C" int hs_partition_kway(const hs_ugraph_t *ug, int32_t k, const double 
   HS_REQUIRE(ug->vwgt_i, HS_EINVAL, "k-way path needs integer vertex weights");
   return partition_impl(ug, 0, ug->n, nullptr, k, tpwgts_host, tol, seed, part_out, stats_host,
                         (cudaStream_t)stream);
+}
+
+extern "C" int hs_partition_kway_starts(const hs_ugraph_t *ug, int32_t k,
+                                        const double *tpwgts_host, double tol, uint64_t seed,
+                                        const int32_t *starts, int32_t n_starts, int32_t *part_out,
+                                        int64_t *stats_host, void *stream) {
+  HS_REQUIRE(ug && tpwgts_host && part_out, HS_EINVAL, "hs_partition_kway_starts: null argument");
+  HS_REQUIRE(k >= 1 && k <= kMaxParts, HS_ELIMIT, "k must be in 1..%d", kMaxParts);
+  HS_REQUIRE(ug->n >= 1, HS_EINVAL, "empty graph");
+  HS_REQUIRE(ug->vwgt_i, HS_EINVAL, "k-way path needs integer vertex weights");
+  HS_REQUIRE(n_starts >= 0 && (n_starts == 0 || starts), HS_EINVAL, "starts missing");
+  HS_REQUIRE(n_starts == 0 || ug->n <= kFmMaxLevel, HS_ELIMIT,
+             "start partitions are taken for graphs of at most %d vertices", kFmMaxLevel);
+  return partition_impl(ug, 0, ug->n, nullptr, k, tpwgts_host, tol, seed, part_out, stats_host,
+                        (cudaStream_t)stream, starts, n_starts);
 }
 
 extern "C" int64_t hs_kway_dist_arena_bytes(int32_t n_global) {

@@ -1,0 +1,452 @@
+// K5/K6 on small levels — CTA-resident Fiduccia–Mattheyses for the k-way
+// partitioner (included by kway.cu; uses G, part_t and mix32 from there).
+//
+// The reference's partitioner is FM (partition.py:137-220): every pass moves
+// vertices one at a time, best gain first, through negative-gain stretches,
+// remembers the best prefix by the key (out of balance, cut) and rolls the
+// rest back (partition.py:169-170, 206-219); a start comes from a greedy
+// balanced fill (partition.py:223-255) under several orders
+// (partition.py:280-295). This file is that algorithm generalised to k parts
+// and to weighted coarse graphs, one CTA per candidate partition:
+//
+//   * candidate state lives on-chip: part ids and move locks in shared
+//     memory, the connectivity rows conn[v][p] (weight of v's edges into part
+//     p) in shared memory when n*k*4 bytes fit, else in global memory read
+//     through L2 (ld.cg; updates are atomics, so L1 could hold stale lines);
+//   * a step is one block-wide arg-max over every unlocked vertex of
+//     (gain, per-pass hash) among the balance-admissible moves, then the
+//     move's neighbour rows are updated by all threads;
+//   * balance: part p must stay within [lo_p, hi_p]; a move is admissible
+//     if the state after it is in bounds or strictly less out of bounds
+//     (the k-way form of partition.py:193-196); prefix key = (violation,
+//     cut) as partition.py:169-170;
+//   * a pass stops after `stall` moves without a new best prefix (the
+//     reference moves every vertex; the early stop is METIS's and changes
+//     only how far a pass looks, not what it accepts);
+//   * initial partitions: recursive bisection inside the CTA — greedy graph
+//     growing from a hashed seed (frontier vertex of best gain first, stop at
+//     the side's target weight) then 2-way FM passes, down to k parts — and
+//     a final k-way FM over all parts. Candidates differ by their hash salt.
+// Every sum is an integer and every tie breaks on a hash of (salt, vertex,
+// pass), so a candidate is a pure function of (graph, start, salt).
+#pragma once
+
+constexpr int kFmThreads = 512;
+constexpr int kFmMaxN = 16384;  // part + lock bytes of a level live in shared memory
+
+struct FmArgs {
+  G g;
+  int k;
+  const int64_t *hi, *lo;  // global k-way bounds [k]
+  const double *cum;       // cumulative target fractions [k+1]
+  double tol_split;        // relative slack of each bisection's sides
+  part_t *parts;           // [C][n] candidate parts (in for refine, out always)
+  int32_t *conn_g;         // [C][n*k] rows in global memory (null: shared memory)
+  int32_t *trail;          // [C][n] moves of the current pass (v * 64 + old part)
+  int64_t *cut;            // [C] out: integer cut (each undirected edge once)
+  int64_t *viol;           // [C] out: total weight outside the k-way bounds
+  int n_init;              // candidates [0, n_init) start from recursive bisection
+  uint64_t salt;
+  int passes, stall;
+};
+
+struct FmCand {
+  unsigned long long key;  // 0 = none
+  int v, q;
+};
+
+__device__ __forceinline__ FmCand fm_better(const FmCand &a, const FmCand &b) {
+  if (a.key != b.key) return a.key > b.key ? a : b;
+  return a.v <= b.v ? a : b;
+}
+
+template <bool SM>
+struct FmCta {
+  const FmArgs &A;
+  int n, k;
+  part_t *part;     // shared
+  uint8_t *lock;    // shared
+  int32_t *conn;    // shared or global rows
+  int32_t *trail;   // global
+  int64_t *pw, *bhi, *blo;  // shared [kMaxParts]
+  // shared scalars
+  int64_t *s_viol, *s_cur, *s_best_cur, *s_best_viol;
+  int *s_moves, *s_best_len, *s_since, *s_done;
+  FmCand *s_red;    // [32]
+  int pa, pb;       // active pair (pa < 0: k-way)
+
+  __device__ FmCta(const FmArgs &a) : A(a) {}
+
+  __device__ __forceinline__ int32_t cget(int64_t i) const {
+    if constexpr (SM) return conn[i];
+    else return __ldcg(conn + i);
+  }
+  __device__ __forceinline__ void cadd(int64_t i, int32_t d) const { atomicAdd(conn + i, d); }
+
+  __device__ __forceinline__ int64_t over(int p, int64_t x) const {
+    int64_t o = 0;
+    if (x > bhi[p]) o += x - bhi[p];
+    if (x < blo[p]) o += blo[p] - x;
+    return o;
+  }
+  __device__ __forceinline__ bool active(int p) const { return pa < 0 || p == pa || p == pb; }
+  // total violation after moving weight w from `own` to `q`
+  __device__ __forceinline__ int64_t viol_after(int own, int q, int64_t w) const {
+    return *s_viol - over(own, pw[own]) - over(q, pw[q]) + over(own, pw[own] - w) +
+           over(q, pw[q] + w);
+  }
+  __device__ int64_t viol_now() const {
+    int64_t s = 0;
+    for (int p = 0; p < k; ++p)
+      if (active(p)) s += over(p, pw[p]);
+    return s;
+  }
+
+  // block-wide arg-max; every thread gets the winner
+  __device__ FmCand reduce(FmCand c) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int off = 16; off; off >>= 1) {
+      FmCand o;
+      o.key = __shfl_down_sync(0xffffffffu, c.key, off);
+      o.v = __shfl_down_sync(0xffffffffu, c.v, off);
+      o.q = __shfl_down_sync(0xffffffffu, c.q, off);
+      c = fm_better(c, o);
+    }
+    if (lane == 0) s_red[wid] = c;
+    __syncthreads();
+    if (wid == 0) {
+      const int nw = blockDim.x >> 5;
+      c = lane < nw ? s_red[lane] : FmCand{0ull, INT_MAX, 0};
+      for (int off = 16; off; off >>= 1) {
+        FmCand o;
+        o.key = __shfl_down_sync(0xffffffffu, c.key, off);
+        o.v = __shfl_down_sync(0xffffffffu, c.v, off);
+        o.q = __shfl_down_sync(0xffffffffu, c.q, off);
+        c = fm_better(c, o);
+      }
+      if (lane == 0) s_red[0] = c;
+    }
+    __syncthreads();
+    FmCand r = s_red[0];
+    __syncthreads();
+    return r;
+  }
+
+  __device__ int64_t block_sum(int64_t x) {
+    __shared__ long long s_sum[32];
+    for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+    if ((threadIdx.x & 31) == 0) s_sum[threadIdx.x >> 5] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      long long t = 0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += s_sum[i];
+      s_sum[0] = t;
+    }
+    __syncthreads();
+    const int64_t r = s_sum[0];
+    __syncthreads();
+    return r;
+  }
+
+  // part[v]: from -> to, every thread updates a share of v's neighbour rows.
+  // The caller synchronises afterwards.
+  __device__ void move(int v, int from, int to) {
+    const G &g = A.g;
+    if (threadIdx.x == 0) {
+      const int64_t w = g.vw[v];
+      part[v] = (part_t)to;
+      pw[from] -= w;
+      pw[to] += w;
+    }
+    const int64_t b = g.xbeg[v];
+    const int d = g.deg[v];
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      const int u = __ldg(g.adj + b + j);
+      const int w = g.ew(b + j);
+      cadd((int64_t)u * k + from, -w);
+      cadd((int64_t)u * k + to, w);
+    }
+  }
+
+  // conn rows and part weights from scratch
+  __device__ void build() {
+    const G &g = A.g;
+    for (int p = threadIdx.x; p < k; p += blockDim.x) pw[p] = 0;
+    __syncthreads();
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+      int32_t *row = conn + (int64_t)v * k;
+      for (int q = 0; q < k; ++q) row[q] = 0;
+      const int64_t b = g.xbeg[v];
+      const int d = g.deg[v];
+      for (int j = 0; j < d; ++j) {
+        const int u = __ldg(g.adj + b + j);
+        row[part[u]] += g.ew(b + j);  // row v is this thread's alone
+      }
+      atomicAdd((unsigned long long *)&pw[part[v]], (unsigned long long)(int64_t)g.vw[v]);
+    }
+    __syncthreads();
+  }
+
+  __device__ __forceinline__ uint32_t hsh(int v, int pass) const {
+    return mix32(A.salt ^ ((uint64_t)(uint32_t)v * 0x9E3779B97F4A7C15ull) ^
+                 ((uint64_t)(uint32_t)pass << 40));
+  }
+
+  // best admissible move of this thread's vertices
+  __device__ FmCand scan(int pass) const {
+    const G &g = A.g;
+    FmCand best{0ull, INT_MAX, 0};
+    const int64_t viol = *s_viol;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+      if (lock[v]) continue;
+      const int own = part[v];
+      if (!active(own)) continue;
+      const int64_t wv = g.vw[v];
+      const int32_t c_own = cget((int64_t)v * k + own);
+      int q0 = 0, q1 = k;
+      if (pa >= 0) {
+        q0 = own == pa ? pb : pa;
+        q1 = q0 + 1;
+      }
+      for (int q = q0; q < q1; ++q) {
+        if (q == own) continue;
+        const int32_t c_q = cget((int64_t)v * k + q);
+        if (viol == 0 && c_q == 0) continue;  // interior with respect to q
+        const int64_t nv = viol_after(own, q, wv);
+        if (!(nv == 0 || nv < viol)) continue;
+        const int64_t gain = (int64_t)c_q - c_own;
+        FmCand c;
+        c.key = ((unsigned long long)(gain + (1ll << 31)) << 32) | hsh(v, pass);
+        c.v = v;
+        c.q = q;
+        best = fm_better(best, c);
+      }
+    }
+    return best;
+  }
+
+  // One FM pass (the active pair, or all parts); true if the prefix key improved.
+  __device__ bool pass(int pass_no) {
+    for (int v = threadIdx.x; v < n; v += blockDim.x) lock[v] = 0;
+    if (threadIdx.x == 0) {
+      *s_viol = viol_now();
+      *s_cur = 0;
+      *s_best_cur = 0;
+      *s_best_viol = *s_viol;
+      *s_moves = 0;
+      *s_best_len = 0;
+      *s_since = 0;
+      *s_done = 0;
+    }
+    __syncthreads();
+    while (true) {
+      FmCand c = reduce(scan(pass_no));
+      if (c.key == 0ull) break;
+      const int v = c.v, q = c.q, own = part[v];
+      const int64_t gain = (int64_t)(c.key >> 32) - (1ll << 31);
+      if (threadIdx.x == 0) {
+        const int64_t w = A.g.vw[v];
+        *s_viol = viol_after(own, q, w);
+        lock[v] = 1;
+        trail[*s_moves] = v * 64 + own;
+        *s_moves += 1;
+        *s_cur -= gain;
+        if (*s_viol < *s_best_viol || (*s_viol == *s_best_viol && *s_cur < *s_best_cur)) {
+          *s_best_viol = *s_viol;
+          *s_best_cur = *s_cur;
+          *s_best_len = *s_moves;
+          *s_since = 0;
+        } else if (++*s_since > A.stall) {
+          *s_done = 1;
+        }
+      }
+      __syncthreads();  // s_viol read by move() of thread 0 only after this
+      move(v, own, q);
+      __syncthreads();
+      if (*s_done) break;
+    }
+    __syncthreads();
+    const int moves = *s_moves, keep = *s_best_len;
+    for (int m = moves - 1; m >= keep; --m) {
+      const int code = trail[m];
+      const int v = code >> 6, old = code & 63;
+      move(v, part[v], old);
+      __syncthreads();
+    }
+    return keep > 0;
+  }
+
+  __device__ void refine(int passes, int pass0) {
+    for (int p = 0; p < passes; ++p)
+      if (!pass(pass0 + p)) break;
+  }
+
+  // Greedy graph growing of side b out of side a (the range's vertices all
+  // hold part a): a hashed seed, then the best-gain frontier vertex, until b
+  // holds its target weight.
+  __device__ void grow(int a, int b, int64_t tgt_b, int salt_no) {
+    const G &g = A.g;
+    while (true) {
+      const bool first = pw[b] == 0;
+      FmCand best{0ull, INT_MAX, 0};
+      for (int v = threadIdx.x; v < n; v += blockDim.x) {
+        if (part[v] != a) continue;
+        FmCand c;
+        if (first) {
+          c.key = 1ull << 32 | hsh(v, salt_no);
+        } else {
+          const int32_t cb = cget((int64_t)v * k + b), ca = cget((int64_t)v * k + a);
+          const int64_t gain = (int64_t)cb - ca;
+          // frontier first (bit 63), then gain (31 bits), then the hash
+          int64_t gc = gain + (1ll << 30);
+          gc = gc < 0 ? 0 : (gc > (1ll << 31) - 1 ? (1ll << 31) - 1 : gc);
+          const unsigned long long gb = (unsigned long long)gc;
+          c.key = (cb > 0 ? 1ull << 63 : 0ull) | gb << 32 | hsh(v, salt_no);
+        }
+        c.v = v;
+        c.q = b;
+        best = fm_better(best, c);
+      }
+      FmCand c = reduce(best);
+      if (c.key == 0ull) break;
+      const int64_t w = g.vw[c.v];
+      // stop when taking the vertex overshoots more than stopping undershoots
+      if (!first && pw[b] + w - tgt_b > tgt_b - pw[b]) break;
+      move(c.v, a, b);
+      __syncthreads();
+      if (pw[b] >= tgt_b) break;
+    }
+  }
+
+  __device__ void bisect_all(int passes) {
+    __shared__ int s_r0[kMaxParts], s_r1[kMaxParts];
+    __shared__ int s_head, s_tail;
+    if (threadIdx.x == 0) {
+      s_r0[0] = 0;
+      s_r1[0] = k;
+      s_head = 0;
+      s_tail = 1;
+    }
+    __syncthreads();
+    int split_no = 0;
+    while (s_head < s_tail) {
+      const int p0 = s_r0[s_head], p1 = s_r1[s_head];
+      __syncthreads();
+      if (threadIdx.x == 0) ++s_head;
+      if (p1 - p0 >= 2) {
+        const int pm = p0 + (p1 - p0) / 2;
+        const double ta = A.cum[pm] - A.cum[p0], tb = A.cum[p1] - A.cum[pm];
+        const int64_t ws = pw[p0];
+        const int64_t tgt_b = (int64_t)llround((double)ws * (tb / (ta + tb)));
+        const int64_t tgt_a = ws - tgt_b;
+        const int64_t slack = (int64_t)floor(A.tol_split * (double)ws);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          bhi[p0] = tgt_a + slack;
+          blo[p0] = tgt_a - slack;
+          bhi[pm] = tgt_b + slack;
+          blo[pm] = tgt_b - slack;
+          s_r0[s_tail] = p0;
+          s_r1[s_tail] = pm;
+          s_r0[s_tail + 1] = pm;
+          s_r1[s_tail + 1] = p1;
+          s_tail += 2;
+        }
+        __syncthreads();
+        grow(p0, pm, tgt_b, 1000 + split_no);
+        pa = p0;
+        pb = pm;
+        refine(passes, 2000 + 64 * split_no);
+        pa = pb = -1;
+        ++split_no;
+      }
+      __syncthreads();
+    }
+  }
+
+  __device__ void set_global_bounds() {
+    for (int p = threadIdx.x; p < k; p += blockDim.x) {
+      bhi[p] = A.hi[p];
+      blo[p] = A.lo[p];
+    }
+    __syncthreads();
+  }
+};
+
+template <bool SM>
+__global__ void __launch_bounds__(kFmThreads) fm_kernel(FmArgs A) {
+  extern __shared__ __align__(16) unsigned char fm_dyn[];
+  __shared__ int64_t pw[kMaxParts], bhi[kMaxParts], blo[kMaxParts];
+  __shared__ int64_t s_viol, s_cur, s_best_cur, s_best_viol;
+  __shared__ int s_moves, s_best_len, s_since, s_done;
+  __shared__ FmCand s_red[32];
+  const int n = A.g.n, k = A.k, c = blockIdx.x;
+  FmCta<SM> C(A);
+  C.n = n;
+  C.k = k;
+  C.part = (part_t *)fm_dyn;
+  C.lock = fm_dyn + ((n + 15) & ~15);
+  C.conn = SM ? (int32_t *)(fm_dyn + 2 * ((n + 15) & ~15)) : A.conn_g + (int64_t)c * n * k;
+  C.trail = A.trail + (int64_t)c * n;
+  C.pw = pw; C.bhi = bhi; C.blo = blo;
+  C.s_viol = &s_viol; C.s_cur = &s_cur; C.s_best_cur = &s_best_cur; C.s_best_viol = &s_best_viol;
+  C.s_moves = &s_moves; C.s_best_len = &s_best_len; C.s_since = &s_since; C.s_done = &s_done;
+  C.s_red = s_red;
+  C.pa = C.pb = -1;
+  part_t *gp = A.parts + (int64_t)c * n;
+  const bool init = c < A.n_init;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) C.part[v] = init ? (part_t)0 : gp[v];
+  __syncthreads();
+  C.build();
+  if (init && k > 1) {
+    C.bisect_all(A.passes);
+    C.set_global_bounds();
+  } else {
+    C.set_global_bounds();
+  }
+  C.refine(A.passes, 0);
+  // outputs: parts, cut (from the rows), violation
+  int64_t cut2 = 0;
+  for (int v = threadIdx.x; v < n; v += blockDim.x) {
+    const int own = C.part[v];
+    gp[v] = C.part[v];
+    for (int q = 0; q < k; ++q)
+      if (q != own) cut2 += C.cget((int64_t)v * k + q);
+  }
+  cut2 = C.block_sum(cut2);
+  if (threadIdx.x == 0) {
+    int64_t vsum = 0;
+    for (int p = 0; p < k; ++p) vsum += C.over(p, pw[p]);
+    A.cut[c] = cut2 / 2;
+    A.viol[c] = vsum;
+  }
+}
+
+// winner = min (violation, cut, candidate index); copied into out
+__global__ void fm_pick(const int64_t *viol, const int64_t *cut, int C, const part_t *parts, int n,
+                        part_t *out, int32_t *winner) {
+  __shared__ int s_best;
+  if (threadIdx.x == 0) {
+    int b = 0;
+    for (int c = 1; c < C; ++c)
+      if (viol[c] < viol[b] || (viol[c] == viol[b] && cut[c] < cut[b])) b = c;
+    s_best = b;
+    if (winner) *winner = b;
+  }
+  __syncthreads();
+  const part_t *src = parts + (int64_t)s_best * n;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+    out[v] = src[v];
+}
+
+__global__ void fm_fill_copies(const part_t *cur, int n, part_t *parts, int c0, int copies) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (int64_t)copies * n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    parts[(int64_t)c0 * n + i] = cur[i % n];
+}
+
+__global__ void fm_fill_starts(const int32_t *starts, int64_t count, part_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (part_t)starts[i];
+}

@@ -179,19 +179,30 @@ class KwayResult:
 
 
 def partition_kway(graph, k: int, tpwgts: Optional[Sequence[float]] = None, tol: float = 0.03,
-                   seed: int = 0, out: Optional[torch.Tensor] = None) -> KwayResult:
+                   seed: int = 0, out: Optional[torch.Tensor] = None,
+                   reference_start: Optional[bool] = None) -> KwayResult:
     """Multilevel k-way partition (K3-K6) of a ``UGraph`` or ``DagCSR``.
 
     Balance: |w_p/total - t_p| <= tol for every part (the k-way
     generalisation of partition.py:72); default targets are uniform 1/k.
+
+    ``reference_start`` (default: graphs of at most ``recursive.MAX_KERNELS``
+    vertices) adds the reference heuristic applied recursively
+    (``recursive.py``) as a start partition; the partitioner refines it with
+    its own candidates and returns the best, so the cut never exceeds that
+    baseline's when the baseline meets the balance constraint.
     """
+    from . import recursive
     ug = graph if isinstance(graph, UGraph) else symmetrize(graph)
     if tpwgts is None:
         tpwgts = [1.0 / k] * k
     if len(tpwgts) != k:
         raise ValueError("need one target fraction per part")
     part = out if out is not None else torch.empty(ug.n, dtype=torch.int32, device=ug.xadj.device)
-    st = _native.partition_kway(ug, k, tpwgts, tol, seed, part)
+    if reference_start is None:
+        reference_start = 2 <= k and 2 <= ug.n <= recursive.MAX_KERNELS
+    starts = recursive.reference_recursive_start(ug, k, tpwgts, tol) if reference_start else None
+    st = _native.partition_kway(ug, k, tpwgts, tol, seed, part, starts)
     return KwayResult(part, st[0] * ug.weight_scale, st[1], st[2], st[3] / 1e9, bool(st[4]),
                       st[5])
 
