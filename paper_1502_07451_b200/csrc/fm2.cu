@@ -183,6 +183,7 @@ __device__ void fm2_body(const FmArgs &A, const int o) {
   }
 
   // ---- fm_refine ----
+  __syncthreads();  // every warp has read s_err in the loop test above
   if (tid == 0) {
     s_cut = cut_of(asg, A);
     s_err = fabs(cpu_weight(asg, A.w, n) / total - r);

@@ -270,7 +270,11 @@ struct FmCta {
     for (int m = moves - 1; m >= keep; --m) {
       const int code = trail[m];
       const int v = code >> 6, old = code & 63;
-      move(v, part[v], old);
+      // every thread reads the current part before thread 0 rewrites it
+      // inside move(): warps are not in lockstep
+      const int from = part[v];
+      __syncthreads();
+      move(v, from, old);
       __syncthreads();
     }
     return keep > 0;
@@ -311,7 +315,9 @@ struct FmCta {
       if (c.key == 0ull) break;
       const int64_t w = g.vw[c.v];
       // stop when taking the vertex overshoots more than stopping undershoots
-      if (!first && pw[b] + w - tgt_b > tgt_b - pw[b]) break;
+      const bool enough = !first && pw[b] + w - tgt_b > tgt_b - pw[b];
+      __syncthreads();  // pw[b] read by every thread before move() changes it
+      if (enough) break;
       move(c.v, a, b);
       __syncthreads();
       if (pw[b] >= tgt_b) break;
