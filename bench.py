@@ -51,6 +51,7 @@ def parse_args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs")
     ap.add_argument("--no-cholesky", action="store_true", help="skip the config-3 Cholesky block")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--profile-json", default=None,
                     help="optional path: dump the per-kernel live profile")
     return ap.parse_args()
@@ -186,14 +187,15 @@ def load_traffic(kernel: str):
     return None if k is None else k.get("dram_bytes_per_launch")
 
 
-def sample_dag_spec(n, seed=0):
-    """Host spec of one layered-DAG sample (for the CPU reference arm)."""
+def sample_dag_spec(n, seed=0, m_edges=None):
+    """Host spec of one layered-DAG sample (for the CPU reference arm): the
+    device generator's family (oracle/layered_oracle.py), 10 edges per task."""
     from oracle import layered_oracle as LO
     from paper_1502_07451_b200.costs import SyntheticCostModel
     m = SyntheticCostModel()
     wc, wg = m.kernel_time("MA", 512, "CPU"), m.kernel_time("MA", 512, "GPU")
     wx = m.transfer_time(512 * 512 * 4)
-    _, edges, _ = LO.generate(n, 10 * n, seed)
+    _, edges, _ = LO.generate(n, 10 * n if m_edges is None else m_edges, seed)
     return {"root": 0,
             "nodes": [[0, "SOURCE", 0, 0.0, 0.0]] + [[i, "MA", 512, wc, wg]
                                                     for i in range(1, n + 1)],
@@ -209,46 +211,202 @@ def _oracle_partition(args):
     return time.perf_counter() - t0
 
 
-def cpu_partition_sample(n: int, workers: int, seed: int = 0):
-    """Wall seconds for `workers` concurrent oracle partitions of n-task samples."""
-    if workers <= 1:
-        return _oracle_partition((n, seed))
+def _fork_pool(workers: int):
     import multiprocessing as mp
-    ctx = mp.get_context("fork")
+    return mp.get_context("fork").Pool(workers)
+
+
+# the reference heuristic cannot finish config 4 (~n^2.2), so it
+# runs on a size ladder of the same DAG family, the exponent is fitted and the
+# 10M-task time extrapolated and labelled as such (DNF above the cap).
+LADDER = (250, 500, 1000, 2000)
+LADDER_OURS = (250, 500, 1000)   # the bounded cpu_baseline leg of our own arm
+CPU_CAP_S = 600.0
+CFG2_N, CFG2_M = 100_000, 1_000_000
+
+
+def fit_power(points):
+    """Least-squares fit of t = a * n^b on log-log axes: (a, b)."""
+    import math
+    xs = [math.log(n) for n, _ in points]
+    ys = [math.log(t) for _, t in points]
+    mx, my = statistics.fmean(xs), statistics.fmean(ys)
+    b = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / sum((x - mx) ** 2 for x in xs)
+    return math.exp(my - b * mx), b
+
+
+def ladder_summary(points):
+    a, b = fit_power(points)
+    t10 = a * N_TASKS ** b
+    return {"points_s": {str(n): t for n, t in points}, "exponent": b,
+            "fit": "t = a*n^b, least squares on log-log", "extrapolated_10m_s": t10,
+            "cap_s": CPU_CAP_S, "dnf_at_10m": t10 > CPU_CAP_S,
+            "label": "extrapolated (the reference heuristic does not finish 10M tasks)"}
+
+
+def cfg2_cpu_count(n_kernels: int) -> int:
+    """The 2-way assignment of the config-2 evaluate comparison: kernel positions
+    [0, n/5) on the CPU, the rest on the GPU (same on both arms)."""
+    return n_kernels // 5
+
+
+def _oracle_cfg2_evaluate(_=None):
+    """The reference's evaluate() (oracle port, partition.py:60-73, incl. its
+    per-call edge sort) on the config-2 DAG (100k tasks / 1M edges)."""
+    from oracle import hetsched_oracle as O
+    g = O.OGraph(sample_dag_spec(CFG2_N, 0, CFG2_M))
+    ids = g.kernel_ids()
+    ncpu = cfg2_cpu_count(len(ids))
+    asg = {i: (O.CPU if j < ncpu else O.GPU) for j, i in enumerate(ids)}
+    r = O.workload_ratio(g)
     t0 = time.perf_counter()
-    with ctx.Pool(workers) as pool:
-        pool.map(_oracle_partition, [(n, seed + i) for i in range(workers)])
-    return time.perf_counter() - t0
+    cut, err, (cw, gw) = O.evaluate(g, asg, r)
+    dt = time.perf_counter() - t0
+    return {"seconds": dt, "cut": cut, "cpu_w": cw, "gpu_w": gw, "err": err}
+
+
+def _cfg5_spec(seed: int):
+    """generate_random_dag(38, 75, "MA", 1024, seed) + SyntheticCostModel weights as
+    an oracle spec (input synthesis: the host restatement of graph.py:180-324)."""
+    from paper_1502_07451_b200.costs import SyntheticCostModel
+    from paper_1502_07451_b200.gen import generate_random_dag
+    from paper_1502_07451_b200.graph import attach_weights
+    g = attach_weights(generate_random_dag(38, 75, "MA", 1024, seed=seed), SyntheticCostModel())
+    return {"root": g.root,
+            "nodes": [[x.id, x.kind, x.size, x.weight_cpu, x.weight_gpu]
+                      for x in sorted(g.nodes.values(), key=lambda x: x.id)],
+            "edges": [[u, v, e.bytes, e.weight_xfer] for (u, v), e in sorted(g.edges.items())]}
+
+
+def _oracle_cfg5_chunk(seeds):
+    """compare(["eager", "dmda", "gp"], factory, MachineModel(3, 1)) iterations
+    (sim.py:269-306): per (policy, iteration) the graph is built by the factory,
+    gp partitions it with the reference heuristic, then simulate()."""
+    from oracle import hetsched_oracle as O
+    t0 = time.process_time()
+    out = {"eager": [], "dmda": [], "gp": []}
+    for s in seeds:
+        for name in ("eager", "dmda", "gp"):
+            g = O.OGraph(_cfg5_spec(s))
+            pin = O.partition_heuristic(g, O.workload_ratio(g)) if name == "gp" else None
+            r = O.simulate(g, name, pin)
+            out[name].append((r["makespan"], r["transfer_count"]))
+    return out, time.process_time() - t0
+
+
+def cfg5_reference_sweep(pool, workers: int, iterations: int = 4096):
+    """The config-5 sweep by the oracle port on `workers` host processes."""
+    chunks = [list(range(i, iterations, workers)) for i in range(workers)]
+    t0 = time.perf_counter()
+    res = pool.map(_oracle_cfg5_chunk, chunks)
+    wall = time.perf_counter() - t0
+    per = {"eager": [None] * iterations, "dmda": [None] * iterations, "gp": [None] * iterations}
+    cpu_s = 0.0
+    for seeds, (out, cs) in zip(chunks, res):
+        cpu_s += cs
+        for name, vals in out.items():
+            for s, v in zip(seeds, vals):
+                per[name][s] = v
+    means = {name: (statistics.fmean([v[0] for v in vals]),
+                    statistics.fmean([float(v[1]) for v in vals])) for name, vals in per.items()}
+    return {"iterations": iterations, "wall_s": wall, "workers": workers,
+            "cpu_s_one_core_equivalent": cpu_s,
+            "means": {k: {"makespan": m, "transfers": t} for k, (m, t) in means.items()},
+            "matches_reference_means_bit_exact": all(means[k] == REF_CFG5[k] for k in REF_CFG5)}
 
 
 # ------------------------------------------------------------- reference --
 def run_reference(args):
+    """The reference's CPU algorithm (oracle port) on this box's host cores.
+
+    value: config-4 partition ms, extrapolated from the measured ladder (the
+    heuristic does not finish 10M tasks; labelled). Each timed step is one
+    bounded sample: partition_heuristic on a 250-task DAG of the family.
+    Measured on the same configs as our arm (no extrapolation): the config-2
+    evaluate() at 100k/1M and the config-5 sweep (3 x 4096 simulations).
+    """
     rank, world, _ = dist_env()
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    n = 300
+    workers = max(1, cores - 1)  # the main process times the steps
+    pool = _fork_pool(workers)
+    lad = {n: pool.apply_async(_oracle_partition, ((n, 0),)) for n in sorted(LADDER, reverse=True)}
+    ev = pool.apply_async(_oracle_cfg2_evaluate)
+    n_step = LADDER[0]
     for _ in range(args.warmup):
-        cpu_partition_sample(n, cores, seed=1000)
-    times = [cpu_partition_sample(n, cores, seed=2000 + 100 * i) for i in range(args.steps)]
-    per_step = statistics.fmean(times)
-    ms_10m = per_step / (cores * n) * N_TASKS * 1e3
+        _oracle_partition((n_step, 1000))
+    times = [_oracle_partition((n_step, 2000 + i)) for i in range(args.steps)]
+    cfg5 = cfg5_reference_sweep(pool, max(1, workers - len(LADDER) - 1))
+    points = [(n, lad[n].get()) for n in LADDER]
+    cfg2 = ev.get()
+    pool.close()
+    pool.join()
+    lsum = ladder_summary(points)
+    value = lsum["extrapolated_10m_s"] * 1e3
     line = {
-        "impl": "reference", "metric": METRIC, "value": ms_10m, "unit": UNIT,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": per_step * 1e3, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg4: layered DAG 10M tasks / 100M edges, k=8 (reference "
-                               "algorithm on bounded samples, scaled linearly)",
-                   "n_tasks": N_TASKS, "n_edges": M_EDGES, "k": K_PARTS},
-        "cpu_baseline": {"value": ms_10m, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{cores} concurrent partition_heuristic runs (oracle port of "
-                                   f"partition.py:258-295) on {n}-task/{10 * n}-edge layered DAGs "
-                                   "per step; linear scaling to 10M tasks is a lower bound "
-                                   "(the algorithm is ~n^2.4)"},
-        "e2e": {"value": ms_10m, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ms_per_step": statistics.fmean(times) * 1e3, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": headline_config(world),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"partition_heuristic (oracle port of partition.py:258-295, "
+                                   f"single-threaded like the reference) on layered DAGs of the "
+                                   f"config-4 family at n = {list(LADDER)} (10 edges/task), fitted "
+                                   f"n^{lsum['exponent']:.2f} and extrapolated to 10M tasks; each "
+                                   f"timed step is one {n_step}-task sample"},
+        "extrapolation": lsum,
+        "measured_same_config": {
+            "cfg2_evaluate": {"workload": "evaluate() of a 2-way assignment, 100k tasks / 1M "
+                                          "edges (config 2), reference semantics",
+                              "ms": cfg2["seconds"] * 1e3, "cores": 1, "cut": cfg2["cut"],
+                              "cpu_w": cfg2["cpu_w"], "gpu_w": cfg2["gpu_w"]},
+            "cfg5_sweep": dict(cfg5, workload="compare(eager, dmda, gp) x 4096 iterations of "
+                                              "generate_random_dag(38, 75, MA, 1024)"),
+        },
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def headline_config(world: int):
+    """The config block both arms print (the driver compares them)."""
+    return {"workload": "cfg4: layered task DAG, 10M tasks / 100M edges, k=8 partition "
+                        "(single-level: the locality probe skips coarsening on this "
+                        "triangle-free DAG; the forced multilevel time is in extra)",
+            "n_tasks": N_TASKS, "n_edges": M_EDGES, "k": K_PARTS, "tol": TOL,
+            "parallelism": ("1 GPU" if world == 1 else
+                            f"sharded x{world}: vertex ranges, NVLink peer arenas"),
+            "l2": "inputs (2.4 GB CSR) larger than L2; no flush"}
+
+
+def cpu_baseline_leg(extra):
+    """Our arm's bounded CPU baseline (rank 0, N=1): the ladder's three smaller
+    points and the config-2 evaluate() run concurrently (~40 s wall), each on
+    one core like the single-threaded reference."""
+    pool = _fork_pool(len(LADDER_OURS) + 1)
+    lad = {n: pool.apply_async(_oracle_partition, ((n, 0),)) for n in LADDER_OURS}
+    ev = pool.apply_async(_oracle_cfg2_evaluate)
+    points = [(n, lad[n].get()) for n in LADDER_OURS]
+    cfg2 = ev.get()
+    pool.close()
+    pool.join()
+    lsum = ladder_summary(points)
+    out = {"value": lsum["extrapolated_10m_s"] * 1e3, "unit": UNIT, "cores": 1, "kind": "port",
+           "sample": f"partition_heuristic (oracle port of partition.py:258-295) at n = "
+                     f"{list(LADDER_OURS)} tasks of the config-4 DAG family, fitted "
+                     f"n^{lsum['exponent']:.2f}, extrapolated to 10M tasks (the reference "
+                     f"does not finish it: DNF > {CPU_CAP_S:.0f} s)",
+           "extrapolation": lsum}
+    gpu = extra.get("cfg2_evaluate_2way") if extra else None
+    out["measured_cfg2_evaluate"] = {
+        "ms": cfg2["seconds"] * 1e3, "cores": 1, "cut": cfg2["cut"], "cpu_w": cfg2["cpu_w"],
+        "gpu_ms": gpu["ms_1"] if gpu else None,
+        "speedup": (cfg2["seconds"] * 1e3 / gpu["ms_1"]) if gpu else None,
+        "bit_exact": (gpu is not None and gpu["cut"] == cfg2["cut"] and
+                      gpu["cpu_w"] == cfg2["cpu_w"] and gpu["gpu_w"] == cfg2["gpu_w"])}
+    return out
 
 
 # ------------------------------------------------------------------ ours --
@@ -288,7 +446,10 @@ def run_ours(args):
 
     def partition(g, w, n, w_in):
         if world == 1:
-            return kway.partition_kway(kway.symmetrize(g, w, n, w_in), K_PARTS, tol=TOL, seed=0)
+            # band start in the DAG's own numbering when it is topological
+            # (creation order, as generated), else in longest-path level order
+            return kway.partition_dag(g, K_PARTS, tol=TOL, seed=0, edge_w_i=w, node_w_i=n,
+                                      edge_w_i_in=w_in, order="auto")
         ug = kway.symmetrize_range(g, kv0, kv1, w, n, w_in, cap=cap)
         return kway.partition_kway_shard(ug, kv0, n_glob, group, rank, K_PARTS, tol=TOL, seed=0,
                                          out=part_buf)
@@ -426,13 +587,8 @@ def run_ours(args):
             chol = cholesky_partitioned(args, dev, rank, world)
 
     cpu = None
-    if rank == 0 and world == 1:
-        n = 600
-        secs = cpu_partition_sample(n, 1)
-        cpu = {"value": secs / n * N_TASKS * 1e3, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": f"one partition_heuristic (oracle port of partition.py:258-295) on a "
-                         f"{n}-task/{10 * n}-edge layered DAG: {secs:.2f} s; scaled linearly to "
-                         "10M tasks (a lower bound, the algorithm is ~n^2.4)"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_leg(extra)
 
     if rank == 0:
         line = {
@@ -440,12 +596,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "int32", "data": "synthetic",
-            "config": {"workload": "cfg4: layered task DAG, 10M tasks / 100M edges, k=8 "
-                                   "multilevel partition (device-resident input)",
-                       "n_tasks": N_TASKS, "n_edges": M_EDGES, "k": K_PARTS, "tol": TOL,
-                       "parallelism": ("1 GPU" if world == 1 else
-                                       f"sharded x{world}: vertex ranges, NVLink peer arenas"),
-                       "l2": "inputs (2.4 GB CSR) larger than L2; no flush"},
+            "config": headline_config(world),
             "quality": {"cut": res.cut, "levels": res.levels, "coarsest": res.coarsest,
                         "max_deviation": res.max_deviation, "feasible": res.feasible,
                         "refine_passes": res.refine_passes},
@@ -662,7 +813,6 @@ def policy_sweep(iterations: int = 4096):
     out["sweep_s_incl_gp_partitions"] = out["gp_partitions_s"] + dev_ms / 1e3
     if iterations == 4096:
         out["matches_reference_means_bit_exact"] = exact
-    out["reference_cpu_s"] = 80.0  # SURVEY §3C probe: reference compare(), 1 core (not re-timed)
     return out
 
 
@@ -695,7 +845,21 @@ def secondary(csr10m, args):
     out["cfg4_forced_coarsening_ms"] = ms
     out["cfg4_forced_coarsening_cut"] = r.cut
     out["cfg4_forced_coarsening_levels"] = r.levels
+    # id-order robustness: the same DAG under a random numbering (auto order:
+    # not topological -> band start in longest-path level order), and the
+    # level order forced on the generated numbering
+    ms, r = timed(lambda: kway.partition_dag(csr10m, 8, tol=TOL, edge_w_i=ew4, node_w_i=nw4,
+                                             order="levels"))
+    out["cfg4_level_order_ms"] = ms
+    out["cfg4_level_order_cut"] = r.cut
     del ew4, nw4
+    rel, _ = kway.relabeled_dag(csr10m, seed=1)
+    ms, r = timed(lambda: kway.partition_dag(rel, 8, tol=TOL))
+    out["cfg4_relabeled_ms"] = ms
+    out["cfg4_relabeled_cut"] = r.cut
+    out["cfg4_relabeled_feasible"] = r.feasible
+    del rel
+    torch.cuda.empty_cache()
     # K7 levels + critical path on the 10M DAG
     ms, (lv, fin, cp, nl) = timed(lambda: kway.levels(csr10m))
     out["cfg4_levels_critical_path_ms"] = ms
@@ -713,17 +877,58 @@ def secondary(csr10m, args):
     out["cfg2_evaluate_64_assignments_ms"] = ms
     out["cfg2_transfer_count"] = int(e["xfer_count"][0])
     out["cfg2_transfer_bytes"] = int(e["xfer_bytes"][0])
+    # the reference's evaluate() (partition.py:60-73) on config 2, K2 mode 0
+    # (bit-exact CPython sum semantics), the assignment of cfg2_cpu_count
+    nk = c2.n - 1
+    two = torch.ones((1, nk), dtype=torch.int8, device=c2.device)
+    two[0, :cfg2_cpu_count(nk)] = 0
+    ms1, (cut2, cw2, tot2) = timed(lambda: _native.evaluate2(c2, two, 1, 0))
+    two64 = two.repeat(64, 1).contiguous()
+    ms64, _ = timed(lambda: _native.evaluate2(c2, two64, 1, 0))
+    out["cfg2_evaluate_2way"] = {"ms_1": ms1, "ms_64": ms64, "cut": float(cut2[0]),
+                                 "cpu_w": float(cw2[0]),
+                                 "gpu_w": float(tot2[0]) - float(cw2[0])}
     # level-synchronous makespan of the k=8 assignment (K7 mode 3)
     node_part = parts[0].contiguous()
     ms, (mk, _) = timed(lambda: kway.assigned_makespan(c2, node_part, k=8))
     out["cfg2_assigned_makespan_ms"] = ms
     out["cfg2_assigned_makespan"] = mk
+    # the config-3 task DAG (tiled Cholesky T=64: 45,760 tasks, 131,040 edges,
+    # calibration weights: POTRF/TRSM/SYRK/GEMM differ) partitioned k=8, and
+    # the smoke-sized 20k/200k layered DAG (multilevel: coarsening + CTA FM)
+    from paper_1502_07451_b200.costs import load_calibration
+    from paper_1502_07451_b200.gen import cholesky_dag
+    chol_csv = ("kind,size,time_cpu_ms,time_gpu_ms\nPOTRF,512,6.0,0.9\nTRSM,512,11.0,0.45\n"
+                "SYRK,512,11.5,0.42\nGEMM,512,22.0,0.6\n[transfer]\n"
+                "latency_ms,bandwidth_bytes_per_ms\n0.01,12000000.0\n")
+    cg = cholesky_dag(64, 512, load_calibration(chol_csv)).csr()
+    ms, r = timed(lambda: kway.partition_dag(cg, 8, tol=TOL))
+    out["cfg3_dag_partition_ms"] = ms
+    out["cfg3_dag_partition"] = {"cut": r.cut, "levels": r.levels, "coarsest": r.coarsest,
+                                 "max_deviation": r.max_deviation, "feasible": r.feasible}
+    s20 = kway.layered_dag(20_000, 200_000, seed=1)
+    ms, r = timed(lambda: kway.partition_dag(s20, 8, tol=TOL))
+    out["smoke_20k_partition_ms"] = ms
+    out["smoke_20k_partition"] = {"cut": r.cut, "levels": r.levels, "feasible": r.feasible}
     out["cfg5_policy_sweep"] = policy_sweep(4096)
     return out
 
 
 def main():
     args = parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # launched without torchrun: spawn one rank per GPU ourselves
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+               f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -194,6 +194,30 @@ int hs_assigned_makespan(const hs_dag_t *g, const int32_t *part, const int8_t *d
 int hs_level_order(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
                    int32_t *order, void *stream);
 
+/* ---- vertex orders for the k-way band start (csrc/order.cu) -----------
+ * The partitioner's band start cuts kernel positions into weight ranges; it
+ * relies on positions following the DAG's layers, as creation-order numbering
+ * does (every edge u -> v with u < v). Other numberings are relabelled in
+ * longest-path level order (ties by position) first.
+ *
+ * result_host = 1 when every non-root edge u -> v has u < v (first entry of
+ * each sorted out-list checked). */
+int hs_dag_is_topological(const hs_dag_t *g, int32_t *result_host, void *stream);
+/* Kernel positions (root excluded) stably sorted by level (hs_levels):
+ * perm[new] = old position, inv[old] = new position; both [n-1]. */
+int hs_level_permutation(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
+                         int32_t *perm, int32_t *inv, void *stream);
+/* The kernel graph relabelled: row i of the output is row perm[i] of g with
+ * every neighbour id u replaced by inv[u]; vwgt_i permuted alike. Output
+ * arrays: xadj [n+1], adjncy/adjwgt_i [nnz] (adjwgt_i only when g has
+ * integer weights), vwgt_i [n]. */
+int hs_ugraph_permute(const hs_ugraph_t *g, const int32_t *perm, const int32_t *inv,
+                      int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i,
+                      void *stream);
+/* part[perm[i]] = part_new[i] for i < n. */
+int hs_parts_unpermute(int32_t n, const int32_t *perm, const int32_t *part_new, int32_t *part,
+                       void *stream);
+
 /* ---- K8 batched discrete-event simulation -----------------------------
  * Replaces sim.simulate (sim.py:68-204) with EagerPolicy / DmdaPolicy /
  * GraphPartitionPolicy (policies.py:19-99), one simulation per thread,

@@ -218,6 +218,48 @@ def level_order(csr, level: torch.Tensor, n_levels: int) -> torch.Tensor:
     return order
 
 
+_is_topological = _opt("hs_dag_is_topological", _P, _P, _P)
+_level_permutation = _opt("hs_level_permutation", _P, _P, _i32, _P, _P, _P)
+_ugraph_permute = _opt("hs_ugraph_permute", _P, _P, _P, _P, _P, _P, _P, _P)
+_parts_unpermute = _opt("hs_parts_unpermute", _i32, _P, _P, _P, _P)
+
+
+def dag_is_topological(csr) -> bool:
+    out = ctypes.c_int32(0)
+    check(_need(_is_topological, "hs_dag_is_topological")(ctypes.byref(csr.struct()),
+                                                          ctypes.byref(out), stream_ptr()))
+    return bool(out.value)
+
+
+def level_permutation(csr, level: torch.Tensor, n_levels: int):
+    nk = csr.n - 1
+    perm = torch.empty(nk, dtype=torch.int32, device=csr.device)
+    inv = torch.empty(nk, dtype=torch.int32, device=csr.device)
+    check(_need(_level_permutation, "hs_level_permutation")(
+        ctypes.byref(csr.struct()), ptr(level), n_levels, ptr(perm), ptr(inv), stream_ptr()))
+    return perm, inv
+
+
+def ugraph_permute(ug, perm: torch.Tensor, inv: torch.Tensor):
+    """(xadj, adjncy, adjwgt or None, vwgt) of the relabelled graph."""
+    dev = ug.xadj.device
+    xadj = torch.empty(ug.n + 1, dtype=torch.int64, device=dev)
+    adjncy = torch.empty(ug.nnz, dtype=torch.int32, device=dev)
+    adjwgt = (torch.empty(ug.nnz, dtype=torch.int32, device=dev)
+              if ug._adjwgt is not None else None)
+    vwgt = torch.empty(ug.n, dtype=torch.int32, device=dev)
+    check(_need(_ugraph_permute, "hs_ugraph_permute")(
+        ctypes.byref(ug.struct()), ptr(perm), ptr(inv), ptr(xadj), ptr(adjncy),
+        ptr(adjwgt) if adjwgt is not None else None, ptr(vwgt), stream_ptr()))
+    return xadj, adjncy, adjwgt, vwgt
+
+
+def parts_unpermute(perm: torch.Tensor, part_new: torch.Tensor, out: torch.Tensor):
+    check(_need(_parts_unpermute, "hs_parts_unpermute")(int(perm.numel()), ptr(perm),
+                                                        ptr(part_new), ptr(out), stream_ptr()))
+    return out
+
+
 def simulate_batch(batch, policy: int, pin: Optional[torch.Tensor], cpu_workers: int,
                    gpu_workers: int, events: bool = False):
     """Runs batch.batch simulations; returns a dict of device tensors."""

@@ -45,32 +45,118 @@ __global__ void round_kernel(const unsigned long long *acc, int count, double *o
 }
 
 // ---------------------------------------------------------------- K2 -----
-// mode 0: one thread per assignment, reference order, CPython sum() semantics.
-__global__ void eval2_ordered(hs_dag_t g, const int8_t *part, int batch, int src_gpu,
-                              double *cut, double *cpu_w, double *total) {
-  int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= batch) return;
+// mode 0: reference order, CPython sum() semantics (partition.py:62-69).
+// The sums are order-dependent (Neumaier-compensated, not associative), so
+// each stays one sequential chain: its cost is one dependent fp64 add per
+// kept term. Everything else runs beside it: eval2_flags marks the cut
+// edges of every assignment in parallel; eval2_seq gives each (sum,
+// assignment) a 2-warp CTA where warp 0 streams the terms (coalesced,
+// filtered and compacted in order into a shared-memory chunk) while lane 0 of
+// warp 1 adds the previous chunk, double-buffered.
+__global__ void eval2_flags(hs_dag_t g, const int8_t *part, uint8_t *flags) {
+  const int b = blockIdx.y;
   const int nk = g.n - 1;
   const int8_t *p = part + (int64_t)b * nk;
-  const double *w = src_gpu ? g.w_gpu : g.w_cpu;
-  hs::PySum sc, scpu, stot;
-  for (int u = 0; u < g.n; ++u) {
-    if (u == g.root) continue;
-    int8_t pu = p[kpos(u, g.root)];
-    for (int64_t e = g.out_ptr[u]; e < g.out_ptr[u + 1]; ++e) {
-      int v = g.out_dst[e];
-      if (v == g.root) continue;
-      if (pu != p[kpos(v, g.root)]) sc.add(g.w_xfer[e]);
+  uint8_t *f = flags + (int64_t)b * g.m;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < g.n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e0 = g.out_ptr[u], e1 = g.out_ptr[u + 1];
+    if (u == g.root) {
+      for (int64_t e = e0; e < e1; ++e) f[e] = 0;
+      continue;
+    }
+    const int8_t pu = p[kpos((int)u, g.root)];
+    for (int64_t e = e0; e < e1; ++e) {
+      const int v = g.out_dst[e];
+      f[e] = (v != g.root && pu != p[kpos(v, g.root)]) ? 1 : 0;
     }
   }
-  for (int v = 0; v < g.n; ++v) {
-    if (v == g.root) continue;
-    if (p[kpos(v, g.root)] == 0) scpu.add(w[v]);
-    stot.add(w[v]);
+}
+
+constexpr int kSeqChunk = 1024;  // terms per producer step (32 per lane)
+
+__global__ void __launch_bounds__(64) eval2_seq(hs_dag_t g, const int8_t *part,
+                                                const uint8_t *flags, int src_gpu, double *cut,
+                                                double *cpu_w, double *total) {
+  __shared__ double buf[2][kSeqChunk];
+  __shared__ int cnt[2];
+  const int which = blockIdx.x, b = blockIdx.y;
+  const int nk = g.n - 1;
+  const int8_t *p = part + (int64_t)b * nk;
+  const uint8_t *f = flags + (int64_t)b * g.m;
+  const double *w = src_gpu ? g.w_gpu : g.w_cpu;
+  const int64_t len = which == 0 ? g.m : (int64_t)g.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  hs::PySum acc;
+  const int64_t steps = (len + kSeqChunk - 1) / kSeqChunk;
+  for (int64_t it = 0; it <= steps; ++it) {
+    if (warp == 0 && it < steps) {  // producer: terms [it*chunk, +chunk) -> buf[it & 1]
+      double *out = buf[it & 1];
+      int c = 0;
+      const int64_t base = it * kSeqChunk;
+      double val[32];
+      bool keep[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int64_t i = base + j * 32 + lane;
+        keep[j] = false;
+        val[j] = 0.0;
+        // unconditional loads: none waits for a flag, all 64 are in flight
+        if (i < len) {
+          if (which == 0) {
+            keep[j] = __ldg(f + i) != 0;
+            val[j] = __ldg(g.w_xfer + i);
+          } else {
+            const int v = (int)i;
+            keep[j] = v != g.root && (which == 2 || __ldg(p + kpos(v, g.root)) == 0);
+            val[j] = __ldg(w + v);
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const unsigned m = __ballot_sync(0xffffffffu, keep[j]);
+        if (keep[j]) out[c + __popc(m & ((1u << lane) - 1))] = val[j];
+        c += __popc(m);
+      }
+      if (lane == 0) cnt[it & 1] = c;
+    }
+    if (warp == 1 && lane == 0 && it > 0) {  // consumer: the previous chunk, in order
+      const double *in = buf[(it - 1) & 1];
+      const int c = cnt[(it - 1) & 1];
+      int i = 0;
+      if (!acc.started && c > 0) acc.add(in[i++]);
+      // PySum::add without the first-term branch; the terms are loaded 8
+      // ahead so only the dependent adds are on the chain
+      double f = acc.f, cc = acc.c;
+      for (; i + 8 <= c; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = in[i + j];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double t = f + x[j];
+          cc += fabs(f) >= fabs(x[j]) ? (f - t) + x[j] : (x[j] - t) + f;
+          f = t;
+        }
+      }
+      for (; i < c; ++i) {
+        const double x = in[i];
+        const double t = f + x;
+        cc += fabs(f) >= fabs(x) ? (f - t) + x : (x - t) + f;
+        f = t;
+      }
+      acc.f = f;
+      acc.c = cc;
+    }
+    __syncthreads();
   }
-  cut[b] = sc.started ? sc.result() : 0.0;
-  cpu_w[b] = scpu.started ? scpu.result() : 0.0;
-  total[b] = stot.started ? stot.result() : 0.0;
+  if (warp == 1 && lane == 0) {
+    const double r = acc.started ? acc.result() : 0.0;
+    if (which == 0) cut[b] = r;
+    else if (which == 1) cpu_w[b] = r;
+    else total[b] = r;
+  }
 }
 
 // mode 1: correctly rounded sums, all nodes/edges in parallel.
@@ -233,8 +319,19 @@ extern "C" int hs_evaluate2(const hs_dag_t *g, const int8_t *part, int32_t batch
   if (batch <= 0) return HS_OK;
   cudaStream_t s = (cudaStream_t)stream;
   if (mode == 0) {
-    eval2_ordered<<<(batch + 63) / 64, 64, 0, s>>>(*g, part, batch, weight_source, cut, cpu_w,
-                                                   total);
+    hs::Scratch<uint8_t> flags;
+    HS_CHECK_CUDA(flags.alloc((size_t)batch * (g->m > 0 ? g->m : 1), s));
+    {
+      hs::Prof P("evaluate2_flags", s, (double)batch * (8.0 * g->n + 5.0 * g->m + 1.0 * g->n +
+                                                        1.0 * g->m));
+      eval2_flags<<<dim3(hs::grid_for(g->n, 256, hs::sm_count() * 4), batch), 256, 0, s>>>(
+          *g, part, flags);
+    }
+    HS_CHECK_LAUNCH();
+    {
+      hs::Prof P("evaluate2_ordered_sums", s, (double)batch * (9.0 * g->m + 17.0 * g->n));
+      eval2_seq<<<dim3(3, batch), 64, 0, s>>>(*g, part, flags, weight_source, cut, cpu_w, total);
+    }
     HS_CHECK_LAUNCH();
     return HS_OK;
   }

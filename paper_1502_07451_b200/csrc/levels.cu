@@ -4,43 +4,36 @@
 // best[v] = max(best[p] for p in preds, default 0.0) + min(w_cpu, w_gpu).
 // max is exact and each node adds once, so any topological schedule gives
 // the reference's bits. Here the schedule is level-synchronous Kahn: frontier
-// i holds exactly the nodes at longest-path depth i, one persistent
-// cooperative kernel walks the frontiers with a grid barrier in between.
+// i holds exactly the nodes at longest-path depth i (so the level is the
+// frontier index), one persistent cooperative kernel walks the frontiers with
+// a grid barrier in between.
+//
+// Push form: a finished node pushes its finish time into every successor
+// (atomicMax on the ordered bits of a non-negative double, = the max over
+// the predecessors, exactly) and decrements the successor's pending count;
+// the count reaching 0 appends it to the next frontier. Every edge is
+// touched once, by one lane: a warp takes 32 frontier nodes and flattens
+// their out-lists across its lanes (warp prefix of the degrees), so a node
+// of degree 10 does not leave 22 lanes idle and the per-edge atomics of
+// different nodes overlap. The state (pending 4 B, reach 8 B per node) is
+// L2-resident at config 4 (120 MB).
 #include "common.cuh"
+#include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
 
 namespace {
 
-__device__ __forceinline__ double pmax(double a, double b) { return b > a ? b : a; }
 __device__ __forceinline__ double pmin(double a, double b) { return b < a ? b : a; }
-
-struct GridBarrier {
-  unsigned *count, *gen;
-  __device__ void sync(unsigned nblocks) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned g0 = *(volatile unsigned *)gen;
-      __threadfence();
-      if (atomicAdd(count, 1u) == nblocks - 1) {
-        *(volatile unsigned *)count = 0;
-        __threadfence();
-        atomicAdd(gen, 1u);
-      } else {
-        while (*(volatile unsigned *)gen == g0) __nanosleep(32);
-      }
-      __threadfence();
-    }
-    __syncthreads();
-  }
-};
 
 struct LevelArgs {
   hs_dag_t g;
   int mode;
-  int32_t *indeg;
+  // per node, interleaved so both atomics of an edge hit one 32-byte sector:
+  // st[2v] = max over pushed predecessor finish bits, st[2v+1] low word =
+  // pending predecessor count
+  unsigned long long *st;
   int32_t *front[3];
   int32_t *counts;    // [3]
-  unsigned *bar;      // [2]
   int32_t *level;
   double *finish;
   int32_t *max_level; // [1]
@@ -52,23 +45,62 @@ struct LevelArgs {
   const int8_t *dev;
 };
 
-constexpr int kStage = 2048;  // frontier entries staged per block and level
+// warp-aggregated append of the lanes with `want` to list/count
+__device__ __forceinline__ void warp_append(bool want, int32_t val, int32_t *list,
+                                            int32_t *count) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(count, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  if (want) list[base + __popc(m & ((1u << lane) - 1))] = val;
+}
 
-__global__ void levels_kernel(LevelArgs A) {
+constexpr int kStage = 4096;  // next-frontier entries staged per block and level
+
+// warp-aggregated append into the block's staging buffer (one shared atomic
+// per warp and step; a global counter hit by every warp serialises in L2);
+// overflow goes to the global list directly
+__device__ __forceinline__ void stage_append(bool want, int32_t val, int32_t *s_buf, int *s_n,
+                                             int32_t *list, int32_t *count) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == __ffs(m) - 1) base = atomicAdd(s_n, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+  const int at = base + __popc(m & ((1u << lane) - 1));
+  const bool spill = want && at >= kStage;
+  if (want && !spill) s_buf[at] = val;
+  warp_append(spill, val, list, count);
+}
+
+__global__ void __launch_bounds__(1024) levels_kernel(LevelArgs A) {
   __shared__ int32_t s_buf[kStage];
   __shared__ int s_n, s_base;
   if (threadIdx.x == 0) s_n = 0;
-  __syncthreads();
-  GridBarrier bar{A.bar, A.bar + 1};
+  auto grid = cooperative_groups::this_grid();
   const hs_dag_t &g = A.g;
+  const int lane = threadIdx.x & 31;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t v = tid; v < g.n; v += stride) {
-    int32_t d = (int32_t)(g.in_ptr[v + 1] - g.in_ptr[v]);
-    A.indeg[v] = d;
-    if (d == 0) A.front[0][atomicAdd(&A.counts[0], 1)] = (int32_t)v;
+  // warp rank interleaved across blocks: a small frontier is spread over
+  // every SM instead of filling the first few blocks
+  const int64_t nwarps = stride >> 5;
+  const int64_t wid = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  for (int64_t base = tid - lane; base < g.n; base += stride) {
+    const int64_t v = base + lane;
+    bool src = false;
+    if (v < g.n) {
+      const int32_t d = (int32_t)(g.in_ptr[v + 1] - g.in_ptr[v]);
+      A.st[2 * v] = 0ull;
+      A.st[2 * v + 1] = (unsigned long long)(uint32_t)d;
+      src = d == 0;
+    }
+    warp_append(src, (int32_t)v, A.front[0], &A.counts[0]);
   }
-  bar.sync(gridDim.x);
+  grid.sync();
   int lmax = -1;
   double cmax = 0.0;
   int32_t done = 0;
@@ -77,49 +109,92 @@ __global__ void levels_kernel(LevelArgs A) {
     const int32_t ncur = __ldcg(&A.counts[cur]);
     if (ncur == 0) break;
     if (tid == 0) A.counts[(it + 2) % 3] = 0;
-    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ncur; base += stride) {
-      const int64_t i = base + threadIdx.x;
-      if (i >= ncur) continue;
-      const int v = __ldcg(&A.front[cur][i]);
-      double reach = 0.0;
-      int lv = 0;
-      bool first = true;
-      const int pv = (A.mode == 3 && v != g.root) ? A.part[v] : 0;
-      for (int64_t j = g.in_ptr[v]; j < g.in_ptr[v + 1]; ++j) {
-        int p = g.in_src[j];
-        double f = __ldcg(&A.finish[p]);
-        if (A.mode == 3) {
-          // an input crosses when it comes from another part; the root's
-          // data starts in host memory, so it crosses into GPU parts only
-          const bool cross = p == g.root ? A.dev[pv] != 0 : A.part[p] != pv;
-          if (cross) f = f + g.w_xfer[g.in_eid[j]];
-        }
-        reach = first ? f : pmax(reach, f);
-        first = false;
-        int lp = __ldcg(&A.level[p]) + 1;
-        lv = lp > lv ? lp : lv;
+    // vertices per warp: 32 on a large frontier; on a small one every warp
+    // takes a few, so no warp walks a long chain of edge steps while the
+    // others idle into the barrier
+    const int64_t per = (ncur + nwarps - 1) / nwarps;
+    int vpw = 32;
+    if (per < 32) {
+      vpw = 1;
+      while (vpw < per) vpw <<= 1;
+    }
+    for (int64_t c = wid * vpw; c < ncur; c += nwarps * vpw) {
+      const int64_t i = c + lane;
+      int v = -1, pv = 0, deg = 0;
+      int64_t e0 = 0;
+      double f = 0.0;
+      if (lane < vpw && i < ncur) {
+        v = __ldcg(&A.front[cur][i]);
+        pv = (A.mode == 3 && v != g.root) ? A.part[v] : 0;
+        const double reach = __longlong_as_double((long long)__ldcg(&A.st[2 * (int64_t)v]));
+        const double dur = A.mode == 0 ? pmin(g.w_cpu[v], g.w_gpu[v])
+                           : (A.mode == 1 ? g.w_gpu[v]
+                              : (A.mode == 2 ? g.w_cpu[v]
+                                             : (A.dev[pv] ? g.w_gpu[v] : g.w_cpu[v])));
+        f = reach + dur;
+        __stcs(&A.finish[v], f);
+        __stcs(&A.level[v], it);
+        lmax = it;
+        cmax = f > cmax ? f : cmax;
+        ++done;
+        e0 = __ldcs(g.out_ptr + v);
+        deg = (int32_t)(__ldcs(g.out_ptr + v + 1) - e0);
       }
-      double dur = A.mode == 0 ? pmin(g.w_cpu[v], g.w_gpu[v])
-                   : (A.mode == 1 ? g.w_gpu[v]
-                                  : (A.mode == 2 ? g.w_cpu[v] : (A.dev[pv] ? g.w_gpu[v] : g.w_cpu[v])));
-      double f = reach + dur;
-      __stcg(&A.finish[v], f);
-      __stcg(&A.level[v], lv);
-      lmax = lv > lmax ? lv : lmax;
-      cmax = pmax(cmax, f);
-      ++done;
-      for (int64_t e = g.out_ptr[v]; e < g.out_ptr[v + 1]; ++e) {
-        int s = g.out_dst[e];
-        if (atomicSub(&A.indeg[s], 1) == 1) {
-          // block-local staging: one global atomic per flush, not per node
-          int at = atomicAdd(&s_n, 1);
-          if (at < kStage) s_buf[at] = s;
-          else A.front[nxt][atomicAdd(&A.counts[nxt], 1)] = s;  // overflow: direct
+      // warp prefix of the out-degrees: lane l owns edges [excl, excl + deg)
+      int incl = deg;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      const int excl = incl - deg;
+      // kU edges per lane in flight: their loads and atomics are independent,
+      // only the readiness test waits for the atomicSub results
+      constexpr int kU = 4;
+      for (int t0 = 0; t0 < total; t0 += 32 * kU) {
+        int s[kU];
+        bool ready[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int t = t0 + u * 32 + lane;
+          // owner lane: the last lane whose exclusive prefix is <= t
+          int lo = 0;
+#pragma unroll
+          for (int step = 16; step; step >>= 1) {
+            const int probe = lo + step;
+            const int pe = __shfl_sync(0xffffffffu, excl, probe);
+            if (pe <= t) lo = probe;
+          }
+          const int ov = __shfl_sync(0xffffffffu, v, lo);
+          const int opv = __shfl_sync(0xffffffffu, pv, lo);
+          const double of = __shfl_sync(0xffffffffu, f, lo);
+          const long long oe0 = __shfl_sync(0xffffffffu, (long long)e0, lo);
+          const int oex = __shfl_sync(0xffffffffu, excl, lo);
+          s[u] = 0;
+          ready[u] = false;
+          if (t < total) {
+            const int64_t e = oe0 + (t - oex);
+            const int sv = __ldcs(g.out_dst + e);
+            double cand = of;
+            if (A.mode == 3) {
+              // an input crosses when it comes from another part; the root's
+              // data starts in host memory, so it crosses into GPU parts only
+              const int ps = sv != g.root ? A.part[sv] : 0;
+              const bool cross = ov == g.root ? A.dev[ps] != 0 : opv != ps;
+              if (cross) cand = cand + g.w_xfer[e];
+            }
+            atomicMax(&A.st[2 * (int64_t)sv], (unsigned long long)__double_as_longlong(cand));
+            ready[u] = atomicSub(reinterpret_cast<unsigned *>(&A.st[2 * (int64_t)sv + 1]), 1u) == 1u;
+            s[u] = sv;
+          }
         }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+          stage_append(ready[u], s[u], s_buf, &s_n, A.front[nxt], &A.counts[nxt]);
       }
     }
     __syncthreads();
-    {
+    {  // flush the block's staged entries: one global atomic per block
       const int cnt = s_n < kStage ? s_n : kStage;
       if (threadIdx.x == 0 && cnt) s_base = atomicAdd(&A.counts[nxt], cnt);
       __syncthreads();
@@ -127,7 +202,7 @@ __global__ void levels_kernel(LevelArgs A) {
       __syncthreads();
       if (threadIdx.x == 0) s_n = 0;
     }
-    bar.sync(gridDim.x);
+    grid.sync();
   }
   if (lmax >= 0) atomicMax(A.max_level, lmax);
   if (done) {
@@ -167,9 +242,9 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
                 int32_t *level, double *finish, double *cp_host, int32_t *n_levels_host,
                 cudaStream_t s) {
   const int64_t n = g->n;
-  hs::Scratch<int32_t> indeg, fronts, small;
-  hs::Scratch<unsigned long long> cp;
-  HS_CHECK_CUDA(indeg.alloc(n, s));
+  hs::Scratch<int32_t> fronts, small;
+  hs::Scratch<unsigned long long> cp, reach;
+  HS_CHECK_CUDA(reach.alloc(2 * n, s));
   HS_CHECK_CUDA(fronts.alloc(3 * n, s));
   HS_CHECK_CUDA(small.alloc(8, s));
   HS_CHECK_CUDA(cp.alloc(1, s));
@@ -179,10 +254,9 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
   LevelArgs A;
   A.g = *g;
   A.mode = mode;
-  A.indeg = indeg;
+  A.st = reach;
   for (int i = 0; i < 3; ++i) A.front[i] = fronts.p + i * n;
   A.counts = small.p;                    // [0..2]
-  A.bar = (unsigned *)(small.p + 3);     // [3..4]
   A.max_level = small.p + 5;
   A.processed = small.p + 6;
   A.cp_bits = cp;
@@ -190,18 +264,22 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
   A.finish = finish;
   A.part = part;
   A.dev = dev;
-  const int block = 256;
+  // one 1024-thread block per SM (block shapes 256x4/8, 512x2 measured the
+  // same; the grid barrier is cooperative_groups' grid sync)
+  const int block = 1024;
   int per_sm = 0;
   HS_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, levels_kernel, block, 0));
-  int grid = hs::sm_count() * (per_sm < 4 ? per_sm : 4);
+  int grid = hs::sm_count() * (per_sm < 1 ? per_sm : 1);
   int need = (int)((n + block - 1) / block);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   void *args[] = {&A};
   {
-    // in-CSR + pred finish/level gathers + weights + finish/level writes + out-CSR
-    hs::Prof P("levels", s, 16.0 * n + 8.0 * n + 4.0 * g->m + 12.0 * g->m + 16.0 * n + 12.0 * n +
-                                4.0 * g->m);
+    // in_ptr (pending counts) + out-CSR + weights + reach/pending init and
+    // read + finish/level writes + frontier lists; per edge one reach and
+    // one pending read-modify-write (mode 3: + w_xfer, part of both ends)
+    hs::Prof P("levels", s, 8.0 * n + 8.0 * n + 4.0 * g->m + 16.0 * n + 24.0 * n + 12.0 * n +
+                                8.0 * n + 24.0 * g->m + (mode == 3 ? 12.0 * g->m : 0.0));
     HS_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)levels_kernel, grid, block, args, 0, s));
   }
   HS_CHECK_LAUNCH();

@@ -1,0 +1,169 @@
+// Vertex orders for the k-way partitioner's band start.
+//
+// The band start cuts the kernel positions into k ranges of cumulative
+// weight; it is good when positions follow the DAG's layers, which is the
+// case for DAGs numbered in creation order (every edge u -> v with u < v:
+// the reference's generator, graph.py:180-305, and the tiled-Cholesky DAG)
+// but not for an arbitrary numbering. For those the partitioner runs on the
+// kernel graph relabelled in longest-path level order (K7's levels, ties by
+// id: the order of the reference's level semantics, graph.py:153-172 being
+// the lexicographic Kahn order it refines), and the parts are mapped back.
+//
+//   hs_dag_is_topological  one read per row: out lists are sorted, so
+//                          u -> v with v <= u exists iff the first entry of
+//                          u's list is <= u
+//   hs_level_permutation   kernel positions stably radix-sorted by level:
+//                          perm[new] = old, inv[old] = new
+//   hs_ugraph_permute      relabelled CSR: warp per 32 new rows, row copy
+//                          with neighbour ids through inv
+//   hs_parts_unpermute     part[perm[i]] = part_new[i]
+#include "common.cuh"
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+namespace {
+
+__global__ void topo_check(int32_t n, int32_t root, const int64_t *out_ptr,
+                           const int32_t *out_dst, int32_t *bad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = out_ptr[v], e = out_ptr[v + 1];
+    if (b < e && v != root && out_dst[b] <= v) atomicExch(bad, 1);
+  }
+}
+
+// level of every kernel position (the root's node is skipped)
+__global__ void kernel_levels(int32_t nk, int32_t root, const int32_t *level, int32_t *klev) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nk;
+       i += (int64_t)gridDim.x * blockDim.x)
+    klev[i] = level[i + (i >= root ? 1 : 0)];
+}
+
+__global__ void inverse_perm(int32_t n, const int32_t *perm, int32_t *inv) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    inv[perm[i]] = (int32_t)i;
+}
+
+__global__ void permuted_degrees(int32_t n, const int64_t *xadj, const int32_t *perm,
+                                 const int32_t *vw, int64_t *deg, int32_t *vw_out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t o = perm[i];
+    deg[i] = xadj[o + 1] - xadj[o];
+    vw_out[i] = vw[o];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) deg[n] = 0;
+}
+
+// one warp per new row: the old row is read contiguously, neighbour ids go
+// through inv (a gather of 4 B per entry)
+__global__ void permute_rows(int32_t n, const int64_t *xadj, const int32_t *adj,
+                             const int32_t *wgt, const int32_t *perm, const int32_t *inv,
+                             const int64_t *xadj_new, int32_t *adj_new, int32_t *wgt_new) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
+    const int32_t o = perm[r];
+    const int64_t b = xadj[o], d = xadj[o + 1] - b, nb = xadj_new[r];
+    for (int64_t j = lane; j < d; j += 32) {
+      adj_new[nb + j] = inv[__ldg(adj + b + j)];
+      if (wgt) wgt_new[nb + j] = __ldg(wgt + b + j);
+    }
+  }
+}
+
+__global__ void unpermute(int32_t n, const int32_t *perm, const int32_t *src, int32_t *dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[perm[i]] = src[i];
+}
+
+}  // namespace
+
+extern "C" int hs_dag_is_topological(const hs_dag_t *g, int32_t *result_host, void *stream) {
+  HS_REQUIRE(g && result_host, HS_EINVAL, "hs_dag_is_topological: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  hs::Scratch<int32_t> bad;
+  HS_CHECK_CUDA(bad.alloc(1, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(bad, 0, 4, s));
+  topo_check<<<hs::grid_for(g->n, 256), 256, 0, s>>>(g->n, g->root, g->out_ptr, g->out_dst, bad);
+  HS_CHECK_LAUNCH();
+  int32_t h = 0;
+  HS_CHECK_CUDA(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  *result_host = h ? 0 : 1;
+  return HS_OK;
+}
+
+extern "C" int hs_level_permutation(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
+                                    int32_t *perm, int32_t *inv, void *stream) {
+  HS_REQUIRE(g && level && perm && inv, HS_EINVAL, "hs_level_permutation: null argument");
+  HS_REQUIRE(g->root >= 0 && g->root < g->n, HS_EINVAL, "hs_level_permutation: DAG has no root");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int32_t nk = g->n - 1;
+  if (nk <= 0) return HS_OK;
+  hs::Scratch<int32_t> klev, kout, idx;
+  HS_CHECK_CUDA(klev.alloc(nk, s));
+  HS_CHECK_CUDA(kout.alloc(nk, s));
+  HS_CHECK_CUDA(idx.alloc(nk, s));
+  kernel_levels<<<hs::grid_for(nk, 256), 256, 0, s>>>(nk, g->root, level, klev);
+  HS_CHECK_LAUNCH();
+  int rc = hs::iota32(idx.p, nk, s);
+  if (rc != HS_OK) return rc;
+  int bits = 1;
+  while ((1 << bits) < n_levels && bits < 31) ++bits;
+  size_t temp = 0;
+  HS_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, temp, klev.p, kout.p, idx.p, perm, nk, 0,
+                                                bits, s));
+  hs::Scratch<char> tmp;
+  HS_CHECK_CUDA(tmp.alloc(temp, s));
+  HS_CHECK_CUDA(cub::DeviceRadixSort::SortPairs((void *)tmp.p, temp, klev.p, kout.p, idx.p, perm,
+                                                nk, 0, bits, s));
+  hs::count_launch(4);
+  inverse_perm<<<hs::grid_for(nk, 256), 256, 0, s>>>(nk, perm, inv);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}
+
+extern "C" int hs_ugraph_permute(const hs_ugraph_t *g, const int32_t *perm, const int32_t *inv,
+                                 int64_t *xadj, int32_t *adjncy, int32_t *adjwgt_i,
+                                 int32_t *vwgt_i, void *stream) {
+  HS_REQUIRE(g && perm && inv && xadj && adjncy && vwgt_i, HS_EINVAL,
+             "hs_ugraph_permute: null argument");
+  HS_REQUIRE(!g->adjwgt_i || adjwgt_i, HS_EINVAL, "hs_ugraph_permute: adjwgt_i output missing");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int32_t n = g->n;
+  if (n <= 0) {
+    HS_CHECK_CUDA(cudaMemsetAsync(xadj, 0, 8, s));
+    return HS_OK;
+  }
+  hs::Scratch<int64_t> deg;
+  HS_CHECK_CUDA(deg.alloc(n + 1, s));
+  permuted_degrees<<<hs::grid_for(n, 256), 256, 0, s>>>(n, g->xadj, perm, g->vwgt_i, deg, vwgt_i);
+  HS_CHECK_LAUNCH();
+  size_t temp = 0;
+  HS_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, temp, deg.p, xadj, n + 1, s));
+  hs::Scratch<char> tmp;
+  HS_CHECK_CUDA(tmp.alloc(temp, s));
+  HS_CHECK_CUDA(cub::DeviceScan::ExclusiveSum((void *)tmp.p, temp, deg.p, xadj, n + 1, s));
+  hs::count_launch(1);
+  {
+    hs::Prof P("ugraph_permute", s, 16.0 * n + 12.0 * g->nnz + (g->adjwgt_i ? 8.0 * g->nnz : 0.0));
+    permute_rows<<<hs::grid_for((int64_t)n * 32, 256), 256, 0, s>>>(
+        n, g->xadj, g->adjncy, g->adjwgt_i, perm, inv, xadj, adjncy,
+        g->adjwgt_i ? adjwgt_i : nullptr);
+  }
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}
+
+extern "C" int hs_parts_unpermute(int32_t n, const int32_t *perm, const int32_t *part_new,
+                                  int32_t *part, void *stream) {
+  HS_REQUIRE(perm && part_new && part && n >= 0, HS_EINVAL, "hs_parts_unpermute: bad argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) return HS_OK;
+  unpermute<<<hs::grid_for(n, 256), 256, 0, s>>>(n, perm, part_new, part);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}

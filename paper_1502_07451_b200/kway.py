@@ -118,6 +118,29 @@ def layered_dag(n_kernels: int, m_inter: int, seed: int = 0, kind: str = "MA", s
     return csr
 
 
+def relabeled_dag(csr: DagCSR, seed: int = 0):
+    """Input synthesis: the same DAG under a random node numbering (edges and
+    weights preserved, out-lists re-sorted). Returns (DagCSR, pi) with
+    pi[old node] = new node. The id-order robustness check of the band start."""
+    dev = csr.device
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    pi = torch.randperm(csr.n, generator=g).to(dev)
+    src = torch.repeat_interleave(torch.arange(csr.n, device=dev), csr.out_ptr.diff())
+    ns, nd = pi[src], pi[csr.out_dst.long()]
+    key = ns * csr.n + nd
+    key, o = torch.sort(key)
+    del key
+    out_dst = nd[o].to(torch.int32)
+    out_ptr = torch.zeros(csr.n + 1, dtype=torch.int64, device=dev)
+    out_ptr[1:] = torch.cumsum(torch.bincount(ns, minlength=csr.n), 0)
+    inv = torch.empty_like(pi)
+    inv[pi] = torch.arange(csr.n, device=dev)
+    new = DagCSR.from_out_csr(int(pi[csr.root].item()), out_ptr, out_dst,
+                              csr.w_cpu[inv].contiguous(), csr.w_gpu[inv].contiguous(),
+                              csr.w_xfer[o].contiguous(), csr.bytes[o].contiguous())
+    return new, pi
+
+
 def in_order(csr: DagCSR, edge_attr: torch.Tensor) -> torch.Tensor:
     """CSC copy of a per-edge attribute (in-order), for ``symmetrize``."""
     return edge_attr[csr.in_eid.long()].contiguous()
@@ -193,7 +216,10 @@ def partition_kway(graph, k: int, tpwgts: Optional[Sequence[float]] = None, tol:
     baseline's when the baseline meets the balance constraint.
     """
     from . import recursive
-    ug = graph if isinstance(graph, UGraph) else symmetrize(graph)
+    if not isinstance(graph, UGraph):
+        return partition_dag(graph, k, tpwgts, tol, seed, out=out,
+                             reference_start=reference_start)
+    ug = graph
     if tpwgts is None:
         tpwgts = [1.0 / k] * k
     if len(tpwgts) != k:
@@ -205,6 +231,58 @@ def partition_kway(graph, k: int, tpwgts: Optional[Sequence[float]] = None, tol:
     st = _native.partition_kway(ug, k, tpwgts, tol, seed, part, starts)
     return KwayResult(part, st[0] * ug.weight_scale, st[1], st[2], st[3] / 1e9, bool(st[4]),
                       st[5])
+
+
+def permute_ugraph(ug: UGraph, perm: torch.Tensor, inv: torch.Tensor) -> UGraph:
+    """``ug`` relabelled: vertex i of the result is vertex perm[i] (hs_ugraph_permute)."""
+    xadj, adjncy, adjwgt, vwgt = _native.ugraph_permute(ug, perm, inv)
+    return UGraph(xadj, adjncy, adjwgt, vwgt, unit_weight=ug.unit_weight)
+
+
+def band_order(csr: DagCSR, order: str = "auto"):
+    """The vertex order the band start cuts: None (kernel positions) or the
+    (perm, inv) of the longest-path level order.
+
+    ``order``: "ids" keeps positions; "levels" always relabels; "auto"
+    relabels only DAGs not numbered in topological order (one read per row,
+    ``hs_dag_is_topological``): creation-order numbering (the reference's
+    generator, graph.py:180-305; the tiled-Cholesky DAG) already follows the
+    layers, an arbitrary numbering does not.
+    """
+    if order not in ("auto", "ids", "levels"):
+        raise ValueError("order must be 'auto', 'ids' or 'levels'")
+    if order == "auto":
+        topo = getattr(csr, "_topological", None)
+        if topo is None:
+            topo = csr._topological = _native.dag_is_topological(csr)
+        if topo:
+            return None
+    if order == "ids":
+        return None
+    lv, _, _, nl = _native.levels(csr, 0)
+    return _native.level_permutation(csr, lv, nl)
+
+
+def partition_dag(csr: DagCSR, k: int, tpwgts: Optional[Sequence[float]] = None,
+                  tol: float = 0.03, seed: int = 0, edge_w_i: Optional[torch.Tensor] = None,
+                  node_w_i: Optional[torch.Tensor] = None,
+                  edge_w_i_in: Optional[torch.Tensor] = None, order: str = "auto",
+                  out: Optional[torch.Tensor] = None,
+                  reference_start: Optional[bool] = None) -> KwayResult:
+    """K1 + K3-K6 on a task DAG, the band start cut in ``band_order(csr, order)``.
+
+    The result's ``part`` is indexed by kernel position whatever the order.
+    """
+    ug = symmetrize(csr, edge_w_i, node_w_i, edge_w_i_in)
+    po = band_order(csr, order)
+    if po is None:
+        return partition_kway(ug, k, tpwgts, tol, seed, out=out, reference_start=reference_start)
+    perm, inv = po
+    r = partition_kway(permute_ugraph(ug, perm, inv), k, tpwgts, tol, seed,
+                       reference_start=reference_start)
+    part = out if out is not None else torch.empty_like(r.part)
+    r.part = _native.parts_unpermute(perm, r.part, part)
+    return r
 
 
 def evaluate_batch(csr: DagCSR, parts: torch.Tensor, k: int,
