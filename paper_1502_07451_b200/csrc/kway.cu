@@ -1522,7 +1522,16 @@ struct Kway {
   refine_cached<KC, CW><<<cg, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st, list,     \
                                                   ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache.p, \
                                                   prethin ? d_flows : nullptr)
-          if (cache.kc == 8) {
+          if (cache.kc == 8 && cache.cw == 1 && st.n == 1 && g.v0 == 0 &&
+              (reinterpret_cast<uintptr_t>(pl) & 3) == 0 &&
+              (reinterpret_cast<uintptr_t>(g.vw) & 15) == 0 &&
+              (reinterpret_cast<uintptr_t>(cache.p) & 15) == 0 &&
+              (reinterpret_cast<uintptr_t>(st.p[0]) & 15) == 0) {
+            const int cg4 = hs::grid_for((g.n + 3) / 4, kTeamBlock, hs::sm_count() * 16);
+            refine_cached_v4<<<cg4, kTeamBlock, 0, s>>>(g, pl, k, d_pw, d_hi, d_lo, st.p[0], list,
+                                                        ctl + CTL_COUNT, ctl + CTL_ACTIVE, cache.p,
+                                                        prethin ? d_flows : nullptr, Lv.vconst);
+          } else if (cache.kc == 8) {
             if (cache.cw == 1) HS_RC(8, 1); else if (cache.cw == 2) HS_RC(8, 2); else HS_RC(8, 4);
           } else {
             if (cache.cw == 1) HS_RC(16, 1); else if (cache.cw == 2) HS_RC(16, 2); else HS_RC(16, 4);

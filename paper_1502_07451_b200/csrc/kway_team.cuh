@@ -431,6 +431,150 @@ refine_cached(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
   }
 }
 
+// refine_cached for 8-byte cache rows (k <= 8, 1-byte counters) on one GPU,
+// four consecutive vertices per thread and step: parts (4 x 1 B), vertex
+// weights (16 B; none when every vertex weighs vconst), cache rows (2 x 16 B)
+// and states (16 B) move as vector accesses. The scalar kernel is issue
+// bound (ncu: 71% issue slots), so the best move is found with byte-SIMD:
+// counters of the parts a move may enter (room >= weight) masked in two
+// words, own part zeroed, max byte by __vmaxu4, first part holding it by
+// __vcmpeq4 + ffs — the scalar loop's choice (strictly larger gain wins, so
+// the smallest part among equal maxima). Same decisions and appended set.
+__global__ void __launch_bounds__(kTeamBlock, 6)
+refine_cached_v4(G g, const part_t *part, int k, const int64_t *pw, const int64_t *hi,
+                 const int64_t *lo, uint32_t *st, int32_t *list, int32_t *count,
+                 const int32_t *run, const uint8_t *cache, int64_t *flows, int32_t vconst) {
+  constexpr int KC = 8;
+  if (run && !*run) return;
+  __shared__ int32_t s_in[KC], s_out[KC];
+  __shared__ unsigned long long sf[2 * KC];
+  __shared__ int32_t s_app[kTeamBlock / 32][kAppendBuf];
+  auto room = [](int64_t r) -> int32_t {
+    return r < 0 ? -1 : (r > (int64_t)INT32_MAX ? INT32_MAX : (int32_t)r);
+  };
+  for (int p = threadIdx.x; p < KC; p += blockDim.x) {
+    s_in[p] = p < k ? room(hi[p] - pw[p]) : -1;
+    s_out[p] = p < k ? room(pw[p] - lo[p]) : -1;
+  }
+  for (int p = threadIdx.x; p < 2 * KC; p += blockDim.x) sf[p] = 0;
+  __syncthreads();
+  int32_t in_[KC];
+#pragma unroll
+  for (int q = 0; q < KC; ++q) in_[q] = s_in[q];
+  // byte masks of the parts a vertex of weight w may enter
+  auto enter_mask = [&](int32_t w, uint32_t &mlo, uint32_t &mhi) {
+    mlo = mhi = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (w <= in_[q]) mlo |= 0xffu << (8 * q);
+      if (w <= in_[q + 4]) mhi |= 0xffu << (8 * q);
+    }
+  };
+  uint32_t clo = 0, chi = 0;
+  if (vconst) enter_mask(vconst, clo, chi);
+  uint32_t fo[KC], fi[KC];
+#pragma unroll
+  for (int q = 0; q < KC; ++q) fo[q] = fi[q] = 0;
+  WarpAppender app{s_app[threadIdx.x >> 5]};
+  const int64_t n4 = ((int64_t)g.n + 3) / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n4; base += stride) {
+    const int64_t t = base + threadIdx.x;
+    const int v0 = (int)(4 * t);
+    const bool full = v0 + 3 < g.n;
+    uint32_t pk = 0, rw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int32_t vw4[4] = {vconst, vconst, vconst, vconst};
+    if (full) {
+      pk = __ldg(reinterpret_cast<const uint32_t *>(part) + t);
+      if (!vconst) {
+        const int4 w = __ldg(reinterpret_cast<const int4 *>(g.vw) + t);
+        vw4[0] = w.x; vw4[1] = w.y; vw4[2] = w.z; vw4[3] = w.w;
+      }
+      const uint4 a = __ldg(reinterpret_cast<const uint4 *>(cache) + 2 * t);
+      const uint4 b = __ldg(reinterpret_cast<const uint4 *>(cache) + 2 * t + 1);
+      rw[0] = a.x; rw[1] = a.y; rw[2] = a.z; rw[3] = a.w;
+      rw[4] = b.x; rw[5] = b.y; rw[6] = b.z; rw[7] = b.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int v = v0 + i;
+        if (v < g.n) {
+          pk |= (uint32_t)(uint8_t)part[v] << (8 * i);
+          vw4[i] = g.vw[v];
+          const uint2 x = __ldg(reinterpret_cast<const uint2 *>(cache) + v);
+          rw[2 * i] = x.x;
+          rw[2 * i + 1] = x.y;
+        }
+      }
+    }
+    uint32_t out[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int v = v0 + i;
+      const bool valid = v < g.n;
+      const int own = (int)((pk >> (8 * i)) & 0xffu);
+      const uint32_t lo32 = rw[2 * i], hi32 = rw[2 * i + 1];
+      const uint32_t own_lo = own < 4 ? 0xffu << (8 * own) : 0u;
+      const uint32_t own_hi = own >= 4 ? 0xffu << (8 * (own - 4)) : 0u;
+      const int cown = (int)(((own < 4 ? lo32 : hi32) >> (8 * (own & 3))) & 0xffu);
+      const int32_t vwv = vw4[i];
+      int bg = 0, bp = -1;
+      // counters of parts >= k are never written (0): no k mask needed
+      if (valid && ((lo32 & ~own_lo) | (hi32 & ~own_hi)) && vwv <= s_out[own]) {
+        uint32_t mlo = clo, mhi = chi;
+        if (!vconst) enter_mask(vwv, mlo, mhi);
+        const uint32_t a = lo32 & mlo & ~own_lo, b = hi32 & mhi & ~own_hi;
+        uint32_t x = __vmaxu4(a, b);
+        x = __vmaxu4(x, x >> 16);
+        x = __vmaxu4(x, x >> 8);
+        const int m = (int)(x & 0xffu);
+        if (m > cown) {
+          const uint32_t rep = (uint32_t)m * 0x01010101u;
+          const uint32_t ea = __vcmpeq4(a, rep), eb = __vcmpeq4(b, rep);
+          bp = ea ? (__ffs(ea) - 1) >> 3 : 4 + ((__ffs(eb) - 1) >> 3);
+          bg = m - cown;
+        }
+      }
+      if (flows && bp >= 0) {
+#pragma unroll
+        for (int q = 0; q < KC; ++q) {
+          fo[q] += own == q ? (uint32_t)vwv : 0u;
+          fi[q] += bp == q ? (uint32_t)vwv : 0u;
+        }
+      }
+      out[i] = pack_state(own, bp, bg);
+      app.push(valid && bp >= 0, v, list, count);
+    }
+    if (full) {
+      reinterpret_cast<uint4 *>(st)[t] = make_uint4(out[0], out[1], out[2], out[3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (v0 + i < g.n) st[v0 + i] = out[i];
+    }
+  }
+  app.flush(list, count);
+  if (flows) {
+#pragma unroll
+    for (int q = 0; q < KC; ++q) {
+      unsigned long long a = fo[q], b = fi[q];
+      for (int off = 16; off; off >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, off);
+        b += __shfl_down_sync(0xffffffffu, b, off);
+      }
+      if ((threadIdx.x & 31) == 0) {
+        if (a) atomicAdd(&sf[q], a);
+        if (b) atomicAdd(&sf[KC + q], b);
+      }
+    }
+    __syncthreads();
+    for (int p = threadIdx.x; p < k; p += blockDim.x) {
+      if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
+      if (sf[KC + p]) atomicAdd((unsigned long long *)&flows[k + p], sf[KC + p]);
+    }
+  }
+}
+
 // Cut from the connectivity cache: sum over vertices of the weight into other
 // parts (each cut edge counted from both ends).
 template <int KC, int CW>
@@ -507,13 +651,34 @@ __device__ __forceinline__ void cache_move_flat(const G &g, const Conn &cache, i
   ms.pre[w][lane] = inc - d;
   ms.od[w][lane] = (own << 16) | (dest & 0xffff);
   __syncwarp();
-  for (int f = lane; f < tot; f += 32) {
-    int t = 0;
-    for (int st = 16; st; st >>= 1)
-      if (ms.pre[w][t + st] <= f) t += st;
-    const int64_t j = ms.b[w][t] + (f - ms.pre[w][t]);
-    const int od = ms.od[w][t];
-    cache.move(__ldg(g.adj + j) - g.v0, od >> 16, od & 0xffff, g.ew(j));
+  // kU entries per lane in flight: the neighbour-id loads of one step are
+  // independent, so their latencies overlap (the loop is load-latency bound)
+  constexpr int kU = 4;
+  for (int f0 = lane; f0 < tot; f0 += 32 * kU) {
+    int64_t jj[kU];
+    int odv[kU], uu[kU], ww[kU];
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      const int f = f0 + q * 32;
+      jj[q] = -1;
+      odv[q] = 0;
+      if (f < tot) {
+        int t = 0;
+#pragma unroll
+        for (int st = 16; st; st >>= 1)
+          if (ms.pre[w][t + st] <= f) t += st;
+        jj[q] = ms.b[w][t] + (f - ms.pre[w][t]);
+        odv[q] = ms.od[w][t];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q) {
+      uu[q] = jj[q] >= 0 ? __ldg(g.adj + jj[q]) : 0;
+      ww[q] = jj[q] >= 0 ? g.ew(jj[q]) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kU; ++q)
+      if (jj[q] >= 0) cache.move(uu[q] - g.v0, odv[q] >> 16, odv[q] & 0xffff, ww[q]);
   }
   __syncwarp();
 }
