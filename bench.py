@@ -871,6 +871,15 @@ def secondary(csr10m, args):
     out["cfg2_partition_ms"] = ms
     out["cfg2_cut"] = r.cut
     out["cfg2_feasible"] = r.feasible
+    # the same DAG with integer weights U[1,100] on every edge and vertex
+    # (SURVEY §8(d) integer-parity run): per-entry weights, 2-byte counters
+    gen_ = torch.Generator(device="cpu").manual_seed(2)
+    ewu = torch.randint(1, 101, (c2.m,), generator=gen_, dtype=torch.int32).to(c2.device)
+    nwu = torch.randint(1, 101, (c2.n,), generator=gen_, dtype=torch.int32).to(c2.device)
+    ms, r = timed(lambda: kway.partition_kway(kway.symmetrize(c2, ewu, nwu), 8, tol=TOL))
+    out["cfg2_u1_100_partition_ms"] = ms
+    out["cfg2_u1_100"] = {"cut": r.cut, "feasible": r.feasible, "max_deviation": r.max_deviation}
+    del ewu, nwu
     parts = kway.kernel_to_node_parts(c2, r.part).unsqueeze(0).repeat(64, 1).contiguous()
     nw64 = nw.to(torch.int64)
     ms, e = timed(lambda: kway.evaluate_batch(c2, parts, 8, nw64, check=False))
