@@ -770,6 +770,7 @@ __global__ void classify_long(const int64_t *ub, const int32_t *ncp, int64_t lo,
 
 // levels up to this many vertices are refined by FM candidates (one GPU)
 constexpr int kFmMaxLevel = 4096;
+static_assert(kFmMaxLevel <= kFmMaxN, "FM levels keep their per-vertex state in shared memory");
 constexpr int kFmInitPasses = 8, kFmRefinePasses = 6, kFmCopies = 16;
 // coarsening stops on density only past this many adjacency entries
 constexpr int64_t kDenseStopNnz = 4ll << 20;
@@ -2084,6 +2085,16 @@ struct Kway {
     return HS_OK;
   }
 
+  // FM runs on graphs whose finest level is an FM level (<= kFmMaxLevel
+  // vertices): there every level gets FM candidates. On larger graphs the
+  // coarse levels of task DAGs are dense (average degree 100-200 at a few
+  // thousand vertices), every FM move dirties most rows, and a level took
+  // 10-100 ms; the band start at the coarsest level with Jet refinement on
+  // every level measured 10-30x faster at an equal or lower cut on layered
+  // DAGs (20k-100k tasks, m/n = 3-10) and the 45,760-task Cholesky DAG at
+  // k = 8, 17% higher at k = 2 (tools/calib2.py).
+  bool fm_levels() const { return levels[0].n_glob <= kFmMaxLevel; }
+
   // FM candidates on a small level (one GPU): n_init recursive-bisection
   // starts, `copies` copies of `cur` (each searches with its own hash salt)
   // and the caller's starts at the finest level; the best by (violation,
@@ -2094,7 +2105,7 @@ struct Kway {
     const int n = g.n;
     const int n_ext = with_starts ? n_starts : 0;
     const int64_t rows = (int64_t)n * k * 4;
-    const int64_t flags = 2 * (int64_t)((n + 15) & ~15);
+    const int64_t flags = fm_vertex_bytes(n);  // per-vertex state (kway_fm.cuh)
     int smem_max = 0;
     HS_CHECK_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                          dev_id()));
@@ -2140,6 +2151,11 @@ struct Kway {
     A.salt = salt2;
     A.passes = passes;
     A.stall = std::max(32, std::min(400, n / 8));
+    A.stats = nullptr;
+    if (timer.on) {
+      HS_CHECK_CUDA(dalloc(&A.stats, 8 * (int64_t)C, s));
+      HS_CHECK_CUDA(cudaMemsetAsync(A.stats, 0, 64 * (int64_t)C, s));
+    }
     const int64_t dyn = flags + (sm ? rows : 0);
     {
       hs::Prof P("fm_level", s, 0.0);
@@ -2156,6 +2172,21 @@ struct Kway {
     HS_CHECK_LAUNCH();
     fm_pick<<<hs::grid_for(n, 256, 64), 256, 0, s>>>(viol, cut, C, parts, n, cur, nullptr);
     HS_CHECK_LAUNCH();
+    if (A.stats) {  // HS_KWAY_TRACE: the slowest candidate's counters
+      std::vector<long long> h(8 * (size_t)C);
+      HS_CHECK_CUDA(cudaMemcpyAsync(h.data(), A.stats, 64 * (int64_t)C, cudaMemcpyDeviceToHost, s));
+      HS_CHECK_CUDA(cudaStreamSynchronize(s));
+      int w = 0;
+      for (int c = 1; c < C; ++c)
+        if (h[8 * c + 6] > h[8 * w + 6]) w = c;
+      const long long *q = h.data() + 8 * w;
+      fprintf(stderr,
+              "[kway] fm level n=%d nnz=%lld C=%d init=%d: slowest cand %d: %.3f Mclk, moves %lld "
+              "passes %lld rolled back %lld, scan %.3f Mclk, move %.3f Mclk, grow steps %lld\n",
+              n, (long long)g.nnz, C, n_init, w, q[6] / 1e6, q[0], q[1], q[2], q[3] / 1e6, q[4] / 1e6,
+              q[5]);
+      cudaFreeAsync(A.stats, s);
+    }
     cudaFreeAsync(parts, s);
     cudaFreeAsync(trail, s);
     cudaFreeAsync(cut, s);
@@ -2200,7 +2231,7 @@ struct Kway {
     // small coarsest graph (one GPU): recursive-bisection FM candidates, the
     // refined band start and (when this is the finest level) the caller's
     // starts; the band start alone otherwise
-    if (nc <= kFmMaxLevel && !D.on() && k > 1) {
+    if (fm_levels() && nc <= kFmMaxLevel && !D.on() && k > 1) {
       const int n_init = nc <= 1024 ? 2 * hs::sm_count() : hs::sm_count();
       return fm_level(Cst, best, n_init, 1, levels.size() == 1, kFmInitPasses,
                       salt ^ 0xC0A25E57ull);
@@ -2574,7 +2605,7 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
       K.free_rep(cur);
       cur = pf;
     }
-    if (!K.D.on() && Lv.g.n <= kFmMaxLevel && k > 1) {
+    if (K.fm_levels() && !K.D.on() && Lv.g.n <= kFmMaxLevel && k > 1) {
       // small level: FM candidates from the projected partition (the
       // coarsest one was refined by its initial candidates already)
       if (li != (int)K.levels.size() - 1) {
