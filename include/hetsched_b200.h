@@ -190,6 +190,16 @@ int hs_validate_dag(const hs_dag_t *g, int64_t *counts_host, int32_t *first_host
 int hs_assigned_makespan(const hs_dag_t *g, const int32_t *part, const int8_t *dev, int32_t k,
                          int32_t *level, double *finish, double *makespan_host, void *stream);
 
+/* topological_order (graph.py:153-172): the lexicographically smallest
+ * topological order (Kahn with an id min-heap, self-loops ignored), bit for
+ * bit. order[n] receives node indices; *count_host = nodes output (n unless
+ * there is a cycle); on a cycle *stuck_host = the smallest index never
+ * released (the reference's CycleError member), else -1. *rounds_host
+ * (optional): batched rounds used (0 = the identity fast path: every edge
+ * points to a larger index). Synchronous. */
+int hs_topological_order(const hs_dag_t *g, int32_t *order, int32_t *count_host,
+                         int32_t *stuck_host, int32_t *rounds_host, void *stream);
+
 /* Level order: nodes sorted by (level, index) — order[n]. */
 int hs_level_order(const hs_dag_t *g, const int32_t *level, int32_t n_levels,
                    int32_t *order, void *stream);

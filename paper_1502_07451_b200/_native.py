@@ -219,6 +219,17 @@ def level_order(csr, level: torch.Tensor, n_levels: int) -> torch.Tensor:
 
 
 _is_topological = _opt("hs_dag_is_topological", _P, _P, _P)
+_topo_order = _opt("hs_topological_order", _P, _P, _P, _P, _P, _P)
+
+
+def topological_order(csr):
+    """(order int32 [n] device, count, stuck index or -1, rounds) — hs_topological_order."""
+    order = torch.empty(max(csr.n, 1), dtype=torch.int32, device=csr.device)
+    cnt, stuck, rounds = ctypes.c_int32(0), ctypes.c_int32(-1), ctypes.c_int32(0)
+    check(_need(_topo_order, "hs_topological_order")(
+        ctypes.byref(csr.struct()), ptr(order), ctypes.byref(cnt), ctypes.byref(stuck),
+        ctypes.byref(rounds), stream_ptr()))
+    return order[:csr.n], cnt.value, stuck.value, rounds.value
 _level_permutation = _opt("hs_level_permutation", _P, _P, _i32, _P, _P, _P)
 _ugraph_permute = _opt("hs_ugraph_permute", _P, _P, _P, _P, _P, _P, _P, _P)
 _parts_unpermute = _opt("hs_parts_unpermute", _i32, _P, _P, _P, _P)

@@ -11,7 +11,6 @@ Reference: /root/reference/pkg/src/hetsched/graph.py (cited per symbol).
 """
 from __future__ import annotations
 
-import heapq
 from dataclasses import dataclass, replace
 from typing import Dict, Iterable, List, Optional, Tuple
 
@@ -174,26 +173,19 @@ def validate(graph: TaskGraph) -> List[str]:
 def topological_order(graph: TaskGraph) -> List[int]:
     """Lexicographically smallest topological order (graph.py:153-172).
 
-    Kahn's algorithm with an id min-heap; on a cycle raises CycleError with
-    the smallest id whose in-degree never reached zero.
+    Kahn's algorithm with an id min-heap, run on the device
+    (``hs_topological_order``: the identity when every edge points to a
+    larger id, batched heap rounds otherwise); on a cycle raises CycleError
+    with the smallest id whose in-degree never reached zero.
     """
-    indeg = dict.fromkeys(graph.nodes, 0)
-    for (u, v) in graph.edges:
-        if u != v and u in indeg and v in indeg:
-            indeg[v] += 1
-    heap = [i for i, d in indeg.items() if d == 0]
-    heapq.heapify(heap)
-    order: List[int] = []
-    while heap:
-        nid = heapq.heappop(heap)
-        order.append(nid)
-        for s in graph.successors(nid):
-            indeg[s] -= 1
-            if indeg[s] == 0:
-                heapq.heappush(heap, s)
-    if len(order) != len(graph.nodes):
-        raise CycleError(min(i for i, d in indeg.items() if d > 0))
-    return order
+    if not graph.nodes:
+        return []
+    from . import _native
+    csr = graph.csr()
+    order, count, stuck, _ = _native.topological_order(csr)
+    if count != csr.n:
+        raise CycleError(int(csr.ids[stuck]))
+    return csr.ids[order.cpu().numpy()].tolist()
 
 
 def attach_weights(graph: TaskGraph, model) -> TaskGraph:

@@ -48,11 +48,13 @@ def test_cholesky_matches_golden(medium_cases):
     assert spec_of(gen.cholesky_dag(8, model=model)) == c["spec"]
 
 
+@pytest.mark.gpu  # topological_order runs on the device (hs_topological_order)
 def test_topological_order_matches_golden(small_cases):
     for c in small_cases:
         assert topological_order(graph_from_spec(c["spec"])) == c["topological_order"]
 
 
+@pytest.mark.gpu  # validate's cycle check is the device topological_order
 def test_validate_messages():
     """Error substrings the reference's tests match (pkg/tests/test_graph.py:23-42)."""
     root = KernelNode(0, "SOURCE", 0)
