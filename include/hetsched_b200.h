@@ -254,6 +254,21 @@ int hs_simulate_batch(const hs_dag_batch_t *g, int policy, const int8_t *pin,
                       hs_event_t *ev, const int64_t *ev_off, int64_t *ev_count,
                       void *stream);
 
+/* Trace products (sim.py:200-236) from a device event buffer of one
+ * simulation (count events, node indices local to the graph):
+ * hs_trace_sort writes perm[count] = event indices in the reference's order
+ * (time, xfer_start < xfer_end < kernel_start < kernel_end, subject as a
+ * string with node ids ids[n] (int64), resource name as a string given by
+ * res_rank[resource + 1] = rank of the name in string order, bus = -1).
+ * hs_trace_metrics: metrics(trace) over the sorted events: out_host[6] =
+ * makespan, transfer count, busy CPU ms, busy GPU ms (fp64 sums in event
+ * order), kernels on CPU, kernels on GPU; workers [0, cpu_workers) are CPU.
+ * Both synchronous. */
+int hs_trace_sort(const hs_event_t *ev, int64_t count, const int64_t *ids,
+                  const int32_t *res_rank, int32_t *perm, void *stream);
+int hs_trace_metrics(const hs_event_t *ev, const int32_t *perm, int64_t count, int32_t n_nodes,
+                     int32_t cpu_workers, double *out_host, void *stream);
+
 /* ---- K5/K6 exact two-way partitioner ----------------------------------
  * Replaces partition_heuristic's restart loop + fm_refine
  * (partition.py:137-295) with the reference's exact semantics: one CTA per

@@ -301,6 +301,29 @@ def simulate_batch(batch, policy: int, pin: Optional[torch.Tensor], cpu_workers:
     return out
 
 
+_trace_sort = _opt("hs_trace_sort", _P, ctypes.c_int64, _P, _P, _P, _P)
+_trace_metrics = _opt("hs_trace_metrics", _P, _P, ctypes.c_int64, _i32, _i32, _P, _P)
+
+
+def trace_sort(ev: torch.Tensor, count: int, ids: torch.Tensor, res_rank: torch.Tensor
+               ) -> torch.Tensor:
+    """perm[count]: the reference's event order (hs_trace_sort); ev is a uint8
+    view of count hs_event_t records."""
+    perm = torch.empty(max(count, 1), dtype=torch.int32, device=ids.device)
+    check(_need(_trace_sort, "hs_trace_sort")(ptr(ev), count, ptr(ids), ptr(res_rank),
+                                              ptr(perm), stream_ptr()))
+    return perm[:count]
+
+
+def trace_metrics(ev: torch.Tensor, perm: torch.Tensor, count: int, n_nodes: int,
+                  cpu_workers: int):
+    """(makespan, transfers, busy_cpu, busy_gpu, kernels_cpu, kernels_gpu) — hs_trace_metrics."""
+    out = (ctypes.c_double * 6)()
+    check(_need(_trace_metrics, "hs_trace_metrics")(ptr(ev), ptr(perm), count, n_nodes,
+                                                    cpu_workers, out, stream_ptr()))
+    return tuple(out)
+
+
 def fm2(ug, edge_w, edge_u, edge_v, weights, r_cpu, tol, orders, start):
     fn = _need(_fm2, "hs_fm2")
     n_orders = orders.shape[0]

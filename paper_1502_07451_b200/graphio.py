@@ -23,7 +23,8 @@ graphs beyond the object model (config 4: 10M vertices, ~2.6 GB of text).
 from __future__ import annotations
 
 import ctypes
-from typing import Optional, Tuple
+import re
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 import torch
@@ -38,6 +39,74 @@ _P = ctypes.c_void_p
 _emit = _native._opt("hs_emit_metis", _P, _P, ctypes.c_int64, _P, _P)
 _parse = _native._opt("hs_parse_partition", _P, ctypes.c_int64, ctypes.c_int32, _P, _P, _P,
                       ctypes.c_int32, _P, _P)
+
+
+# ---- canonical DOT emission (graphio.py:27-47, 221-270) ---------------------
+# Text formatting of the object model (DOT parsing stays out of scope): the
+# trace products annotated_dot / emit_partitioned_dot are built on it.
+_ID_RE = re.compile(r"[A-Za-z_][A-Za-z0-9_]*$")
+_NUM_RE = re.compile(r"-?(\.\d+|\d+(\.\d*)?)$")
+CPU_COLOR = "lightblue"
+GPU_COLOR = "palegreen"
+
+
+def _quote(value: str) -> str:
+    """graphio.py:32-35"""
+    if _ID_RE.match(value) or _NUM_RE.match(value):
+        return value
+    return '"' + value.replace('"', '\\"') + '"'
+
+
+def _fmt_attrs(pairs: List[Tuple[str, str]]) -> str:
+    return "[" + ", ".join(f"{k}={_quote(v)}" for k, v in pairs) + "]"
+
+
+def _node_attr_pairs(n) -> List[Tuple[str, str]]:
+    """graphio.py:221-225 (floats as repr)"""
+    return [("kind", n.kind), ("size", str(n.size)), ("weight_cpu", repr(n.weight_cpu)),
+            ("weight_gpu", repr(n.weight_gpu))] + list(getattr(n, "attrs", ()))
+
+
+def _edge_attr_pairs(e) -> List[Tuple[str, str]]:
+    """graphio.py:228-231"""
+    return [("bytes", str(e.bytes)), ("weight_xfer", repr(e.weight_xfer))] + \
+        list(getattr(e, "attrs", ()))
+
+
+def emit_dot(graph: TaskGraph,
+             node_extra: Optional[Dict[int, List[Tuple[str, str]]]] = None,
+             edge_extra: Optional[Dict[Tuple[int, int], List[Tuple[str, str]]]] = None) -> str:
+    """Canonical DOT: nodes ascending by id, then edges by (src, dst) (graphio.py:234-250)."""
+    node_extra = node_extra or {}
+    edge_extra = edge_extra or {}
+    lines = [f"digraph {graph.name} {{"]
+    for nid in sorted(graph.nodes):
+        pairs = _node_attr_pairs(graph.nodes[nid]) + node_extra.get(nid, [])
+        lines.append(f"  n{nid} {_fmt_attrs(pairs)};")
+    for (u, v) in sorted(graph.edges):
+        pairs = _edge_attr_pairs(graph.edges[(u, v)]) + edge_extra.get((u, v), [])
+        lines.append(f"  n{u} -> n{v} {_fmt_attrs(pairs)};")
+    lines.append("}")
+    return "\n".join(lines) + "\n"
+
+
+def emit_partitioned_dot(graph: TaskGraph, partition: Partition) -> str:
+    """emit_dot with part / fill colour per group and dashed red cut edges (graphio.py:253-270)."""
+    for nid in graph.kernel_ids():
+        if nid not in partition.assignment:
+            raise PartitionError(f"partition is missing kernel {nid}")
+    node_extra: Dict[int, List[Tuple[str, str]]] = {}
+    for nid, group in partition.assignment.items():
+        color = CPU_COLOR if group == CPU else GPU_COLOR
+        node_extra[nid] = [("part", group), ("style", "filled"), ("fillcolor", color)]
+    node_extra[graph.root] = [("part", CPU), ("style", "filled"), ("fillcolor", CPU_COLOR)]
+    edge_extra: Dict[Tuple[int, int], List[Tuple[str, str]]] = {}
+    for (u, v) in sorted(graph.edges):
+        if u == graph.root or v == graph.root:
+            continue
+        if partition.assignment[u] != partition.assignment[v]:
+            edge_extra[(u, v)] = [("style", "dashed"), ("color", "red")]
+    return emit_dot(graph, node_extra, edge_extra)
 
 
 def _scaled(w: torch.Tensor, scale: int) -> torch.Tensor:

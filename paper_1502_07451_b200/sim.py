@@ -110,7 +110,20 @@ def _worker_names(machine: MachineModel) -> List[str]:
             + [f"gpu{i}" for i in range(machine.gpu_workers)])
 
 
+def _resource_ranks(names: List[str]) -> List[int]:
+    """rank[resource + 1] of every resource name ("bus" = -1) in string order."""
+    allr = ["bus"] + names
+    order = sorted(range(len(allr)), key=lambda i: allr[i])
+    rank = [0] * len(allr)
+    for r, i in enumerate(order):
+        rank[i] = r
+    return rank
+
+
 def _events_to_trace(graph: TaskGraph, raw: np.ndarray, names: List[str]) -> List[TraceEvent]:
+    """Python events of device records already in the reference's order
+    (hs_trace_sort: sim.py:200-201 — time, kind, subject as a string,
+    resource as a string)."""
     ids = graph.csr().host.ids
     out = []
     for rec in raw:
@@ -122,8 +135,6 @@ def _events_to_trace(graph: TaskGraph, raw: np.ndarray, names: List[str]) -> Lis
             subject = f"d{int(ids[a])}.{int(ids[b])}" if b >= 0 else f"d{int(ids[a])}"
             resource = "bus"
         out.append(TraceEvent(float(rec["time"]), kind, subject, resource))
-    # sim.py:200 — subject compared as a string
-    out.sort(key=lambda e: (e.time, EVENT_ORDER[e.kind], e.subject, e.resource))
     return out
 
 
@@ -136,7 +147,7 @@ def _run(graphs: Sequence[TaskGraph], policies, machine: MachineModel, events: b
     host = {k: v.cpu().numpy() for k, v in out.items()}
     if (host["status"] != 0).any():
         raise AssertionError("simulation deadlocked on a valid DAG (bug)")
-    return batch, host
+    return batch, host, out
 
 
 def simulate(graph: TaskGraph, policy, machine: Optional[MachineModel] = None,
@@ -145,16 +156,27 @@ def simulate(graph: TaskGraph, policy, machine: Optional[MachineModel] = None,
     machine = machine or MachineModel()
     _policy_id(policy)
     _check_graph(graph)
-    batch, h = _run([graph], [policy], machine, events=True)
+    batch, h, d = _run([graph], [policy], machine, events=True)
     names = _worker_names(machine)
     cnt = int(h["ev_count"][0])
-    raw = h["events"].view(_native.EVENT_DTYPE)[int(h["ev_off"][0]):int(h["ev_off"][0]) + cnt]
+    isz = _native.EVENT_DTYPE.itemsize
+    off = int(h["ev_off"][0])
+    ev_dev = d["events"][off * isz:(off + cnt) * isz]
+    dev = ev_dev.device
+    ids = torch.from_numpy(np.ascontiguousarray(graph.csr().host.ids, dtype=np.int64)).to(dev)
+    rank = torch.tensor(_resource_ranks(names), dtype=torch.int32, device=dev)
+    perm = _native.trace_sort(ev_dev, cnt, ids, rank)
+    raw = h["events"].view(_native.EVENT_DTYPE)[off:off + cnt][perm.cpu().numpy()]
     events = _events_to_trace(graph, raw, names)
-    return Trace(events, float(h["makespan"][0]), int(h["transfer_count"][0]),
-                 int(h["transfer_bytes"][0]),
-                 {CPU: float(h["busy"][0, 0]), GPU: float(h["busy"][0, 1])},
-                 {CPU: int(h["kpd"][0, 0]), GPU: int(h["kpd"][0, 1])},
-                 policy=getattr(policy, "name", ""))
+    tr = Trace(events, float(h["makespan"][0]), int(h["transfer_count"][0]),
+               int(h["transfer_bytes"][0]),
+               {CPU: float(h["busy"][0, 0]), GPU: float(h["busy"][0, 1])},
+               {CPU: int(h["kpd"][0, 0]), GPU: int(h["kpd"][0, 1])},
+               policy=getattr(policy, "name", ""))
+    # the device buffer and order behind the events: metrics() reduces it
+    # on the device while the events are unchanged
+    tr._device = (ev_dev, perm, cnt, graph.csr().n, machine.cpu_workers, events)
+    return tr
 
 
 @dataclass
@@ -186,13 +208,31 @@ def simulate_batch(graphs: Sequence[TaskGraph], policies, machine: Optional[Mach
     if validate_graphs:
         for g in graphs:
             _check_graph(g)
-    _, h = _run(graphs, policies, machine, events=False)
+    _, h, _ = _run(graphs, policies, machine, events=False)
     return BatchResult(h["makespan"], h["transfer_count"], h["transfer_bytes"], h["busy"],
                        h["kpd"])
 
 
 def metrics(trace: Trace) -> Dict[str, object]:
-    """Summary recomputed from the events (sim.py:207-236)."""
+    """Summary recomputed from the events (sim.py:207-236).
+
+    A trace from simulate() keeps its device event buffer: the summary is
+    reduced there (hs_trace_metrics, busy times summed in event order as the
+    reference does). Traces built or edited on the host take the host loop.
+    """
+    dv = getattr(trace, "_device", None)
+    if dv is not None and dv[5] is trace.events and len(trace.events) == dv[2]:
+        ev, perm, cnt, n_nodes, cpu_workers, _ = dv
+        mk, nx, b0, b1, k0, k1 = _native.trace_metrics(ev, perm, cnt, n_nodes, cpu_workers)
+        busy = {CPU: b0, GPU: b1}
+        return {
+            "makespan": mk,
+            "transfer_count": int(nx),
+            "transfer_bytes": trace.transfer_bytes,
+            "busy_ms": busy,
+            "busy_fraction": {d: (busy[d] / mk if mk else 0.0) for d in busy},
+            "kernels_per_device": {CPU: int(k0), GPU: int(k1)},
+        }
     starts: Dict[Tuple[str, str], float] = {}
     busy = {CPU: 0.0, GPU: 0.0}
     counts = {CPU: 0, GPU: 0}
@@ -243,6 +283,22 @@ def trace_csv(trace: Trace) -> str:
     for e in trace.events:
         out.write(f"{e.time!r},{e.kind},{e.subject},{e.resource}\n")
     return out.getvalue()
+
+
+def annotated_dot(graph: TaskGraph, trace: Trace) -> str:
+    """DOT with each kernel's device and start/end times from a finished
+    trace (sim.py:319-331); canonical emission as graphio.emit_dot."""
+    from .graphio import emit_dot
+    info: Dict[int, Dict[str, str]] = {}
+    for e in trace.events:
+        if e.kind in ("kernel_start", "kernel_end"):
+            kid = int(e.subject)
+            d = info.setdefault(kid, {})
+            d["device"] = CPU if e.resource.startswith("cpu") else GPU
+            d["start" if e.kind == "kernel_start" else "end"] = repr(e.time)
+    node_extra = {kid: [("device", d["device"]), ("start", d["start"]), ("end", d["end"])]
+                  for kid, d in info.items()}
+    return emit_dot(graph, node_extra=node_extra)
 
 
 @dataclass
