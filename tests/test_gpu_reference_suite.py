@@ -6,9 +6,9 @@ the vendored files and a `hetsched` package whose submodules ARE this
 package's modules — in a child pytest process on the GPU. Every call the
 tests make therefore goes through the drop-in API and the CUDA kernels.
 
-DOT text I/O (parse_dot / emit_dot / annotated_dot) is out of scope (SURVEY.md
-§2 row 6); the shim supplies those names as stubs that raise, so the modules
-import and exactly the tests that exercise DOT fail. Those are listed in
+DOT text parsing (parse_dot) is not implemented (emit_dot, emit_partitioned_dot
+and annotated_dot are); the shim supplies the missing names as stubs that
+raise, so the modules import and exactly the tests that parse DOT fail. Those are listed in
 tests/golden/reference_suite_expected.json; every other test must pass.
 """
 import hashlib
