@@ -254,6 +254,31 @@ int hs_simulate_batch(const hs_dag_batch_t *g, int policy, const int8_t *pin,
                       hs_event_t *ev, const int64_t *ev_off, int64_t *ev_count,
                       void *stream);
 
+/* ---- weight attachment (attach_weights, graph.py:308-324) -------------
+ * One entry per distinct (kind, size) pair: form 0 = the value pair cpu/gpu
+ * (read from the cost model on the host once), 1 = synthetic MA closed form
+ * (ma_cpu * s^2, ma_gpu * s^2 + launch_ms), 2 = synthetic MM (s^3),
+ * 3 = zero weights (SOURCE kind / the root), -1 = no cost entry. Device
+ * pointers. Transfers: latency_ms + bytes / bandwidth (costs.py:52-55). */
+typedef struct hs_cost_table {
+    int32_t n_pairs;
+    const int32_t *form;   /* [n_pairs] */
+    const double *cpu;     /* [n_pairs] (form 0) */
+    const double *gpu;     /* [n_pairs] (form 0) */
+    double ma_cpu, ma_gpu, mm_cpu, mm_gpu, launch_ms;
+    double latency_ms, bandwidth;
+} hs_cost_table_t;
+/* w_cpu/w_gpu [n] from pair[n] (entry index) and size[n]; w_xfer[m] from
+ * bytes[m], or copied from xfer_tab[m] when given (custom transfer models).
+ * rank[n] (optional) orders nodes for the error report: *bad_node_host =
+ * the smallest rank among nodes without a cost entry (-1 if none);
+ * *bad_edge_host = the first edge with a negative byte count (-1 if none).
+ * Synchronous. */
+int hs_attach_weights(const hs_cost_table_t *t, int32_t n, const int32_t *pair,
+                      const int64_t *size, const int32_t *rank, double *w_cpu, double *w_gpu,
+                      int64_t m, const int64_t *bytes, const double *xfer_tab, double *w_xfer,
+                      int32_t *bad_node_host, int64_t *bad_edge_host, void *stream);
+
 /* Trace products (sim.py:200-236) from a device event buffer of one
  * simulation (count events, node indices local to the graph):
  * hs_trace_sort writes perm[count] = event indices in the reference's order

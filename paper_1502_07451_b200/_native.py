@@ -301,6 +301,40 @@ def simulate_batch(batch, policy: int, pin: Optional[torch.Tensor], cpu_workers:
     return out
 
 
+class HsCostTable(ctypes.Structure):
+    _fields_ = [("n_pairs", ctypes.c_int32), ("form", _P), ("cpu", _P), ("gpu", _P),
+                ("ma_cpu", ctypes.c_double), ("ma_gpu", ctypes.c_double),
+                ("mm_cpu", ctypes.c_double), ("mm_gpu", ctypes.c_double),
+                ("launch_ms", ctypes.c_double), ("latency_ms", ctypes.c_double),
+                ("bandwidth", ctypes.c_double)]
+
+
+_attach = _opt("hs_attach_weights", _P, _i32, _P, _P, _P, _P, _P, ctypes.c_int64, _P, _P, _P,
+               _P, _P, _P)
+
+
+def attach_weights(form, cpu, gpu, transfer, pair, size, rank, nbytes, xfer_tab, dev):
+    """(w_cpu, w_gpu, w_xfer, bad_node_rank, bad_edge) — hs_attach_weights."""
+    from . import costs as C
+    f = torch.tensor(form or [0], dtype=torch.int32, device=dev)
+    c = torch.tensor(cpu or [0.0], dtype=torch.float64, device=dev)
+    g = torch.tensor(gpu or [0.0], dtype=torch.float64, device=dev)
+    t = HsCostTable(len(form), ptr(f), ptr(c), ptr(g), C.MA_CPU_COEFF, C.MA_GPU_COEFF,
+                    C.MM_CPU_COEFF, C.MM_GPU_COEFF, C.GPU_LAUNCH_MS,
+                    transfer.latency_ms if transfer is not None else 0.0,
+                    transfer.bandwidth_bytes_per_ms if transfer is not None else 1.0)
+    n, m = int(pair.numel()), int(nbytes.numel())
+    w_cpu = torch.empty(n, dtype=torch.float64, device=dev)
+    w_gpu = torch.empty(n, dtype=torch.float64, device=dev)
+    w_xfer = torch.empty(m, dtype=torch.float64, device=dev)
+    bn, be = ctypes.c_int32(-1), ctypes.c_int64(-1)
+    check(_need(_attach, "hs_attach_weights")(ctypes.byref(t), n, ptr(pair), ptr(size), ptr(rank),
+                                              ptr(w_cpu), ptr(w_gpu), m, ptr(nbytes),
+                                              ptr(xfer_tab), ptr(w_xfer), ctypes.byref(bn),
+                                              ctypes.byref(be), stream_ptr()))
+    return w_cpu, w_gpu, w_xfer, bn.value, be.value
+
+
 _trace_sort = _opt("hs_trace_sort", _P, ctypes.c_int64, _P, _P, _P, _P)
 _trace_metrics = _opt("hs_trace_metrics", _P, _P, ctypes.c_int64, _i32, _i32, _P, _P)
 

@@ -191,24 +191,49 @@ def topological_order(graph: TaskGraph) -> List[int]:
 def attach_weights(graph: TaskGraph, model) -> TaskGraph:
     """Copy of ``graph`` with node/edge weights from ``model`` (graph.py:308-324).
 
-    Per-node work is two closed-form cost-model lookups; the root (or any
-    SOURCE node) is forced to zero weight.
+    The weights are computed on the device (``hs_attach_weights``, one entry
+    per distinct (kind, size) pair: the synthetic closed forms per node, any
+    other model read once per pair); the root (or any SOURCE node) is forced
+    to zero weight. The first node in the graph's node order without a cost
+    entry raises GraphError with the model's own message, a negative byte
+    count the model's CostModelError, as the reference does.
     """
-    nodes = []
-    for node in graph.nodes.values():
-        if node.id == graph.root or node.kind == SOURCE_KIND:
-            nodes.append(replace(node, weight_cpu=0.0, weight_gpu=0.0))
-            continue
+    import numpy as np
+    import torch
+    from . import _native
+    from .costs import device_weights
+    nodes = list(graph.nodes.values())
+    edges = list(graph.edges.values())
+    keys, index = [], {}
+    pair = np.empty(len(nodes), dtype=np.int32)
+    size = np.empty(len(nodes), dtype=np.int64)
+    for r, node in enumerate(nodes):
+        key = None if (node.id == graph.root or node.kind == SOURCE_KIND) else (node.kind, node.size)
+        if key not in index:
+            index[key] = len(keys)
+            keys.append(key)
+        pair[r] = index[key]
+        size[r] = node.size if -2 ** 63 <= node.size < 2 ** 63 else 0
+    dev = _native.device()
+    t = lambda a: torch.from_numpy(a).to(dev)  # noqa: E731
+    nbytes = np.fromiter((e.bytes for e in edges), dtype=np.int64, count=len(edges))
+    w_cpu, w_gpu, w_xfer, bad_node, bad_edge = device_weights(
+        model, keys, t(pair), t(size), t(nbytes), rank=None, device=dev)
+    if bad_node >= 0:
+        node = nodes[bad_node]
         try:
-            wc = model.kernel_time(node.kind, node.size, CPU)
-            wg = model.kernel_time(node.kind, node.size, GPU)
+            model.kernel_time(node.kind, node.size, CPU)
+            model.kernel_time(node.kind, node.size, GPU)
         except Exception as exc:
             raise GraphError(f"no cost entry for kernel {node.id} "
                              f"({node.kind}, {node.size}): {exc}") from exc
-        nodes.append(replace(node, weight_cpu=wc, weight_gpu=wg))
-    edges = [replace(e, weight_xfer=model.transfer_time(e.bytes))
-             for e in graph.edges.values()]
-    return graph.replace_nodes(nodes, edges)
+        raise GraphError(f"no cost entry for kernel {node.id} ({node.kind}, {node.size})")
+    if bad_edge >= 0:
+        model.transfer_time(edges[bad_edge].bytes)  # raises the model's CostModelError
+    wc, wg, wx = (x.cpu().numpy().tolist() for x in (w_cpu, w_gpu, w_xfer))
+    new_nodes = [replace(node, weight_cpu=wc[r], weight_gpu=wg[r]) for r, node in enumerate(nodes)]
+    new_edges = [replace(e, weight_xfer=wx[i]) for i, e in enumerate(edges)]
+    return graph.replace_nodes(new_nodes, new_edges)
 
 
 def total_weights(graph: TaskGraph) -> Tuple[float, float, float]:

@@ -103,18 +103,59 @@ def layered_dag(n_kernels: int, m_inter: int, seed: int = 0, kind: str = "MA", s
     layer_of = torch.empty(n_nodes, dtype=torch.int32, device=dev)
     _native.layered_generate(n_kernels, m_inter, seed, out_ptr, out_dst, in_ptr, in_src, in_eid,
                              layer_of)
-    wc = model.kernel_time(kind, size, "CPU")
-    wg = model.kernel_time(kind, size, "GPU")
-    w_cpu = torch.full((n_nodes,), wc, dtype=torch.float64, device=dev)
-    w_gpu = torch.full((n_nodes,), wg, dtype=torch.float64, device=dev)
-    w_cpu[0] = 0.0
-    w_gpu[0] = 0.0
     payload = size * size * 4
     nbytes = torch.full((m,), payload, dtype=torch.int64, device=dev)
-    w_xfer = torch.full((m,), model.transfer_time(payload), dtype=torch.float64, device=dev)
+    w_cpu = w_gpu = w_xfer = None
     csr = DagCSR(n_nodes, m, 0, out_ptr, out_dst, in_ptr, in_src, in_eid, w_cpu, w_gpu, w_xfer,
                  nbytes, ids=None, host=None)
     csr.layer_of = layer_of
+    attach_weights_csr(csr, torch.zeros(n_nodes, dtype=torch.int32, device=dev), [kind],
+                       torch.full((n_nodes,), size, dtype=torch.int64, device=dev), model)
+    return csr
+
+
+def attach_weights_csr(csr: DagCSR, kind_code: torch.Tensor, kinds: Sequence[str],
+                       size: torch.Tensor, model) -> DagCSR:
+    """attach_weights (graph.py:308-324) for a device DAG: node v has kind
+    ``kinds[kind_code[v]]`` and size ``size[v]`` (device tensors); the root
+    gets zero weights; w_cpu / w_gpu / w_xfer are (re)computed on the device
+    (hs_attach_weights) from ``model`` and the edges' byte counts. Raises the
+    reference's GraphError for the smallest node index without a cost entry
+    and the model's CostModelError for a negative byte count."""
+    from .costs import _EXACT_SIZE, _closed_form, device_weights
+    from .graph import GraphError
+    dev = csr.device
+    code = kind_code.to(torch.int64)
+    closed = _closed_form(model) and int(size.abs().max()) <= min(
+        (_EXACT_SIZE.get(k, 0) for k in kinds), default=0) if size.numel() else _closed_form(model)
+    if closed:  # one entry per kind, the size per node
+        keys = [(k, None) for k in kinds]
+        pair = code.to(torch.int32)
+    else:  # one entry per distinct (kind, size)
+        packed = code << 40 | size.to(torch.int64)
+        uniq, inv = torch.unique(packed, return_inverse=True)
+        u = uniq.cpu().numpy().tolist()
+        keys = [(kinds[x >> 40], x & ((1 << 40) - 1)) for x in u]
+        pair = inv.to(torch.int32)
+    if 0 <= csr.root < csr.n:
+        keys.append(None)
+        pair = pair.clone()
+        pair[csr.root] = len(keys) - 1
+    w_cpu, w_gpu, w_xfer, bad_node, bad_edge = device_weights(
+        model, keys, pair.contiguous(), size.to(torch.int64).contiguous(), csr.bytes, device=dev)
+    if bad_node >= 0:
+        kind, sz = kinds[int(kind_code[bad_node])], int(size[bad_node])
+        nid = int(csr.ids[bad_node]) if csr.ids is not None else bad_node
+        try:
+            model.kernel_time(kind, sz, "CPU")
+            model.kernel_time(kind, sz, "GPU")
+        except Exception as exc:
+            raise GraphError(f"no cost entry for kernel {nid} ({kind}, {sz}): {exc}") from exc
+        raise GraphError(f"no cost entry for kernel {nid} ({kind}, {sz})")
+    if bad_edge >= 0:
+        model.transfer_time(int(csr.bytes[bad_edge]))
+    csr.w_cpu, csr.w_gpu, csr.w_xfer = w_cpu, w_gpu, w_xfer
+    csr._struct = None
     return csr
 
 

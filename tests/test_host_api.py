@@ -11,19 +11,37 @@ from paper_1502_07451_b200.sim import MachineModel, SimulationError
 from _util import graph_from_spec, make_graph, random_weighted_graph, spec_of
 
 
+def _structure(spec):
+    """A spec without its weights (ids, kinds, sizes, edges, byte counts)."""
+    return {"root": spec["root"], "nodes": [r[:3] for r in spec["nodes"]],
+            "edges": [r[:3] for r in spec["edges"]]}
+
+
 def test_generator_reproduces_reference_graphs(small_cases, medium_cases):
-    """generate_random_dag + attach_weights == the reference's (graph.py:180-324)."""
+    """generate_random_dag == the reference's (graph.py:180-305), structure only
+    (the weights come from the device, tests/test_gpu_api_edges.py)."""
     for s in range(40):
-        assert spec_of(random_weighted_graph(s)) == small_cases[s]["spec"]
-    for s in range(10):
-        g = random_weighted_graph(100 + s, kind="MM", size=1024)
-        assert spec_of(g) == small_cases[40 + s]["spec"]
+        g = gen.generate_random_dag(*_small_shape(s), "MA", 256, seed=s)
+        assert _structure(spec_of(g)) == _structure(small_cases[s]["spec"])
     for s, (n, m, kind) in enumerate([(38, 75, "MA"), (120, 240, "MA"), (120, 240, "MM"),
                                       (250, 500, "MA")]):
-        g = costs.SyntheticCostModel()
         gg = gen.generate_random_dag(n, m, kind, 1024, seed=s)
-        from paper_1502_07451_b200.graph import attach_weights
-        assert spec_of(attach_weights(gg, g)) == medium_cases[s]["spec"]
+        assert _structure(spec_of(gg)) == _structure(medium_cases[s]["spec"])
+
+
+def _small_shape(seed, max_kernels=15):
+    """(n, m) of _util.random_weighted_graph(seed) (the reference's conftest recipe)."""
+    import random
+    from paper_1502_07451_b200.graph import InfeasibleGraphError
+    rng = random.Random(seed)
+    n = rng.randint(2, max_kernels)
+    m = rng.randint(0, 2 * (n - 1))
+    while True:
+        try:
+            gen.generate_random_dag(n, m, "MA", 256, seed=seed)
+            return n, m
+        except InfeasibleGraphError:
+            m -= 1
 
 
 def test_count_root_mode_matches_shape():
@@ -39,6 +57,7 @@ def test_cholesky_dag_shape():
     assert len(tasks) == 45760 and len(deps) == 131040
 
 
+@pytest.mark.gpu  # attach_weights runs on the device
 def test_cholesky_matches_golden(medium_cases):
     c = [c for c in medium_cases if c["name"] == "cholesky_T8"][0]
     model = costs.load_calibration(
