@@ -70,6 +70,44 @@ struct G {
   __device__ __forceinline__ int ew(int64_t j) const { return wconst ? wconst : __ldg(wgt + j); }
 };
 
+// L2 residency of the connectivity cache. Its rows (80 MB on config 4) are
+// re-read and updated every pass, while the adjacency and state streams of the
+// same pass (GBs) would evict them: cache-row accesses carry an evict_last
+// policy, one-touch adjacency gathers evict_first (PTX cache hints).
+__device__ __forceinline__ uint64_t l2_keep() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint2 ld_keep2(const void *ptr, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;"
+               : "=r"(r.x), "=r"(r.y) : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_keep4(const void *ptr, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_keep2(void *ptr, unsigned long long v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(ptr), "l"(v), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void red_keep(unsigned long long *ptr, unsigned long long v,
+                                         uint64_t pol) {
+  asm volatile("red.global.add.L2::cache_hint.u64 [%0], %1, %2;" :: "l"(ptr), "l"(v), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ int32_t ld_once(const int32_t *ptr) {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  int32_t r;
+  asm volatile("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+  return r;
+}
+
 // Connectivity (gain) cache: row v holds kc counters of cw bytes (1, 2 or 4;
 // the host picks the narrowest width that cannot overflow: every counter is at
 // most v's weighted degree). Narrow rows keep the cache L2-resident.
@@ -96,7 +134,7 @@ struct Conn {
                          // borrow/carry can cross a counter, as below)
       const unsigned long long delta = ((unsigned long long)(unsigned)w << (8 * cw * dest)) -
                                        ((unsigned long long)(unsigned)w << (8 * cw * own));
-      atomicAdd(reinterpret_cast<unsigned long long *>(p + row), delta);
+      red_keep(reinterpret_cast<unsigned long long *>(p + row), delta, l2_keep());
       return;
     }
     const int64_t bo = row + own * cw, bd = row + dest * cw;
@@ -120,7 +158,7 @@ __device__ __forceinline__ void conn_row(const uint8_t *p, int64_t v, int (&c)[K
   uint32_t w[WORDS];
   const uint8_t *row = p + v * KC * CW;
   if constexpr (WORDS == 2) {
-    const uint2 x = __ldg(reinterpret_cast<const uint2 *>(row));
+    const uint2 x = ld_keep2(row, l2_keep());
     w[0] = x.x; w[1] = x.y;
   } else {
 #pragma unroll

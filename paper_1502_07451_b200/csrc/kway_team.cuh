@@ -254,7 +254,8 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       }
       if (row8) {
         for (int off = T / 2; off; off >>= 1) row |= __shfl_xor_sync(0xffffffffu, row, off, T);
-        if (valid && lane == 0) reinterpret_cast<unsigned long long *>(cache.p)[v] = row;
+        if (valid && lane == 0) st_keep2(reinterpret_cast<unsigned long long *>(cache.p) + v, row,
+                                         l2_keep());
       }
       __syncwarp();
       team_argmax<T>(bg, bp);
@@ -490,8 +491,9 @@ refine_cached_v4(G g, const part_t *part, int k, const int64_t *pw, const int64_
         const int4 w = __ldg(reinterpret_cast<const int4 *>(g.vw) + t);
         vw4[0] = w.x; vw4[1] = w.y; vw4[2] = w.z; vw4[3] = w.w;
       }
-      const uint4 a = __ldg(reinterpret_cast<const uint4 *>(cache) + 2 * t);
-      const uint4 b = __ldg(reinterpret_cast<const uint4 *>(cache) + 2 * t + 1);
+      const uint64_t keep = l2_keep();
+      const uint4 a = ld_keep4(reinterpret_cast<const uint4 *>(cache) + 2 * t, keep);
+      const uint4 b = ld_keep4(reinterpret_cast<const uint4 *>(cache) + 2 * t + 1, keep);
       rw[0] = a.x; rw[1] = a.y; rw[2] = a.z; rw[3] = a.w;
       rw[4] = b.x; rw[5] = b.y; rw[6] = b.z; rw[7] = b.w;
     } else {
@@ -673,7 +675,7 @@ __device__ __forceinline__ void cache_move_flat(const G &g, const Conn &cache, i
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      uu[q] = jj[q] >= 0 ? __ldg(g.adj + jj[q]) : 0;
+      uu[q] = jj[q] >= 0 ? ld_once(g.adj + jj[q]) : 0;
       ww[q] = jj[q] >= 0 ? g.ew(jj[q]) : 0;
     }
 #pragma unroll
@@ -736,7 +738,7 @@ afterburner_t(G g, const uint32_t *st, const int32_t *list, const int32_t *count
 #pragma unroll
         for (int q = 0; q < AU; ++q) {
           const int j = j0 + q * T;
-          u[q] = j < d ? __ldg(g.adj + b + j) : -1;
+          u[q] = j < d ? ld_once(g.adj + b + j) : -1;
           w[q] = j < d ? g.ew(b + j) : 0;
         }
 #pragma unroll
