@@ -211,6 +211,115 @@ __global__ void __launch_bounds__(1024) levels_kernel(LevelArgs A) {
   }
 }
 
+// ---- dataflow form for DAGs numbered in topological order --------------
+// When every edge u -> v has u < v, no grid barrier is needed: CTAs take
+// consecutive vertex chunks from a ticket counter and every vertex pulls its
+// predecessors (in-CSR), waiting until each has published its level. A
+// vertex only waits on smaller ids — in its own chunk or in chunks ticketed
+// earlier to warps that are already running — so the wait always ends. Both
+// outputs are their own ready flags: level -1 and finish all-ones bits (a
+// NaN no arithmetic produces) until written. A predecessor's level and finish
+// are polled together with relaxed loads (aligned 4- and 8-byte accesses do
+// not tear), so no fence orders them. Same max/add per vertex as the
+// frontier kernel, so the same bits.
+constexpr int kFlowBlock = 512;
+
+__device__ __forceinline__ int32_t ld_relaxed(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const double *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(int32_t *p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed64(double *p, double v) {
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
+}
+__global__ void all_edges_up(int32_t n, const int64_t *out_ptr, const int32_t *out_dst,
+                             int32_t *bad) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = out_ptr[v], e = out_ptr[v + 1];
+    if (b < e && out_dst[b] <= v) atomicExch(bad, 1);
+  }
+}
+
+__global__ void __launch_bounds__(kFlowBlock) levels_flow(LevelArgs A, int32_t *ticket) {
+  const hs_dag_t &g = A.g;
+  const int lane = threadIdx.x & 31;
+  int lmax = -1;
+  double cmax = 0.0;
+  int32_t done = 0;
+  // warp-granular tickets: 32 consecutive vertices per ticket, no CTA barrier
+  for (;;) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(ticket, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const int64_t v = (int64_t)t * 32 + lane;
+    if ((int64_t)t * 32 >= g.n) break;
+    if (v >= g.n) continue;
+    const int64_t j0 = g.in_ptr[v], j1 = g.in_ptr[v + 1];
+    const int pv = (A.mode == 3 && v != g.root) ? A.part[v] : 0;
+    const double dur = A.mode == 0 ? pmin(g.w_cpu[v], g.w_gpu[v])
+                       : (A.mode == 1 ? g.w_gpu[v]
+                          : (A.mode == 2 ? g.w_cpu[v] : (A.dev[pv] ? g.w_gpu[v] : g.w_cpu[v])));
+    int lev = -1;
+    unsigned long long reach = 0ull;  // max of non-negative doubles as ordered bits
+    constexpr int kB = 8;
+    for (int64_t jb = j0; jb < j1; jb += kB) {
+      int32_t u[kB], lv[kB];
+      unsigned long long fb[kB];
+      const int nb = (int)(j1 - jb < kB ? j1 - jb : kB);
+#pragma unroll
+      for (int q = 0; q < kB; ++q) u[q] = q < nb ? __ldg(g.in_src + jb + q) : 0;
+      // poll: every predecessor of the batch published its level and finish
+      bool ready;
+      do {
+        ready = true;
+#pragma unroll
+        for (int q = 0; q < kB; ++q) {
+          if (q < nb) {
+            lv[q] = ld_relaxed(A.level + u[q]);
+            fb[q] = ld_relaxed64(A.finish + u[q]);
+            ready = ready && lv[q] >= 0 && fb[q] != ~0ull;
+          }
+        }
+        if (!ready) __nanosleep(32);
+      } while (!ready);
+#pragma unroll
+      for (int q = 0; q < kB; ++q) {
+        if (q < nb) {
+          double c = __longlong_as_double((long long)fb[q]);
+          if (A.mode == 3) {
+            const int pu = u[q] != g.root ? A.part[u[q]] : 0;
+            const bool cross = u[q] == g.root ? A.dev[pv] != 0 : pu != pv;
+            if (cross) c = c + g.w_xfer[__ldg(g.in_eid + jb + q)];
+          }
+          const unsigned long long cb = (unsigned long long)__double_as_longlong(c);
+          reach = cb > reach ? cb : reach;
+          lev = lv[q] > lev ? lv[q] : lev;
+        }
+      }
+    }
+    const double f = __longlong_as_double((long long)reach) + dur;
+    st_relaxed64(A.finish + v, f);
+    st_relaxed(A.level + v, lev + 1);
+    lmax = lev + 1 > lmax ? lev + 1 : lmax;
+    cmax = f > cmax ? f : cmax;
+    ++done;
+  }
+  if (lmax >= 0) atomicMax(A.max_level, lmax);
+  if (done) {
+    atomicMax(A.cp_bits, (unsigned long long)__double_as_longlong(cmax));
+    atomicAdd(A.processed, done);
+  }
+}
+
 }  // namespace
 
 namespace {
@@ -273,8 +382,34 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
   int need = (int)((n + block - 1) / block);
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
-  void *args[] = {&A};
+  // DAG numbered in topological order: the barrier-free dataflow kernel
   {
+    HS_CHECK_CUDA(cudaMemsetAsync(small.p + 7, 0, sizeof(int32_t), s));
+    all_edges_up<<<hs::grid_for(n, 256), 256, 0, s>>>((int32_t)n, g->out_ptr, g->out_dst,
+                                                       small.p + 7);
+    HS_CHECK_LAUNCH();
+    int32_t bad = 1;
+    HS_CHECK_CUDA(cudaMemcpyAsync(&bad, small.p + 7, 4, cudaMemcpyDeviceToHost, s));
+    HS_CHECK_CUDA(cudaStreamSynchronize(s));
+    if (!bad && n > 0) {
+      HS_CHECK_CUDA(cudaMemsetAsync(level, 0xff, n * sizeof(int32_t), s));
+      HS_CHECK_CUDA(cudaMemsetAsync(finish, 0xff, n * sizeof(double), s));
+      HS_CHECK_CUDA(cudaMemsetAsync(small.p + 7, 0, sizeof(int32_t), s));
+      int fper = 0;
+      HS_CHECK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fper, levels_flow, kFlowBlock, 0));
+      int fgrid = hs::sm_count() * (fper < 1 ? 1 : fper);
+      const int64_t chunks = (n + kFlowBlock - 1) / kFlowBlock;  // CTAs worth of warps
+      if (fgrid > chunks) fgrid = (int)chunks;
+      // in-CSR + in_src + level/finish gathers per edge + weights + writes
+      hs::Prof P("levels", s, 8.0 * n + 4.0 * g->m + 12.0 * g->m + 16.0 * n + 12.0 * n +
+                                  (mode == 3 ? 16.0 * g->m : 0.0));
+      levels_flow<<<fgrid, kFlowBlock, 0, s>>>(A, small.p + 7);
+      HS_CHECK_LAUNCH();
+      goto results;
+    }
+  }
+  {
+    void *args[] = {&A};
     // in_ptr (pending counts) + out-CSR + weights + reach/pending init and
     // read + finish/level writes + frontier lists; per edge one reach and
     // one pending read-modify-write (mode 3: + w_xfer, part of both ends)
@@ -283,6 +418,7 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
     HS_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)levels_kernel, grid, block, args, 0, s));
   }
   HS_CHECK_LAUNCH();
+results:
   if (cp_host || n_levels_host) {
     int32_t h[8];
     unsigned long long cpb = 0;

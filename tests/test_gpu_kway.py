@@ -269,3 +269,24 @@ def test_assigned_makespan_layered_partition():
     want = O.assigned_makespan(O.OGraph(spec), {i: int(p[i]) for i in range(csr.n)},
                                set(range(8)))
     assert ms == want and ms > 0
+
+
+@pytest.mark.parametrize("n,m", [(3000, 20000), (200_000, 2_000_000)])
+def test_levels_dataflow_equals_frontier(n, m):
+    """K7 on a creation-order DAG (every edge points up: the barrier-free
+    dataflow kernel) equals K7 on the same DAG randomly renumbered (the
+    frontier kernel), node for node under the permutation: levels, finish
+    times (bits), critical path; and mode 3 on an assignment."""
+    csr = kway.layered_dag(n, m, seed=4)
+    rel, pi = kway.relabeled_dag(csr, seed=2)
+    lv, fin, cp, nl = kway.levels(csr)
+    lv2, fin2, cp2, nl2 = kway.levels(rel)
+    pil = pi.long()
+    assert cp == cp2 and nl == nl2
+    assert torch.equal(lv2[pil], lv) and torch.equal(fin2[pil], fin)
+    part = torch.randint(0, 4, (csr.n,), dtype=torch.int32, device=csr.device)
+    part2 = torch.empty_like(part)
+    part2[pil] = part
+    ms, f1 = kway.assigned_makespan(csr, part, [1, 3], k=4)
+    ms2, f2 = kway.assigned_makespan(rel, part2, [1, 3], k=4)
+    assert ms == ms2 and torch.equal(f2[pil], f1)
