@@ -752,51 +752,41 @@ REF_CFG5 = {  # reference compare(), seeds 0..4095, MA-1024 38/
 
 
 def policy_sweep(iterations: int = 4096):
-    """Config 5: 4096 x (generate_random_dag(38, 75, MA, 1024), gp/eager/dmda)."""
+    """Config 5: 4096 x (generate_random_dag(38, 75, MA, 1024), gp/eager/dmda).
+
+    The public API call (sim.compare over gen.RandomDagFactory: graphs built
+    on the device, identical to the factory's TaskGraphs) timed end to end,
+    then its stages: device generation + weights, gp partitions, one K8
+    launch per policy."""
     import time as _t
     import torch
-    import paper_1502_07451_b200 as H
-    from paper_1502_07451_b200.sim import MachineModel, simulate_batch
-    from paper_1502_07451_b200.policies import EagerPolicy, DmdaPolicy, gp_build_batch
-    model = H.SyntheticCostModel()
+    from paper_1502_07451_b200 import _native, gen, sim
+    from paper_1502_07451_b200.policies import gp_pins_batch
+    fac = gen.RandomDagFactory(38, 75, "MA", 1024)
+    machine = sim.MachineModel(3, 1)
+    sim.compare(["eager", "dmda", "gp"], fac, machine, iterations=64)  # warm-up
+    torch.cuda.synchronize()
     t0 = _t.perf_counter()
-    graphs = [H.attach_weights(H.generate_random_dag(38, 75, "MA", 1024, seed=i), model)
-              for i in range(iterations)]
-    for g in graphs:
-        g.csr()  # lower to device CSR once
-    host_prep = _t.perf_counter() - t0
-    machine = MachineModel(3, 1)
-    out = {"iterations": iterations, "host_graph_prep_s": host_prep}
+    rows = sim.compare(["eager", "dmda", "gp"], fac, machine, iterations=iterations)
     torch.cuda.synchronize()
-    t1 = _t.perf_counter()
-    gp = gp_build_batch(graphs)
-    torch.cuda.synchronize()
-    out["gp_partitions_s"] = _t.perf_counter() - t1
-    sims = 0
-    dev_ms = 0.0
+    api_s = _t.perf_counter() - t0
+    out = {"iterations": iterations, "compare_public_api_s": api_s,
+           "simulations_per_s_public_api": 3 * iterations / api_s}
     exact = True
-    for name, pols in (("eager", [EagerPolicy()] * iterations),
-                       ("dmda", [DmdaPolicy()] * iterations), ("gp", gp)):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        res = simulate_batch(graphs, pols, machine, validate_graphs=False)
-        b.record()
-        torch.cuda.synchronize()
-        dev_ms += a.elapsed_time(b)
-        sims += iterations
-        mk = statistics.fmean([float(x) for x in res.makespan])
-        tr = statistics.fmean([float(x) for x in res.transfer_count])
-        out[f"{name}_mean_makespan"] = mk
-        out[f"{name}_mean_transfers"] = tr
+    for r in rows:
+        out[f"{r.policy}_mean_makespan"] = r.mean_makespan
+        out[f"{r.policy}_mean_transfers"] = r.mean_transfers
         if iterations == 4096:
-            exact &= (mk, tr) == REF_CFG5[name]
-    out["simulate_calls_ms"] = dev_ms  # public API incl. host batch packing
-    # device-only: one packed batch, K8 launch per policy timed with events
-    from paper_1502_07451_b200 import _native
-    from paper_1502_07451_b200.csr import DagBatch
-    from paper_1502_07451_b200.sim import _pin_array
-    batch = DagBatch([g.csr().host for g in graphs])
-    pin = _pin_array(graphs, gp)
+            exact &= (r.mean_makespan, r.mean_transfers) == REF_CFG5[r.policy]
+    # stages
+    t1 = _t.perf_counter()
+    batch = fac.batch(range(iterations))
+    torch.cuda.synchronize()
+    out["device_graph_generation_s"] = _t.perf_counter() - t1
+    t2 = _t.perf_counter()
+    pin = gp_pins_batch(batch)
+    torch.cuda.synchronize()
+    out["gp_partitions_s"] = _t.perf_counter() - t2
     kern_ms = 0.0
     for pid, p in ((0, None), (1, None), (2, pin)):
         _native.simulate_batch(batch, pid, p, 3, 1)
@@ -808,9 +798,7 @@ def policy_sweep(iterations: int = 4096):
         torch.cuda.synchronize()
         kern_ms += a.elapsed_time(b)
     out["des_kernel_ms_3x4096"] = kern_ms
-    out["simulations_per_s"] = sims / (kern_ms / 1e3)
-    out["simulations_per_s_public_api"] = sims / (dev_ms / 1e3)
-    out["sweep_s_incl_gp_partitions"] = out["gp_partitions_s"] + dev_ms / 1e3
+    out["simulations_per_s"] = 3 * iterations / (kern_ms / 1e3)
     if iterations == 4096:
         out["matches_reference_means_bit_exact"] = exact
     return out

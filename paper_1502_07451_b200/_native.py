@@ -335,6 +335,34 @@ def attach_weights(form, cpu, gpu, transfer, pair, size, rank, nbytes, xfer_tab,
     return w_cpu, w_gpu, w_xfer, bn.value, be.value
 
 
+_rgen = _opt("hs_random_dag_batch", _i32, _P, _i32, _i32, _P, ctypes.c_int64, ctypes.c_int64,
+             ctypes.c_int64, _i32, ctypes.c_int64, ctypes.c_int64, _P, _P, _P, _P, _P, _P,
+             ctypes.c_int64, _P)
+
+
+def random_dag_batch(seeds: torch.Tensor, shape: dict, n_nodes: int):
+    """(edge_counts, out_ptr, out_dst, in_ptr, in_src, in_eid) of hs_random_dag_batch."""
+    fn = _need(_rgen, "hs_random_dag_batch")
+    b = int(seeds.numel())
+    dev = seeds.device
+    first = torch.tensor(shape["first"], dtype=torch.int32, device=dev)
+    counts = (ctypes.c_int64 * max(b, 1))()
+    args = (b, ptr(seeds), shape["n_real"], shape["n_layers"], ptr(first), shape["base_capacity"],
+            shape["inter_target"], shape["extra"], shape["mode"], shape["pop_cap"],
+            shape["edge_cap"], counts)
+    check(fn(*args, None, None, None, None, None, 0, stream_ptr()))
+    m = np.frombuffer(counts, dtype=np.int64, count=b).copy()
+    total = int(m.sum())
+    out_ptr = torch.empty(b * (n_nodes + 1), dtype=torch.int64, device=dev)
+    in_ptr = torch.empty(b * (n_nodes + 1), dtype=torch.int64, device=dev)
+    out_dst = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    in_src = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    in_eid = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+    check(fn(*args, ptr(out_ptr), ptr(out_dst), ptr(in_ptr), ptr(in_src), ptr(in_eid), total,
+             stream_ptr()))
+    return m, out_ptr, out_dst[:total], in_ptr, in_src[:total], in_eid[:total]
+
+
 _trace_sort = _opt("hs_trace_sort", _P, ctypes.c_int64, _P, _P, _P, _P)
 _trace_metrics = _opt("hs_trace_metrics", _P, _P, ctypes.c_int64, _i32, _i32, _P, _P)
 

@@ -266,6 +266,50 @@ class DagBatch:
         self.bytes = cat([h.bytes for h in hosts], np.int64)
         self._struct = None
 
+    @classmethod
+    def from_device(cls, node_counts: np.ndarray, edge_counts: np.ndarray, root, out_ptr,
+                    out_dst, in_ptr, in_src, in_eid, w_cpu, w_gpu, w_xfer, nbytes) -> "DagBatch":
+        """A batch whose arrays were written on the device (gen.generate_random_dag_batch)."""
+        self = cls.__new__(cls)
+        self.device = out_ptr.device
+        self.hosts = None
+        self.batch = len(node_counts)
+        self.node_counts = np.asarray(node_counts, dtype=np.int64)
+        self.edge_counts = np.asarray(edge_counts, dtype=np.int64)
+        self.node_off_h = np.zeros(self.batch + 1, dtype=np.int64)
+        self.edge_off_h = np.zeros(self.batch + 1, dtype=np.int64)
+        np.cumsum(self.node_counts, out=self.node_off_h[1:])
+        np.cumsum(self.edge_counts, out=self.edge_off_h[1:])
+        t = lambda a: torch.from_numpy(a).to(self.device)  # noqa: E731
+        self.node_off, self.edge_off = t(self.node_off_h), t(self.edge_off_h)
+        self.root = root
+        self.out_ptr, self.out_dst, self.in_ptr = out_ptr, out_dst, in_ptr
+        self.in_src, self.in_eid = in_src, in_eid
+        self.w_cpu, self.w_gpu, self.w_xfer, self.bytes = w_cpu, w_gpu, w_xfer, nbytes
+        self._struct = None
+        return self
+
+    def host_dags(self) -> List[HostDag]:
+        """Per-graph HostDag views (numpy) of the batch (ids 0..n_b-1)."""
+        if self.hosts is not None:
+            return self.hosts
+        op = self.out_ptr.cpu().numpy()
+        dst = self.out_dst.cpu().numpy()
+        wc, wg = self.w_cpu.cpu().numpy(), self.w_gpu.cpu().numpy()
+        wx, nb = self.w_xfer.cpu().numpy(), self.bytes.cpu().numpy()
+        root = self.root.cpu().numpy()
+        out = []
+        for b in range(self.batch):
+            n0, n1 = self.node_off_h[b], self.node_off_h[b + 1]
+            e0, e1 = self.edge_off_h[b], self.edge_off_h[b + 1]
+            ptr = op[n0 + b:n1 + b + 1]
+            src = np.repeat(np.arange(n1 - n0, dtype=np.int32), np.diff(ptr))
+            out.append(HostDag(np.arange(n1 - n0, dtype=np.int64), int(root[b]), src,
+                               dst[e0:e1].copy(), wc[n0:n1].copy(), wg[n0:n1].copy(),
+                               wx[e0:e1].copy(), nb[e0:e1].copy()))
+        self.hosts = out
+        return out
+
     def struct(self) -> _native.HsDagBatch:
         if self._struct is None:
             p = _native.ptr

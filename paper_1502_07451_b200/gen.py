@@ -119,6 +119,113 @@ def generate_random_dag(n_kernels: int, n_edges: int, kind: str, size: int,
     return TaskGraph(nodes, edges)
 
 
+def random_dag_shape(n_kernels: int, n_edges: int, layers: Optional[int] = None,
+                     count_root: bool = False) -> dict:
+    """The seed-independent part of generate_random_dag (graph.py:195-252):
+    layer bounds, slot capacity, targets; raises the reference's
+    InfeasibleGraphError exactly where generate_random_dag does."""
+    from .graph import InfeasibleGraphError
+    n_real = n_kernels - 1 if count_root else n_kernels
+    if n_real < 1:
+        raise InfeasibleGraphError("need at least one kernel")
+    n_layers = min(layers if layers else max(1, math.ceil(math.sqrt(n_real))), n_real)
+    sizes = _split_even(n_real, n_layers)
+    first = [1]
+    for s in sizes:
+        first.append(first[-1] + s)
+    base_capacity = sum(min(2, first[li] - 1) * sizes[li] for li in range(1, n_layers))
+    n_earlier_last = first[-2] - 1
+    if count_root:
+        inter_target = n_edges - sizes[0]
+        min_inter = n_real - sizes[0]
+        if inter_target < min_inter:
+            raise InfeasibleGraphError(f"{n_edges} total edges cannot cover {n_real} kernels")
+    else:
+        inter_target, min_inter = n_edges, 0
+    overflow = (sizes[-1] * max(0, n_earlier_last - 2)) if n_layers > 1 else 0
+    if inter_target > base_capacity + overflow:
+        raise InfeasibleGraphError(f"{n_edges} edges infeasible for {n_real} two-input kernels")
+    if inter_target >= base_capacity:
+        mode, extra = 0, inter_target - base_capacity
+    else:
+        mode, extra = (2 if min_inter else 1), 0
+    # (the reference's second check, extra > unused sink pairs, graph.py:288,
+    # cannot fire past the first: with every slot used each last-layer kernel
+    # holds min(2, earlier) inputs, so the unused pairs are exactly the overflow)
+    n_cand = sizes[-1] * n_earlier_last if n_layers > 1 else 0
+    return {"n_real": n_real, "n_layers": n_layers, "first": first,
+            "base_capacity": base_capacity, "inter_target": inter_target, "extra": extra,
+            "mode": mode, "pop_cap": 2 * max(base_capacity, n_real, n_cand) + 2,
+            "edge_cap": inter_target + n_real}
+
+
+def generate_random_dag_batch(n_kernels: int, n_edges: int, kind: str, size: int, seeds,
+                              model=None, layers: Optional[int] = None,
+                              count_root: bool = False):
+    """generate_random_dag(n_kernels, n_edges, kind, size, seed) for every seed,
+    built on the device (csrc/rgen.cu: CPython's Random per graph, same draw
+    order) and weighted by ``model`` (default SyntheticCostModel, the
+    attach_weights of configs 1 and 5) on the device: a DagBatch, graph b
+    identical to attach_weights(generate_random_dag(..., seeds[b]), model)."""
+    import numpy as np
+    import torch
+    from . import _native
+    from .costs import SyntheticCostModel, device_weights
+    from .csr import DagBatch
+    model = model or SyntheticCostModel()
+    shape = random_dag_shape(n_kernels, n_edges, layers, count_root)
+    seeds = [int(x) for x in seeds]
+    if any(abs(x) >= 2 ** 63 for x in seeds):
+        raise ValueError("seeds must fit in 64 bits")
+    dev = _native.device()
+    sd = torch.tensor(seeds, dtype=torch.int64, device=dev)
+    n = shape["n_real"] + 1
+    m, out_ptr, out_dst, in_ptr, in_src, in_eid = _native.random_dag_batch(sd, shape, n)
+    b = len(seeds)
+    node_counts = np.full(b, n, dtype=np.int64)
+    # weights: the root zero, every kernel (kind, size); every edge one size^2 fp32 matrix
+    pair = torch.zeros(b * n, dtype=torch.int32, device=dev)
+    pair[::n] = 1
+    sizes = torch.full((b * n,), size, dtype=torch.int64, device=dev)
+    nbytes = torch.full((int(m.sum()),), size * size * 4, dtype=torch.int64, device=dev)
+    w_cpu, w_gpu, w_xfer, bad_node, bad_edge = device_weights(model, [(kind, size), None], pair,
+                                                             sizes, nbytes, device=dev)
+    if bad_node >= 0:
+        from .graph import GraphError
+        try:
+            model.kernel_time(kind, size, "CPU")
+            model.kernel_time(kind, size, "GPU")
+        except Exception as exc:
+            raise GraphError(f"no cost entry for kernel 1 ({kind}, {size}): {exc}") from exc
+    root = torch.zeros(b, dtype=torch.int32, device=dev)
+    return DagBatch.from_device(node_counts, m, root, out_ptr, out_dst, in_ptr, in_src, in_eid,
+                                w_cpu, w_gpu, w_xfer, nbytes)
+
+
+class RandomDagFactory:
+    """``seed -> attach_weights(generate_random_dag(n, m, kind, size, seed), model)``.
+
+    Called with a seed it builds the TaskGraph exactly as the reference does
+    (graph_factory of sim.compare); ``compare`` recognises it and generates
+    all iterations at once on the device instead (``batch``)."""
+
+    def __init__(self, n_kernels: int, n_edges: int, kind: str = "MA", size: int = 1024,
+                 model=None, layers: Optional[int] = None, count_root: bool = False):
+        self.n_kernels, self.n_edges, self.kind, self.size = n_kernels, n_edges, kind, size
+        self.model, self.layers, self.count_root = model, layers, count_root
+
+    def __call__(self, seed: int):
+        from .costs import SyntheticCostModel
+        from .graph import attach_weights
+        g = generate_random_dag(self.n_kernels, self.n_edges, self.kind, self.size, seed,
+                                self.layers, self.count_root)
+        return attach_weights(g, self.model or SyntheticCostModel())
+
+    def batch(self, seeds):
+        return generate_random_dag_batch(self.n_kernels, self.n_edges, self.kind, self.size,
+                                         seeds, self.model, self.layers, self.count_root)
+
+
 def cholesky_tasks(tiles: int) -> Tuple[List[Tuple[str, Tuple[int, ...]]], List[Tuple[int, int]]]:
     """Right-looking tiled Cholesky task list and last-writer dependencies.
 

@@ -239,25 +239,65 @@ def partition_heuristic_batch(graphs: Sequence[TaskGraph], targets: Sequence[Par
     short-circuit, otherwise 1 + restarts start orders refined by FM on the
     device (one CTA per graph x order), winner by (not feasible, cut, err, lex).
     """
-    from .csr import TwoWayBatch
     config = config or PartitionConfig()
-    source, tol = config.node_weight_source, config.imbalance_tolerance
-    out: List[Optional[Dict[int, str]]] = [None] * len(graphs)
-    work = []
-    for gi, (g, t) in enumerate(zip(graphs, targets)):
+    source = config.node_weight_source
+    hosts, ws = [], []
+    for g in graphs:
         ids = g.kernel_ids()
         if not ids:
             raise PartitionError("graph has no non-root kernels")
-        w = np.array([_node_weight(g.nodes[i], source) for i in ids], dtype=np.float64)
+        hosts.append(g.csr().host)
+        ws.append(np.array([_node_weight(g.nodes[i], source) for i in ids], dtype=np.float64))
+    rows = partition_rows_batch(hosts, ws, [t.r_cpu for t in targets], config)
+    return [_assignment_dict(g.csr(), r) for g, r in zip(graphs, rows)]
+
+
+def partition_rows_batch(hosts, ws, r_cpu, config: PartitionConfig) -> List[np.ndarray]:
+    """The device part of partition_heuristic_batch on HostDags: per graph
+    the winning assignment as an int8 row over its kernels (0 CPU, 1 GPU).
+    ws[b] = kernel weights (kernel position order), r_cpu[b] = target."""
+    from .csr import TwoWayBatch
+    tol = config.imbalance_tolerance
+    out: List[Optional[np.ndarray]] = [None] * len(hosts)
+    work = []
+    for gi, (h, w, r) in enumerate(zip(hosts, ws, r_cpu)):
+        if not len(w):
+            raise PartitionError("graph has no non-root kernels")
         if not np.any(w):
             raise PartitionError("zero total node weight; attach weights first")
-        if t.r_cpu == 0.0 or t.r_cpu == 1.0:
-            side = GPU if t.r_cpu == 0.0 else CPU
-            out[gi] = {i: side for i in ids}
+        if r == 0.0 or r == 1.0:
+            out[gi] = np.full(len(w), 1 if r == 0.0 else 0, dtype=np.int8)
         else:
-            work.append((gi, g, t, w))
+            work.append((gi, h, r, w))
     if not work:
         return out
+    R = config.restarts + 1
+    tb = TwoWayBatch([h for _, h, _, _ in work])
+    orders = []
+    for _, _, _, w in work:
+        o = np.empty((R, len(w)), dtype=np.int32)
+        o[0] = np.argsort(-w, kind="stable")
+        o[1:] = _shuffles(len(w), config)
+        orders.append(o.reshape(-1))
+    dev = tb.xadj.device
+    weights = torch.from_numpy(np.concatenate([w for *_, w in work])).to(dev)
+    rt = torch.tensor([r for _, _, r, _ in work], dtype=torch.float64, device=dev)
+    ordt = torch.from_numpy(np.concatenate(orders)).to(dev)
+    assign, cut, err, status = _native.fm2_batch(tb, weights, rt, tol, ordt, R)
+    if bool((status != 0).any()):
+        raise PartitionError("zero total node weight; attach weights first")
+    assign, cut, err = assign.cpu().numpy(), cut.cpu().numpy(), err.cpu().numpy()
+    for b, (gi, _, _, w) in enumerate(work):
+        n = len(w)
+        rows = assign[R * tb.node_off_h[b]: R * tb.node_off_h[b] + R * n].reshape(R, n)
+        best = None
+        for k in range(R):
+            key = (not bool(err[b, k] <= tol), float(cut[b, k]), float(err[b, k]),
+                   tuple(rows[k].tolist()))
+            if best is None or key < best[0]:
+                best = (key, k)
+        out[gi] = rows[best[1]].astype(np.int8)
+    return out
     R = config.restarts + 1
     tb = TwoWayBatch([g.csr().host for _, g, _, _ in work])
     orders = []

@@ -326,6 +326,9 @@ def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGrap
     """
     if iterations < 1:
         raise SimulationError("iterations must be >= 1")
+    if policy_builder is None and hasattr(graph_factory, "batch"):
+        return _compare_generated(policy_names, graph_factory, machine or MachineModel(),
+                                  iterations, seed)
     batched_gp = policy_builder is None
     if policy_builder is None:
         from .policies import build_policy
@@ -345,6 +348,39 @@ def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGrap
         makespans = [float(x) for x in res.makespan]
         transfers = [float(x) for x in res.transfer_count]
         t_bytes = [float(x) for x in res.transfer_bytes]
+        rows.append(CompareRow(
+            policy=name,
+            mean_makespan=statistics.fmean(makespans),
+            sd_makespan=statistics.stdev(makespans) if len(makespans) > 1 else 0.0,
+            mean_transfers=statistics.fmean(transfers),
+            sd_transfers=statistics.stdev(transfers) if len(transfers) > 1 else 0.0,
+            mean_transfer_bytes=statistics.fmean(t_bytes),
+        ))
+    return rows
+
+
+def _compare_generated(policy_names, factory, machine, iterations, seed) -> List[CompareRow]:
+    """compare() over a generator factory (gen.RandomDagFactory): every
+    iteration's graph built on the device at once (csrc/rgen.cu, identical to
+    the factory's own graphs), gp pins from one batched partition launch, one
+    DES launch per policy. Same rows as the object path."""
+    from .policies import DMDA_ID, EAGER_ID, GP_ID, POLICY_NAMES, gp_pins_batch
+    ids = {"eager": EAGER_ID, "dmda": DMDA_ID, "gp": GP_ID}
+    for name in policy_names:
+        if name not in ids:  # build_policy's error (policies.py:111-120)
+            raise ValueError(f"unknown policy {name!r}; expected one of {POLICY_NAMES}")
+    batch = factory.batch([seed + i for i in range(iterations)])
+    rows: List[CompareRow] = []
+    for name in policy_names:
+        pin = gp_pins_batch(batch) if name == "gp" else None
+        out = _native.simulate_batch(batch, ids[name], pin, machine.cpu_workers,
+                                     machine.gpu_workers, events=False)
+        h = {k: v.cpu().numpy() for k, v in out.items()}
+        if (h["status"] != 0).any():
+            raise AssertionError("simulation deadlocked on a valid DAG (bug)")
+        makespans = [float(x) for x in h["makespan"]]
+        transfers = [float(x) for x in h["transfer_count"]]
+        t_bytes = [float(x) for x in h["transfer_bytes"]]
         rows.append(CompareRow(
             policy=name,
             mean_makespan=statistics.fmean(makespans),
