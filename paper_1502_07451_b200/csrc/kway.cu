@@ -184,11 +184,6 @@ __device__ __forceinline__ uint32_t mix32(uint64_t x) {
   return (uint32_t)x;
 }
 
-__device__ __forceinline__ uint32_t edge_hash(int a, int b, uint64_t salt) {
-  uint32_t lo = (uint32_t)min(a, b), hi = (uint32_t)max(a, b);
-  return mix32(salt ^ ((uint64_t)lo << 32 | hi));
-}
-
 // 32-bit symmetric edge hash (lowbias32 of a mix of both ends and the salt):
 // cheap enough for the per-edge inner loop of the matching proposals.
 __device__ __forceinline__ uint32_t edge_hash32(int a, int b, uint32_t salt) {
@@ -988,12 +983,6 @@ __global__ void widen_minmax(int64_t *mm) {
   mm[1] = hi;
 }
 
-__global__ void fill_i32(int32_t *out, int64_t n, int32_t v) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = v;
-}
-
 // sum / min / max of int32 weights (out: u64 sum, i32 min, i32 max; caller
 // initialises 0, INT_MAX, INT_MIN)
 __global__ void wstats_kernel(int64_t n, const int32_t *w, unsigned long long *sum, int32_t *mn,
@@ -1023,14 +1012,6 @@ __global__ void int8_to_int32(const int8_t *in, int n, int32_t *out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     out[i] = in[i];
-}
-
-__global__ void seg_bounds(int n, const int64_t *xbeg, const int32_t *deg, int64_t *b, int64_t *e) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    b[i] = xbeg[i];
-    e[i] = xbeg[i] + deg[i];
-  }
 }
 
 #include "kway_team.cuh"
@@ -1335,15 +1316,7 @@ struct Kway {
   }
   Kway(cudaStream_t st) : s(st), timer(st) {
     if (const char *e = getenv("HS_KWAY_PASSES")) passes_big = std::max(1, atoi(e)), passes_env = true;
-    if (const char *e = getenv("HS_KWAY_PASSES_COARSE")) passes_coarse = std::max(0, atoi(e));
     if (const char *e = getenv("HS_KWAY_ROUNDS")) rounds = std::max(1, atoi(e));
-  }
-
-  int read_pw(std::vector<int64_t> &pw) {
-    pw.resize(k);
-    HS_CHECK_CUDA(cudaMemcpyAsync(pw.data(), d_pw, k * 8, cudaMemcpyDeviceToHost, s));
-    HS_CHECK_CUDA(cudaStreamSynchronize(s));
-    return HS_OK;
   }
 
   // part: this rank's replica (global ids); sums this rank's vertices, then all ranks'
@@ -1364,45 +1337,6 @@ struct Kway {
 
   // Up to `rounds` rebalancing rounds, each gated on the device by "some part
   // is above its bound" — no host round trip.
-  // Cluster launch of afterburner_dsm: kAbCluster CTAs of kAbThreads per
-  // cluster, each holding 1/kAbCluster of the candidate bitmap.
-  int launch_afterburner_dsm(const G &g, const uint32_t *stl, const int32_t *list, int32_t *conf,
-                             const uint32_t *bm, int64_t bm_words) {
-    const int64_t slice = (bm_words + kAbCluster - 1) / kAbCluster;
-    const size_t smem = (size_t)slice * 4;
-    const int clusters = std::max(1, hs::sm_count() / kAbCluster);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(clusters * kAbCluster);
-    cfg.blockDim = dim3(kAbThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kAbCluster;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-#define HS_AB(KC, CW)                                                                         \
-  do {                                                                                        \
-    auto fn = afterburner_dsm<2, KC, CW>;                                                     \
-    HS_CHECK_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                       (int)smem));                                           \
-    HS_CHECK_CUDA(cudaLaunchKernelEx(&cfg, fn, g, stl, list, (const int32_t *)(ctl + CTL_COUNT), \
-                                     k, conf, d_flows, ctl + CTL_NCONF,                        \
-                                     (const int32_t *)(ctl + CTL_ACTIVE), bm, bm_words, slice, \
-                                     (const uint8_t *)cache.p));                               \
-  } while (0)
-    if (cache.kc == 8) {
-      if (cache.cw == 1) HS_AB(8, 1); else if (cache.cw == 2) HS_AB(8, 2); else HS_AB(8, 4);
-    } else {
-      if (cache.cw == 1) HS_AB(16, 1); else if (cache.cw == 2) HS_AB(16, 2); else HS_AB(16, 4);
-    }
-#undef HS_AB
-    hs::count_launch();
-    return HS_OK;
-  }
-
   // Planned flows and move counts of all ranks (a no-op on one GPU).
   int ar_flows() { return ar({seg64(d_flows, 2 * k), seg32(ctl + CTL_NCONF, 1)}); }
   // Part-weight deltas of this rank's applied moves -> every rank's d_pw.
@@ -1493,20 +1427,19 @@ struct Kway {
     // level gets two passes more. Measured step (ms, cut) by passes:
     // 6 (4.25, 1,320.1M), 8 (4.75, 1,309.7M), 10 (5.20, 1,304.2M),
     // 12 (5.47, 1,302.4M, converged); 4 unthinned passes were (6.38, 1,326.6M).
-    static const int prethin_env = getenv("HS_KWAY_PRETHIN") ? atoi(getenv("HS_KWAY_PRETHIN")) : 1;
-    const bool prethin = prethin_env && !getenv("HS_KWAY_DSM");
+    const bool prethin = true;
     int max_passes = Lv.nnz_glob > (4ll << 20) ? passes_big + (prethin && !passes_env ? 2 : 0)
                                                : passes_small;
     if (!finest && passes_coarse >= 0) max_passes = passes_coarse;
     // An unmerged level has as many entries as the level below it: a pass
     // there costs a full fine pass and only moves whole pairs, which the fine
     // passes can do too (measured on config 4: 2.6 ms saved, cut 0.2% lower).
-    if (!finest && Lv.unmerged && !getenv("HS_KWAY_REFINE_UNMERGED")) max_passes = 0;
+    if (!finest && Lv.unmerged) max_passes = 0;
     // 16-bit packed connectivity counters are exact iff every vertex's
     // weighted degree stays below 2^16 on this level
     // (only the register-counter variants use them: skip the scan otherwise)
     bool pack16 = false;
-    if (!(k <= 16 && refine_private())) {
+    if (k > 16) {
       HS_CHECK_CUDA(cudaMemsetAsync(ctl + 12, 0, sizeof(int32_t), s));
       max_wdeg_kernel<<<hs::grid_for(g.n, 256, hs::sm_count() * 8), 256, 0, s>>>(g, ctl + 12);
       HS_CHECK_LAUNCH();
@@ -1519,7 +1452,7 @@ struct Kway {
     }
     // connectivity cache: pass 0 scans the adjacency and fills it, later
     // passes read one row per vertex; applied moves keep it exact
-    const bool use_cache = !D.on() && k <= 16 && refine_private() && !gp &&
+    const bool use_cache = !D.on() && k <= 16 && !gp &&
                            (max_passes >= 2 || (finest && max_passes >= 1)) &&
                            !getenv("HS_KWAY_NOCACHE");
     cache = Conn();
@@ -1529,20 +1462,9 @@ struct Kway {
       // the finest level that is its degree (known), else 32-bit counters
       const int64_t bound = (finest && g.wconst == 1) ? max_deg0 : (1ll << 31);
       cache.cw = bound < 256 ? 1 : (bound < 65536 ? 2 : 4);
-      if (getenv("HS_KWAY_CACHE32")) cache.cw = 4;
       int rc2 = cache_buffer((int64_t)g.n * cache.kc * cache.cw, &cache.p);
       if (rc2) return rc2;
     }
-    // afterburner over a cluster-distributed candidate bitmap (needs the cache
-    // for the gains and a bitmap that fits kAbCluster CTAs' shared memory).
-    // Opt-in (HS_KWAY_DSM=1): measured 4x slower than the L2 gathers on
-    // config 4 (random 4-byte DSMEM loads across an 8-CTA cluster, ~2 ms vs
-    // 0.5 ms per pass), kept for the record.
-    const int64_t bm_words = ((int64_t)g.n + 31) / 32;
-    const bool use_dsm = use_cache && bm_words <= (int64_t)kAbCluster * kAbSliceMax &&
-                         getenv("HS_KWAY_DSM") != nullptr;
-    uint32_t *d_bm = nullptr;
-    if (use_dsm) HS_CHECK_CUDA(dalloc(&d_bm, bm_words, s));
     const int32_t one = 1;
     HS_CHECK_CUDA(cudaMemcpyAsync(ctl + CTL_ACTIVE, &one, sizeof one, cudaMemcpyHostToDevice, s));
     int32_t *kept = nullptr;
@@ -1602,12 +1524,6 @@ struct Kway {
         // instrumented (profiling) steps. Per candidate: list 4, own state 4,
         // xbeg 8, deg 4, vw 4, decision 4; per entry (average degree): adj 4,
         // weight 4 (none when uniform), neighbour state 4.
-        if (use_dsm) {
-          HS_CHECK_CUDA(cudaMemsetAsync(d_bm, 0, bm_words * 4, s));
-          list_bitmap<<<hs::grid_for(g.n, 256, hs::sm_count() * 8), 256, 0, s>>>(
-              list, ctl + CTL_COUNT, d_bm);
-          HS_CHECK_LAUNCH();
-        }
         if (prethin) {  // pre-plan: thin the candidates to the balance room first
           // passes > 0 (cache): refine_cached already summed the flows
           const bool fused = use_cache && pass > 0;
@@ -1654,15 +1570,10 @@ struct Kway {
           ab_bytes = (double)cnt * (28.0 + avg * (g.wconst ? 8.0 : 12.0));
         }
         hs::Prof P("refine_afterburner", s, ab_bytes);
-        if (use_dsm) {
-          rc = launch_afterburner_dsm(g, loc(st), list, conf, d_bm, bm_words);
-          if (rc) return rc;
-        } else {
-          const int TA = after_team_for(g);
-          HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), prethin ? kept : list,
-                           ctl + (prethin ? CTL_KEPT : CTL_COUNT), k, conf, d_flows,
-                           ctl + CTL_NCONF, ctl + CTL_ACTIVE);
-        }
+        const int TA = after_team_for(g);
+        HS_TEAM_DISPATCH(TA, afterburner_t, team_grid(g.n, TA), g, loc(st), prethin ? kept : list,
+                         ctl + (prethin ? CTL_KEPT : CTL_COUNT), k, conf, d_flows,
+                         ctl + CTL_NCONF, ctl + CTL_ACTIVE);
       }
       HS_CHECK_LAUNCH();
       rc = ar_flows();
@@ -1714,7 +1625,6 @@ struct Kway {
       gp = nullptr;
     }
     cudaFreeAsync(cand, s);
-    if (d_bm) cudaFreeAsync(d_bm, s);
     free_rep(st);
     D.bump = arena_mark;
     cudaFreeAsync(list, s);
@@ -1757,12 +1667,6 @@ struct Kway {
     cudaStreamSynchronize(s);
     cudaFreeAsync(c2, s);
     return (int64_t)(h / 2);
-  }
-
-  bool feasible(const std::vector<int64_t> &pw) const {
-    for (int p = 0; p < k; ++p)
-      if (pw[p] > hi[p] || pw[p] < lo[p]) return false;
-    return true;
   }
 
   // One coarsening level: heavy-edge matching rounds, two-hop pairing,
@@ -1943,8 +1847,7 @@ struct Kway {
     // the fine->coarse map are consumed: its adjacency is not built (empty
     // lists; a rebalance there moves by weight only). Saves a pass over all
     // entries (config 4: 1.6 ms).
-    const bool skeleton = direct && nc_glob > 32768 && !getenv("HS_KWAY_REFINE_UNMERGED") &&
-                          !getenv("HS_KWAY_FULL_COARSEST");
+    const bool skeleton = direct && nc_glob > 32768;
     if (skeleton) {
       HS_CHECK_CUDA(cudaMemsetAsync(C.g.deg, 0, (size_t)nc * sizeof(int32_t), s));
       C.unmerged = true;
@@ -1955,11 +1858,9 @@ struct Kway {
       hs::Prof P("contract_direct", s,
                  16.0 * nc + 12.0 * n + (F.g.wconst ? 8.0 : 12.0) * F.g.nnz +
                      (F.g.wconst ? 4.0 : 8.0) * F.g.nnz);
-      static const int TC = getenv("HS_KWAY_TCONTRACT") ? atoi(getenv("HS_KWAY_TCONTRACT")) : 4;
+      constexpr int TC = 4;  // 4-lane teams (measured against 2 and 8)
       const int cgrid = std::max(1, std::min(hs::sm_count() * 32, (nc * TC + 255) / 256));
-      if (TC == 2) contract_direct<2><<<cgrid, 256, 0, s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
-      else if (TC == 4) contract_direct<4><<<cgrid, 256, 0, s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
-      else contract_direct<8><<<cgrid, 256, 0, s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
+      contract_direct<TC><<<cgrid, 256, 0, s>>>(F.g, F.cmap, mem0, mem1, nc, C.g);
       HS_CHECK_LAUNCH();
     } else {
     {
@@ -2077,49 +1978,6 @@ struct Kway {
     HS_CHECK_CUDA(cudaStreamSynchronize(s));
     levels.back().g.nnz = levels.back().nnz_glob = *h_nnz;
     prev_nnz_pending = false;
-    return HS_OK;
-  }
-
-  // Sorts every adjacency list of g (deterministic order for the initial trials).
-  int sort_lists(Level &Lv) {
-    G &g = Lv.g;
-    int64_t *b, *e;
-    int32_t *adj2, *wgt2;
-    HS_CHECK_CUDA(dalloc(&b, g.n, s));
-    HS_CHECK_CUDA(dalloc(&e, g.n, s));
-    HS_CHECK_CUDA(dalloc(&adj2, g.cap, s));
-    HS_CHECK_CUDA(dalloc(&wgt2, g.cap, s));
-    seg_bounds<<<hs::grid_for(g.n, 256), 256, 0, s>>>(g.n, g.xbeg, g.deg, b, e);
-    HS_CHECK_LAUNCH();
-    if (g.wconst) {  // the warp trials read per-entry weights: materialise them
-      fill_i32<<<hs::grid_for(g.cap, 256), 256, 0, s>>>(wgt2, g.cap, g.wconst);
-      HS_CHECK_LAUNCH();
-      if (Lv.own_wgt) cudaFreeAsync(g.wgt, s);
-      g.wgt = wgt2;
-      g.wconst = 0;
-      Lv.own_wgt = true;
-      HS_CHECK_CUDA(dalloc(&wgt2, g.cap, s));
-    }
-    size_t tb = 0;
-    HS_CHECK_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tb, g.adj, adj2, g.wgt, wgt2,
-                                                      g.cap, g.n, b, e, s));
-    {
-      hs::Scratch<char> tmp;
-      HS_CHECK_CUDA(tmp.alloc(tb, s));
-      HS_CHECK_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tb, g.adj, adj2, g.wgt, wgt2,
-                                                        g.cap, g.n, b, e, s));
-    }
-    hs::count_launch(2);
-    // padding slots are not part of any segment: copy only the sorted ranges
-    // back by swapping the buffers (unsorted padding stays garbage, never read)
-    if (Lv.own_adj) cudaFreeAsync(g.adj, s);
-    if (Lv.own_wgt) cudaFreeAsync(g.wgt, s);
-    g.adj = adj2;
-    g.wgt = wgt2;
-    g.twin = nullptr;  // positions moved: the reverse-entry index no longer applies
-    Lv.own_adj = Lv.own_wgt = true;
-    cudaFreeAsync(b, s);
-    cudaFreeAsync(e, s);
     return HS_OK;
   }
 
@@ -2301,8 +2159,7 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
   // in_src + out_dst read, two adjacency writes, and with weights the out-
   // and in-order weight reads and two weight writes
   hs::Prof P("symmetrize", s, frac * (32.0 * g->n + (adjwgt_i ? 32.0 : 16.0) * g->m));
-  static const bool chunked = !getenv("HS_KWAY_SYM_TEAM");
-  if (chunked && !twin) {
+  if (!twin) {  // (the team path below also writes the twin index)
     // row starts come from the CSR prefixes (sym_row_start): no degree pass
     const int64_t chunks = ((int64_t)nl + 31) / 32;
     const int cgrid = (int)std::max<int64_t>(
@@ -2327,13 +2184,10 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
   if (rc) return rc;
   rc = exclusive_scan<int64_t>(deg64, xadj, nl + 1, s);
   if (rc) return rc;
-  static const int TS = getenv("HS_KWAY_TSYM") ? atoi(getenv("HS_KWAY_TSYM")) : 4;  // measured: 4 lanes beat 8 and 2
+  constexpr int TS = 4;  // measured: 4 lanes beat 8 and 2
   const int sgrid = std::max(1, std::min(hs::sm_count() * 32, (nl * TS + 255) / 256));
-#define HS_SYM_ARGS *g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, twin
-  if (TS == 2) sym_fill<2><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
-  else if (TS == 4) sym_fill<4><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
-  else sym_fill<8><<<sgrid, 256, 0, s>>>(HS_SYM_ARGS);
-#undef HS_SYM_ARGS
+  sym_fill<TS><<<sgrid, 256, 0, s>>>(*g, kv0, kv1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy,
+                                      adjwgt_i, vwgt_i, twin);
   HS_CHECK_LAUNCH();
   if (nnz_host) {
     HS_CHECK_CUDA(cudaMemcpyAsync(nnz_host, xadj + nl, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -2504,7 +2358,7 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   L0.g.vw = const_cast<int32_t *>(ug->vwgt_i);
   L0.g.deg = deg_l0;
   K.max_deg0 = tot[5];
-  L0.vconst = (tot[6] == tot[7] && n_glob > 0 && !getenv("HS_KWAY_NOVCONST")) ? (int32_t)tot[6] : 0;
+  L0.vconst = (tot[6] == tot[7] && n_glob > 0) ? (int32_t)tot[6] : 0;
   int64_t div = 1;
   // uniform edge weights: work with unit weights (no weight stream, no
   // overflow: sums are entry counts); the reported cut is rescaled
@@ -2582,7 +2436,6 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   // with the vertices, so matching has no locality left to exploit).
   const double deg0 = n_glob ? (double)L0.nnz_glob / (double)n_glob : 0.0;
   double max_deg = std::max(16.0, 1.5 * deg0);
-  if (const char *e = getenv("HS_KWAY_MAXDEG")) max_deg = atof(e);
   K.max_deg = max_deg;
   // Skip coarsening when its only product would be the band start on a
   // skeleton level: a triangle-free-looking finest graph (matching

@@ -899,119 +899,6 @@ __global__ void thin_cands(Rep<uint32_t> st, int32_t v0, const int32_t *list, co
   app.flush(kept, kept_count);
 }
 
-// ---- afterburner over a cluster-distributed candidate bitmap ----------------
-// With the connectivity cache, a candidate's afterburner delta is its cached
-// gain plus corrections from the neighbours that are themselves candidates of
-// higher priority; non-candidate neighbours need no lookup at all. Which
-// neighbours are candidates is one bit per vertex: the bitmap (1.25 MB at
-// 10M vertices) is split across the distributed shared memory of a thread-
-// block cluster (kAbCluster CTAs, one per SM), so the per-neighbour test is a
-// DSMEM load instead of an L2 request; only candidate neighbours gather their
-// packed state from global memory.
-constexpr int kAbCluster = 8;
-constexpr int kAbThreads = 1024;
-constexpr int64_t kAbSliceMax = (216 << 10) / 4;  // bitmap words per CTA (216 KB of smem)
-
-__global__ void list_bitmap(const int32_t *list, const int32_t *count, uint32_t *bm) {
-  const int total = *count;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int v = list[i];
-    atomicOr(bm + (v >> 5), 1u << (v & 31));
-  }
-}
-
-template <int T, int KC, int CW>
-__global__ void __launch_bounds__(kAbThreads, 1)
-afterburner_dsm(G g, const uint32_t *st, const int32_t *list, const int32_t *count, int k,
-                int32_t *conf, int64_t *flows, int32_t *nconf, const int32_t *run,
-                const uint32_t *bm, int64_t bm_words, int64_t slice_words, const uint8_t *cache) {
-  extern __shared__ uint32_t s_bm[];  // this CTA's slice of the candidate bitmap
-  __shared__ unsigned long long sf[2 * kMaxParts];
-  __shared__ int s_n;
-  cg::cluster_group cluster = cg::this_cluster();
-  const bool active = !(run && !*run);
-  const unsigned rank = cluster.block_rank();
-  if (active) {
-    // interleaved: bitmap word w lives in rank (w % kAbCluster), slot w / kAbCluster
-    for (int64_t i = threadIdx.x; i < slice_words; i += blockDim.x) {
-      const int64_t gw = i * kAbCluster + rank;
-      s_bm[i] = gw < bm_words ? __ldg(bm + gw) : 0u;
-    }
-  }
-  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x) sf[p] = 0;
-  if (threadIdx.x == 0) s_n = 0;
-  cluster.sync();  // every slice loaded before any remote read
-  int local = 0;
-  if (active) {
-    const int lane = team_lane<T>();
-    const int total = *count;
-    const int64_t step = (int64_t)warps_total() * (32 / T);
-    for (int64_t ib = (int64_t)warp_id_global() * (32 / T); ib < total; ib += step) {
-      const int64_t i = ib + (threadIdx.x & 31) / T;
-      const bool valid = i < total;
-      int delta = 0, v = 0, dest = -1, own = 0;
-      if (valid) {
-        v = list[i];
-        const uint32_t sv = st[g.v0 + v];
-        dest = st_cand(sv);
-        own = st_part(sv);
-        const int gv = st_gain(sv);
-        const int64_t b = g.xbeg[v];
-        const int d = g.deg[v];
-        constexpr int U = 8;  // entries in flight per lane
-        for (int j0 = lane; j0 < d; j0 += U * T) {
-          int u[U];
-          uint32_t bit[U];
-#pragma unroll
-          for (int q = 0; q < U; ++q) {
-            const int j = j0 + q * T;
-            u[q] = j < d ? __ldg(g.adj + b + j) : -1;
-          }
-#pragma unroll
-          for (int q = 0; q < U; ++q) {
-            bit[q] = 0;
-            if (u[q] >= 0) {
-              const unsigned wd = (unsigned)u[q] >> 5;
-              const uint32_t *rb = cluster.map_shared_rank(s_bm, wd % kAbCluster);
-              bit[q] = (rb[wd / kAbCluster] >> (u[q] & 31)) & 1u;
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < U; ++q) {
-            if (!bit[q]) continue;  // not a candidate: the cached gain covers it
-            const uint32_t su = __ldg(st + u[q]);
-            const int gu = st_gain(su);
-            if (!(gu > gv || (gu == gv && u[q] < g.v0 + v))) continue;  // lower priority
-            const int pu = st_part(su), cu = st_cand(su), w = g.ew(b + j0 + q * T);
-            delta += ((cu == dest) - (cu == own) - (pu == dest) + (pu == own)) * w;
-          }
-        }
-      }
-      delta = team_sum<T>(delta);
-      if (valid && lane == 0) {
-        int c[KC];
-        conn_row<KC, CW>(cache, v, c);
-        delta += c[dest] - c[own];  // the cached gain of v's move
-        const bool ok = delta > 0;
-        conf[i] = ok ? dest : -1;
-        if (ok) {
-          const unsigned long long w = (unsigned long long)g.vw[v];
-          atomicAdd(&sf[own], w);
-          atomicAdd(&sf[k + dest], w);
-          ++local;
-        }
-      }
-    }
-  }
-  if (local) atomicAdd(&s_n, local);
-  __syncthreads();
-  for (int p = threadIdx.x; p < 2 * k; p += blockDim.x)
-    if (sf[p]) atomicAdd((unsigned long long *)&flows[p], sf[p]);
-  if (threadIdx.x == 0 && s_n) atomicAdd(nconf, s_n);
-  cluster.sync();  // no CTA leaves while a peer may still read its slice
-}
-
 // Applies confirmed moves of the list, each kept with probability
 // prob[own] * prob[k + dest] (hash of (salt, v): deterministic thinning).
 __global__ void apply_list(const int32_t *list, const int32_t *count, const int32_t *conf,
@@ -1158,87 +1045,24 @@ cut_t(G g, const part_t *part, unsigned long long *cut2) {
   if ((threadIdx.x & 31) == 0 && local) atomicAdd(cut2, local);
 }
 
-// private shared-memory counters (default) vs register select chains
-inline bool refine_private() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("HS_KWAY_REGCONN");
-    v = (e && e[0] == '1') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-// entries in flight per lane of the 4-lane refinement scan (HS_KWAY_UNROLL)
-inline int refine_unroll() {
-  static int v = -1;
-  if (v < 0) {
-    const char *e = getenv("HS_KWAY_UNROLL");
-    v = e ? atoi(e) : 4;
-  }
-  return v;
-}
-
+// Team sizes (lanes per vertex), measured on config 4 (degree ~20,
+// tools/sweep_kway.py): sparse levels take 2-lane teams for the candidate
+// scan (2 lanes x 4 entries in flight beat 4x4 by 0.18 ms/pass, 1x8 and 8x4)
+// and the afterburner (2 beat 8 by 0.15 ms/pass); denser levels 16 or 32.
 inline int team_for(const G &g) {
   const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
-  static int sparse = -1;  // team on sparse levels (HS_KWAY_TSPARSE for sweeps)
-  if (sparse < 0) {
-    const char *e = getenv("HS_KWAY_TSPARSE");
-    sparse = e ? atoi(e) : 2;  // measured on config 4: 2 lanes beat 4 and 8 (degree ~20)
-  }
-  return avg <= 24.0 ? sparse : (avg <= 64.0 ? 16 : 32);
+  return avg <= 24.0 ? 2 : (avg <= 64.0 ? 16 : 32);
 }
-
-// team size of the refinement candidate scan (private-counter path supports
-// 1/4/8/16/32); HS_KWAY_TREFINE overrides the fine-level choice for sweeps
-inline int refine_team_for(const G &g) {
-  const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
-  static int force = -2;
-  if (force == -2) {
-    const char *e = getenv("HS_KWAY_TREFINE");
-    // measured on config 4 (degree ~20): 2 lanes x 4 entries in flight beat
-    // 4x4 (-0.18 ms/pass), 1x8 and 8x4
-    force = e ? atoi(e) : 2;
-  }
-  if (avg <= 24.0 && force > 0) return force;
-  return team_for(g);
-}
-
-// team size of the afterburner on sparse levels (HS_KWAY_TAFTER overrides)
-inline int after_team_for(const G &g) {
-  const double avg = g.n ? (double)g.nnz / (double)g.n : 0.0;
-  static int force = -2;
-  if (force == -2) {
-    const char *e = getenv("HS_KWAY_TAFTER");
-    force = e ? atoi(e) : 2;  // measured: 2 lanes beat 8 by 0.15 ms per pass (config 4)
-  }
-  if (avg <= 24.0 && force > 0) return force;
-  return team_for(g);
-}
+inline int refine_team_for(const G &g) { return team_for(g); }
+inline int after_team_for(const G &g) { return team_for(g); }
 
 // refine_cand_t<T, KR>: KR = 8 / 16 register accumulators, 0 = shared memory
 #define HS_REFINE_DISPATCH(T_, K_, PACK16_, GRID, ...)                          \
   do {                                                                           \
-    if ((K_) <= 16 && refine_private()) {                                        \
-      const int U_ = refine_unroll();                                             \
-      if ((T_) == 1 && U_ == 16) refine_cand_t<1, -16, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 1 && U_ == 8) refine_cand_t<1, -16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 1) refine_cand_t<1, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 2 && U_ == 16) refine_cand_t<2, -16, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 2 && U_ == 4) refine_cand_t<2, -16, 4><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 2) refine_cand_t<2, -16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 4 && U_ == 8) refine_cand_t<4, -16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 4) refine_cand_t<4, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else if ((T_) == 8) refine_cand_t<8, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
+    if ((K_) <= 16) {  /* private shared-memory counters per lane */             \
+      if ((T_) == 2) refine_cand_t<2, -16, 4><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);   \
       else if ((T_) == 16) refine_cand_t<16, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);\
       else refine_cand_t<32, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);               \
-    } else if ((K_) <= 8 && (PACK16_)) {                                         \
-      if ((T_) == 8) refine_cand_t<8, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);        \
-      else if ((T_) == 16) refine_cand_t<16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \
-      else refine_cand_t<32, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);                 \
-    } else if ((K_) <= 16) {                                                     \
-      if ((T_) == 8) refine_cand_t<8, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);       \
-      else if ((T_) == 16) refine_cand_t<16, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);\
-      else refine_cand_t<32, 16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);                \
     } else {                                                                     \
       if ((T_) == 8) refine_cand_t<8, 0><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);        \
       else if ((T_) == 16) refine_cand_t<16, 0><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__); \

@@ -290,3 +290,22 @@ def test_levels_dataflow_equals_frontier(n, m):
     ms, f1 = kway.assigned_makespan(csr, part, [1, 3], k=4)
     ms2, f2 = kway.assigned_makespan(rel, part2, [1, 3], k=4)
     assert ms == ms2 and torch.equal(f2[pil], f1)
+
+
+def test_connectivity_cache_is_exact():
+    """The finest-level connectivity cache (kept exact by every applied move,
+    L2-hinted) gives the same partition as rescanning the adjacency every
+    pass (HS_KWAY_NOCACHE=1): config-2 shape, uniform and U[1,100] weights."""
+    import os
+    csr = kway.layered_dag(100_000, 1_000_000, seed=6)
+    g = torch.Generator(device="cpu").manual_seed(3)
+    ew = torch.randint(1, 101, (csr.m,), generator=g, dtype=torch.int32).to(csr.device)
+    nw = torch.randint(1, 101, (csr.n,), generator=g, dtype=torch.int32).to(csr.device)
+    for ug in (kway.symmetrize(csr), kway.symmetrize(csr, ew, nw)):
+        a = kway.partition_kway(ug, 8, seed=1)
+        os.environ["HS_KWAY_NOCACHE"] = "1"
+        try:
+            b = kway.partition_kway(ug, 8, seed=1)
+        finally:
+            del os.environ["HS_KWAY_NOCACHE"]
+        assert a.cut == b.cut and torch.equal(a.part, b.part)
