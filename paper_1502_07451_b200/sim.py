@@ -319,10 +319,13 @@ def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGrap
             ) -> List[CompareRow]:
     """Mean/sd of makespan and transfers per policy over iterations (sim.py:269-306).
 
-    Iteration i simulates graph_factory(seed + i). All iterations of a policy
-    run as one device batch; the factory is called once per iteration and
-    its graph shared by every policy (the reference calls it once per
-    (policy, iteration); identical for deterministic factories).
+    As the reference: for every policy, iteration i calls graph_factory(seed
+    + i), builds the policy on that graph and simulates it; the calls happen
+    in the reference's order (policy-major), so stateful factories and
+    builders see the same sequence. The simulations of a policy then run as
+    one device batch (and the default gp builds as one batched partition).
+    A gen.RandomDagFactory is generated on the device instead (identical
+    graphs, see _compare_generated).
     """
     if iterations < 1:
         raise SimulationError("iterations must be >= 1")
@@ -334,16 +337,19 @@ def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGrap
         from .policies import build_policy
         policy_builder = lambda name, g: build_policy(name, g)  # noqa: E731
     machine = machine or MachineModel()
-    graphs = [graph_factory(seed + i) for i in range(iterations)]
-    for g in graphs:
-        _check_graph(g)
     rows: List[CompareRow] = []
     for name in policy_names:
-        if name == "gp" and batched_gp:  # all gp decisions in one device launch
+        graphs, policies = [], []
+        gp_batch = name == "gp" and batched_gp
+        for i in range(iterations):
+            g = graph_factory(seed + i)
+            if not gp_batch:
+                policies.append(policy_builder(name, g))
+            _check_graph(g)  # simulate's validation (sim.py:72-78)
+            graphs.append(g)
+        if gp_batch:  # all gp decisions in one device launch
             from .policies import gp_build_batch
             policies = gp_build_batch(graphs)
-        else:
-            policies = [policy_builder(name, g) for g in graphs]
         res = simulate_batch(graphs, policies, machine, validate_graphs=False)
         makespans = [float(x) for x in res.makespan]
         transfers = [float(x) for x in res.transfer_count]
