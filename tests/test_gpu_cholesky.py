@@ -39,3 +39,19 @@ def test_not_spd_raises():
     A = -torch.eye(1024, dtype=torch.float64, device="cuda")
     with pytest.raises(ValueError):
         TiledCholesky(1024).factor(A)
+
+
+def test_config3_factor_n32768():
+    """Config 3 itself (n = 32768, 64 x 64 tiles, 45,760 tasks): the leading
+    4096 x 4096 block of L equals LAPACK's factor of the leading principal
+    submatrix (a Cholesky factor's leading block is the factor of the leading
+    block), and 64 sampled columns of L L^T reproduce A."""
+    n = 32768
+    A = spd_matrix(n, seed=7)
+    L = TiledCholesky(n).factor(A)
+    ref = np.linalg.cholesky(A[:4096, :4096].cpu().numpy())
+    err = np.abs(L[:4096, :4096].cpu().numpy() - ref).max() / np.abs(ref).max()
+    assert err <= 1e-10, err
+    cols = torch.randint(0, n, (64,), generator=torch.Generator().manual_seed(1)).to(A.device)
+    R = (L @ L[cols, :].T - A[:, cols]).abs().max().item() / A.abs().max().item()
+    assert R <= 1e-12, R
