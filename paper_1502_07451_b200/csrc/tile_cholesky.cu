@@ -133,87 +133,83 @@ __device__ void mma_block(double *smem, const double *A, int lda, const double *
   }
   cp_wait<0>();
   __syncthreads();  // every read of A/B done before C (possibly aliasing A) is written
+  // epilogue by 16-row slab: the slab's 8 loads of C are issued together
+  // (one round trip instead of eight: a store may alias the next load, so
+  // interleaved load/store pairs would serialise), then updated and stored
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt)
+  for (int mt = 0; mt < 4; ++mt) {
+    double2 o[4][2];
+    if (mode == 0) {
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = wm + mt * 16 + gid + 8 * h, c = wn + nt * 8 + 2 * tig;
+          o[nt][h] = __ldcg((const double2 *)(C + (size_t)r * ldc + c));
+        }
+    }
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = wm + mt * 16 + gid + 8 * h, c = wn + nt * 8 + 2 * tig;
-        double *p = C + (size_t)r * ldc + c;
         double2 v;
         if (mode == 0) {
-          double2 o = __ldcg((const double2 *)p);
-          v.x = o.x - acc[mt][nt][2 * h];
-          v.y = o.y - acc[mt][nt][2 * h + 1];
+          v.x = o[nt][h].x - acc[mt][nt][2 * h];
+          v.y = o[nt][h].y - acc[mt][nt][2 * h + 1];
         } else {
           v.x = acc[mt][nt][2 * h];
           v.y = acc[mt][nt][2 * h + 1];
         }
-        __stcg((double2 *)p, v);
+        __stcg((double2 *)(C + (size_t)r * ldc + c), v);
       }
+  }
   __syncthreads();
 }
 
-// 128x128 diagonal block, blocked by 32 columns, in shared memory:
-//  A) Cholesky: per 32-block one warp factors the diagonal 32x32, one thread
-//     per row solves the panel below, all threads apply the trailing update;
+// 128x128 diagonal block in shared memory:
+//  A) Cholesky, right-looking by columns with every thread (see below);
 //  B) Dinv = L^-1: warp s inverts diagonal 32x32 block s (lane = column), then
 //     off-diagonal 32x32 blocks by increasing distance d = bi - bj:
 //     Linv[bi][bj] = -Linv[bi][bi] * sum_{m=bj}^{bi-1} L[bi][m] Linv[m][bj].
 // L goes back to D (zeros above the diagonal), Dinv to global (128x128).
-constexpr int DIAG_SCRATCH = 3 * 32 * 32;  // doubles after the 128x128 block
-__device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *fail) {
+__device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *fail,
+                            unsigned long long *st = nullptr) {
+  long long t0 = clock64();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double *scr = sm + BB * BB;
   for (int e = tid; e < BB * BB; e += THREADS) sm[e] = __ldcg(D + (size_t)(e / BB) * ldd + e % BB);
   __syncthreads();
-  for (int s = 0; s < 4; ++s) {
-    const int o = 32 * s;
-    if (warp == 0) {
-      for (int j = 0; j < 32; ++j) {
-        if (lane == j) {
-          double d = sm[(o + j) * BB + o + j];
-          if (!(d > 0.0)) { *fail = 1; d = 1.0; }
-          sm[(o + j) * BB + o + j] = sqrt(d);
-        }
-        __syncwarp();
-        const double djj = sm[(o + j) * BB + o + j];
-        if (lane > j) sm[(o + lane) * BB + o + j] /= djj;
-        __syncwarp();
-        if (lane > j) {
-          const double lij = sm[(o + lane) * BB + o + j];
-          for (int l = j + 1; l <= lane; ++l)
-            sm[(o + lane) * BB + o + l] -= lij * sm[(o + l) * BB + o + j];
-        }
-        __syncwarp();
-      }
+  // A) right-looking column Cholesky, every thread on every column: each
+  // thread takes the pivot's square root itself, scales its share of the
+  // column below it (kept twice: in place, and as a contiguous vector for
+  // conflict-free reads), then the rank-1 update of the trailing lower
+  // triangle in 16 x 16 thread tiles: 2 barriers per column (the former
+  // one-warp 32x32 factor + per-row panel solves took ~4x longer)
+  double *colv = scr;  // [BB] the current column
+  const int ti = tid >> 4, tl = tid & 15;
+  for (int j = 0; j < BB; ++j) {
+    double d = sm[j * BB + j];
+    if (!(d > 0.0)) {
+      if (tid == 0) *fail = 1;
+      d = 1.0;
+    }
+    const double djj = sqrt(d);
+    for (int i = j + 1 + tid; i < BB; i += THREADS) {
+      const double v = sm[i * BB + j] / djj;
+      sm[i * BB + j] = v;
+      colv[i] = v;
     }
     __syncthreads();
-    const int R = BB - o - 32;
-    if (tid < R) {  // panel row r: x L_ss^T = row
-      double *row = sm + (o + 32 + tid) * BB + o;
-      for (int c = 0; c < 32; ++c) {
-        double v = row[c];
-        const double *lc = sm + (o + c) * BB + o;
-        for (int m = 0; m < c; ++m) v -= row[m] * lc[m];
-        row[c] = v / lc[c];
-      }
-    }
-    __syncthreads();
-    if (R > 0) {  // trailing update of the lower triangle
-      const int ti = tid >> 4, tj = tid & 15;
-      for (int i = o + 32 + ti; i < BB; i += 16)
-        for (int j = o + 32 + tj; j <= i; j += 16) {
-          const double *ri = sm + i * BB + o, *rj = sm + j * BB + o;
-          double acc = 0.0;
-#pragma unroll 8
-          for (int m = 0; m < 32; ++m) acc += ri[m] * rj[m];
-          sm[i * BB + j] -= acc;
-        }
+    if (tid == 0) sm[j * BB + j] = djj;
+    for (int i = j + 1 + ti; i < BB; i += 16) {
+      const double lij = colv[i];
+      for (int l = j + 1 + tl; l <= i; l += 16) sm[i * BB + l] -= lij * colv[l];
     }
     __syncthreads();
   }
+  if (st && tid == 0) atomicAdd(st + 11, (unsigned long long)(clock64() - t0));
+  t0 = clock64();
   for (int e = tid; e < BB * BB; e += THREADS) {
     const int i = e / BB, l = e % BB;
     __stcg(D + (size_t)i * ldd + l, l <= i ? sm[e] : 0.0);
@@ -244,6 +240,8 @@ __device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *f
   }
   __threadfence_block();
   __syncthreads();
+  if (st && tid == 0) atomicAdd(st + 12, (unsigned long long)(clock64() - t0));
+  t0 = clock64();
   // B2: off-diagonal blocks by distance
   for (int d = 1; d < 4; ++d) {
     const int nb = 4 - d;
@@ -252,9 +250,15 @@ __device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *f
       const int b = e >> 10, r = (e >> 5) & 31, c = e & 31;
       const int bj = b, bi = b + d;
       const double *lr = sm + (bi * 32 + r) * BB;
+      // 8 independent L2 reads in flight (Dinv was just written by this CTA)
       double acc = 0.0;
-      for (int m = bj * 32; m < bi * 32; ++m)
-        acc += lr[m] * __ldcg(Dinv + (size_t)m * BB + bj * 32 + c);
+      for (int m0 = bj * 32; m0 < bi * 32; m0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldcg(Dinv + (size_t)(m0 + u) * BB + bj * 32 + c);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc += lr[m0 + u] * v[u];
+      }
       scr[e] = acc;
     }
     __syncthreads();
@@ -263,13 +267,21 @@ __device__ void diag_factor(double *sm, double *D, int ldd, double *Dinv, int *f
       const int b = e >> 10, r = (e >> 5) & 31, c = e & 31;
       const int bj = b, bi = b + d;
       double acc = 0.0;
-      for (int q = 0; q <= r; ++q)
-        acc += __ldcg(Dinv + (size_t)(bi * 32 + r) * BB + bi * 32 + q) * scr[(b << 10) + q * 32 + c];
+      const double *lrow = Dinv + (size_t)(bi * 32 + r) * BB + bi * 32;
+      for (int q0 = 0; q0 <= r; q0 += 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = q0 + u <= r ? __ldcg(lrow + q0 + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (q0 + u <= r) acc += v[u] * scr[(b << 10) + (q0 + u) * 32 + c];
+      }
       __stcg(Dinv + (size_t)(bi * 32 + r) * BB + bj * 32 + c, -acc);
     }
     __threadfence_block();
     __syncthreads();
   }
+  if (st && tid == 0) atomicAdd(st + 13, (unsigned long long)(clock64() - t0));
 }
 
 struct Task {
@@ -369,7 +381,7 @@ __device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
                   Akk + (size_t)rb * BB * B + cb * BB, B, 0);
       long long c1 = clock64();
       double *dinv = E.dinv + ((size_t)k * 4 + cb) * BB * BB;
-      diag_factor(smem, Akk + (size_t)cb * BB * B + cb * BB, B, dinv, E.fail);
+      diag_factor(smem, Akk + (size_t)cb * BB * B + cb * BB, B, dinv, E.fail, E.stats);
       long long c2 = clock64();
       for (int rb = cb + 1; rb < B / BB; ++rb)  // panel: X = A Dinv^T
         mma_block(smem, Akk + (size_t)rb * BB * B + cb * BB, B, dinv, BB, BB,
@@ -416,7 +428,6 @@ __device__ void send_output(const ExecArgs &E, int t, int q) {
 __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
   extern __shared__ __align__(16) double smem[];
   __shared__ long long s_item;
-  __shared__ int s_last;
   __shared__ unsigned s_mask;
   while (true) {
     if (threadIdx.x == 0) {
@@ -485,7 +496,7 @@ __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
             if (q != E.rank) mask |= 1u << q;
           }
       }
-      s_last = last;
+
       s_mask = mask;
     }
     __syncthreads();

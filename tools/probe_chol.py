@@ -20,6 +20,7 @@ for n in [int(x) for x in sys.argv[1:]]:
     print("  per item us:", {names[i]: round(st[2*i] / max(1, st[2*i+1]) / ghz * 1e3, 1) for i in range(4)},
           "items:", {names[i]: st[2*i+1] for i in range(4)},
           "POTRF phases us/call:", [round(x / max(1, st[1]) / ghz * 1e3, 1) for x in st[8:11]],
+          "diag A/B1/B2 us/call:", [round(x / max(1, st[1]) / ghz * 1e3, 1) for x in st[11:14]],
           "busy CTA-ms:", round(sum(st[0:8:2]) / ghz, 1), flush=True)
     L = c.result()
     res = ((L @ L.T - A).abs().max() / A.abs().max()).item()
