@@ -324,6 +324,18 @@ int hs_fm2_batch(int32_t G, const int64_t *node_off, const int64_t *adj_off,
                  const int32_t *orders, int32_t n_orders, int8_t *assign, double *cut,
                  double *err, int32_t *status, void *stream);
 
+/* gp_build for every graph of a batch (policies.py:102-108) as the DES pin
+ * array: pin[node] = 1 when the graph's gp partition puts the kernel on the
+ * GPU (root 0). Workload ratios from the fsum totals, the reference's start
+ * orders (stable descending weight, then `restarts` shuffles [restarts][n]
+ * drawn on the host with the reference's random.Random — every graph must
+ * have n_shuffle kernels), hs_fm2_batch, the reference's winner key.
+ * flags_host[G]: per graph 1 no kernels, 2 zero total time, 4 zero kernel
+ * weight (nothing is partitioned when any flag is set). Synchronous. */
+int hs_gp_pins_batch(const hs_dag_batch_t *g, int32_t restarts, const int32_t *shuffles,
+                     int32_t n_shuffle, double tol, int8_t *pin, int32_t *flags_host,
+                     void *stream);
+
 /* Exhaustive 2-way oracle (brute_force_partition, partition.py:87-134) on
  * the device for n <= 30 (the Python API keeps the reference's limit of 20).
  * Writes the winning mask (bit n-1-k set = kernel k on GPU) to *mask_host

@@ -542,6 +542,20 @@ _fm2_batch = _opt("hs_fm2_batch", _i32, _P, _P, _P, _i64, _i32, _P, _P, _P, _P, 
 _exact_totals_batch = _opt("hs_exact_totals_batch", _P, ctypes.c_int, _P, _P)
 
 
+_gp_pins = _opt("hs_gp_pins_batch", _P, _i32, _P, _i32, ctypes.c_double, _P, _P, _P)
+
+
+def gp_pins_batch(batch, restarts: int, shuffles: Optional[torch.Tensor], n_shuffle: int,
+                  tol: float):
+    """(pin int8 [total nodes], flags np.int32 [G]) — hs_gp_pins_batch."""
+    pin = torch.empty(max(int(batch.node_off_h[-1]), 1), dtype=torch.int8, device=batch.device)
+    flags = np.zeros(max(batch.batch, 1), dtype=np.int32)
+    check(_need(_gp_pins, "hs_gp_pins_batch")(
+        ctypes.byref(batch.struct()), restarts, ptr(shuffles), n_shuffle, float(tol), ptr(pin),
+        flags.ctypes.data_as(ctypes.c_void_p), stream_ptr()))
+    return pin[:int(batch.node_off_h[-1])], flags[:batch.batch]
+
+
 def fm2_batch(tb, weights, r_cpu, tol, orders, n_orders):
     """Batched exact 2-way partitioner; returns (assign int8 flat, cut [G,R], err [G,R], status)."""
     fn = _need(_fm2_batch, "hs_fm2_batch")
