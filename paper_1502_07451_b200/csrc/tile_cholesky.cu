@@ -20,9 +20,15 @@
 //                          (GEMM updates, 128x128 diagonal factor + inverse
 //                          in shared memory, panel X = A Dinv^T), keeping
 //                          the 4 inverted diagonal blocks Dinv[k] for TRSM.
-// Data produced inside the kernel is read with L1-bypassing loads (cp.async.cg
-// / ld.cg): L1 is not coherent across SMs.
+// Operands stream into shared memory by TMA (cp.async.bulk.tensor, 128-byte
+// hardware swizzle) through a ring of mbarrier-tracked stages: one thread
+// issues a stage's two tile loads, every warp waits on the stage's full
+// barrier and releases it on its empty barrier — no CTA-wide barrier per k
+// chunk. Other data produced inside the kernel is read with L1-bypassing
+// loads (ld.cg): L1 is not coherent across SMs; a proxy fence orders those
+// generic-proxy writes before the async-proxy (TMA) reads.
 #include "common.cuh"
+#include <cuda.h>
 #include <vector>
 
 namespace {
@@ -30,10 +36,11 @@ namespace {
 constexpr int B = 512;        // tile size
 constexpr int BB = 128;       // block size of the MMA engine
 constexpr int KC = 16;        // k chunk per pipeline stage
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int THREADS = 256;  // 8 warps: 2 (M) x 4 (N), warp tile 64 x 32
 constexpr int STAGE_DBL = 2 * BB * KC;                 // A + B doubles per stage
 constexpr int SMEM_GEMM = STAGES * STAGE_DBL * 8;      // 96 KB
+constexpr unsigned STAGE_BYTES = STAGE_DBL * 8;        // 32 KB: two 128 x 16 fp64 boxes
 constexpr int SMEM_DIAG = (BB * BB + 3 * 32 * 32) * 8;  // 152 KB (diagonal block + scratch)
 constexpr int SMEM_BYTES = SMEM_DIAG > SMEM_GEMM ? SMEM_DIAG : SMEM_GEMM;
 
@@ -44,17 +51,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
-// element (r, k) of a [BB][KC] stage block; XOR swizzle of k bits 2-3 by
-// r & 3 makes every fragment load hit 16 distinct bank pairs (2 wavefronts)
-__device__ __forceinline__ int sw(int r, int k) { return r * KC + (k ^ ((r & 3) << 2)); }
-
 __device__ __forceinline__ void dmma(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
   asm volatile(
       "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
@@ -63,25 +59,68 @@ __device__ __forceinline__ void dmma(double (&c)[4], const double (&a)[4], const
       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
-// Loads k columns [k0, k0+KC) of 128 rows of A (ld lda) and of B into a stage.
-__device__ __forceinline__ void load_stage(double *st, const double *A, int lda, const double *Bm,
-                                           int ldb, int k0) {
-  double *As = st, *Bs = st + BB * KC;
-  // 128 rows x 16 doubles = 1024 16-byte chunks per operand; 4 per thread
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int c = threadIdx.x + q * THREADS;
-    const int r = c >> 3, kk = (c & 7) * 2;
-    cp_async16(As + sw(r, kk), A + (size_t)r * lda + k0 + kk);
-    cp_async16(Bs + sw(r, kk), Bm + (size_t)r * ldb + k0 + kk);
-  }
+// element (r, k) of a [BB][KC] stage box written by TMA with the 128-byte
+// swizzle: the 16-byte chunk k / 2 of row r sits at chunk (k / 2) ^ (r & 7),
+// so the 8 rows x 4 columns of a fragment load hit 32 distinct doubles of
+// the bank space (2 wavefronts, the minimum for 8-byte lanes)
+__device__ __forceinline__ int sw(int r, int k) {
+  return r * KC + ((((k >> 1) ^ (r & 7)) << 1) | (k & 1));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// The stage ring's barriers (static shared memory: the dynamic buffer is
+// reused by the diagonal factor) and the CTA's running chunk count (the same
+// in every thread): chunk g uses stage g % STAGES, parity (g / STAGES) & 1.
+struct Pipe {
+  uint64_t *full, *empty;
+  uint32_t seq;
+  const CUtensorMap *tm_tiles, *tm_dinv;
+  const double *tiles, *dinv;
+};
+
+// TMA box coordinates (column, row) of the 128-row operand starting at p
+// (tiles: ld = B, the 2D view [T*T*B][B]; Dinv blocks: ld = BB, [T*4*BB][BB])
+__device__ __forceinline__ void box_of(const Pipe &P, const double *p, int ld,
+                                       const CUtensorMap *&map, int &col, int &row) {
+  const int64_t off = ld == B ? p - P.tiles : p - P.dinv;
+  map = ld == B ? P.tm_tiles : P.tm_dinv;
+  row = (int)(off / ld);
+  col = (int)(off % ld);
 }
 
 // C[128x128] (ld ldc) = (mode 0) C - A B^T  |  (mode 1) A B^T, K % 16 == 0.
-// A, B: pointers to row 0 of the 128-row operand blocks. K may be 0 (no-op
+// A, B: pointers to row 0 of the 128-row operand blocks (in the tile array,
+// ld = B, or among the inverted diagonal blocks, ld = BB). K may be 0 (no-op
 // for mode 0). Ends with __syncthreads (safe to overwrite A/B/C after).
-__device__ void mma_block(double *smem, const double *A, int lda, const double *Bm, int ldb,
-                          int K, double *C, int ldc, int mode) {
+__device__ void mma_block(Pipe &P, double *smem, const double *A, int lda, const double *Bm,
+                          int ldb, int K, double *C, int ldc, int mode) {
   if (K == 0 && mode == 0) return;  // nothing to subtract
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gid = lane >> 2, tig = lane & 3;
@@ -94,20 +133,31 @@ __device__ void mma_block(double *smem, const double *A, int lda, const double *
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
   const int nk = K / KC;
-  // prologue
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage(smem + s * STAGE_DBL, A, lda, Bm, ldb, s * KC);
-    cp_commit();
+  const CUtensorMap *ma, *mb;
+  int ca, ra, cbx, rbx;
+  box_of(P, A, lda, ma, ca, ra);
+  box_of(P, Bm, ldb, mb, cbx, rbx);
+  const uint32_t g0 = P.seq;
+  // chunk c of this block: A box (ca + c*KC, ra), B box (cbx + c*KC, rbx)
+  auto issue = [&](int c) {
+    const uint32_t g = g0 + c, st = g % STAGES;
+    if (g >= STAGES) mbar_wait(P.empty + st, ((g / STAGES) & 1) ^ 1);  // slot released
+    double *dst = smem + st * STAGE_DBL;
+    mbar_expect_tx(P.full + st, STAGE_BYTES);
+    tma_load_2d(dst, ma, ca + c * KC, ra, P.full + st);
+    tma_load_2d(dst + BB * KC, mb, cbx + c * KC, rbx, P.full + st);
+  };
+  if (threadIdx.x == 0) {
+    // generic-proxy writes (epilogues of this and other CTAs, the diagonal
+    // factor's shared-memory use) before the async-proxy reads and writes
+    asm volatile("fence.proxy.async;" ::: "memory");
+    for (int c = 0; c < STAGES - 1 && c < nk; ++c) issue(c);
   }
   for (int kc = 0; kc < nk; ++kc) {
-    cp_wait<STAGES - 2>();
-    __syncthreads();
-    // prefetch chunk kc + STAGES - 1 into the slot consumed at kc - 1
-    const int nx = kc + STAGES - 1;
-    if (nx < nk) load_stage(smem + (nx % STAGES) * STAGE_DBL, A, lda, Bm, ldb, nx * KC);
-    cp_commit();
-    const double *As = smem + (kc % STAGES) * STAGE_DBL, *Bs = As + BB * KC;
+    if (threadIdx.x == 0 && kc + STAGES - 1 < nk) issue(kc + STAGES - 1);
+    const uint32_t g = g0 + kc, st = g % STAGES;
+    mbar_wait(P.full + st, (g / STAGES) & 1);
+    const double *As = smem + st * STAGE_DBL, *Bs = As + BB * KC;
 #pragma unroll
     for (int ks = 0; ks < KC; ks += 8) {
       double a[4][4], b[4][2];
@@ -130,8 +180,10 @@ __device__ void mma_block(double *smem, const double *A, int lda, const double *
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma(acc[mt][nt], a[mt], b[nt]);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(P.empty + st);  // this warp is done with the stage
   }
-  cp_wait<0>();
+  P.seq = g0 + nk;
   __syncthreads();  // every read of A/B done before C (possibly aliasing A) is written
   // epilogue by 16-row slab: the slab's 8 loads of C are issued together
   // (one round trip instead of eight: a store may alias the next load, so
@@ -290,6 +342,8 @@ struct Task {
 };
 
 struct ExecArgs {
+  CUtensorMap tm_tiles;  // TMA view of the tiles: [T*T*B rows][B] fp64, box 128 x 16
+  CUtensorMap tm_dinv;   // TMA view of the inverted diagonal blocks: [T*4*BB][BB]
   double *tiles;     // T*T tiles (lower used)
   double *dinv;      // T * 4 * 128*128 inverted diagonal blocks
   int T;
@@ -347,18 +401,18 @@ __device__ __forceinline__ void stat_add(const ExecArgs &E, int idx, unsigned lo
   if (E.stats && threadIdx.x == 0) atomicAdd(&E.stats[idx], v);
 }
 
-__device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
+__device__ void run_item(const ExecArgs &E, Pipe &P, double *smem, int t, int it) {
   const int kd = E.kind[t], i = E.ti[t], j = E.tj[t], k = E.tk[t];
   if (kd == K_GEMM) {
     const int rb = it >> 2, cb = it & 3;
-    mma_block(smem, tile(E, i, k) + (size_t)rb * BB * B, B, tile(E, j, k) + (size_t)cb * BB * B, B,
+    mma_block(P, smem, tile(E, i, k) + (size_t)rb * BB * B, B, tile(E, j, k) + (size_t)cb * BB * B, B,
               B, tile(E, i, j) + (size_t)rb * BB * B + cb * BB, B, 0);
   } else if (kd == K_SYRK) {
     // lower blocks (rb, cb), rb >= cb, enumerated row by row
     int rb = 0, rem = it;
     while (rem > rb) { rem -= rb + 1; ++rb; }
     const int cb = rem;
-    mma_block(smem, tile(E, i, k) + (size_t)rb * BB * B, B, tile(E, i, k) + (size_t)cb * BB * B, B,
+    mma_block(P, smem, tile(E, i, k) + (size_t)rb * BB * B, B, tile(E, i, k) + (size_t)cb * BB * B, B,
               B, tile(E, i, i) + (size_t)rb * BB * B + cb * BB, B, 0);
   } else if (kd == K_TRSM) {
     // row block rb of A_ik: X = A L_kk^-T by block columns
@@ -367,9 +421,9 @@ __device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
     const double *Lkk = tile(E, k, k);
     for (int cb = 0; cb < B / BB; ++cb) {
       // R = A[:, cb] - X[:, :cb] L[cb, :cb]^T
-      mma_block(smem, Aik, B, Lkk + (size_t)cb * BB * B, B, cb * BB, Aik + cb * BB, B, 0);
+      mma_block(P, smem, Aik, B, Lkk + (size_t)cb * BB * B, B, cb * BB, Aik + cb * BB, B, 0);
       // X[:, cb] = R Dinv_cb^T (in place)
-      mma_block(smem, Aik + cb * BB, B, E.dinv + ((size_t)k * 4 + cb) * BB * BB, BB, BB,
+      mma_block(P, smem, Aik + cb * BB, B, E.dinv + ((size_t)k * 4 + cb) * BB * BB, BB, BB,
                 Aik + cb * BB, B, 1);
     }
   } else {  // POTRF(k): blocked by 128 columns
@@ -377,14 +431,14 @@ __device__ void run_item(const ExecArgs &E, double *smem, int t, int it) {
     for (int cb = 0; cb < B / BB; ++cb) {
       long long c0 = clock64();
       for (int rb = cb; rb < B / BB; ++rb)  // A[rb, cb] -= L[rb, :cb] L[cb, :cb]^T
-        mma_block(smem, Akk + (size_t)rb * BB * B, B, Akk + (size_t)cb * BB * B, B, cb * BB,
+        mma_block(P, smem, Akk + (size_t)rb * BB * B, B, Akk + (size_t)cb * BB * B, B, cb * BB,
                   Akk + (size_t)rb * BB * B + cb * BB, B, 0);
       long long c1 = clock64();
       double *dinv = E.dinv + ((size_t)k * 4 + cb) * BB * BB;
       diag_factor(smem, Akk + (size_t)cb * BB * B + cb * BB, B, dinv, E.fail, E.stats);
       long long c2 = clock64();
       for (int rb = cb + 1; rb < B / BB; ++rb)  // panel: X = A Dinv^T
-        mma_block(smem, Akk + (size_t)rb * BB * B + cb * BB, B, dinv, BB, BB,
+        mma_block(P, smem, Akk + (size_t)rb * BB * B + cb * BB, B, dinv, BB, BB,
                   Akk + (size_t)rb * BB * B + cb * BB, B, 1);
       long long c3 = clock64();
       stat_add(E, 8, c1 - c0);
@@ -425,8 +479,18 @@ __device__ void send_output(const ExecArgs &E, int t, int q) {
   }
 }
 
-__global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
-  extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(THREADS, 1) exec_kernel(const __grid_constant__ ExecArgs E) {
+  extern __shared__ __align__(1024) double smem[];
+  __shared__ __align__(8) uint64_t s_full[STAGES], s_empty[STAGES];
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(s_full + i, 1);
+      mbar_init(s_empty + i, THREADS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  Pipe P{s_full, s_empty, 0u, &E.tm_tiles, &E.tm_dinv, E.tiles, E.dinv};
   __shared__ long long s_item;
   __shared__ unsigned s_mask;
   while (true) {
@@ -479,7 +543,7 @@ __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
     if (item == -2) break;
     const int t = (int)(item >> 8), it = (int)(item & 0xff);
     const long long c0 = clock64();
-    run_item(E, smem, t, it);
+    run_item(E, P, smem, t, it);
     stat_add(E, E.kind[t] * 2, clock64() - c0);
     stat_add(E, E.kind[t] * 2 + 1, 1);
     __threadfence();
@@ -518,6 +582,45 @@ __global__ void __launch_bounds__(THREADS, 1) exec_kernel(ExecArgs E) {
 }
 
 // tiled <-> row-major conversion (lower tiles only); blockIdx.y = tile
+// TMA descriptors of the two operand arrays (driver entry point fetched
+// through the runtime: no -lcuda link): 128 rows x 16 fp64 boxes, 128-byte
+// swizzle, L2 promotion of 128-byte lines.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_tensor_maps(ExecArgs *E, double *tiles, double *dinv, int T) {
+  static EncodeTiledFn encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    HS_CHECK_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    HS_REQUIRE(fn && q == cudaDriverEntryPointSuccess, HS_ECUDA, "cuTensorMapEncodeTiled missing");
+    encode = (EncodeTiledFn)fn;
+  }
+  const cuuint32_t box[2] = {(cuuint32_t)KC, (cuuint32_t)BB}, estr[2] = {1, 1};
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)T * T * B};
+    const cuuint64_t strides[1] = {(cuuint64_t)B * sizeof(double)};
+    const CUresult r = encode(&E->tm_tiles, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, tiles, dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    HS_REQUIRE(r == CUDA_SUCCESS, HS_ECUDA, "tile tensor map: CUresult %d", (int)r);
+  }
+  {
+    const cuuint64_t dims[2] = {(cuuint64_t)BB, (cuuint64_t)T * 4 * BB};
+    const cuuint64_t strides[1] = {(cuuint64_t)BB * sizeof(double)};
+    const CUresult r = encode(&E->tm_dinv, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, dinv, dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    HS_REQUIRE(r == CUDA_SUCCESS, HS_ECUDA, "Dinv tensor map: CUresult %d", (int)r);
+  }
+  return HS_OK;
+}
+
 __global__ void pack_kernel(double *A, int n, int T, double *tiles, int to_tiles) {
   const int tl = blockIdx.y;
   int ti = 0;
@@ -627,6 +730,10 @@ extern "C" int hs_chol_execute_part(double *tiles, double *dinv, int32_t T, int3
     HS_CHECK_CUDA(cudaMemcpyAsync(qb, q1.data(), q1.size() * 8, cudaMemcpyHostToDevice, s));
   ExecArgs E;
   memset(&E, 0, sizeof E);
+  {
+    int rc = make_tensor_maps(&E, tiles, dinv, T);
+    if (rc) return rc;
+  }
   E.tiles = tiles; E.dinv = dinv; E.T = T; E.n_tasks = n_tasks;
   E.kind = kind; E.ti = ti; E.tj = tj; E.tk = tk; E.succ_ptr = succ_ptr; E.succ = succ;
   E.pending = pending; E.items_left = items_left;
