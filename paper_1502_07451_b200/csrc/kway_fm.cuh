@@ -436,7 +436,7 @@ struct FmCta {
   }
 
   __device__ void bisect_all(int passes) {
-    __shared__ int s_r0[kMaxParts], s_r1[kMaxParts];
+    __shared__ int s_r0[2 * kMaxParts], s_r1[2 * kMaxParts];  // every range of the split tree: 2k - 1
     __shared__ int s_head, s_tail;
     if (threadIdx.x == 0) {
       s_r0[0] = 0;

@@ -125,3 +125,18 @@ def test_cholesky_dag_calibration_weights(tiles, k):
     assert torch.equal(r1.part, r2.part)
     cut = _check(csr, r1, k, ew, nw)
     assert cut < 0.9 * _band_cut(csr, k, ew, nw)  # measured 0.52-0.75
+
+
+@pytest.mark.parametrize("k", [16, 33, 64])
+def test_fm_levels_large_k(k):
+    """Graphs inside the FM range (<= 4096 vertices) at large k: the CTA FM
+    keeps its rows in global memory (n*k*4 bytes beyond shared memory) and,
+    past 16 parts, takes the generic best-target path. Valid, balanced,
+    deterministic, and the reported cut is the partition's."""
+    csr = kway.layered_dag(3000, 20_000, seed=3)
+    ew, nw = _random_weights(csr, 1, 100, seed=k)
+    ug = kway.symmetrize(csr, ew, nw)
+    r1 = kway.partition_kway(ug, k, tol=TOL, seed=2)
+    r2 = kway.partition_kway(ug, k, tol=TOL, seed=2)
+    assert torch.equal(r1.part, r2.part) and r1.cut == r2.cut
+    _check(csr, r1, k, ew, nw)
