@@ -32,6 +32,8 @@
 // |w_p / total - t_p| <= tol for every part p.
 #include "common.cuh"
 #include <cub/device/device_scan.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
 #include <cub/device/device_reduce.cuh>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_segmented_sort.cuh>
@@ -46,7 +48,6 @@ namespace cg = cooperative_groups;
 #include <memory>
 #include "dist.cuh"
 
-int hs_widen32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s);
 
 namespace {
 
@@ -422,16 +423,23 @@ __global__ void __launch_bounds__(kSymWarps * 32, 8) sym_fill_chunk(
 }
 
 // ------------------------------------------------------------------ K3 ---
-__global__ void deg_from_xadj(const int64_t *xadj, int n, int32_t *deg, int32_t *max_deg) {
+__global__ void __launch_bounds__(256) deg_from_xadj(const int64_t *xadj, int n, int32_t *deg,
+                                                     int32_t *max_deg) {
   int mx = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int d = (int32_t)(xadj[i + 1] - xadj[i]);
+    const int d = (int32_t)(__ldg(xadj + i + 1) - __ldg(xadj + i));
     deg[i] = d;
     mx = max(mx, d);
   }
   for (int off = 16; off; off >>= 1) mx = max(mx, __shfl_down_sync(0xffffffffu, mx, off));
-  if (max_deg && (threadIdx.x & 31) == 0) atomicMax(max_deg, mx);
+  __shared__ int sm[8];
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (max_deg && threadIdx.x == 0) {
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) mx = max(mx, sm[q]);
+    atomicMax(max_deg, mx);
+  }
 }
 
 // Edge rating w^2 / (c(u) c(v)) ("expansion*2"): prefers heavy edges between
@@ -821,26 +829,61 @@ __global__ void project(int n, const int32_t *cmap, const part_t *cpart, part_t 
     part[i] = cpart[cmap[i]];
 }
 
-// Per-part weight sums: one warp-wide __reduce_add per part per 32 vertices
-// (shared-memory atomics here serialised: neighbouring ids share a part).
-__global__ void part_weights(int n, const int32_t *vw, const part_t *part, int k, int64_t *pw) {
-  __shared__ unsigned long long s[kMaxParts];
+// Per-part weight sums. Each thread walks 16 consecutive vertices (one
+// 16-byte part load, four 16-byte weight loads when aligned) keeping a run
+// (part, sum) and flushing it to shared memory when the part changes — parts
+// come in long runs after the band start, so flushes are rare; the last run
+// of every thread goes through one warp-wide __reduce_add per distinct part.
+// Sums fit 32 bits: the total vertex weight is < 2^31 (the weight guard).
+constexpr int kPwChunk = 16;
+__global__ void __launch_bounds__(256) part_weights(int n, const int32_t *vw, const part_t *part,
+                                                    int k, int64_t *pw) {
+  __shared__ unsigned s[kMaxParts];
   for (int p = threadIdx.x; p < k; p += blockDim.x) s[p] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
+  const bool vec = (((uintptr_t)vw | (uintptr_t)part) & 15) == 0;
+  const int64_t chunks = ((int64_t)n + kPwChunk - 1) / kPwChunk;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
-    const int64_t i = base + threadIdx.x;
-    const int p = i < n ? part[i] : -1;
-    const unsigned w = i < n ? (unsigned)vw[i] : 0u;  // 32 x vw < 2^31
-    // one reduction per distinct part present in the warp
-    const unsigned peers = __match_any_sync(0xffffffffu, p);
-    const unsigned sum = __reduce_add_sync(peers, w);
-    if (p >= 0 && lane == __ffs(peers) - 1 && sum) atomicAdd(&s[p], (unsigned long long)sum);
+  const int64_t trips = (chunks + stride - 1) / stride;  // warp-uniform trip count
+  int cur = -1;
+  unsigned acc = 0;
+  for (int64_t t = 0; t < trips; ++t) {
+    const int64_t c = t * stride + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= chunks) break;
+    const int64_t i0 = c * kPwChunk;
+    int8_t pb[kPwChunk];
+    int32_t wb[kPwChunk];
+    int cnt = kPwChunk;
+    if (vec && i0 + kPwChunk <= n) {
+      *(int4 *)pb = __ldg((const int4 *)(part + i0));
+#pragma unroll
+      for (int q = 0; q < kPwChunk / 4; ++q) *(int4 *)(wb + 4 * q) = __ldg((const int4 *)(vw + i0) + q);
+    } else {
+      cnt = (int)(n - i0 < kPwChunk ? n - i0 : kPwChunk);
+#pragma unroll
+      for (int q = 0; q < kPwChunk; ++q) {
+        pb[q] = q < cnt ? part[i0 + q] : 0;
+        wb[q] = q < cnt ? vw[i0 + q] : 0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kPwChunk; ++q) {
+      if (q >= cnt) break;
+      const int p = pb[q];
+      if (p != cur) {
+        if (cur >= 0 && acc) atomicAdd(&s[cur], acc);
+        cur = p;
+        acc = 0;
+      }
+      acc += (unsigned)wb[q];
+    }
   }
+  const unsigned peers = __match_any_sync(0xffffffffu, cur);
+  const unsigned sum = __reduce_add_sync(peers, acc);
+  if (cur >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1 && sum) atomicAdd(&s[cur], sum);
   __syncthreads();
   for (int p = threadIdx.x; p < k; p += blockDim.x)
-    if (s[p]) atomicAdd((unsigned long long *)&pw[p], s[p]);
+    if (s[p]) atomicAdd((unsigned long long *)&pw[p], (unsigned long long)s[p]);
 }
 
 constexpr int kRefWarps = 8;
@@ -984,24 +1027,44 @@ __global__ void widen_minmax(int64_t *mm) {
 }
 
 // sum / min / max of int32 weights (out: u64 sum, i32 min, i32 max; caller
-// initialises 0, INT_MAX, INT_MIN)
-__global__ void wstats_kernel(int64_t n, const int32_t *w, unsigned long long *sum, int32_t *mn,
-                              int32_t *mx) {
+// initialises 0, INT_MAX, INT_MIN): 16-byte loads over the aligned body, one
+// atomic triple per block
+__global__ void __launch_bounds__(256) wstats_kernel(int64_t n, const int32_t *w,
+                                                     unsigned long long *sum, int32_t *mn,
+                                                     int32_t *mx) {
   unsigned long long s = 0;
   int lo = INT_MAX, hi = INT_MIN;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
-       j += (int64_t)gridDim.x * blockDim.x) {
-    const int x = __ldg(w + j);
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t h0 = ((16 - ((uintptr_t)w & 15)) & 15) / 4, head = n < h0 ? n : h0;
+  const int64_t n4 = (n - head) / 4;
+  const int4 *w4 = (const int4 *)(w + head);
+  auto take = [&](int x) {
     s += (unsigned long long)(long long)x;
     lo = min(lo, x);
     hi = max(hi, x);
+  };
+  for (int64_t j = tid; j < n4; j += 2 * stride) {
+    const int4 a = __ldg(w4 + j);
+    const bool two = j + stride < n4;
+    const int4 b = two ? __ldg(w4 + j + stride) : make_int4(a.x, a.x, a.x, a.x);
+    take(a.x), take(a.y), take(a.z), take(a.w);
+    if (two) take(b.x), take(b.y), take(b.z), take(b.w);
   }
+  for (int64_t j = tid; j < head; j += stride) take(__ldg(w + j));
+  for (int64_t j = head + 4 * n4 + tid; j < n; j += stride) take(__ldg(w + j));
   for (int off = 16; off; off >>= 1) {
     s += __shfl_down_sync(0xffffffffu, s, off);
     lo = min(lo, __shfl_down_sync(0xffffffffu, lo, off));
     hi = max(hi, __shfl_down_sync(0xffffffffu, hi, off));
   }
-  if ((threadIdx.x & 31) == 0) {
+  __shared__ unsigned long long ss[8];
+  __shared__ int sl[8], sh[8];
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) ss[warp] = s, sl[warp] = lo, sh[warp] = hi;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < nw; ++q) s += ss[q], lo = min(lo, sl[q]), hi = max(hi, sh[q]);
     atomicAdd(sum, s);
     atomicMin(mn, lo);
     atomicMax(mx, hi);
@@ -1145,6 +1208,24 @@ int exclusive_scan(const T *in, T *out, int64_t n, cudaStream_t s) {
   hs::Scratch<char> tmp;
   HS_CHECK_CUDA(tmp.alloc(tb, s));
   HS_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, out, n, s));
+  hs::count_launch(1);
+  return HS_OK;
+}
+
+// out[0..n] = exclusive prefix of in[0..n) widened to int64 on the fly (no
+// int64 copy of the input; out[n] is the total)
+struct Widen32 {
+  const int32_t *in;
+  int64_t n;
+  __host__ __device__ int64_t operator()(int64_t i) const { return i < n ? (int64_t)in[i] : 0; }
+};
+int exclusive_scan_widen(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s) {
+  auto it = thrust::make_transform_iterator(thrust::counting_iterator<int64_t>(0), Widen32{in, n});
+  size_t tb = 0;
+  HS_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, it, out, n + 1, s));
+  hs::Scratch<char> tmp;
+  HS_CHECK_CUDA(tmp.alloc(tb, s));
+  HS_CHECK_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, it, out, n + 1, s));
   hs::count_launch(1);
   return HS_OK;
 }
@@ -1322,8 +1403,9 @@ struct Kway {
   // part: this rank's replica (global ids); sums this rank's vertices, then all ranks'
   int weights(const G &g, const part_t *part) {
     HS_CHECK_CUDA(cudaMemsetAsync(d_pw, 0, k * sizeof(int64_t), s));
-    part_weights<<<hs::grid_for(g.n, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw,
-                                                                           part + g.v0, k, d_pw);
+    const int64_t chunks = ((int64_t)g.n + kPwChunk - 1) / kPwChunk;
+    part_weights<<<hs::grid_for(chunks, 256, hs::sm_count() * 4), 256, 0, s>>>(g.n, g.vw,
+                                                                              part + g.v0, k, d_pw);
     HS_CHECK_LAUNCH();
     return ar({seg64(d_pw, k)});
   }
@@ -2100,13 +2182,9 @@ struct Kway {
     part_t *best = loc(best_rep);
     // trial 0: id-range bands (global prefix of the weights when sharded)
     {
-      int64_t *vw64, *prefix;
-      HS_CHECK_CUDA(dalloc(&vw64, nc + 1, s));
+      int64_t *prefix;
       HS_CHECK_CUDA(dalloc(&prefix, nc + 1, s));
-      int rc = hs_widen32(g.vw, vw64, nc, s);
-      if (rc) return rc;
-      HS_CHECK_CUDA(cudaMemsetAsync(vw64 + nc, 0, sizeof(int64_t), s));
-      rc = exclusive_scan<int64_t>(vw64, prefix, nc + 1, s);
+      int rc = exclusive_scan_widen(g.vw, prefix, nc, s);
       if (rc) return rc;
       int64_t woff = 0;
       if (D.on()) {
@@ -2119,7 +2197,6 @@ struct Kway {
       range_parts<<<hs::grid_for(nc, 256), 256, 0, s>>>(nc, prefix, woff, g.vw, d_cum, k,
                                                         total_vw, g.v0, best_rep);
       HS_CHECK_LAUNCH();
-      cudaFreeAsync(vw64, s);
       cudaFreeAsync(prefix, s);
       rc = barrier();  // every rank's bands are in place
       if (rc) return rc;
@@ -2174,15 +2251,10 @@ extern "C" int hs_symmetrize_range(const hs_dag_t *g, int32_t kv0, int32_t kv1,
     return HS_OK;
   }
   hs::Scratch<int32_t> deg;
-  hs::Scratch<int64_t> deg64;
   HS_CHECK_CUDA(deg.alloc(nl + 1, s));
-  HS_CHECK_CUDA(deg64.alloc(nl + 1, s));
   sym_degree<<<hs::grid_for(nl, 256), 256, 0, s>>>(*g, kv0, kv1, deg);
   HS_CHECK_LAUNCH();
-  HS_CHECK_CUDA(cudaMemsetAsync(deg64.p + nl, 0, sizeof(int64_t), s));
-  int rc = hs_widen32(deg, deg64, nl, s);
-  if (rc) return rc;
-  rc = exclusive_scan<int64_t>(deg64, xadj, nl + 1, s);
+  int rc = exclusive_scan_widen(deg, xadj, nl, s);
   if (rc) return rc;
   constexpr int TS = 4;  // measured: 4 lanes beat 8 and 2
   const int sgrid = std::max(1, std::min(hs::sm_count() * 32, (nl * TS + 255) / 256));
@@ -2225,21 +2297,6 @@ extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i,
   HS_REQUIRE(g, HS_EINVAL, "hs_symmetrize: null argument");
   return hs_symmetrize_range(g, 0, g->n - 1, edge_w_i, edge_w_i_in, node_w_i, xadj, adjncy,
                              adjwgt_i, vwgt_i, twin, nnz_host, stream);
-}
-
-namespace {
-__global__ void widen_kernel(const int32_t *in, int64_t *out, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    out[i] = in[i];
-}
-}  // namespace
-
-int hs_widen32(const int32_t *in, int64_t *out, int64_t n, cudaStream_t s) {
-  if (n <= 0) return HS_OK;
-  widen_kernel<<<hs::grid_for(n, 256), 256, 0, s>>>(in, out, n);
-  HS_CHECK_LAUNCH();
-  return HS_OK;
 }
 
 namespace {
@@ -2483,6 +2540,7 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   const int coarsest_n = K.levels.back().n_glob;
 
   // ---- uncoarsening + refinement ----
+  bool pw_exact = false;
   for (int li = (int)K.levels.size() - 1; li >= 0; --li) {
     Level &Lv = K.levels[li];
     if (li != (int)K.levels.size() - 1) {
@@ -2513,6 +2571,7 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
     rc = K.refine(Lv, cur, K.salt ^ ((uint64_t)li << 40), li == 0);
     if (ncu_win) cudaProfilerStop();
     if (rc) return rc;
+    pw_exact = li == 0;  // refine keeps d_pw in step with every applied move
     K.timer.mark("refine level");
   }
   int8_to_int32<<<hs::grid_for(n_glob, 256), 256, 0, s>>>(K.loc(cur), n_glob, part_out);
@@ -2530,8 +2589,12 @@ int partition_impl(const hs_ugraph_t *ug, int32_t v0, int32_t n_glob, const hs_d
   if (K.cut_of(g0, K.loc(cur), cached_cut, &cut_dev) < 0 || !cut_dev)
     HS_REQUIRE(false, HS_ECUDA, "k-way: cut failed");
   K.cache = Conn();
-  rc = K.weights(g0, K.loc(cur));
-  if (rc) return rc;
+  // the finest level's refinement left d_pw exact (all ranks' moves, the
+  // caller's unscaled vertex weights); FM levels do not maintain it
+  if (!pw_exact) {
+    rc = K.weights(g0, K.loc(cur));
+    if (rc) return rc;
+  }
   // one host read for the cut and the part weights
   std::vector<int64_t> pw(k);
   unsigned long long cut2 = 0;

@@ -193,6 +193,12 @@ def test_kway_valid_balanced_deterministic(n, m, k):
     assert (p1 == r2.part.cpu().numpy()).all(), "not deterministic"
     assert p1.min() >= 0 and p1.max() < k
     assert r1.feasible and r1.max_deviation <= 0.03
+    # the reported deviation is the one of the returned parts (the finest
+    # refinement's running part weights stand in for a final recount)
+    vw = ug.vwgt.cpu().numpy().astype(np.int64)
+    pw = np.bincount(p1, weights=vw, minlength=k)
+    dev = float(np.abs(pw / float(vw.sum()) - 1.0 / k).max())
+    assert abs(r1.max_deviation - dev) <= 2e-9
     # integer cut from the partitioner == K2 on the directed DAG == oracle
     nodep = kway.kernel_to_node_parts(csr, r1.part)
     ev = kway.evaluate_batch(csr, nodep.unsqueeze(0), k,
