@@ -537,6 +537,62 @@ int hs_ipc_handle(void *dev_ptr, char *handle64);
 int hs_ipc_open(const char *handle64, void **dev_ptr);
 int hs_ipc_close(void *dev_ptr);
 
+/* ---- DOT ingestion (replaces parse_dot, graphio.py:79-199) ---------------
+ * hs_dot_parse parses the UTF-8 bytes text[len] (DEVICE memory) with the
+ * reference's DOT subset. A text the reference rejects returns HS_OK with
+ * info->status = the DotParseError kind (1 expected a digraph header, got
+ * {line!r}; 2 undirected graphs are not supported; 3 cannot parse statement
+ * {stmt!r}; 4 bad attribute syntax near {text[pos:pos+20]!r}; 5 no digraph
+ * found; 6 missing closing brace), info->err_line its 1-based line and
+ * err_a/err_b/err_c byte offsets into text (1: the stripped line [a, b);
+ * 3: the statement [a, b); 4: the attribute text [a, b) and the failing
+ * position c), and *handle = NULL. Otherwise *handle holds the parse:
+ *   names in order of first appearance with their ids (graphio.py:145-158),
+ *   the last kind/size/weight_cpu/weight_gpu of each (size via int(float())),
+ *   edge declarations in order with bytes/weight_xfer, every attribute's key
+ *   and value spans, class (0 kind, 1 size, 2 weight_cpu, 3 weight_gpu,
+ *   4 bytes, 5 weight_xfer, 6 style, 7 other) and owner (name rank >= 0, or
+ *   -1 - edge index);
+ *   info->conv_err = (order << 3) | kind of the first float()/int() failure
+ *   in the reference's evaluation order (order = 3 * rank + {0 size, 1
+ *   weight_cpu, 2 weight_gpu}, then 3 * n_names + 2 * edge + {0 bytes,
+ *   1 weight_xfer}; kind 1 ValueError, 2 int(inf), 3 int(nan)), -1 if none;
+ *   info->n_slow literals listed as (order, attribute) for the caller to
+ *   convert: > 19 significant digits whose rounding the Eisel-Lemire bounds
+ *   leave open, and int(float()) values beyond int64 (Python ints).
+ * hs_dot_fetch copies the parse to caller HOST arrays (any may be NULL);
+ * hs_dot_csr_size / hs_dot_csr build the device CSR of the graph TaskGraph
+ * would hold (ids ascending, edges by (src, dst), a later duplicate edge
+ * wins, the synthesized root and its edges when no SOURCE node exists);
+ * hs_dot_release frees the handle. */
+typedef struct hs_dot_info {
+    int32_t status, err_line, err_a, err_b, err_c;
+    int32_t name_b, name_e;      /* digraph name group [b, e), b < 0: none */
+    int32_t n_names, n_edges, n_attrs, n_slow;
+    int32_t root_rank;           /* first name of kind SOURCE, -1: none */
+    int64_t conv_err;
+    int64_t max_id;              /* the largest assigned id */
+} hs_dot_info_t;
+
+typedef struct hs_dot_host {
+    int64_t *id; int32_t *kind_attr; uint64_t *kind_hash; int64_t *size;
+    double *w_cpu, *w_gpu; uint8_t *has_pred;                 /* [n_names] */
+    int32_t *src, *dst; int64_t *bytes; double *w_xfer;       /* [n_edges] */
+    int32_t *k0, *k1, *v0, *v1, *owner; uint8_t *cls;          /* [n_attrs] */
+    int64_t *slow;                                            /* [2 n_slow] */
+} hs_dot_host_t;
+
+int hs_dot_parse(const uint8_t *text, int64_t len, hs_dot_info_t *info, void **handle,
+                 void *stream);
+int hs_dot_fetch(void *handle, const hs_dot_host_t *out, void *stream);
+int hs_dot_csr_size(void *handle, int64_t *n, int64_t *m, void *stream);
+int hs_dot_csr(void *handle, int64_t *out_ptr, int32_t *out_dst, int64_t *ids, double *w_cpu,
+               double *w_gpu, double *w_xfer, int64_t *bytes, int32_t *root_host, void *stream);
+int hs_dot_release(void *handle);
+/* Python float(bytes) with the device's conversion, on the host (tests):
+ * 0 ok, 1 ValueError, 2 undecided (> 19 digits) */
+int hs_dot_py_float(const uint8_t *bytes, int64_t len, double *out);
+
 #ifdef __cplusplus
 }
 #endif

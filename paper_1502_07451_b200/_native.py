@@ -577,3 +577,105 @@ def exact_totals_batch(batch, include_root: bool) -> torch.Tensor:
     out = torch.empty(batch.batch, 3, dtype=torch.float64, device=batch.device)
     check(fn(ctypes.byref(batch.struct()), int(include_root), ptr(out), stream_ptr()))
     return out
+
+
+# ---- DOT ingestion (hs_dot_*) ------------------------------------------------
+class HsDotInfo(ctypes.Structure):
+    _fields_ = [("status", _i32), ("err_line", _i32), ("err_a", _i32), ("err_b", _i32),
+                ("err_c", _i32), ("name_b", _i32), ("name_e", _i32), ("n_names", _i32),
+                ("n_edges", _i32), ("n_attrs", _i32), ("n_slow", _i32), ("root_rank", _i32),
+                ("conv_err", _i64), ("max_id", _i64)]
+
+
+class HsDotHost(ctypes.Structure):
+    _fields_ = [(f, _c_void_p) for f in (
+        "id", "kind_attr", "kind_hash", "size", "w_cpu", "w_gpu", "has_pred",
+        "src", "dst", "bytes", "w_xfer", "k0", "k1", "v0", "v1", "owner", "cls", "slow")]
+
+
+_dot_parse = _opt("hs_dot_parse", _P, _i64, _P, _P, _P)
+_dot_fetch = _opt("hs_dot_fetch", _P, _P, _P)
+_dot_csr_size = _opt("hs_dot_csr_size", _P, _P, _P, _P)
+_dot_csr = _opt("hs_dot_csr", _P, _P, _P, _P, _P, _P, _P, _P, _P, _P)
+_dot_release = _opt("hs_dot_release", _P)
+_dot_py_float = _opt("hs_dot_py_float", ctypes.c_char_p, _i64, _P)
+
+_DOT_FIELDS = {  # field -> (dtype, count key)
+    "id": (np.int64, "n_names"), "kind_attr": (np.int32, "n_names"),
+    "kind_hash": (np.uint64, "n_names"), "size": (np.int64, "n_names"),
+    "w_cpu": (np.float64, "n_names"), "w_gpu": (np.float64, "n_names"),
+    "has_pred": (np.uint8, "n_names"), "src": (np.int32, "n_edges"),
+    "dst": (np.int32, "n_edges"), "bytes": (np.int64, "n_edges"),
+    "w_xfer": (np.float64, "n_edges"), "k0": (np.int32, "n_attrs"),
+    "k1": (np.int32, "n_attrs"), "v0": (np.int32, "n_attrs"), "v1": (np.int32, "n_attrs"),
+    "owner": (np.int32, "n_attrs"), "cls": (np.uint8, "n_attrs"),
+}
+
+
+class DotHandle:
+    """A device parse (hs_dot_parse); released when collected or by ``close``."""
+
+    def __init__(self, text_dev: torch.Tensor, info: HsDotInfo, handle: int):
+        self.text_dev = text_dev  # the parse keeps offsets into it
+        self.info = info
+        self.handle = handle
+
+    def fetch(self) -> dict:
+        info = self.info
+        out = {k: np.empty(getattr(info, n), dtype=t) for k, (t, n) in _DOT_FIELDS.items()}
+        out["slow"] = np.empty(2 * info.n_slow, dtype=np.int64)
+        h = HsDotHost(**{k: v.ctypes.data if v.size else None for k, v in out.items()})
+        check(_need(_dot_fetch, "hs_dot_fetch")(self.handle, ctypes.byref(h), stream_ptr()))
+        return out
+
+    def csr(self):
+        """(root index, out_ptr, out_dst, ids, w_cpu, w_gpu, w_xfer, bytes) on the device."""
+        n, m = ctypes.c_int64(), ctypes.c_int64()
+        check(_need(_dot_csr_size, "hs_dot_csr_size")(self.handle, ctypes.byref(n),
+                                                      ctypes.byref(m), stream_ptr()))
+        n, m = n.value, m.value
+        dev = self.text_dev.device
+        e = lambda k, t: torch.empty(max(k, 1), dtype=t, device=dev)  # noqa: E731
+        out_ptr, ids = e(n + 1, torch.int64), e(n, torch.int64)
+        w_cpu, w_gpu = e(n, torch.float64), e(n, torch.float64)
+        out_dst, w_xfer, nbytes = e(m, torch.int32), e(m, torch.float64), e(m, torch.int64)
+        root = ctypes.c_int32()
+        check(_need(_dot_csr, "hs_dot_csr")(self.handle, ptr(out_ptr), ptr(out_dst), ptr(ids),
+                                            ptr(w_cpu), ptr(w_gpu), ptr(w_xfer), ptr(nbytes),
+                                            ctypes.byref(root), stream_ptr()))
+        return (root.value, out_ptr[:n + 1], out_dst[:m], ids[:n], w_cpu[:n], w_gpu[:n],
+                w_xfer[:m], nbytes[:m])
+
+    def close(self) -> None:
+        if self.handle:
+            _dot_release(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def dot_parse(data: bytes, device=None) -> Tuple[HsDotInfo, Optional[DotHandle]]:
+    """Parse DOT bytes on the device (hs_dot_parse): (info, handle or None)."""
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    host = torch.frombuffer(bytearray(data), dtype=torch.uint8) if data else \
+        torch.empty(0, dtype=torch.uint8)
+    text = torch.empty(max(len(data), 1), dtype=torch.uint8, device=dev)
+    if data:
+        text[:len(data)].copy_(host.pin_memory() if len(data) > (1 << 20) else host,
+                               non_blocking=False)
+    info = HsDotInfo()
+    handle = ctypes.c_void_p()
+    check(_need(_dot_parse, "hs_dot_parse")(ptr(text), len(data), ctypes.byref(info),
+                                            ctypes.byref(handle), stream_ptr()))
+    return info, (DotHandle(text, info, handle.value) if handle.value else None)
+
+
+def dot_py_float(data: bytes) -> Tuple[int, float]:
+    """(status, value) of the device's float() restated on the host (tests)."""
+    out = ctypes.c_double()
+    st = _need(_dot_py_float, "hs_dot_py_float")(data, len(data), ctypes.byref(out))
+    return int(st), out.value

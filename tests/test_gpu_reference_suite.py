@@ -6,10 +6,9 @@ the vendored files and a `hetsched` package whose submodules ARE this
 package's modules — in a child pytest process on the GPU. Every call the
 tests make therefore goes through the drop-in API and the CUDA kernels.
 
-DOT text parsing (parse_dot) is not implemented (emit_dot, emit_partitioned_dot
-and annotated_dot are); the shim supplies the missing names as stubs that
-raise, so the modules import and exactly the tests that parse DOT fail. Those are listed in
-tests/golden/reference_suite_expected.json; every other test must pass.
+All eight vendored modules run, test_graphio.py (DOT parsing on the device,
+METIS export, partition files) included; tests/golden/reference_suite_expected.json
+lists the expected failures (none) and the minimum pass count.
 """
 import hashlib
 import json
@@ -35,21 +34,6 @@ from paper_1502_07451_b200 import costs, graph, graphio, partition, policies, si
 from paper_1502_07451_b200 import *  # noqa: F401,F403
 
 
-class DotParseError(Exception):
-    """Stub: DOT text I/O is out of scope for the B200 hot path."""
-
-
-def _out_of_scope(*_a, **_k):
-    raise NotImplementedError("DOT text I/O is out of scope for the B200 hot path")
-
-
-for _name in ("parse_dot", "emit_dot", "emit_partitioned_dot"):
-    if not hasattr(graphio, _name):
-        setattr(graphio, _name, _out_of_scope)
-if not hasattr(graphio, "DotParseError"):
-    graphio.DotParseError = DotParseError
-if not hasattr(sim, "annotated_dot"):
-    sim.annotated_dot = _out_of_scope
 for _m in ("costs", "graph", "graphio", "partition", "policies", "sim"):
     sys.modules["hetsched." + _m] = getattr(_p, _m)
 __version__ = _p.__version__
@@ -63,7 +47,7 @@ def _sha_list():
 
 def test_reference_suite(tmp_path):
     shas = _sha_list()
-    assert len(shas) == 7
+    assert len(shas) == 8
     work = tmp_path / "ref"
     (work / "tests").mkdir(parents=True)
     (work / "hetsched").mkdir()
