@@ -399,6 +399,19 @@ def cpu_baseline_leg(extra):
                      f"n^{lsum['exponent']:.2f}, extrapolated to 10M tasks (the reference "
                      f"does not finish it: DNF > {CPU_CAP_S:.0f} s)",
            "extrapolation": lsum}
+    if _DOT_SAMPLE is not None:  # parse_dot (oracle port of graphio.py:79-199), one core
+        from oracle import dot_oracle
+        t0 = time.perf_counter()
+        dot_oracle.parse(_DOT_SAMPLE)
+        dt = time.perf_counter() - t0
+        ing = extra.get("cfg2_dot_ingest", {})
+        mbs = len(_DOT_SAMPLE.encode()) / dt / 1e6
+        out["measured_cfg2_dot_ingest"] = {
+            "sample": "first 40000 lines of the config-2 DOT text", "cores": 1,
+            "mb_per_s": mbs,
+            "full_text_s_at_that_rate": ing.get("text_mb", 0.0) / mbs if mbs else None,
+            "gpu_e2e_ms": ing.get("e2e_ms"),
+            "speedup_e2e": (ing["text_mb"] / mbs * 1e3 / ing["e2e_ms"]) if ing else None}
     gpu = extra.get("cfg2_evaluate_2way") if extra else None
     out["measured_cfg2_evaluate"] = {
         "ms": cfg2["seconds"] * 1e3, "cores": 1, "cut": cfg2["cut"], "cpu_w": cfg2["cpu_w"],
@@ -816,6 +829,74 @@ def policy_sweep(iterations: int = 4096):
     return out
 
 
+_DOT_SAMPLE = None  # a bounded prefix of the config-2 DOT text for the CPU leg
+
+
+def cfg2_dot_text(c, kind="MA", size=512) -> str:
+    """emit_dot's format (graphio.py:234-250) for a device CSR: nodes by id,
+    edges by (src, dst), floats as repr."""
+    import numpy as np
+    op, od = c.out_ptr.cpu().numpy(), c.out_dst.cpu().numpy()
+    wc, wg = c.w_cpu.cpu().numpy().tolist(), c.w_gpu.cpu().numpy().tolist()
+    wx, nb = c.w_xfer.cpu().numpy().tolist(), c.bytes.cpu().numpy().tolist()
+    lines = ["digraph cfg2 {"]
+    for i in range(c.n):
+        k, sz = ("SOURCE", 0) if i == c.root else (kind, size)
+        lines.append(f"  n{i} [kind={k}, size={sz}, weight_cpu={wc[i]!r}, weight_gpu={wg[i]!r}];")
+    src, dst = np.repeat(np.arange(c.n), np.diff(op)).tolist(), od.tolist()
+    lines += [f"  n{src[j]} -> n{dst[j]} [bytes={nb[j]}, weight_xfer={wx[j]!r}];"
+              for j in range(c.m)]
+    lines.append("}")
+    return "\n".join(lines) + "\n"
+
+
+def dot_ingest(c2):
+    """the config-2 DAG as DOT text (emit_dot format) ->
+    parse_dot_csr -> device CSR. e2e = host bytes in, device CSR out (H2D copy,
+    hs_dot_parse, hs_dot_csr); device = the same with the text resident in HBM.
+    The CSR must equal the generated DAG's."""
+    import time as _t
+    import torch
+    from paper_1502_07451_b200 import _native
+    from paper_1502_07451_b200.graphio import parse_dot_csr
+    global _DOT_SAMPLE
+    text = cfg2_dot_text(c2)
+    data = text.encode()
+    head = text.split("\n", 40001)
+    _DOT_SAMPLE = "\n".join(head[:40000]) + "\n}\n"
+    del head
+    for _ in range(2):
+        csr = parse_dot_csr(data)
+    torch.cuda.synchronize()
+    reps = 5
+    t0 = _t.perf_counter()
+    for _ in range(reps):
+        csr = parse_dot_csr(data)
+    torch.cuda.synchronize()
+    e2e = (_t.perf_counter() - t0) / reps
+    ok = (csr.n == c2.n and csr.m == c2.m and torch.equal(csr.out_ptr, c2.out_ptr)
+          and torch.equal(csr.out_dst, c2.out_dst) and torch.equal(csr.w_xfer, c2.w_xfer)
+          and torch.equal(csr.w_cpu, c2.w_cpu) and torch.equal(csr.w_gpu, c2.w_gpu)
+          and torch.equal(csr.bytes, c2.bytes))
+    dev_text = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(c2.device)
+    best = None
+    for _ in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        info, h = _native.dot_parse_device(dev_text, len(data))
+        h.csr()
+        b.record()
+        torch.cuda.synchronize()
+        h.close()
+        ms = a.elapsed_time(b)
+        best = ms if best is None else min(best, ms)
+    return {"text_mb": len(data) / 1e6, "lines": text.count("\n"), "nodes": csr.n,
+            "edges": csr.m, "e2e_ms": e2e * 1e3, "e2e_gb_s": len(data) / e2e / 1e9,
+            "device_ms": best, "device_gb_s": len(data) / best / 1e6,
+            "csr_identical_to_generated": ok}
+
+
 def secondary(csr10m, args):
     """Config 2, K7 on config 4, config 5 — reported beside the headline."""
     import torch
@@ -871,6 +952,7 @@ def secondary(csr10m, args):
     out["cfg2_partition_ms"] = ms
     out["cfg2_cut"] = r.cut
     out["cfg2_feasible"] = r.feasible
+    out["cfg2_dot_ingest"] = dot_ingest(c2)
     # the same DAG with integer weights U[1,100] on every edge and vertex
     # (SURVEY §8(d) integer-parity run): per-entry weights, 2-byte counters
     gen_ = torch.Generator(device="cpu").manual_seed(2)

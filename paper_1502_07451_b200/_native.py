@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import warnings
 from typing import Optional, Tuple
 
 import numpy as np
@@ -661,15 +662,20 @@ class DotHandle:
 def dot_parse(data: bytes, device=None) -> Tuple[HsDotInfo, Optional[DotHandle]]:
     """Parse DOT bytes on the device (hs_dot_parse): (info, handle or None)."""
     dev = device or torch.device("cuda", torch.cuda.current_device())
-    host = torch.frombuffer(bytearray(data), dtype=torch.uint8) if data else \
-        torch.empty(0, dtype=torch.uint8)
     text = torch.empty(max(len(data), 1), dtype=torch.uint8, device=dev)
     if data:
-        text[:len(data)].copy_(host.pin_memory() if len(data) > (1 << 20) else host,
-                               non_blocking=False)
+        with warnings.catch_warnings():  # read-only view of the bytes: never written
+            warnings.simplefilter("ignore", UserWarning)
+            host = torch.frombuffer(data, dtype=torch.uint8)
+        text[:len(data)].copy_(host)
+    return dot_parse_device(text, len(data))
+
+
+def dot_parse_device(text: torch.Tensor, nbytes: int) -> Tuple[HsDotInfo, Optional[DotHandle]]:
+    """hs_dot_parse on DOT bytes already in device memory (uint8 tensor)."""
     info = HsDotInfo()
     handle = ctypes.c_void_p()
-    check(_need(_dot_parse, "hs_dot_parse")(ptr(text), len(data), ctypes.byref(info),
+    check(_need(_dot_parse, "hs_dot_parse")(ptr(text), int(nbytes), ctypes.byref(info),
                                             ctypes.byref(handle), stream_ptr()))
     return info, (DotHandle(text, info, handle.value) if handle.value else None)
 

@@ -595,36 +595,79 @@ enum : int {
 };
 
 // ------------------------------------------------------------ kernels -----
-// line terminators of str.splitlines: flag[i] = terminator length at i
-__global__ void mark_terms(const u8 *s, int L, u8 *flag, int32_t *g) {
-  int nl = 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < L;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const u8 c = s[i];
-    u8 f = 0;
-    if (c == '\n') {
-      ++nl;
-      f = (i > 0 && s[i - 1] == '\r') ? 0 : 1;
-    } else if (c == '\r') {
-      f = (i + 1 < L && s[i + 1] == '\n') ? 2 : 1;
-    } else if (c == 0x0b || c == 0x0c || c == 0x1c || c == 0x1d || c == 0x1e) {
-      f = 1;
-    } else if (c == 0xC2) {
-      f = (i + 1 < L && s[i + 1] == 0x85) ? 2 : 0;
-    } else if (c == 0xE2) {
-      f = (i + 2 < L && s[i + 1] == 0x80 && (s[i + 2] == 0xA8 || s[i + 2] == 0xA9)) ? 3 : 0;
-    }
-    flag[i] = f;
-  }
-  for (int off = 16; off; off >>= 1) nl += __shfl_down_sync(0xffffffffu, nl, off);
-  if ((threadIdx.x & 31) == 0 && nl) atomicAdd(g + G_NL, nl);
+// line terminators of str.splitlines: length of the terminator starting at
+// byte i (0: none); \r\n is one terminator
+__device__ __forceinline__ int term_at(const u8 *s, int L, int i, u8 c) {
+  if (c == '\n') return (i > 0 && s[i - 1] == '\r') ? 0 : 1;
+  if (c == '\r') return (i + 1 < L && s[i + 1] == '\n') ? 2 : 1;
+  if (c == 0x0b || c == 0x0c || c == 0x1c || c == 0x1d || c == 0x1e) return 1;
+  if (c == 0xC2) return (i + 1 < L && s[i + 1] == 0x85) ? 2 : 0;
+  if (c == 0xE2) return (i + 2 < L && s[i + 1] == 0x80 && (s[i + 2] == 0xA8 || s[i + 2] == 0xA9)) ? 3 : 0;
+  return 0;
 }
 
+__device__ __forceinline__ bool maybe_term(u8 c) {
+  return c == '\n' || c == '\r' || c == 0x0b || c == 0x0c || (c >= 0x1c && c <= 0x1e) ||
+         c == 0xC2 || c == 0xE2;
+}
+
+constexpr int kChunk = 16;  // bytes per thread (one 16-byte load)
+
+// pass 1: terminators per 16-byte chunk (and the '\n' count); pass 2 writes
+// their positions at the scanned offsets
+template <bool kWrite>
+__global__ void __launch_bounds__(256) terms(const u8 *s, int L, int32_t *cnt, const int32_t *off,
+                                             int32_t *term, int32_t *g) {
+  const int64_t nch = ((int64_t)L + kChunk - 1) / kChunk;
+  int nl = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nch;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i0 = (int)(t * kChunk);
+    u8 b[kChunk];
+    if (i0 + kChunk <= L) {
+      *(uint4 *)b = __ldg((const uint4 *)(s + i0));
+    } else {
+#pragma unroll
+      for (int q = 0; q < kChunk; ++q) b[q] = i0 + q < L ? s[i0 + q] : 0;
+    }
+    // fast reject: no byte <= 0x1e and no U+0085 / U+2028 lead byte in the chunk
+    uint32_t any = 0;
+#pragma unroll
+    for (int q = 0; q < kChunk / 4; ++q) {
+      const uint32_t x = ((const uint32_t *)b)[q];
+      any |= __vcmpleu4(x, 0x1e1e1e1eu) | __vcmpeq4(x, 0xC2C2C2C2u) | __vcmpeq4(x, 0xE2E2E2E2u);
+    }
+    if (!any) {
+      if (!kWrite) cnt[t] = 0;
+      continue;
+    }
+    int c = 0, w = kWrite ? off[t] : 0;
+#pragma unroll
+    for (int q = 0; q < kChunk; ++q) {
+      if (!maybe_term(b[q]) || i0 + q >= L) continue;
+      nl += b[q] == '\n';
+      const int len = term_at(s, L, i0 + q, b[q]);
+      if (len) {
+        if (kWrite) term[w++] = i0 + q;
+        ++c;
+      }
+    }
+    if (!kWrite) cnt[t] = c;
+  }
+  if (!kWrite) {
+    for (int o = 16; o; o >>= 1) nl += __shfl_down_sync(0xffffffffu, nl, o);
+    if ((threadIdx.x & 31) == 0 && nl) atomicAdd(g + G_NL, nl);
+  }
+}
+
+// terminator length at a recorded position
+__device__ __forceinline__ int term_len(const u8 *s, int L, int i) { return term_at(s, L, i, s[i]); }
+
 // per line: '//' cut + strip -> [lb, le); content lines (non-empty, not '#')
-__global__ void line_spans(const u8 *s, int L, const int32_t *term, int nterm, const u8 *flag,
-                           int nlines, int32_t *lb, int32_t *le, u8 *kind, int32_t *g) {
+__global__ void line_spans(const u8 *s, int L, const int32_t *term, int nterm, int nlines,
+                           int32_t *lb, int32_t *le, u8 *kind, int32_t *g) {
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nlines; k += gridDim.x * blockDim.x) {
-    const int b = k == 0 ? 0 : term[k - 1] + flag[term[k - 1]];
+    const int b = k == 0 ? 0 : term[k - 1] + term_len(s, L, term[k - 1]);
     int e = k < nterm ? term[k] : L;
     for (int p = b; p + 1 < e; ++p)
       if (s[p] == '/' && s[p + 1] == '/') {
@@ -830,22 +873,33 @@ __global__ void number_insert(const u8 *s, int U, const int32_t *uniq_occ, const
 }
 
 // ids: numbered names that won their number keep it; flags the rest
+// (warp-uniform trips: the max reduction runs on full warps)
 __global__ void number_assign(int U, const int64_t *num, const uint64_t *key,
                               const uint32_t *first, uint32_t mask, int64_t *id, int32_t *rest,
                               unsigned long long *max_taken, int32_t *g) {
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < U; r += gridDim.x * blockDim.x) {
-    const int64_t v = num[r];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < U; base += stride) {
+    const int64_t r = base + threadIdx.x;
     bool won = false;
-    if (v >= 0) {
-      const uint64_t h = (uint64_t)v + 1;
-      uint32_t slot = (uint32_t)mix64(h) & mask;
-      while (key[slot] != h) slot = (slot + 1) & mask;
-      won = first[slot] == (uint32_t)r;
+    int64_t v = -1;
+    if (r < U) {
+      v = num[r];
+      if (v >= 0) {
+        const uint64_t h = (uint64_t)v + 1;
+        uint32_t slot = (uint32_t)mix64(h) & mask;
+        while (key[slot] != h) slot = (slot + 1) & mask;
+        won = first[slot] == (uint32_t)r;
+      }
+      id[r] = won ? v : -1;
+      rest[r] = !won;
+      if (won && v == 0) g[G_ZERO] = 1;
     }
-    id[r] = won ? v : -1;
-    rest[r] = !won;
-    if (won) atomicMax(max_taken, (unsigned long long)v);
-    if (won && v == 0) g[G_ZERO] = 1;
+    unsigned long long mx = won ? (unsigned long long)v : 0ull;
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+      mx = y > mx ? y : mx;
+    }
+    if ((threadIdx.x & 31) == 0 && mx) atomicMax(max_taken, mx);
   }
 }
 
@@ -987,18 +1041,25 @@ __global__ void csr_invert(int n, const int32_t *order, int32_t *pos) {
 // edge keys (src index << 32 | dst index): declarations, then root -> every
 // name without a predecessor (graphio.py:192-198)
 __global__ void csr_edge_keys(int E, const int32_t *src, const int32_t *dst, const int32_t *pos,
-                              int R, const int32_t *nopred, int root_pos, uint64_t *key,
+                              int R, const int32_t *nopred, int root_pos, int shift, uint64_t *key,
                               int32_t *val) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < E + R; i += gridDim.x * blockDim.x) {
     const uint32_t a = i < E ? pos[src[i]] : root_pos;
     const uint32_t b = i < E ? pos[dst[i]] : pos[nopred[i - E]];
-    key[i] = ((uint64_t)a << 32) | b;
+    key[i] = ((uint64_t)a << shift) | b;
     val[i] = i;
   }
 }
 
 // a later duplicate edge replaces the earlier one (graph.py:66-69): keep the
 // last of every run of equal keys (the sort is stable)
+// 1 if key[] is not non-decreasing (then a stable radix sort is needed;
+// emit_dot's output is already in order)
+__global__ void not_sorted(int n, const uint64_t *key, int32_t *flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i + 1 < n; i += gridDim.x * blockDim.x)
+    if (key[i] > key[i + 1]) *flag = 1;
+}
+
 __global__ void csr_keep_last(int M, const uint64_t *key, u8 *keep) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < M; i += gridDim.x * blockDim.x)
     keep[i] = i + 1 == M || key[i] != key[i + 1];
@@ -1017,16 +1078,16 @@ __global__ void csr_nodes(int n, int U, const uint64_t *skey, const int32_t *ord
   }
 }
 
-__global__ void csr_edges(int m, int E, const uint64_t *key, const int32_t *val,
+__global__ void csr_edges(int m, int E, int shift, const uint64_t *key, const int32_t *val,
                           const int64_t *nbytes, const double *wx, int32_t *out_dst,
                           double *w_xfer, int64_t *bytes, unsigned long long *deg) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
     const uint64_t k = key[j];
     const int t = val[j];
-    out_dst[j] = (int32_t)(k & 0xffffffffu);
+    out_dst[j] = (int32_t)(k & ((1ull << shift) - 1));
     w_xfer[j] = t < E ? wx[t] : 0.0;
     bytes[j] = t < E ? nbytes[t] : 0;
-    atomicAdd(&deg[(k >> 32) + 1], 1ull);
+    atomicAdd(&deg[(k >> shift) + 1], 1ull);
   }
 }
 
@@ -1060,7 +1121,7 @@ struct DotParse {
   int32_t *owner = nullptr;
   int64_t *slow = nullptr;
   // CSR (hs_dot_csr_size)
-  int csr_n = -1, csr_m = 0, csr_root = -1;
+  int csr_n = -1, csr_m = 0, csr_root = -1, csr_shift = 32;
   uint64_t *node_key = nullptr, *edge_key = nullptr;
   int32_t *node_order = nullptr, *edge_val = nullptr;
   template <typename T>
@@ -1119,33 +1180,37 @@ extern "C" int hs_dot_parse(const uint8_t *text, int64_t len, hs_dot_info_t *inf
   if (cudaMemcpyAsync(g, g0, sizeof g0, cudaMemcpyHostToDevice, s)) return fail(HS_ECUDA);
 
   // 1. line terminators
-  u8 *flag;
-  int32_t *term, *nterm_d;
-  if (P->alloc(&flag, L) || P->alloc(&term, L) || P->alloc(&nterm_d, 1)) return fail(HS_ECUDA);
+  const int64_t nch = ((int64_t)L + kChunk - 1) / kChunk;
+  int32_t *tcnt, *toff, *term = nullptr;
+  if (P->alloc(&tcnt, nch + 1) || P->alloc(&toff, nch + 1)) return fail(HS_ECUDA);
   int nterm = 0, nlines = 0;
   if (L > 0) {
-    mark_terms<<<hs::grid_for(L, B), B, 0, s>>>(text, L, flag, g);
+    const int tg = hs::grid_for(nch, B);
+    terms<false><<<tg, B, 0, s>>>(text, L, tcnt, nullptr, nullptr, g);
     hs::count_launch();
-    size_t tb = 0;
-    thrust::counting_iterator<int32_t> it(0);
-    if (cub::DeviceSelect::Flagged(nullptr, tb, it, flag, term, nterm_d, L, s)) return fail(HS_ECUDA);
-    {
-      hs::Scratch<char> tmp;
-      if (tmp.alloc(tb, s)) return fail(HS_ECUDA);
-      if (cub::DeviceSelect::Flagged(tmp.p, tb, it, flag, term, nterm_d, L, s)) return fail(HS_ECUDA);
-      hs::count_launch();
-    }
-    if (cudaMemcpyAsync(&nterm, nterm_d, 4, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+    if (cudaMemsetAsync(tcnt + nch, 0, 4, s)) return fail(HS_ECUDA);
+    if (exscan(tcnt, toff, nch + 1, s)) return fail(HS_ECUDA);
+    if (cudaMemcpyAsync(&nterm, toff + nch, 4, cudaMemcpyDeviceToHost, s) ||
+        cudaStreamSynchronize(s))
       return fail(HS_ECUDA);
+    if (P->alloc(&term, (size_t)nterm + 1)) return fail(HS_ECUDA);
+    terms<true><<<tg, B, 0, s>>>(text, L, nullptr, toff, term, g);
+    hs::count_launch();
     int last_end = 0;
     if (nterm > 0) {
       int32_t t = 0;
-      u8 f = 0;
+      u8 tail[3] = {0, 0, 0};
       if (cudaMemcpyAsync(&t, term + nterm - 1, 4, cudaMemcpyDeviceToHost, s) ||
           cudaStreamSynchronize(s) ||
-          cudaMemcpyAsync(&f, flag + t, 1, cudaMemcpyDeviceToHost, s) || cudaStreamSynchronize(s))
+          cudaMemcpyAsync(tail, text + t, L - t < 3 ? L - t : 3, cudaMemcpyDeviceToHost, s) ||
+          cudaStreamSynchronize(s))
         return fail(HS_ECUDA);
-      last_end = t + f;
+      // the last terminator's length (\r\n, U+0085 and U+2028/9 are longer)
+      int len = 1;
+      if (tail[0] == '\r' && L - t > 1 && tail[1] == '\n') len = 2;
+      if (tail[0] == 0xC2) len = 2;
+      if (tail[0] == 0xE2) len = 3;
+      last_end = t + len;
     }
     nlines = nterm + (last_end < L ? 1 : 0);
   }
@@ -1160,7 +1225,7 @@ extern "C" int hs_dot_parse(const uint8_t *text, int64_t len, hs_dot_info_t *inf
     return fail(HS_ECUDA);
   if (nlines > 0) {
     const int lg = hs::grid_for(nlines, B);
-    line_spans<<<lg, B, 0, s>>>(text, L, term, nterm, flag, nlines, lb, le, kind, g);
+    line_spans<<<lg, B, 0, s>>>(text, L, term, nterm, nlines, lb, le, kind, g);
     header<<<1, 1, 0, s>>>(text, lb, le, kind, g);
     find_close<<<lg, B, 0, s>>>(text, lb, le, kind, nlines, g);
     count_lines<<<lg, B, 0, s>>>(text, lb, le, kind, nlines, g, cnt, err);
@@ -1359,18 +1424,41 @@ struct NoPred {
   __host__ __device__ bool operator()(int r) const { return !hp[r]; }
 };
 
-template <typename K, typename V>
-int sort_pairs(const K *kin, K *kout, const V *vin, V *vout, int n, cudaStream_t s) {
+// stable sort of (key, value) pairs over key bits [0, bits); keys already in
+// order are copied instead
+int sort_pairs(const uint64_t *kin, uint64_t *kout, const int32_t *vin, int32_t *vout, int n,
+               int bits, cudaStream_t s) {
   if (n <= 0) return HS_OK;
+  hs::Scratch<int32_t> flag;
+  HS_CHECK_CUDA(flag.alloc(1, s));
+  HS_CHECK_CUDA(cudaMemsetAsync(flag.p, 0, 4, s));
+  not_sorted<<<hs::grid_for(n, 256), 256, 0, s>>>(n, kin, flag.p);
+  HS_CHECK_LAUNCH();
+  int32_t unsorted = 0;
+  HS_CHECK_CUDA(cudaMemcpyAsync(&unsorted, flag.p, 4, cudaMemcpyDeviceToHost, s));
+  HS_CHECK_CUDA(cudaStreamSynchronize(s));
+  if (!unsorted) {
+    HS_CHECK_CUDA(cudaMemcpyAsync(kout, kin, 8ull * n, cudaMemcpyDeviceToDevice, s));
+    HS_CHECK_CUDA(cudaMemcpyAsync(vout, vin, 4ull * n, cudaMemcpyDeviceToDevice, s));
+    return HS_OK;
+  }
+  bits = bits < 1 ? 1 : (bits > 64 ? 64 : bits);
   size_t tb = 0;
-  HS_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0,
-                                                (int)sizeof(K) * 8, s));
+  HS_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, kin, kout, vin, vout, n, 0, bits, s));
   hs::Scratch<char> tmp;
   HS_CHECK_CUDA(tmp.alloc(tb, s));
-  HS_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, kin, kout, vin, vout, n, 0,
-                                                (int)sizeof(K) * 8, s));
+  HS_CHECK_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tb, kin, kout, vin, vout, n, 0, bits, s));
   hs::count_launch(4);
   return HS_OK;
+}
+
+int bit_width(uint64_t x) {
+  int b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
 }
 }  // namespace
 
@@ -1435,7 +1523,8 @@ extern "C" int hs_dot_csr_size(void *handle, int64_t *n_out, int64_t *m_out, voi
     csr_node_keys<<<hs::grid_for(n, B), B, 0, s>>>(U, P->id, root_id, synth, nk.p, nv.p);
     HS_CHECK_LAUNCH();
   }
-  int rc = sort_pairs(nk.p, P->node_key, nv.p, P->node_order, n, s);
+  const int64_t top_id = root_id > P->max_id ? root_id : P->max_id;
+  int rc = sort_pairs(nk.p, P->node_key, nv.p, P->node_order, n, bit_width((uint64_t)top_id), s);
   if (rc) return rc;
   if (n > 0) {
     csr_invert<<<hs::grid_for(n, B), B, 0, s>>>(n, P->node_order, pos.p);
@@ -1464,6 +1553,7 @@ extern "C" int hs_dot_csr_size(void *handle, int64_t *n_out, int64_t *m_out, voi
   }
   HS_CHECK_CUDA(cudaStreamSynchronize(s));
   const int M = E + R;
+  P->csr_shift = bit_width((uint64_t)(n > 1 ? n - 1 : 1));
   hs::Scratch<uint64_t> ek, eks;
   hs::Scratch<int32_t> ev, evs;
   hs::Scratch<u8> keep;
@@ -1474,10 +1564,10 @@ extern "C" int hs_dot_csr_size(void *handle, int64_t *n_out, int64_t *m_out, voi
   HS_CHECK_CUDA(keep.alloc(M, s));
   if (M > 0) {
     csr_edge_keys<<<hs::grid_for(M, B), B, 0, s>>>(E, P->src, P->dst, pos.p, R, nopred.p,
-                                                   root_pos, ek.p, ev.p);
+                                                   root_pos, P->csr_shift, ek.p, ev.p);
     HS_CHECK_LAUNCH();
   }
-  rc = sort_pairs(ek.p, eks.p, ev.p, evs.p, M, s);
+  rc = sort_pairs(ek.p, eks.p, ev.p, evs.p, M, 2 * P->csr_shift, s);
   if (rc) return rc;
   int m = 0;
   if (M > 0) {
@@ -1526,7 +1616,8 @@ extern "C" int hs_dot_csr(void *handle, int64_t *out_ptr, int32_t *out_dst, int6
                                                  P->wg, ids, w_cpu, w_gpu, out_ptr);
   HS_CHECK_LAUNCH();
   if (m > 0) {
-    csr_edges<<<hs::grid_for(m, B), B, 0, s>>>(m, P->E, P->edge_key, P->edge_val, P->nbytes,
+    csr_edges<<<hs::grid_for(m, B), B, 0, s>>>(m, P->E, P->csr_shift, P->edge_key, P->edge_val,
+                                               P->nbytes,
                                                P->wx, out_dst, w_xfer, bytes,
                                                (unsigned long long *)out_ptr);
     HS_CHECK_LAUNCH();
