@@ -365,37 +365,95 @@ def compare(policy_names: Sequence[str], graph_factory: Callable[[int], TaskGrap
     return rows
 
 
-def _compare_generated(policy_names, factory, machine, iterations, seed) -> List[CompareRow]:
-    """compare() over a generator factory (gen.RandomDagFactory): every
-    iteration's graph built on the device at once (csrc/rgen.cu, identical to
-    the factory's own graphs), gp pins from one batched partition launch, one
-    DES launch per policy. Same rows as the object path."""
+def _generated_results(policy_names, factory, machine, seeds) -> dict:
+    """Per-iteration (makespan, transfers, transfer bytes) of every policy over
+    the factory's graphs for `seeds`, built and simulated on the device."""
     from .policies import DMDA_ID, EAGER_ID, GP_ID, POLICY_NAMES, gp_pins_batch
     ids = {"eager": EAGER_ID, "dmda": DMDA_ID, "gp": GP_ID}
     for name in policy_names:
         if name not in ids:  # build_policy's error (policies.py:111-120)
             raise ValueError(f"unknown policy {name!r}; expected one of {POLICY_NAMES}")
-    batch = factory.batch([seed + i for i in range(iterations)])
-    rows: List[CompareRow] = []
+    out = {}
+    if not len(seeds):
+        return {name: (np.zeros(0), np.zeros(0), np.zeros(0)) for name in policy_names}
+    batch = factory.batch(list(seeds))
     for name in policy_names:
         pin = gp_pins_batch(batch) if name == "gp" else None
-        out = _native.simulate_batch(batch, ids[name], pin, machine.cpu_workers,
+        res = _native.simulate_batch(batch, ids[name], pin, machine.cpu_workers,
                                      machine.gpu_workers, events=False)
-        h = {k: v.cpu().numpy() for k, v in out.items()}
+        h = {k: v.cpu().numpy() for k, v in res.items()}
         if (h["status"] != 0).any():
             raise AssertionError("simulation deadlocked on a valid DAG (bug)")
-        makespans = [float(x) for x in h["makespan"]]
-        transfers = [float(x) for x in h["transfer_count"]]
-        t_bytes = [float(x) for x in h["transfer_bytes"]]
-        rows.append(CompareRow(
-            policy=name,
-            mean_makespan=statistics.fmean(makespans),
-            sd_makespan=statistics.stdev(makespans) if len(makespans) > 1 else 0.0,
-            mean_transfers=statistics.fmean(transfers),
-            sd_transfers=statistics.stdev(transfers) if len(transfers) > 1 else 0.0,
-            mean_transfer_bytes=statistics.fmean(t_bytes),
-        ))
+        out[name] = (h["makespan"].astype(np.float64), h["transfer_count"].astype(np.float64),
+                     h["transfer_bytes"].astype(np.float64))
+    return out
+
+
+def _row(name, makespans, transfers, t_bytes) -> CompareRow:
+    """sim.py:296-306: fmean / stdev over the iterations in seed order."""
+    makespans, transfers, t_bytes = ([float(x) for x in a] for a in (makespans, transfers, t_bytes))
+    return CompareRow(
+        policy=name,
+        mean_makespan=statistics.fmean(makespans),
+        sd_makespan=statistics.stdev(makespans) if len(makespans) > 1 else 0.0,
+        mean_transfers=statistics.fmean(transfers),
+        sd_transfers=statistics.stdev(transfers) if len(transfers) > 1 else 0.0,
+        mean_transfer_bytes=statistics.fmean(t_bytes),
+    )
+
+
+def _compare_generated(policy_names, factory, machine, iterations, seed) -> List[CompareRow]:
+    """compare() over a generator factory (gen.RandomDagFactory): every
+    iteration's graph built on the device at once (csrc/rgen.cu, identical to
+    the factory's own graphs), gp pins from one batched partition launch, one
+    DES launch per policy. Same rows as the object path."""
+    res = _generated_results(policy_names, factory, machine, [seed + i for i in range(iterations)])
+    return [_row(name, *res[name]) for name in policy_names]
+
+
+def iteration_split(iterations: int, world: int, rank: int) -> range:
+    """The iterations rank `rank` simulates: contiguous, sizes differing by at most one."""
+    q, r = divmod(iterations, world)
+    lo = rank * q + min(rank, r)
+    return range(lo, lo + q + (1 if rank < r else 0))
+
+
+def gather_rows(policy_names, local: dict, group=None) -> List[CompareRow]:
+    """Every rank's per-iteration results (its iteration_split share) gathered in
+    iteration order, then the reference's rows: identical on every rank and to
+    one device running all iterations."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world > 1:
+        parts = [None] * world
+        dist.all_gather_object(parts, {k: tuple(np.asarray(a) for a in v) for k, v in local.items()},
+                               group=group)
+    else:
+        parts = [local]
+    rows = []
+    for name in policy_names:
+        cols = [np.concatenate([p[name][c] for p in parts]) for c in range(3)]
+        rows.append(_row(name, *cols))
     return rows
+
+
+def compare_distributed(policy_names: Sequence[str], factory, machine: Optional[MachineModel] = None,
+                        iterations: int = 1, seed: int = 0, group=None) -> List[CompareRow]:
+    """compare() over a gen.RandomDagFactory with the iterations split across the
+    ranks of torch.distributed (independent simulations, no
+    inter-GPU traffic on the critical path): rank r generates and simulates its
+    contiguous share of the seeds on its own GPU, then the small per-iteration
+    arrays are all-gathered in seed order. Every rank returns the rows compare()
+    returns on one GPU, bit for bit. Without a process group it is compare()."""
+    import torch.distributed as dist
+    if iterations < 1:
+        raise SimulationError("iterations must be >= 1")
+    machine = machine or MachineModel()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    mine = iteration_split(iterations, world, rank)
+    local = _generated_results(policy_names, factory, machine, [seed + i for i in mine])
+    return gather_rows(policy_names, local, group)
 
 
 def compare_csv(rows: Sequence[CompareRow]) -> str:

@@ -149,3 +149,50 @@ def test_split_bounds_edge_cases():
     assert [e - a for a, e in b] == [1, 1, 1, 1]
     with pytest.raises(ValueError):
         split_bounds(cs, 5)
+
+
+def _compare_arrays(iterations):
+    rng = np.random.default_rng(9)
+    return {name: (rng.uniform(10, 40, iterations), rng.integers(0, 30, iterations).astype(float),
+                   rng.integers(0, 10 ** 9, iterations).astype(float))
+            for name in ("eager", "dmda", "gp")}
+
+
+def _compare_worker(rank, world, port, iterations, q):
+    """sim.compare_distributed's host half: each rank holds the per-iteration
+    results of its iteration_split share; gather_rows must give every rank the
+    rows of all iterations in seed order."""
+    from paper_1502_07451_b200.sim import gather_rows, iteration_split
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    full = _compare_arrays(iterations)
+    mine = iteration_split(iterations, world, rank)
+    local = {k: tuple(a[mine.start:mine.stop] for a in v) for k, v in full.items()}
+    rows = gather_rows(["eager", "dmda", "gp"], local)
+    q.put((rank, [vars(r) for r in rows], (mine.start, mine.stop)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("iterations", [4096, 1001, 1])
+def test_two_rank_compare_rows_match_one_device(iterations):
+    from paper_1502_07451_b200.sim import _row
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_compare_worker, args=(r, 2, port, iterations, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    full = _compare_arrays(iterations)
+    want = [vars(_row(k, *full[k])) for k in ("eager", "dmda", "gp")]
+    spans = sorted(g[2] for g in got)
+    assert spans[0][0] == 0 and spans[-1][1] == iterations and spans[0][1] == spans[1][0]
+    for _, rows, _ in got:
+        assert rows == want  # bit-identical on every rank
