@@ -558,8 +558,8 @@ int hs_ipc_close(void *dev_ptr);
  *   weight_cpu, 2 weight_gpu}, then 3 * n_names + 2 * edge + {0 bytes,
  *   1 weight_xfer}; kind 1 ValueError, 2 int(inf), 3 int(nan)), -1 if none;
  *   info->n_slow literals listed as (order, attribute) for the caller to
- *   convert: > 19 significant digits whose rounding the Eisel-Lemire bounds
- *   leave open, and int(float()) values beyond int64 (Python ints).
+ *   convert: int(float()) values beyond int64 (Python ints) and exponents
+ *   beyond +-100000 with more than 19 significant digits.
  * hs_dot_fetch copies the parse to caller HOST arrays (any may be NULL);
  * hs_dot_csr_size / hs_dot_csr build the device CSR of the graph TaskGraph
  * would hold (ids ascending, edges by (src, dst), a later duplicate edge
@@ -590,7 +590,7 @@ int hs_dot_csr(void *handle, int64_t *out_ptr, int32_t *out_dst, int64_t *ids, d
                double *w_gpu, double *w_xfer, int64_t *bytes, int32_t *root_host, void *stream);
 int hs_dot_release(void *handle);
 /* Python float(bytes) with the device's conversion, on the host (tests):
- * 0 ok, 1 ValueError, 2 undecided (> 19 digits) */
+ * 0 ok, 1 ValueError, 2 undecided (exponent beyond +-100000) */
 int hs_dot_py_float(const uint8_t *bytes, int64_t len, double *out);
 
 #ifdef __cplusplus

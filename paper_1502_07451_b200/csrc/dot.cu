@@ -19,8 +19,10 @@
 //     (first appearance wins), the rest count up from max + 1;
 //  6. attributes (graphio.py:160-183): last value per known key, Python
 //     float() on the device (Eisel-Lemire with the published 128-bit powers of
-//     five, exact for <= 19 significant digits; longer literals whose two
-//     bounds disagree are listed for the host), int(float()) for size/bytes.
+//     five, exact for <= 19 significant digits; a longer literal whose two
+//     bounds disagree is decided by a big-integer comparison with the
+//     midpoint), int(float()) for size/bytes (values beyond int64 — Python
+//     ints — are listed for the host).
 //
 // The caller gets counts and the first error from hs_dot_parse, then copies
 // the per-name / per-edge / per-attribute arrays with hs_dot_fetch, or builds
@@ -245,6 +247,129 @@ __host__ __device__ inline bool ieq(const u8 *s, int b, int e, const char *lit) 
   return b + i == e;
 }
 
+// Exact decision for a literal whose 19-digit bounds round differently: the
+// full significand (up to kMaxDigits digits, a nonzero tail kept as a sticky
+// bit) against the halfway point between the two candidates, in big integers
+// (the "digit comparison" fallback of the Eisel-Lemire literature).
+constexpr int kLimbs = 100;       // 3200 bits
+constexpr int kMaxDigits = 800;   // > 767, the most a binary64 midpoint needs
+
+struct Big {
+  uint32_t v[kLimbs];
+  int n;  // used limbs
+  __host__ __device__ void set(uint64_t x) {
+    n = 0;
+    while (x) {
+      v[n++] = (uint32_t)x;
+      x >>= 32;
+    }
+  }
+  __host__ __device__ void mul_add(uint32_t m, uint32_t a) {
+    uint64_t c = a;
+    for (int i = 0; i < n; ++i) {
+      const uint64_t t = (uint64_t)v[i] * m + c;
+      v[i] = (uint32_t)t;
+      c = t >> 32;
+    }
+    if (c && n < kLimbs) v[n++] = (uint32_t)c;
+  }
+  __host__ __device__ void mul_pow5(int k) {
+    while (k >= 13) {
+      mul_add(1220703125u, 0);  // 5^13
+      k -= 13;
+    }
+    uint32_t m = 1;
+    while (k-- > 0) m *= 5;
+    if (m > 1) mul_add(m, 0);
+  }
+  __host__ __device__ void shl(int bits) {
+    if (n == 0 || bits <= 0) return;
+    const int w = bits / 32, b = bits % 32;
+    int nn = n + w + 1;
+    if (nn > kLimbs) nn = kLimbs;
+    for (int i = nn - 1; i >= 0; --i) {
+      const int s0 = i - w;
+      uint32_t hi = s0 >= 0 && s0 < n ? v[s0] : 0;
+      uint32_t lo = s0 - 1 >= 0 && s0 - 1 < n ? v[s0 - 1] : 0;
+      v[i] = b ? (hi << b) | (lo >> (32 - b)) : hi;
+    }
+    n = nn;
+    while (n > 0 && v[n - 1] == 0) --n;
+  }
+};
+
+__host__ __device__ int big_cmp(const Big &a, const Big &b) {
+  if (a.n != b.n) return a.n < b.n ? -1 : 1;
+  for (int i = a.n - 1; i >= 0; --i)
+    if (a.v[i] != b.v[i]) return a.v[i] < b.v[i] ? -1 : 1;
+  return 0;
+}
+
+// bits of the correctly rounded binary64 of the decimal literal [b, e)
+// (already validated: digits, '.', '_', exponent), given the lower candidate
+__host__ __device__ uint64_t round_exact(const u8 *s, int b, int e, uint64_t lo_bits) {
+  Big D, H;
+  D.n = 0;
+  int nd = 0;
+  bool sticky = false;
+  int64_t e10 = 0, ex = 0;
+  bool frac = false, exp = false, eneg = false;
+  for (int p = b; p < e; ++p) {
+    const u8 c = s[p];
+    if (c == '_') continue;
+    if (exp) {
+      if (c == '-') eneg = true;
+      else if (c >= '0' && c <= '9' && ex < 100000000000ll) ex = ex * 10 + (c - '0');
+      continue;
+    }
+    if (c == '.') {
+      frac = true;
+      continue;
+    }
+    if (c == 'e' || c == 'E') {
+      exp = true;
+      continue;
+    }
+    if (c < '0' || c > '9') continue;  // sign
+    const int d = c - '0';
+    if (nd == 0 && d == 0) {
+      if (frac) --e10;
+      continue;
+    }
+    if (nd < kMaxDigits) {
+      D.mul_add(10, d);
+      ++nd;
+      if (frac) --e10;
+    } else {
+      sticky |= d != 0;
+      if (!frac) ++e10;
+    }
+  }
+  int64_t E = e10 + (eneg ? -ex : ex);
+  // halfway point above the lower candidate: (2 m1 + 1) 2^(e1 - 1)
+  const uint64_t f = lo_bits & ((1ull << 52) - 1);
+  const int be = (int)(lo_bits >> 52);
+  const uint64_t m1 = be ? (f | (1ull << 52)) : f;
+  const int e1 = be ? be - 1075 : -1074;
+  H.set(2 * m1 + 1);
+  // D 10^E  vs  H 2^(e1 - 1)
+  if (E >= 0) {
+    D.mul_pow5((int)E);
+    const int64_t k = E - (e1 - 1);
+    if (k >= 0) D.shl((int)k);
+    else H.shl((int)-k);
+  } else {
+    H.mul_pow5((int)-E);
+    const int64_t t = (int64_t)e1 - 1 - E;
+    if (t >= 0) H.shl((int)t);
+    else D.shl((int)-t);
+  }
+  int c = big_cmp(D, H);
+  if (c == 0 && sticky) c = 1;
+  if (c > 0 || (c == 0 && (m1 & 1))) return lo_bits + 1;
+  return lo_bits;
+}
+
 enum : int { kFloatOk = 0, kFloatBad = 1, kFloatSlow = 2 };
 
 // Python float(str) on the canonical bytes of [b, e): surrounding Unicode
@@ -334,7 +459,10 @@ __host__ __device__ int py_float(const u8 *raw, int rb, int re, double *out) {
     if (w != 0) {
       const int64_t q = e10 < -100000 ? -100000 : (e10 > 100000 ? 100000 : e10);
       bits = eisel_lemire(q, w);
-      if (trunc && eisel_lemire(q, w + 1) != bits) return kFloatSlow;
+      if (trunc && eisel_lemire(q, w + 1) != bits) {
+        if (e10 < -100000 || e10 > 100000) return kFloatSlow;  // absurd exponents
+        bits = round_exact(s, b, e, bits);
+      }
     }
     v = bits_double(bits);
   }

@@ -183,8 +183,8 @@ def _dot_device(text: str):
 
 
 def _dot_values(t: _DotText, info, a: dict) -> List[Tuple[int, object]]:
-    """Literals the device left open (> 19 digits) and the first conversion
-    failure, in the reference's evaluation order (graphio.py:160-183): the
+    """Values the device left to CPython (int(float()) beyond int64) and the
+    first conversion failure, in the reference's evaluation order (graphio.py:160-183): the
     failing literal is re-evaluated here so the exception is Python's own."""
     U = info.n_names
     fail = info.conv_err >> 3 if info.conv_err >= 0 else None
@@ -293,8 +293,7 @@ def parse_dot_csr(text, device=None) -> DagCSR:
     device (``hs_dot_csr``): node ids ascending (``.ids``), edges by (src, dst)
     with a later duplicate winning, the synthesized root and its edges. For
     texts whose node count makes the object model impractical (config 2/4).
-    Weight literals the device left to CPython (> 19 significant digits) are
-    patched into the CSR; byte counts beyond int64 have no CSR form."""
+    Byte counts beyond int64 (Python ints) have no CSR form."""
     data = text if isinstance(text, (bytes, bytearray)) else text.encode("utf-8", "surrogatepass")
     info, h = _native.dot_parse(bytes(data), device)
     t = _DotText(bytes(data))

@@ -55,8 +55,7 @@ def _py_float_cases(n, seed):
 
 def test_device_float_restatement_matches_cpython():
     """hs_dot_py_float is the device's conversion compiled for the host: every
-    literal of <= 19 significant digits converts bit-exactly or is rejected as
-    float() rejects it."""
+    literal converts bit-exactly or is rejected as float() rejects it."""
     from paper_1502_07451_b200 import _native as N
     for s in _py_float_cases(20000, 7):
         st, v = N.dot_py_float(s.encode())
@@ -65,9 +64,48 @@ def test_device_float_restatement_matches_cpython():
         except ValueError:
             assert st == 1, s
             continue
-        if st == 2:  # undecided: only literals beyond 19 significant digits
-            mant = s.strip().lstrip("+-").lower().split("e")[0].replace("_", "")
-            assert len(mant.replace(".", "").lstrip("0")) > 19, s
-            continue
         assert st == 0, s
         assert struct.pack("<d", v) == struct.pack("<d", ref) or (v != v and ref != ref), s
+
+
+def _halfway_literals(n, seed):
+    """Decimal literals at and around the exact midpoint of two adjacent doubles,
+    written with 20 to 800 significant digits (the big-integer path)."""
+    import math
+    from decimal import Decimal, getcontext
+    getcontext().prec = 1200
+    rng = random.Random(seed)
+    out = []
+    for _ in range(n):
+        k = rng.random()
+        if k < 0.1:
+            x = struct.unpack("<d", struct.pack("<Q", rng.getrandbits(52)))[0]  # subnormal
+        else:
+            x = abs(struct.unpack("<d", struct.pack("<Q", rng.getrandbits(63)))[0])
+        if not math.isfinite(x):
+            continue
+        y = math.nextafter(x, math.inf)
+        if not math.isfinite(y):
+            continue
+        mid = (Decimal(x) + Decimal(y)) / 2
+        txt = format(mid, "f") if rng.random() < 0.5 else format(mid, "e")
+        out.append(txt)
+        sig = "".join(c for c in format(mid, "e").split("e")[0] if c.isdigit())
+        ex = int(format(mid, "e").split("e")[1])
+        for nd in (20, 25, 40, len(sig)):
+            if nd <= len(sig):
+                t = sig[:nd]
+                out.append(f"{t[0]}.{t[1:]}e{ex}")
+                out.append(f"{t[0]}.{t[1:]}1e{ex}")  # just above a truncated midpoint
+    return out
+
+
+def test_device_float_long_literals_exact():
+    """> 19 significant digits (midpoints of adjacent doubles and their
+    neighbours): the big-integer comparison rounds like CPython."""
+    from paper_1502_07451_b200 import _native as N
+    for s in _halfway_literals(400, 3):
+        st, v = N.dot_py_float(s.encode())
+        ref = float(s)
+        assert st == 0, s
+        assert struct.pack("<d", v) == struct.pack("<d", ref), (s[:80], v, ref)

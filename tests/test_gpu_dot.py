@@ -149,14 +149,17 @@ def test_parse_dot_csr_large_roundtrip():
     assert csr.validate() == []
 
 
-def test_slow_literal_finished_on_host():
-    """> 19 significant digits whose two Eisel-Lemire bounds differ: listed by the
-    device, converted by CPython's float() (graphio.py:166-169)."""
+def test_long_literals_exact_on_device():
+    """> 19 significant digits whose two Eisel-Lemire bounds differ are decided
+    on the device (big-integer midpoint comparison); only int(float()) values
+    beyond int64 (Python ints) go to the host."""
     from paper_1502_07451_b200 import _native
     from paper_1502_07451_b200.graphio import parse_dot
     lit = "1.00000000000000011102230246251565404236316680908203125"
-    info, h = _native.dot_parse(f"digraph g {{ a [weight_cpu={lit}]; }}".encode())
-    assert info.status == 0 and info.n_slow == 1
+    text = f"digraph g {{ a [weight_cpu={lit}]; a -> b [bytes=1e20]; }}"
+    info, h = _native.dot_parse(text.encode())
+    assert info.status == 0 and info.n_slow == 1  # only the bytes value
     h.close()
-    g = parse_dot(f"digraph g {{ a [weight_cpu={lit}]; }}")
+    g = parse_dot(text)
     assert g.nodes[1].weight_cpu == float(lit)
+    assert g.edges[(1, 2)].bytes == 10 ** 20
