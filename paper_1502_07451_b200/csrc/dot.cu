@@ -734,11 +734,6 @@ __device__ __forceinline__ int term_at(const u8 *s, int L, int i, u8 c) {
   return 0;
 }
 
-__device__ __forceinline__ bool maybe_term(u8 c) {
-  return c == '\n' || c == '\r' || c == 0x0b || c == 0x0c || (c >= 0x1c && c <= 0x1e) ||
-         c == 0xC2 || c == 0xE2;
-}
-
 constexpr int kChunk = 16;  // bytes per thread (one 16-byte load)
 
 // pass 1: terminators per 16-byte chunk (and the '\n' count); pass 2 writes
@@ -751,31 +746,36 @@ __global__ void __launch_bounds__(256) terms(const u8 *s, int L, int32_t *cnt, c
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nch;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int i0 = (int)(t * kChunk);
-    u8 b[kChunk];
+    uint32_t x[4];
     if (i0 + kChunk <= L) {
-      *(uint4 *)b = __ldg((const uint4 *)(s + i0));
+      const uint4 v = __ldg((const uint4 *)(s + i0));
+      x[0] = v.x, x[1] = v.y, x[2] = v.z, x[3] = v.w;
     } else {
 #pragma unroll
-      for (int q = 0; q < kChunk; ++q) b[q] = i0 + q < L ? s[i0 + q] : 0;
-    }
-    // fast reject: no byte <= 0x1e and no U+0085 / U+2028 lead byte in the chunk
-    uint32_t any = 0;
+      for (int q = 0; q < 4; ++q) x[q] = 0;
 #pragma unroll
-    for (int q = 0; q < kChunk / 4; ++q) {
-      const uint32_t x = ((const uint32_t *)b)[q];
-      any |= __vcmpleu4(x, 0x1e1e1e1eu) | __vcmpeq4(x, 0xC2C2C2C2u) | __vcmpeq4(x, 0xE2E2E2E2u);
+      for (int q = 0; q < kChunk; ++q)
+        if (i0 + q < L) x[q >> 2] |= (uint32_t)s[i0 + q] << (8 * (q & 3));
     }
-    if (!any) {
-      if (!kWrite) cnt[t] = 0;
-      continue;
+    // candidate bytes (<= 0x1e, or a U+0085 / U+2028/9 lead byte) as a 16-bit
+    // mask: the loop below runs once per candidate, not once per byte
+    uint32_t mask = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t hit = __vcmpleu4(x[q], 0x1e1e1e1eu) | __vcmpeq4(x[q], 0xC2C2C2C2u) |
+                           __vcmpeq4(x[q], 0xE2E2E2E2u);
+      const uint32_t y = (hit >> 7) & 0x01010101u;
+      mask |= (((y * 0x01020408u) >> 24) & 0xFu) << (4 * q);
     }
+    if (L - i0 < kChunk) mask &= (1u << (L - i0)) - 1;
     int c = 0, w = kWrite ? off[t] : 0;
-#pragma unroll
-    for (int q = 0; q < kChunk; ++q) {
-      if (!maybe_term(b[q]) || i0 + q >= L) continue;
-      nl += b[q] == '\n';
-      const int len = term_at(s, L, i0 + q, b[q]);
-      if (len) {
+    while (mask) {
+      const int q = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint32_t word = q < 4 ? x[0] : (q < 8 ? x[1] : (q < 12 ? x[2] : x[3]));
+      const u8 ch = (u8)(word >> (8 * (q & 3)));
+      nl += ch == '\n';
+      if (term_at(s, L, i0 + q, ch)) {
         if (kWrite) term[w++] = i0 + q;
         ++c;
       }
@@ -797,11 +797,22 @@ __global__ void line_spans(const u8 *s, int L, const int32_t *term, int nterm, i
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nlines; k += gridDim.x * blockDim.x) {
     const int b = k == 0 ? 0 : term[k - 1] + term_len(s, L, term[k - 1]);
     int e = k < nterm ? term[k] : L;
-    for (int p = b; p + 1 < e; ++p)
-      if (s[p] == '/' && s[p + 1] == '/') {
+    // first "//": 16-byte aligned windows, byte scan only where a '/' shows up
+    // (the text is 16-byte aligned, so a window never crosses its end)
+    for (int w0 = b & ~15; w0 < e - 1; w0 += 16) {
+      const uint4 v = w0 + 16 <= L ? __ldg((const uint4 *)(s + w0)) : make_uint4(~0u, ~0u, ~0u, ~0u);
+      const uint32_t hit = __vcmpeq4(v.x, 0x2f2f2f2fu) | __vcmpeq4(v.y, 0x2f2f2f2fu) |
+                           __vcmpeq4(v.z, 0x2f2f2f2fu) | __vcmpeq4(v.w, 0x2f2f2f2fu);
+      if (!hit && w0 + 16 <= L) continue;
+      int p = w0 > b ? w0 : b;
+      const int pe = w0 + 16 < e - 1 ? w0 + 16 : e - 1;
+      for (; p < pe; ++p)
+        if (s[p] == '/' && s[p + 1] == '/') break;
+      if (p < pe) {
         e = p;
         break;
       }
+    }
     const int x = skip_ws(s, b, e), y = rskip_ws(s, x, e);
     lb[k] = x;
     le[k] = y;
