@@ -1,7 +1,8 @@
 """Small invocations of every hot-path kernel family for compute-sanitizer
 (memcheck / racecheck / synccheck): k-way (CTA FM levels and Jet levels),
 K1/K2/K7 (dataflow and frontier), device topological order, validation,
-weights, DES with trace products, batched generator, exact 2-way FM."""
+weights, DES with trace products, batched generator, exact 2-way FM, DOT
+ingestion (every golden text plus the device CSR of the emitted graphs)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -34,5 +35,19 @@ print("heuristic", H.partition_heuristic(g, H.workload_ratio(g)).edge_cut)
 b = gen.generate_random_dag_batch(38, 75, "MA", 1024, range(64))
 print("rgen", int(b.edge_counts.sum()))
 print("compare", sim.compare(["gp"], gen.RandomDagFactory(38, 75), iterations=16)[0].mean_makespan)
+import json
+from paper_1502_07451_b200.graphio import parse_dot, parse_dot_csr
+with open(os.path.join(ROOT, "tests", "golden", "dot_cases.json")) as f:
+    cases = json.load(f)["cases"]
+ok = 0
+for cse in cases:
+    try:
+        parse_dot(cse["text"])
+        if "error" not in cse:
+            parse_dot_csr(cse["text"])
+        ok += 1
+    except Exception:  # noqa: BLE001 - the expected parse errors
+        pass
+print("dot", ok, len(cases))
 torch.cuda.synchronize()
 print("done")
