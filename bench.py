@@ -537,17 +537,48 @@ def run_ours(args):
     # the caller's DAG as a sorted edge list (out-CSR) plus the integer edge
     # and node weights; the in-CSR is derived on the device (hs_dag_transpose)
     # rather than shipped; fp64 weights and byte counts are not inputs of K1-K6
-    host = {name: getattr(csr, name).cpu().pin_memory() for name in ("out_ptr", "out_dst")}
-    host_ew, host_nw = ew.cpu().pin_memory(), nw.cpu().pin_memory()
-    h2d = sum(t.numel() * t.element_size() for t in host.values())
-    h2d += host_ew.numel() * 4 + host_nw.numel() * 4
-    d2h = (csr.n - 1) * 4
+    if world > 1:
+        # N > 1: each rank is handed only its rows (kway.row_slice: the rows'
+        # in- and out-lists with global ids, their weights, which rows the
+        # root feeds) and reads back only its rows' parts
+        arrs = [a.cpu().numpy() for a in (csr.out_ptr, csr.out_dst, csr.in_ptr, csr.in_src,
+                                          ew, ew_in, nw)]
+        sl = kway.row_slice(*arrs, kv0, kv1)
+        del arrs
+        host = {k: torch.from_numpy(sl[k]).pin_memory() for k in kway.ROW_SLICE_KEYS}
+        r_feed = int(sl["out_ptr"][1])
+        h2d = sum(t.numel() * t.element_size() for t in host.values())
+        d2h = (kv1 - kv0) * 4
+        part_host = torch.empty(kv1 - kv0, dtype=torch.int32).pin_memory()
+    else:
+        host = {name: getattr(csr, name).cpu().pin_memory() for name in ("out_ptr", "out_dst")}
+        host_ew, host_nw = ew.cpu().pin_memory(), nw.cpu().pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in host.values())
+        h2d += host_ew.numel() * 4 + host_nw.numel() * 4
+        d2h = (csr.n - 1) * 4
+        part_host = torch.empty(n_glob, dtype=torch.int32).pin_memory()
     from paper_1502_07451_b200.csr import DagCSR
 
     side = torch.cuda.Stream(device=dev)
-    part_host = torch.empty(n_glob, dtype=torch.int32).pin_memory()
+
+    def e2e_step_rows():
+        d = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        # the unit-weight decision over every rank's weights (all ranks alike)
+        mm = torch.stack([torch.cat([d["ew"][r_feed:], d["ew_in"]]).min(),
+                          -torch.cat([d["ew"][r_feed:], d["ew_in"]]).max()]).to(torch.int64)
+        mm = mm.to(dev if dist.get_backend() == "nccl" else "cpu")
+        dist.all_reduce(mm, op=dist.ReduceOp.MIN)
+        lo, hi = int(mm[0]), -int(mm[1])
+        w0 = lo if lo == hi and lo > 0 and os.environ.get("HS_KWAY_WEIGHTS") != "1" else 0
+        ug = kway.symmetrize_slice({**sl, **d}, unit_weight=w0)
+        r = kway.partition_kway_shard(ug, kv0, n_glob, group, rank, K_PARTS, tol=TOL, seed=0,
+                                      out=part_buf)
+        part_host.copy_(r.part[kv0:kv1], non_blocking=True)  # this rank's rows
+        return part_host
 
     def e2e_step():
+        if world > 1:
+            return e2e_step_rows()
         # the edge list first; the weights' copy (side stream, queued behind
         # it on the copy engine) overlaps the device transpose
         main = torch.cuda.current_stream()
@@ -582,8 +613,10 @@ def run_ours(args):
     if os.environ.get("HS_BENCH_DEBUG"):
         print("e2e steps ms", e2e_each, "reserved GB", torch.cuda.memory_reserved() / 1e9,
               file=sys.stderr, flush=True)
+    h2d_all, d2h_all = h2d, d2h
     if world > 1:
         e2e_ms = allmax(e2e_ms, dev)
+        h2d_all, d2h_all = int(allsum(float(h2d), dev)), int(allsum(float(d2h), dev))
     del host
 
     # ---- secondary configs ----
@@ -618,8 +651,13 @@ def run_ours(args):
             "roofline": roof,
             "step_roofline": step_roof,
             "kernels": kernels,
-            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
+            "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d_all,
+                    "d2h_bytes_per_step": d2h_all,
+                    "input": ("each rank its row slice (kway.row_slice: its rows' in/out lists, "
+                              "weights, root-fed rows); reads back its rows' parts"
+                              if world > 1 else
+                              "sorted edge list (out-CSR) + integer edge/node weights; in-CSR "
+                              "built on the device; the whole part array read back")},
             "cpu_baseline": cpu,
             "cholesky": chol,
             "extra": extra,

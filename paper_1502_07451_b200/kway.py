@@ -455,6 +455,74 @@ def symmetrize_range(csr: DagCSR, kv0: int, kv1: int, edge_w_i: Optional[torch.T
                   unit_weight=w0 or 1)
 
 
+# ---- row-range input for one rank (e2e at N > 1) -------------
+# Rank r of a sharded partition needs, for its kernel rows [kv0, kv1), only
+# their in- and out-lists (global neighbour ids), the out- and in-order edge
+# weights of those lists, their node weights, and — the halo K1's row starts
+# need — which of its rows the root feeds. row_slice packs exactly that, on
+# the caller's side, as a small DAG: node 0 stands in for the root (no inputs,
+# one edge to every local row the root feeds, local ids), nodes 1..nl are the
+# rows. K1 (hs_symmetrize_range over all local rows) then writes the same
+# rows, entry for entry, as over the whole graph.
+ROW_SLICE_KEYS = ("out_ptr", "out_dst", "in_ptr", "in_src", "ew", "ew_in", "nw")
+
+
+def row_slice(out_ptr, out_dst, in_ptr, in_src, ew, ew_in, nw, kv0: int, kv1: int) -> dict:
+    """numpy (caller-side) slice of a DAG whose root is node 0 for kernel rows
+    [kv0, kv1): a dict of the local DAG's arrays (ROW_SLICE_KEYS) plus
+    ``nnz`` (undirected entries of the rows), ``kv0``, ``kv1``."""
+    v0, v1 = kv0 + 1, kv1 + 1  # node ids of the rows (root = node 0)
+    o0, o1 = int(out_ptr[v0]), int(out_ptr[v1])
+    i0, i1 = int(in_ptr[v0]), int(in_ptr[v1])
+    starts = in_ptr[v0:v1]
+    nonempty = in_ptr[v0 + 1:v1 + 1] > starts
+    fed = np.zeros(v1 - v0, dtype=bool)
+    fed[nonempty] = in_src[starts[nonempty]] == 0  # in-lists ascend: the root sorts first
+    fed_ids = (np.nonzero(fed)[0] + 1).astype(np.int32)
+    R = len(fed_ids)
+    l_out_ptr = np.empty(v1 - v0 + 2, dtype=np.int64)
+    l_out_ptr[0] = 0
+    l_out_ptr[1:] = R + (out_ptr[v0:v1 + 1] - o0)
+    l_in_ptr = np.empty(v1 - v0 + 2, dtype=np.int64)
+    l_in_ptr[0] = 0
+    l_in_ptr[1:] = in_ptr[v0:v1 + 1] - i0
+    return {"out_ptr": l_out_ptr,
+            "out_dst": np.concatenate([fed_ids, out_dst[o0:o1].astype(np.int32)]),
+            "in_ptr": l_in_ptr, "in_src": np.ascontiguousarray(in_src[i0:i1], dtype=np.int32),
+            "ew": np.concatenate([np.zeros(R, np.int32), ew[o0:o1].astype(np.int32)]),
+            "ew_in": np.ascontiguousarray(ew_in[i0:i1], dtype=np.int32),
+            "nw": np.concatenate([np.zeros(1, np.int32), nw[v0:v1].astype(np.int32)]),
+            "nnz": (i1 - i0) - R + (o1 - o0), "kv0": kv0, "kv1": kv1}
+
+
+def symmetrize_slice(sl: dict, unit_weight: Optional[int] = None) -> UGraph:
+    """K1 of one rank's rows from its row_slice (arrays as device tensors):
+    the UGraph symmetrize_range(csr, kv0, kv1, ...) builds from the whole DAG.
+    ``unit_weight``: the sharded graph's common edge weight (0 if weights
+    differ) — every rank must decide alike, so a caller holding only a slice
+    passes the decision over all ranks' weights; None decides on this slice."""
+    t = {k: sl[k] for k in ROW_SLICE_KEYS}
+    n_loc = int(t["out_ptr"].numel()) - 1
+    nl = n_loc - 1
+    dev = t["out_ptr"].device
+    if unit_weight is None:
+        R = int(t["out_ptr"][1].item())
+        both = torch.cat([t["ew"][R:], t["ew_in"]])
+        unit_weight = _uniform_weight(both)
+    g = DagCSR(n_loc, int(t["out_dst"].numel()), 0, t["out_ptr"], t["out_dst"], t["in_ptr"],
+               t["in_src"], None, None, None, None, None)
+    cap = int(sl["nnz"])
+    xadj = torch.empty(nl + 1, dtype=torch.int64, device=dev)
+    adjncy = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    adjwgt = None if unit_weight else torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+    vwgt = torch.empty(max(nl, 1), dtype=torch.int32, device=dev)
+    nnz = _native.symmetrize_range(g, 0, nl, None if unit_weight else t["ew"], t["nw"], xadj,
+                                   adjncy, adjwgt, vwgt, None if unit_weight else t["ew_in"])
+    assert nnz == cap
+    return UGraph(xadj, adjncy[:nnz], adjwgt[:nnz] if adjwgt is not None else None, vwgt[:nl],
+                  unit_weight=unit_weight or 1)
+
+
 class PartitionGroup:
     """Exchange arenas of a sharded partition, one whole device allocation per rank.
 

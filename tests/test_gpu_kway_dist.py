@@ -145,3 +145,36 @@ def test_two_process_ipc_matches_loopback():
     p = lb.part.long()
     assert res[0] == [lb.cut, int(p.sum().item()),
                       int((p * torch.arange(csr.n - 1, device="cuda")).sum().item())]
+
+
+@pytest.mark.parametrize("nranks,uniform", [(2, True), (3, False)])
+def test_row_slices_give_the_same_shards_and_partition(nranks, uniform):
+    """e2e at N > 1 ships each rank only its rows (kway.row_slice): K1 over a
+    slice writes the rank's rows of the whole graph bit for bit, so the
+    sharded partition is the same."""
+    csr = kway.layered_dag(100_000, 1_000_000, seed=11)
+    if uniform:
+        ew = kway.integer_weights(csr.w_xfer)
+    else:
+        gen_ = torch.Generator(device="cpu").manual_seed(5)
+        ew = torch.randint(1, 101, (csr.m,), generator=gen_, dtype=torch.int32).to(csr.device)
+    ew_in = kway.in_order(csr, ew)
+    nw = kway.integer_weights(csr.w_gpu)
+    h = [a.cpu().numpy() for a in (csr.out_ptr, csr.out_dst, csr.in_ptr, csr.in_src, ew, ew_in, nw)]
+    w0 = kway._uniform_weight(ew)  # the decision over all ranks' weights
+    ranges = kway.shard_ranges(csr, nranks)
+    full = [kway.symmetrize_range(csr, a, b, ew, nw, ew_in) for a, b in ranges]
+    sliced = []
+    for (a, b), f in zip(ranges, full):
+        sl = kway.row_slice(*h, a, b)
+        dev = {k: torch.from_numpy(sl[k]).to(csr.device) for k in kway.ROW_SLICE_KEYS}
+        ug = kway.symmetrize_slice({**sl, **dev}, unit_weight=w0)
+        assert torch.equal(ug.xadj, f.xadj) and torch.equal(ug.adjncy, f.adjncy)
+        assert torch.equal(ug.vwgt, f.vwgt) and ug.unit_weight == f.unit_weight
+        assert (ug._adjwgt is None) == (f._adjwgt is None)
+        if f._adjwgt is not None:
+            assert torch.equal(ug._adjwgt, f._adjwgt)
+        sliced.append(ug)
+    a = kway.partition_kway_loopback(csr, nranks, 8, seed=3, shards=full)[0]
+    b = kway.partition_kway_loopback(csr, nranks, 8, seed=3, shards=sliced)[0]
+    assert a.cut == b.cut and torch.equal(a.part, b.part)

@@ -196,3 +196,89 @@ def test_two_rank_compare_rows_match_one_device(iterations):
     assert spans[0][0] == 0 and spans[-1][1] == iterations and spans[0][1] == spans[1][0]
     for _, rows, _ in got:
         assert rows == want  # bit-identical on every rank
+
+
+def _small_dag(n, m, seed):
+    """Random DAG with root 0 feeding every node without a predecessor: the
+    host CSR arrays (out sorted by (src, dst), in ascending by source)."""
+    rng = np.random.default_rng(seed)
+    src = rng.integers(1, n - 1, m)
+    dst = np.minimum(n - 1, src + 1 + rng.integers(0, 50, m))
+    e = np.unique(np.stack([src, dst], 1), axis=0)
+    has_pred = np.zeros(n, bool)
+    has_pred[e[:, 1]] = True
+    roots = np.nonzero(~has_pred[1:])[0] + 1
+    e = np.concatenate([np.stack([np.zeros_like(roots), roots], 1), e])
+    e = e[np.lexsort((e[:, 1], e[:, 0]))]
+    out_ptr = np.zeros(n + 1, np.int64)
+    np.add.at(out_ptr, e[:, 0] + 1, 1)
+    out_ptr = np.cumsum(out_ptr)
+    ew = rng.integers(1, 100, len(e)).astype(np.int32)
+    order = np.lexsort((e[:, 0], e[:, 1]))
+    in_ptr = np.zeros(n + 1, np.int64)
+    np.add.at(in_ptr, e[:, 1] + 1, 1)
+    in_ptr = np.cumsum(in_ptr)
+    nw = rng.integers(1, 100, n).astype(np.int32)
+    return (out_ptr, e[:, 1].astype(np.int32), in_ptr, e[order, 0].astype(np.int32), ew,
+            ew[order], nw)
+
+
+def _rows(out_ptr, out_dst, in_ptr, in_src, ew, ew_in, nw, v0, v1):
+    """K1's rows for nodes [v0, v1) of a DAG with root 0: in-list (root dropped)
+    then out-list, kernel ids u - 1, with weights (the kernel's definition)."""
+    rows = []
+    for v in range(v0, v1):
+        a, b = in_ptr[v], in_ptr[v + 1]
+        ins = [(int(in_src[j]) - 1, int(ew_in[j])) for j in range(a, b) if in_src[j] != 0]
+        outs = [(int(out_dst[j]) - 1, int(ew[j])) for j in range(out_ptr[v], out_ptr[v + 1])]
+        rows.append((int(nw[v]), ins + outs))
+    return rows
+
+
+def _slice_worker(rank, world, port, q):
+    from paper_1502_07451_b200.kway import row_slice, split_bounds
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    full = _small_dag(3000, 12000, 4)
+    out_ptr, out_dst, in_ptr, in_src, ew, ew_in, nw = full
+    n = len(out_ptr) - 1
+    deg = (np.diff(in_ptr) + np.diff(out_ptr))[1:]
+    kv0, kv1 = split_bounds(np.cumsum(deg), world)[rank]
+    sl = row_slice(*full, kv0, kv1)
+    # the rank's rows from its slice alone (local rows 1..nl, global neighbour ids)
+    mine = _rows(sl["out_ptr"], sl["out_dst"], sl["in_ptr"], sl["in_src"], sl["ew"],
+                 sl["ew_in"], sl["nw"], 1, kv1 - kv0 + 1)
+    want = _rows(*full, kv0 + 1, kv1 + 1)
+    sizes = torch.tensor([sum(len(r[1]) for r in mine), int(sl["nnz"]),
+                          sum(int(sl[k].nbytes) for k in ("out_ptr", "out_dst", "in_ptr",
+                                                            "in_src", "ew", "ew_in", "nw"))])
+    alls = [torch.zeros(3, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(alls, sizes)
+    full_nnz = sum(len(r[1]) for r in _rows(*full, 1, n))
+    full_bytes = sum(int(a.nbytes) for a in full)
+    q.put((rank, mine == want, [x.tolist() for x in alls], full_nnz, full_bytes))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_row_slices_carry_their_rows():
+    """The e2e row-range split: each rank's row_slice alone
+    yields exactly its K1 rows of the whole graph, the slices' entries add up
+    to the graph's, and each rank ships a fraction of the whole DAG."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_slice_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    for rank, same, alls, full_nnz, full_bytes in got:
+        assert same
+        assert all(a[0] == a[1] for a in alls)  # nnz predicted = entries built
+        assert sum(a[0] for a in alls) == full_nnz
+        assert all(a[2] < 0.75 * full_bytes for a in alls)
