@@ -47,6 +47,20 @@ class MachineModel:
             raise SimulationError("need at least one worker")
 
 
+class Worker:
+    """A worker as the policy hooks see it (sim.py:39-46): id (CPU workers
+    first), device, memory node, name, the time it next idles, busy flag.
+    The device simulator keeps the same state per worker in its scratch."""
+
+    def __init__(self, wid: int, device: str, name: str):
+        self.id = wid
+        self.device = device
+        self.name = name
+        self.mem_node = DEVICE if device == GPU else HOST
+        self.free_time = 0.0
+        self.busy = False
+
+
 @dataclass(frozen=True)
 class TraceEvent:
     """sim.py:49-54"""
@@ -70,6 +84,15 @@ class Trace:
 
 def _policy_id(policy) -> int:
     pid = getattr(policy, "native_id", None)
+    # a subclass that overrides a hook is a custom policy: the device runs
+    # only the built-in state machines
+    if pid is not None:
+        from . import policies as _p
+        base = (_p.EagerPolicy, _p.DmdaPolicy, _p.GraphPartitionPolicy)[pid]
+        cls = type(policy)
+        if any(getattr(cls, h, None) is not getattr(base, h, None)
+               for h in ("on_ready", "next_for_worker", "_estimate")):
+            pid = None
     if pid is None:
         raise SimulationError(
             f"policy {type(policy).__name__} not supported by native backend "
