@@ -427,6 +427,12 @@ int hs_dag_transpose(int32_t n, int64_t m, const int64_t *out_ptr, const int32_t
  * uniform-weight test before K1). Synchronous on stream. */
 int hs_int32_stats(const int32_t *w, int64_t n, int64_t *sum_min_max_host, void *stream);
 
+/* METIS integer weights of n fp64 weights, elementwise on the device (one
+ * pass): out[i] = max(1, floor(w[i] * scale + 0.5)) with the reference's two
+ * fp64 roundings (graphio.py:272-274, _scaled), saturated at INT32_MAX (NaN
+ * maps to 1). Asynchronous on stream. */
+int hs_integer_weights(const double *w, int64_t n, int32_t scale, int32_t *out, void *stream);
+
 /* ---- sharded k-way partition (config 4 at 2/4/8 GPUs) ---------------------
  * One call per rank, all ranks concurrently (one process per GPU, or one host
  * thread per rank in loopback mode on a single GPU). Rank r passes the rows

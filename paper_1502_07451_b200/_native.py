@@ -106,6 +106,7 @@ _symmetrize_range = _opt("hs_symmetrize_range", _P, _i32, _i32, _P, _P, _P, _P, 
                          _P, _P)
 _dag_transpose = _opt("hs_dag_transpose", _i32, _i64, _P, _P, _P, _P, _P, _P)
 _int32_stats = _opt("hs_int32_stats", _P, _i64, _P, _P)
+_integer_weights = _opt("hs_integer_weights", _P, _i64, _i32, _P, _P)
 _partition_kway_dist = _opt("hs_partition_kway_dist", _P, _i32, _i32, _P, _i32, _P, _f64,
                             ctypes.c_uint64, _P, _P, _P)
 if hasattr(_lib, "hs_kway_dist_arena_bytes"):
@@ -443,6 +444,17 @@ def int32_stats(t: torch.Tensor) -> Tuple[int, int, int]:
     out = (ctypes.c_int64 * 3)()
     check(fn(ptr(t), t.numel(), out, stream_ptr()))
     return out[0], out[1], out[2]
+
+
+def integer_weights(w: torch.Tensor, scale: int) -> torch.Tensor:
+    """max(1, floor(w * scale + 0.5)) as int32 on the device (hs_integer_weights)."""
+    fn = _need(_integer_weights, "hs_integer_weights")
+    w = w.contiguous()
+    if w.dtype != torch.float64 or not w.is_cuda:
+        raise TypeError("integer_weights: fp64 device tensor expected")
+    out = torch.empty(w.shape, dtype=torch.int32, device=w.device)
+    check(fn(ptr(w), w.numel(), int(scale), ptr(out), stream_ptr()))
+    return out
 
 
 def symmetrize(csr, edge_w_i, node_w_i, xadj, adjncy, adjwgt_i, vwgt_i, edge_w_i_in=None,

@@ -43,6 +43,29 @@ int sm_count() {
   return cached;
 }
 
+static __global__ void first_edge_below_kernel(int32_t n, int32_t skip, bool strict,
+                                               const int64_t *out_ptr, const int32_t *out_dst,
+                                               int32_t *bad) {
+  bool any = false;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = out_ptr[v], e = out_ptr[v + 1];
+    if (b < e && v != skip) {
+      const int32_t d = __ldg(out_dst + b);
+      any |= strict ? d < v : d <= v;
+    }
+  }
+  block_flag(any, bad);
+}
+
+int first_edge_below(int32_t n, int32_t skip, bool strict, const int64_t *out_ptr,
+                     const int32_t *out_dst, int32_t *bad, cudaStream_t s) {
+  if (n <= 0) return HS_OK;
+  first_edge_below_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, skip, strict, out_ptr, out_dst, bad);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}
+
 static __global__ void iota32_kernel(int32_t *out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)

@@ -64,6 +64,24 @@ inline int grid_for(int64_t work, int block, int max_blocks = 148 * 32) {
   return (int)g;
 }
 
+#ifdef __CUDACC__
+// Raise *flag when any thread of the block saw `any` (call once per block,
+// by every thread, after its grid-stride loop): one store per block instead
+// of one same-address atomic per offending element, which serialised the
+// check on graphs where most elements offend.
+__device__ __forceinline__ void block_flag(bool any, int32_t *flag) {
+  if (__syncthreads_or(any) && threadIdx.x == 0) *(volatile int32_t *)flag = 1;
+}
+#endif
+
+// Graph-order check shared by K7, the band order and topological_order
+// (stream-ordered launch): *bad = 1 when some row's first out-neighbour (the
+// lists are sorted) lies at or below the row (strict = false) / strictly
+// below it (strict = true); rows equal to `skip` are ignored (-1: none).
+// *bad is not cleared here.
+int first_edge_below(int32_t n, int32_t skip, bool strict, const int64_t *out_ptr,
+                     const int32_t *out_dst, int32_t *bad, cudaStream_t s);
+
 // out[i] = i for i < n (stream-ordered).
 int iota32(int32_t *out, int64_t n, cudaStream_t s);
 

@@ -2290,6 +2290,41 @@ extern "C" int hs_int32_stats(const int32_t *w, int64_t n, int64_t *sum_min_max_
   return HS_OK;
 }
 
+namespace {
+// two float4-wide loads per thread-iteration; the products and sums round
+// like the reference's w * scale + 0.5 (this file builds with --fmad=false)
+__device__ __forceinline__ int32_t scaled_weight(double w, double scale) {
+  const double f = floor(w * scale + 0.5);
+  return f >= 2147483647.0 ? INT32_MAX : (f >= 1.0 ? (int32_t)f : 1);
+}
+__global__ void integer_weights_kernel(const double *w, int64_t n, double scale, int32_t *out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = ((reinterpret_cast<uintptr_t>(w) | reinterpret_cast<uintptr_t>(out)) & 15)
+                         ? 0 : n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const double2 a = __ldcs(reinterpret_cast<const double2 *>(w) + 2 * i);
+    const double2 b = __ldcs(reinterpret_cast<const double2 *>(w) + 2 * i + 1);
+    __stcs(reinterpret_cast<int4 *>(out) + i,
+           make_int4(scaled_weight(a.x, scale), scaled_weight(a.y, scale),
+                     scaled_weight(b.x, scale), scaled_weight(b.y, scale)));
+  }
+  for (int64_t i = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = scaled_weight(w[i], scale);
+}
+}  // namespace
+
+extern "C" int hs_integer_weights(const double *w, int64_t n, int32_t scale, int32_t *out,
+                                  void *stream) {
+  HS_REQUIRE(n >= 0 && (n == 0 || (w && out)), HS_EINVAL, "hs_integer_weights: null argument");
+  if (n == 0) return HS_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  hs::Prof P("integer_weights", s, 12.0 * n);
+  integer_weights_kernel<<<hs::grid_for((n + 3) / 4, 256, hs::sm_count() * 8), 256, 0, s>>>(
+      w, n, (double)scale, out);
+  HS_CHECK_LAUNCH();
+  return HS_OK;
+}
+
 extern "C" int hs_symmetrize(const hs_dag_t *g, const int32_t *edge_w_i,
                              const int32_t *edge_w_i_in, const int32_t *node_w_i, int64_t *xadj,
                              int32_t *adjncy, int32_t *adjwgt_i, int32_t *vwgt_i, int32_t *twin,

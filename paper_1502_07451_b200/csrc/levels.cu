@@ -240,15 +240,6 @@ __device__ __forceinline__ void st_relaxed(int32_t *p, int32_t v) {
 __device__ __forceinline__ void st_relaxed64(double *p, double v) {
   asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" :: "l"(p), "d"(v) : "memory");
 }
-__global__ void all_edges_up(int32_t n, const int64_t *out_ptr, const int32_t *out_dst,
-                             int32_t *bad) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = out_ptr[v], e = out_ptr[v + 1];
-    if (b < e && out_dst[b] <= v) atomicExch(bad, 1);
-  }
-}
-
 __global__ void __launch_bounds__(kFlowBlock) levels_flow(LevelArgs A, int32_t *ticket) {
   const hs_dag_t &g = A.g;
   const int lane = threadIdx.x & 31;
@@ -385,9 +376,11 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
   // DAG numbered in topological order: the barrier-free dataflow kernel
   {
     HS_CHECK_CUDA(cudaMemsetAsync(small.p + 7, 0, sizeof(int32_t), s));
-    all_edges_up<<<hs::grid_for(n, 256), 256, 0, s>>>((int32_t)n, g->out_ptr, g->out_dst,
-                                                       small.p + 7);
-    HS_CHECK_LAUNCH();
+    {
+      const int rc = hs::first_edge_below((int32_t)n, -1, false, g->out_ptr, g->out_dst,
+                                          small.p + 7, s);
+      if (rc != HS_OK) return rc;
+    }
     int32_t bad = 1;
     HS_CHECK_CUDA(cudaMemcpyAsync(&bad, small.p + 7, 4, cudaMemcpyDeviceToHost, s));
     HS_CHECK_CUDA(cudaStreamSynchronize(s));

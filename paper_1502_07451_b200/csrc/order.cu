@@ -23,15 +23,6 @@
 
 namespace {
 
-__global__ void topo_check(int32_t n, int32_t root, const int64_t *out_ptr,
-                           const int32_t *out_dst, int32_t *bad) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = out_ptr[v], e = out_ptr[v + 1];
-    if (b < e && v != root && out_dst[b] <= v) atomicExch(bad, 1);
-  }
-}
-
 // level of every kernel position (the root's node is skipped)
 __global__ void kernel_levels(int32_t nk, int32_t root, const int32_t *level, int32_t *klev) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nk;
@@ -56,19 +47,63 @@ __global__ void permuted_degrees(int32_t n, const int64_t *xadj, const int32_t *
   if (blockIdx.x == 0 && threadIdx.x == 0) deg[n] = 0;
 }
 
-// one warp per new row: the old row is read contiguously, neighbour ids go
-// through inv (a gather of 4 B per entry)
+// one warp per 32 new rows, flattened: the rows' entries are contiguous in
+// the new CSR, so lane l writes entries l, l+32, ... of the chunk; each finds
+// its old row with a 5-step search over the warp's degree prefix (no lane
+// idles on short rows, and the loads of different rows overlap). Neighbour
+// ids go through inv (a gather of 4 B per entry). kU entries per lane are in
+// flight per trip.
 __global__ void permute_rows(int32_t n, const int64_t *xadj, const int32_t *adj,
                              const int32_t *wgt, const int32_t *perm, const int32_t *inv,
                              const int64_t *xadj_new, int32_t *adj_new, int32_t *wgt_new) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += warps) {
-    const int32_t o = perm[r];
-    const int64_t b = xadj[o], d = xadj[o + 1] - b, nb = xadj_new[r];
-    for (int64_t j = lane; j < d; j += 32) {
-      adj_new[nb + j] = inv[__ldg(adj + b + j)];
-      if (wgt) wgt_new[nb + j] = __ldg(wgt + b + j);
+  for (int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; base < n;
+       base += warps * 32) {
+    const int64_t r = base + lane;
+    int64_t b = 0;
+    int32_t d = 0;
+    if (r < n) {
+      const int32_t o = __ldg(perm + r);
+      b = __ldg(xadj + o);
+      d = (int32_t)(__ldg(xadj + o + 1) - b);
+    }
+    int32_t incl = d;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const int32_t excl = incl - d;
+    const int64_t nb = __shfl_sync(0xffffffffu, (long long)__ldg(xadj_new + (r < n ? r : base)), 0);
+    // old start relative to the new offset: entry t of the chunk reads
+    // adj[b_q + t - excl_q], q = its row
+    const int64_t rel = b - excl;
+    constexpr int kU = 4;
+    for (int t0 = 0; t0 < total; t0 += 32 * kU) {
+      int64_t src[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = t0 + u * 32 + lane;
+        int q = 0;  // last lane whose exclusive prefix is <= t (a non-empty row)
+#pragma unroll
+        for (int step = 16; step; step >>= 1)
+          if (__shfl_sync(0xffffffffu, excl, q + step) <= t) q += step;
+        const int64_t rq = __shfl_sync(0xffffffffu, (long long)rel, q);  // every lane shuffles
+        src[u] = t < total ? rq + t : -1;
+      }
+      int32_t a[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) a[u] = src[u] >= 0 ? __ldcs(adj + src[u]) : 0;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int t = t0 + u * 32 + lane;
+        if (t < total) {
+          __stcs(adj_new + nb + t, __ldg(inv + a[u]));
+          if (wgt) __stcs(wgt_new + nb + t, __ldcs(wgt + src[u]));
+        }
+      }
     }
   }
 }
@@ -87,8 +122,10 @@ extern "C" int hs_dag_is_topological(const hs_dag_t *g, int32_t *result_host, vo
   hs::Scratch<int32_t> bad;
   HS_CHECK_CUDA(bad.alloc(1, s));
   HS_CHECK_CUDA(cudaMemsetAsync(bad, 0, 4, s));
-  topo_check<<<hs::grid_for(g->n, 256), 256, 0, s>>>(g->n, g->root, g->out_ptr, g->out_dst, bad);
-  HS_CHECK_LAUNCH();
+  {
+    const int rc = hs::first_edge_below(g->n, g->root, false, g->out_ptr, g->out_dst, bad, s);
+    if (rc != HS_OK) return rc;
+  }
   int32_t h = 0;
   HS_CHECK_CUDA(cudaMemcpyAsync(&h, bad.p, 4, cudaMemcpyDeviceToHost, s));
   HS_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -150,7 +187,7 @@ extern "C" int hs_ugraph_permute(const hs_ugraph_t *g, const int32_t *perm, cons
   hs::count_launch(1);
   {
     hs::Prof P("ugraph_permute", s, 16.0 * n + 12.0 * g->nnz + (g->adjwgt_i ? 8.0 * g->nnz : 0.0));
-    permute_rows<<<hs::grid_for((int64_t)n * 32, 256), 256, 0, s>>>(
+    permute_rows<<<hs::grid_for(n, 256, hs::sm_count() * 8), 256, 0, s>>>(
         n, g->xadj, g->adjncy, g->adjwgt_i, perm, inv, xadj, adjncy,
         g->adjwgt_i ? adjwgt_i : nullptr);
   }

@@ -33,15 +33,6 @@ namespace {
 
 constexpr int kTopoThreads = 1024;
 
-__global__ void topo_up_check(int32_t n, const int64_t *out_ptr, const int32_t *out_dst,
-                              int32_t *bad) {
-  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = out_ptr[v], e = out_ptr[v + 1];
-    if (b < e && out_dst[b] < v) atomicExch(bad, 1);
-  }
-}
-
 __global__ void iota_order(int32_t n, int32_t *order) {
   for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x)
@@ -249,8 +240,10 @@ extern "C" int hs_topological_order(const hs_dag_t *g, int32_t *order, int32_t *
   hs::Scratch<int32_t> flag;
   HS_CHECK_CUDA(flag.alloc(4, s));
   HS_CHECK_CUDA(cudaMemsetAsync(flag, 0, 4 * sizeof(int32_t), s));
-  topo_up_check<<<hs::grid_for(n, 256), 256, 0, s>>>(n, g->out_ptr, g->out_dst, flag);
-  HS_CHECK_LAUNCH();
+  {
+    const int rc = hs::first_edge_below(n, -1, true, g->out_ptr, g->out_dst, flag, s);
+    if (rc != HS_OK) return rc;
+  }
   int32_t bad = 0;
   HS_CHECK_CUDA(cudaMemcpyAsync(&bad, flag, 4, cudaMemcpyDeviceToHost, s));
   HS_CHECK_CUDA(cudaStreamSynchronize(s));

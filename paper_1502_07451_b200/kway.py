@@ -188,8 +188,9 @@ def in_order(csr: DagCSR, edge_attr: torch.Tensor) -> torch.Tensor:
 
 
 def integer_weights(w: torch.Tensor, scale: int = 100) -> torch.Tensor:
-    """``_scaled`` (graphio.py:272-274) elementwise: max(1, floor(w*scale + 0.5)), int32."""
-    return torch.clamp(torch.floor(w * scale + 0.5), min=1).to(torch.int32)
+    """``_scaled`` (graphio.py:272-274) elementwise: max(1, floor(w*scale + 0.5)), int32
+    (saturated at 2^31 - 1), one device pass (hs_integer_weights)."""
+    return _native.integer_weights(w, scale)
 
 
 def symmetrize(csr: DagCSR, edge_w_i: Optional[torch.Tensor] = None,

@@ -140,3 +140,22 @@ def test_fm_levels_large_k(k):
     r2 = kway.partition_kway(ug, k, tol=TOL, seed=2)
     assert torch.equal(r1.part, r2.part) and r1.cut == r2.cut
     _check(csr, r1, k, ew, nw)
+
+
+def test_integer_weights_match_scaled():
+    """hs_integer_weights == the reference's _scaled (graphio.py:272-274)
+    value for value: half-way products, values below 1/scale, tiny and huge
+    magnitudes (saturated at 2^31 - 1), unaligned starts and ragged tails."""
+    import math
+    import random
+    rng = random.Random(5)
+    vals = [0.0, 1e-300, 0.004999, 0.005, 0.015, 0.025, 1.005, 2.675, 0.125, 1e6,
+            21474836.47, 21474836.475, 21474836.48, 1e300]
+    vals += [rng.random() * 10 ** rng.randint(-4, 5) for _ in range(5000)]
+    vals += [k / 200 for k in range(4000)]  # every x.5 product of the 1/200 grid
+    w = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    for scale in (100, 1, 7):
+        want = [min(max(1, math.floor(v * scale + 0.5)), 2 ** 31 - 1) for v in vals]
+        for off in (0, 1, 3):  # unaligned views take the scalar path
+            got = kway.integer_weights(w[off:], scale).cpu().tolist()
+            assert got == want[off:]
