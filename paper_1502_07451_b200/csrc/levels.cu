@@ -8,15 +8,17 @@
 // frontier index), one persistent cooperative kernel walks the frontiers with
 // a grid barrier in between.
 //
-// Push form: a finished node pushes its finish time into every successor
-// (atomicMax on the ordered bits of a non-negative double, = the max over
-// the predecessors, exactly) and decrements the successor's pending count;
-// the count reaching 0 appends it to the next frontier. Every edge is
-// touched once, by one lane: a warp takes 32 frontier nodes and flattens
-// their out-lists across its lanes (warp prefix of the degrees), so a node
-// of degree 10 does not leave 22 lanes idle and the per-edge atomics of
-// different nodes overlap. The state (pending 4 B, reach 8 B per node) is
-// L2-resident at config 4 (120 MB).
+// Pull reach, push readiness: a frontier node first pulls its predecessors'
+// finish times over its in-list (all of them finished at earlier levels;
+// max of (finish + crossing transfer), the same max as the dataflow kernel,
+// so the same bits), then decrements each successor's pending count; the
+// count reaching 0 appends it to the next frontier. Both edge loops are
+// flattened across the warp's lanes (warp prefix of the degrees), so a node
+// of degree 10 does not leave 22 lanes idle. The only per-edge atomic is the
+// 4-byte pending decrement: the pending array (40 MB at config 4) stays in
+// L2, where the former pushed 8-byte reach next to it (160 MB of 16-byte
+// node states) missed L2 on most edges (ncu: 14 GB of DRAM traffic for
+// 100M edges, profiles/r03_ncu_k7_frontier_relabelled.json).
 #include "common.cuh"
 #include <cooperative_groups.h>
 #include <cub/device/device_radix_sort.cuh>
@@ -28,10 +30,8 @@ __device__ __forceinline__ double pmin(double a, double b) { return b < a ? b : 
 struct LevelArgs {
   hs_dag_t g;
   int mode;
-  // per node, interleaved so both atomics of an edge hit one 32-byte sector:
-  // st[2v] = max over pushed predecessor finish bits, st[2v+1] low word =
-  // pending predecessor count
-  unsigned long long *st;
+  // pending predecessor count per node
+  uint32_t *pend;
   int32_t *front[3];
   int32_t *counts;    // [3]
   int32_t *level;
@@ -79,6 +79,7 @@ __device__ __forceinline__ void stage_append(bool want, int32_t val, int32_t *s_
 __global__ void __launch_bounds__(1024) levels_kernel(LevelArgs A) {
   __shared__ int32_t s_buf[kStage];
   __shared__ int s_n, s_base;
+  __shared__ unsigned long long s_reach[1024 / 32][32];  // per warp: its nodes' pulled reach
   if (threadIdx.x == 0) s_n = 0;
   auto grid = cooperative_groups::this_grid();
   const hs_dag_t &g = A.g;
@@ -94,8 +95,7 @@ __global__ void __launch_bounds__(1024) levels_kernel(LevelArgs A) {
     bool src = false;
     if (v < g.n) {
       const int32_t d = (int32_t)(g.in_ptr[v + 1] - g.in_ptr[v]);
-      A.st[2 * v] = 0ull;
-      A.st[2 * v + 1] = (unsigned long long)(uint32_t)d;
+      A.pend[v] = (uint32_t)d;
       src = d == 0;
     }
     warp_append(src, (int32_t)v, A.front[0], &A.counts[0]);
@@ -120,27 +120,79 @@ __global__ void __launch_bounds__(1024) levels_kernel(LevelArgs A) {
     }
     for (int64_t c = wid * vpw; c < ncur; c += nwarps * vpw) {
       const int64_t i = c + lane;
-      int v = -1, pv = 0, deg = 0;
-      int64_t e0 = 0;
-      double f = 0.0;
+      int v = -1, pv = 0, deg = 0, ind = 0;
+      int64_t e0 = 0, j0 = 0;
+      double dur = 0.0;
       if (lane < vpw && i < ncur) {
         v = __ldcg(&A.front[cur][i]);
         pv = (A.mode == 3 && v != g.root) ? A.part[v] : 0;
-        const double reach = __longlong_as_double((long long)__ldcg(&A.st[2 * (int64_t)v]));
-        const double dur = A.mode == 0 ? pmin(g.w_cpu[v], g.w_gpu[v])
-                           : (A.mode == 1 ? g.w_gpu[v]
-                              : (A.mode == 2 ? g.w_cpu[v]
-                                             : (A.dev[pv] ? g.w_gpu[v] : g.w_cpu[v])));
-        f = reach + dur;
-        __stcs(&A.finish[v], f);
+        dur = A.mode == 0 ? pmin(g.w_cpu[v], g.w_gpu[v])
+              : (A.mode == 1 ? g.w_gpu[v]
+                 : (A.mode == 2 ? g.w_cpu[v] : (A.dev[pv] ? g.w_gpu[v] : g.w_cpu[v])));
+        j0 = __ldcs(g.in_ptr + v);
+        ind = (int32_t)(__ldcs(g.in_ptr + v + 1) - j0);
+        e0 = __ldcs(g.out_ptr + v);
+        deg = (int32_t)(__ldcs(g.out_ptr + v + 1) - e0);
+      }
+      constexpr int kU = 4;
+      // ---- pull: reach = max over the in-list of (finish + crossing transfer)
+      unsigned long long *my_reach = s_reach[threadIdx.x >> 5];
+      my_reach[lane] = 0ull;  // max of non-negative doubles as ordered bits
+      __syncwarp();
+      {
+        int incl = ind;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        const int excl = incl - ind;
+        for (int t0 = 0; t0 < total; t0 += 32 * kU) {
+          int owner[kU], opv[kU];
+          int64_t jj[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int t = t0 + u * 32 + lane;
+            int lo = 0;
+#pragma unroll
+            for (int step = 16; step; step >>= 1)
+              if (__shfl_sync(0xffffffffu, excl, lo + step) <= t) lo += step;
+            const long long oj = __shfl_sync(0xffffffffu, (long long)j0, lo);
+            const int oex = __shfl_sync(0xffffffffu, excl, lo);
+            owner[u] = lo;
+            opv[u] = __shfl_sync(0xffffffffu, pv, lo);
+            jj[u] = t < total ? oj + (t - oex) : -1;
+          }
+          int us[kU];
+#pragma unroll
+          for (int u = 0; u < kU; ++u) us[u] = jj[u] >= 0 ? __ldcs(g.in_src + jj[u]) : 0;
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            if (jj[u] < 0) continue;
+            // finished at an earlier level, written by another SM: L2, not L1
+            double c = __ldcg(A.finish + us[u]);
+            if (A.mode == 3) {
+              // an input crosses when it comes from another part; the root's
+              // data starts in host memory, so it crosses into GPU parts only
+              const int pu = us[u] != g.root ? A.part[us[u]] : 0;
+              const bool cross = us[u] == g.root ? A.dev[opv[u]] != 0 : pu != opv[u];
+              if (cross) c = c + g.w_xfer[__ldg(g.in_eid + jj[u])];
+            }
+            atomicMax(&my_reach[owner[u]], (unsigned long long)__double_as_longlong(c));
+          }
+        }
+      }
+      __syncwarp();
+      double f = 0.0;
+      if (v >= 0) {
+        f = __longlong_as_double((long long)my_reach[lane]) + dur;
+        __stcg(&A.finish[v], f);
         __stcs(&A.level[v], it);
         lmax = it;
         cmax = f > cmax ? f : cmax;
         ++done;
-        e0 = __ldcs(g.out_ptr + v);
-        deg = (int32_t)(__ldcs(g.out_ptr + v + 1) - e0);
       }
-      // warp prefix of the out-degrees: lane l owns edges [excl, excl + deg)
+      // ---- push: one pending decrement per out-edge
       int incl = deg;
       for (int o = 1; o < 32; o <<= 1) {
         const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -148,16 +200,12 @@ __global__ void __launch_bounds__(1024) levels_kernel(LevelArgs A) {
       }
       const int total = __shfl_sync(0xffffffffu, incl, 31);
       const int excl = incl - deg;
-      // kU edges per lane in flight: their loads and atomics are independent,
-      // only the readiness test waits for the atomicSub results
-      constexpr int kU = 4;
       for (int t0 = 0; t0 < total; t0 += 32 * kU) {
         int s[kU];
         bool ready[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int t = t0 + u * 32 + lane;
-          // owner lane: the last lane whose exclusive prefix is <= t
           int lo = 0;
 #pragma unroll
           for (int step = 16; step; step >>= 1) {
@@ -165,26 +213,13 @@ __global__ void __launch_bounds__(1024) levels_kernel(LevelArgs A) {
             const int pe = __shfl_sync(0xffffffffu, excl, probe);
             if (pe <= t) lo = probe;
           }
-          const int ov = __shfl_sync(0xffffffffu, v, lo);
-          const int opv = __shfl_sync(0xffffffffu, pv, lo);
-          const double of = __shfl_sync(0xffffffffu, f, lo);
           const long long oe0 = __shfl_sync(0xffffffffu, (long long)e0, lo);
           const int oex = __shfl_sync(0xffffffffu, excl, lo);
           s[u] = 0;
           ready[u] = false;
           if (t < total) {
-            const int64_t e = oe0 + (t - oex);
-            const int sv = __ldcs(g.out_dst + e);
-            double cand = of;
-            if (A.mode == 3) {
-              // an input crosses when it comes from another part; the root's
-              // data starts in host memory, so it crosses into GPU parts only
-              const int ps = sv != g.root ? A.part[sv] : 0;
-              const bool cross = ov == g.root ? A.dev[ps] != 0 : opv != ps;
-              if (cross) cand = cand + g.w_xfer[e];
-            }
-            atomicMax(&A.st[2 * (int64_t)sv], (unsigned long long)__double_as_longlong(cand));
-            ready[u] = atomicSub(reinterpret_cast<unsigned *>(&A.st[2 * (int64_t)sv + 1]), 1u) == 1u;
+            const int sv = __ldcs(g.out_dst + oe0 + (t - oex));
+            ready[u] = atomicSub(A.pend + sv, 1u) == 1u;
             s[u] = sv;
           }
         }
@@ -343,8 +378,9 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
                 cudaStream_t s) {
   const int64_t n = g->n;
   hs::Scratch<int32_t> fronts, small;
-  hs::Scratch<unsigned long long> cp, reach;
-  HS_CHECK_CUDA(reach.alloc(2 * n, s));
+  hs::Scratch<unsigned long long> cp;
+  hs::Scratch<uint32_t> pend;
+  HS_CHECK_CUDA(pend.alloc(n, s));
   HS_CHECK_CUDA(fronts.alloc(3 * n, s));
   HS_CHECK_CUDA(small.alloc(8, s));
   HS_CHECK_CUDA(cp.alloc(1, s));
@@ -354,7 +390,7 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
   LevelArgs A;
   A.g = *g;
   A.mode = mode;
-  A.st = reach;
+  A.pend = pend;
   for (int i = 0; i < 3; ++i) A.front[i] = fronts.p + i * n;
   A.counts = small.p;                    // [0..2]
   A.max_level = small.p + 5;
@@ -403,11 +439,12 @@ int levels_impl(const hs_dag_t *g, int mode, const int32_t *part, const int8_t *
   }
   {
     void *args[] = {&A};
-    // in_ptr (pending counts) + out-CSR + weights + reach/pending init and
-    // read + finish/level writes + frontier lists; per edge one reach and
-    // one pending read-modify-write (mode 3: + w_xfer, part of both ends)
-    hs::Prof P("levels", s, 8.0 * n + 8.0 * n + 4.0 * g->m + 16.0 * n + 24.0 * n + 12.0 * n +
-                                8.0 * n + 24.0 * g->m + (mode == 3 ? 12.0 * g->m : 0.0));
+    // per node: in_ptr for the pending init (8) + pending init (4), frontier
+    // read (4), in_ptr/out_ptr pairs (32), weights (16), finish/level writes
+    // (12), frontier append (4); per edge: in_src (4) + pulled finish (8) +
+    // out_dst (4) + pending read-modify-write (8); mode 3 + part (4), in_eid
+    // (4) and w_xfer (8) per in-edge
+    hs::Prof P("levels", s, 80.0 * n + 24.0 * g->m + (mode == 3 ? 16.0 * g->m : 0.0));
     HS_CHECK_CUDA(cudaLaunchCooperativeKernel((void *)levels_kernel, grid, block, args, 0, s));
   }
   HS_CHECK_LAUNCH();
