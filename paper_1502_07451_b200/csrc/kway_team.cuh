@@ -171,9 +171,11 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       const int tcol = threadIdx.x, base_col = threadIdx.x - lane;
       if (bands_unit) {
         // band start, unit weights, k <= 8: per-lane suffix counters in
-        // registers (ge[i] = neighbours with id >= band i's start), no
-        // per-entry shared-memory read-modify-write; the part counts go to
-        // the private columns once, so the team reduction below is unchanged
+        // registers (ge[i] = neighbours with id >= band i's start), summed
+        // over the team with shuffles; every lane then holds the vertex's
+        // eight part counts and picks the move itself (ascending parts,
+        // strict >: the largest gain, ties to the smaller part, as
+        // team_argmax) — no shared-memory columns, no per-part team loop
         int ge[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) ge[i] = 0;
@@ -191,13 +193,39 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
             for (int i = 1; i < 8; ++i) ge[i] += u[q] >= kb[i];
           }
         }
+        int cnt[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const int c = ge[q] - (q < 7 ? ge[q + 1] : 0);
-          if (q < k) priv_s[q][tcol] = c;
-          bnd |= (q != own) && c > 0;
+          int x = ge[q] - (q < 7 ? ge[q + 1] : 0);
+          for (int off = T / 2; off; off >>= 1) x += __shfl_xor_sync(0xffffffffu, x, off, T);
+          cnt[q] = q < k ? x : 0;
         }
-      } else
+        int cown = 0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          cown = q == own ? cnt[q] : cown;
+          bnd |= q != own && cnt[q] > 0;
+        }
+        const bool can = valid && bnd && s_pw[own] - vwv >= s_lo[own];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (can && q < k && q != own && s_pw[q] + vwv <= s_hi[q] && cnt[q] - cown > bg) {
+            bg = cnt[q] - cown;
+            bp = q;
+          }
+        }
+        if (cache.p && valid) {
+          if (cache.kc * cache.cw == 8 && cache.cw == 1) {  // one 8-byte row
+            unsigned long long row = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) row |= (unsigned long long)(cnt[q] & 0xff) << (8 * q);
+            if (lane == 0) st_keep2(reinterpret_cast<unsigned long long *>(cache.p) + v, row,
+                                    l2_keep());
+          } else {
+            for (int q = lane; q < k; q += T) cache.set(v, q, cnt[q]);
+          }
+        }
+      } else {
       for (int j0 = lane; j0 < d; j0 += U * T) {
         int w[U], p[U];
         if (gp) {
@@ -259,6 +287,7 @@ refine_cand_t(G g, const part_t *part, int k, const int64_t *pw, const int64_t *
       }
       __syncwarp();
       team_argmax<T>(bg, bp);
+      }
     } else if constexpr (KR > 0) {
       // PK = 2: two 16-bit counters per register (host guarantees every
       // vertex's weighted degree < 2^16 on this level); PK = 1: 32-bit.
