@@ -267,15 +267,25 @@ def _oracle_cfg2_evaluate(_=None):
 
 def _cfg5_spec(seed: int):
     """generate_random_dag(38, 75, "MA", 1024, seed) + SyntheticCostModel weights as
-    an oracle spec (input synthesis: the host restatement of graph.py:180-324)."""
+    an oracle spec, all on the host (input synthesis for the CPU arm: the host
+    restatement of graph.py:180-305 and the scalar cost model of costs.py:82-104,
+    applied per node and edge as attach_weights does, graph.py:308-324 — no
+    device code on the reference arm)."""
     from paper_1502_07451_b200.costs import SyntheticCostModel
     from paper_1502_07451_b200.gen import generate_random_dag
-    from paper_1502_07451_b200.graph import attach_weights
-    g = attach_weights(generate_random_dag(38, 75, "MA", 1024, seed=seed), SyntheticCostModel())
+    from paper_1502_07451_b200.graph import CPU, GPU, SOURCE_KIND
+    g = generate_random_dag(38, 75, "MA", 1024, seed=seed)
+    model = SyntheticCostModel()
+
+    def node_row(x):
+        if x.id == g.root or x.kind == SOURCE_KIND:
+            return [x.id, x.kind, x.size, 0.0, 0.0]
+        return [x.id, x.kind, x.size, model.kernel_time(x.kind, x.size, CPU),
+                model.kernel_time(x.kind, x.size, GPU)]
     return {"root": g.root,
-            "nodes": [[x.id, x.kind, x.size, x.weight_cpu, x.weight_gpu]
-                      for x in sorted(g.nodes.values(), key=lambda x: x.id)],
-            "edges": [[u, v, e.bytes, e.weight_xfer] for (u, v), e in sorted(g.edges.items())]}
+            "nodes": [node_row(x) for x in sorted(g.nodes.values(), key=lambda x: x.id)],
+            "edges": [[u, v, e.bytes, model.transfer_time(e.bytes)]
+                      for (u, v), e in sorted(g.edges.items())]}
 
 
 def _oracle_cfg5_chunk(seeds):
