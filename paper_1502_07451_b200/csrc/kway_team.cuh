@@ -1089,7 +1089,8 @@ inline int after_team_for(const G &g) { return team_for(g); }
 #define HS_REFINE_DISPATCH(T_, K_, PACK16_, GRID, ...)                          \
   do {                                                                           \
     if ((K_) <= 16) {  /* private shared-memory counters per lane */             \
-      if ((T_) == 2) refine_cand_t<2, -16, 4><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);   \
+      if ((T_) == 1) refine_cand_t<1, -16, 8><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);   \
+      else if ((T_) == 2) refine_cand_t<2, -16, 4><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);   \
       else if ((T_) == 16) refine_cand_t<16, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);\
       else refine_cand_t<32, -16><<<GRID, kTeamBlock, 0, s>>>(__VA_ARGS__);               \
     } else {                                                                     \
